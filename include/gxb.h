@@ -1,0 +1,203 @@
+/*
+ * gxb.h — C ABI of libgxb200.so, the B200-native daemon for GX-Plug's
+ * per-iteration graph compute path (MSGGen -> MSGMerge -> MSGApply plus the
+ * per-iteration mirror exchange).
+ *
+ * Every entry point returns an int status: GXB_OK (0) or a negative GXB_E*
+ * code; gxb_last_error() returns a thread-local message for the last failure.
+ * Plain pointers and sizes only. Streams are passed as `void*` (a
+ * cudaStream_t; NULL = the legacy default stream). Calls on one gxb_ctx must be
+ * serialised by the caller — the role the agent<->daemon region queue plays in
+ * the reference (`A/channel.py:74-130`).
+ *
+ * Reference interfaces replaced (A/ = pkg/src/accelgraph/):
+ *   gxb_init / gxb_shutdown / gxb_init_count ..... Daemon.initialize / shutdown /
+ *                                                   init_count (A/daemon.py:133-168),
+ *                                                   daemon_init (A/daemon.py:207-212)
+ *   gxb_graph_build .............................. partition_graph (A/graph.py:175-212)
+ *                                                   + Agent._remote_dsts (A/agent.py:156-166)
+ *   gxb_graph_get_info / gxb_graph_ids ............... PartitionedGraph.num_vertices /
+ *                                                   vertex_ids / out_degree (A/graph.py:109-128)
+ *   gxb_state_create ............................. make_algorithm + initial_attr /
+ *                                                   initially_active (A/algorithms.py:208-229,
+ *                                                   96-100, 141-145, 179-183)
+ *   gxb_request(GXB_OP_GEN|MERGE|APPLY) .......... execute_request (A/daemon.py:86-130) over a
+ *                                                   WorkItem range descriptor; Agent.request
+ *                                                   (A/agent.py:234-276)
+ *   gxb_iterate .................................. one BSP iteration Gen∘Merge∘Apply
+ *                                                   (A/agent.py:469-498, A/algorithms.py:318-341)
+ *   gxb_stats .................................... round_closed / vote inputs, max_stat,
+ *                                                   next frontier (A/agent.py:404-417, 533-540)
+ *   gxb_exchange_* ............................... sync round gqq/gdq + skip
+ *                                                   (A/engine.py:242-266, A/sync.py:163-208,
+ *                                                   A/agent.py:542-592)
+ *   gxb_read_attrs ............................... dump of Engine.store / run_reference attrs
+ *                                                   (A/engine.py:370, 430-433)
+ */
+#ifndef GXB_H
+#define GXB_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define GXB_OK            0
+#define GXB_EINVAL       -22   /* bad argument (Python: ValueError) */
+#define GXB_EPROTO       -71   /* protocol violation, e.g. re-init (Python: ProtocolError) */
+#define GXB_ENOMEM       -12   /* device allocation failed (Python: MemoryError) */
+#define GXB_ECUDA        -5    /* CUDA runtime error (Python: RuntimeError) */
+#define GXB_ERANGE       -34   /* value outside the device representation (Python: ValueError) */
+#define GXB_ENOTOWNED    -66   /* apply target not owned by this partition (Python: ValueError) */
+#define GXB_ESTATE       -77   /* call out of order for the current phase (Python: ProtocolError) */
+
+/* algorithms (A/algorithms.py:81-205; CC per SURVEY.md Appendix A) */
+#define GXB_ALGO_SSSP      0
+#define GXB_ALGO_PAGERANK  1
+#define GXB_ALGO_LP        2
+#define GXB_ALGO_CC        3
+
+/* template operations (A/channel.py:25-28) */
+#define GXB_OP_GEN    0
+#define GXB_OP_MERGE  1
+#define GXB_OP_APPLY  2
+
+/* gxb_graph_build flags */
+#define GXB_BUILD_HOST_INPUT   0x1u  /* src/dst/w are host pointers (else device pointers) */
+#define GXB_BUILD_NO_CSR       0x2u  /* skip the push-mode CSR (PR/LP never push) */
+
+/* gxb_iterate direction policy */
+#define GXB_DIR_AUTO  0
+#define GXB_DIR_PULL  1
+#define GXB_DIR_PUSH  2
+
+typedef struct gxb_ctx gxb_ctx;
+typedef struct gxb_graph gxb_graph;
+typedef struct gxb_state gxb_state;
+
+typedef struct gxb_graph_info {
+    uint64_t num_vertices;     /* present ids (A/graph.py:163-164) */
+    uint64_t num_edges;        /* all edges of the graph (duplicates, self-loops kept) */
+    uint64_t owned_lo;         /* owned slot range [owned_lo, owned_hi) in device order */
+    uint64_t owned_hi;
+    uint64_t owned_edges;      /* in-edges of the owned destinations (CSC slice) */
+    uint64_t owned_out_edges;  /* out-edges of owned sources (push CSR slice), 0 if not built */
+    uint32_t max_id;           /* largest present original id */
+    uint32_t max_in_degree;
+    int32_t  part;             /* partition index / world size */
+    int32_t  nparts;
+    int32_t  weighted;
+    int32_t  has_csr;
+} gxb_graph_info;
+
+typedef struct gxb_iter_stats {
+    uint64_t iteration;        /* apply rounds completed */
+    uint64_t changed;          /* owned vertices whose attribute changed (A/agent.py:406-409) */
+    uint64_t next_active;      /* owned vertices active next iteration (A/agent.py:416) */
+    uint64_t next_units;       /* out-edges of the next frontier = next GEN units (A/daemon.py:102) */
+    uint64_t units;            /* GEN units processed in the last iteration */
+    uint64_t targets;          /* vertices that received >= 1 message (|merged|, A/algorithms.py:327) */
+    uint64_t remote_active;    /* next-active vertices with a cross-partition consumer (A/agent.py:533-535) */
+    double   max_stat;         /* max convergence_stat over changed vertices (A/algorithms.py:335) */
+    int32_t  voted;            /* local convergence vote (A/algorithms.py:70-72, 164-165) */
+    int32_t  direction;        /* GXB_DIR_PULL / GXB_DIR_PUSH used by the last iteration */
+} gxb_iter_stats;
+
+typedef struct gxb_rmat_args {
+    uint32_t scale, edge_factor;
+    uint64_t seed;
+    uint32_t a, b, c;          /* quadrant thresholds * 2^32 (include/gxb_rmat.h) */
+    uint32_t wmax, scramble, symmetric;
+} gxb_rmat_args;
+
+/* ---- errors / lifecycle (A/daemon.py:133-212) ---- */
+const char* gxb_last_error(void);
+const char* gxb_version(void);
+int gxb_init(int device, gxb_ctx** out);            /* Daemon.initialize: exactly once */
+int gxb_reinit(gxb_ctx* ctx);                       /* always GXB_EPROTO (A/daemon.py:150-154) */
+int gxb_init_count(const gxb_ctx* ctx, int* out);
+int gxb_shutdown(gxb_ctx* ctx);                     /* idempotent (A/daemon.py:163-168) */
+
+/* ---- device R-MAT ingest ---- */
+/* Fills device arrays src/dst[/w] (num = gxb_rmat_num_edges) on `stream`. */
+int gxb_rmat_generate(gxb_ctx* ctx, const gxb_rmat_args* args, uint32_t* d_src,
+                      uint32_t* d_dst, uint32_t* d_w, void* stream);
+
+/* ---- graph store (A/graph.py:175-212) ----
+ * Builds the device store from E edges (src[i] -> dst[i], weight w[i] or 1).
+ * Weights are non-negative integers (u32); the float64 reference weights are
+ * accepted by the Python layer only when integral.
+ * nparts/part: destination-range partition (part in [0, nparts)); every rank
+ * passes the SAME full edge list and receives the in-edges of its own
+ * destination range, balanced by in-edge count (Lemma 2 with equal c_j,
+ * A/balancer.py:79-98). nparts = 1 for a single GPU. */
+int gxb_graph_build(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint32_t* w,
+                    uint64_t num_edges, int part, int nparts, uint32_t flags, void* stream,
+                    gxb_graph** out);
+int gxb_graph_get_info(const gxb_graph* g, gxb_graph_info* out);
+/* ascending present ids (host buffer of num_vertices) */
+int gxb_graph_ids(const gxb_graph* g, uint32_t* host_out);
+/* global out-degree per present id in ascending-id order (host, num_vertices) */
+int gxb_graph_out_degree(const gxb_graph* g, uint32_t* host_out);
+/* partition boundaries in device slot order (host, nparts+1) */
+int gxb_graph_part_bounds(const gxb_graph* g, uint64_t* host_out);
+int gxb_graph_free(gxb_graph* g);
+
+/* ---- algorithm state ---- */
+/* sources: original ids for SSSP (NULL/nsrc=0 = 4 lowest present ids,
+ * A/algorithms.py:219-222), at most 4. */
+int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc,
+                     gxb_state** out);
+int gxb_state_free(gxb_state* s);
+int gxb_state_arity(const gxb_state* s, int* out);
+
+/* One fused BSP iteration over the owned partition: Gen∘Merge∘Apply in one
+ * pull pass (or push over the CSR for sparse SSSP/CC frontiers). Leaves the
+ * stats on the device; gxb_stats() synchronises `stream` and reads them. */
+int gxb_iterate(gxb_state* s, int direction, void* stream);
+
+/* API-faithful template ops over a WorkItem range descriptor (A/daemon.py:86-130):
+ *   GEN:   [lo, hi) = owned CSC edge range; materialises one message per edge
+ *          whose source is active (A/algorithms.py:232-240)
+ *   MERGE: [lo, hi) = owned destination slots; folds each slot's messages
+ *          (A/algorithms.py:243-263)
+ *   APPLY: [lo, hi) = owned destination slots; applies, detects changes, builds
+ *          the next frontier (A/algorithms.py:266-295). Targets outside the owned
+ *          range fail with GXB_ENOTOWNED (A/daemon.py:121-122).
+ * After all APPLY ranges of an iteration, gxb_commit() closes the round. */
+int gxb_request(gxb_state* s, int op, uint64_t lo, uint64_t hi, void* stream);
+int gxb_commit(gxb_state* s, void* stream);
+
+int gxb_stats(gxb_state* s, void* stream, gxb_iter_stats* out);
+
+/* ---- mirror exchange (A/engine.py:242-266) ----
+ * Multi-partition runs keep a full-length replica of every source value. After
+ * an iteration each rank publishes its changed owned values; the caller moves
+ * the bytes with NCCL (torch.distributed) between these device buffers:
+ *   dense (PR): the owned slice of the value replica is all-gathered in place;
+ *   delta (SSSP/CC/LP): gxb_exchange_pack writes (slot, value) records of
+ *     changed owned vertices; gxb_exchange_unpack installs received records
+ *     into the replica and marks them active for the next iteration. */
+int gxb_exchange_buffer(gxb_state* s, int which, void** dev_ptr, uint64_t* bytes);
+int gxb_exchange_pack(gxb_state* s, void* stream, uint64_t* count_out);
+int gxb_exchange_unpack(gxb_state* s, const void* d_records, uint64_t count, void* stream);
+int gxb_exchange_finish(gxb_state* s, void* stream);
+#define GXB_BUF_VALUES      0   /* the value replica (contributions / distances / labels) */
+#define GXB_BUF_SEND        1   /* packed (slot, value) records of this rank */
+#define GXB_BUF_RECV        2   /* receive area for peers' records */
+#define GXB_BUF_RECORD_SIZE 3   /* bytes per record in *bytes */
+
+/* attributes in ascending original-id order (host buffer num_vertices * arity;
+ * SSSP: float64 distances, +inf unreachable; PR: float64 rank; LP/CC: float64 label).
+ * Only owned vertices are meaningful on a partitioned run (owned_only = 1
+ * writes NaN elsewhere). */
+int gxb_read_attrs(gxb_state* s, double* host_out, int owned_only, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GXB_H */

@@ -1,0 +1,1056 @@
+// gxb_algo.cu — MSGGen / MSGMerge / MSGApply kernels (K1, K2, K4, K5) and the
+// per-iteration driver of the device daemon.
+//
+// Fused path (gxb_iterate): one pull pass over the owned CSC computes, for each
+// destination slot, Gen (the per-edge message, A/algorithms.py:102-105,
+// 147-149) folded with Merge (A/algorithms.py:107-108, 151-152) and finishes
+// with Apply (A/algorithms.py:113-115, 157-159) plus change detection, the
+// next-frontier bitmap/list and the vote statistics (A/agent.py:404-417,
+// A/algorithms.py:327-341). Destinations are degree-binned (slots are sorted
+// by in-degree, so every bin is a contiguous range): groups of 1..32 lanes per
+// destination, and above kChunkMinDeg one warp per kChunkEdges-edge chunk with
+// the chunks of a hub combined by the last-arriving warp (deterministic order).
+//
+// SSSP and CC also have a push pass over the CSR for sparse frontiers
+// (SURVEY.md §8(f) row 3): atomicMin into the next-value array plus a touched
+// bitmap; synchronous BSP semantics are kept because every message is built
+// from the frozen current values (A/algorithms.py:319-325).
+//
+// Request path (gxb_request): GEN materialises one message per CSC edge
+// (coalesced, edge-parallel), MERGE folds them per destination with the same
+// binned segmented reduction, APPLY runs the vertex update — the reference's
+// execute_request over a WorkItem (A/daemon.py:86-130) with range descriptors
+// instead of Python triplet blocks.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "gxb_state.cuh"
+
+namespace gxb {
+
+// ======================================================================
+// algorithm semantics
+// ======================================================================
+
+struct PrOps {  // PageRank (A/algorithms.py:125-171)
+    struct Acc {
+        double s;
+    };
+    using Msg = double;
+    const double* contrib_cur;
+    double* rank;
+    double* contrib_next;
+    FrontierView f;
+
+    __device__ static Acc identity() { return {0.0}; }
+    __device__ static Acc combine(Acc a, Acc b) { return {a.s + b.s}; }
+    __device__ static Acc shfl(Acc a, int off) { return {__shfl_xor_sync(kFull, a.s, off)}; }
+    __device__ static void st_cg(Acc* p, Acc a) { __stcg(&p->s, a.s); }
+    __device__ static Acc ld_cg(const Acc* p) { return {__ldcg(&p->s)}; }
+    __device__ static bool has(const Acc&) { return true; }
+    // Gen: rank / out_deg of the source (every vertex is active, 144-145)
+    __device__ bool gen(uint32_t s, uint64_t, const uint32_t*, Msg& m) const {
+        m = __ldg(contrib_cur + s);
+        return true;
+    }
+    __device__ static void fold(Acc& a, Msg m) { a.s += m; }
+    // Apply: 0.15 + 0.85 * sum with two roundings (157-159; no FMA contraction),
+    // convergence_stat |new - old| (161-162), always active.
+    __device__ void apply(uint32_t slot, Acc a, LocalStats& st) const {
+        const double old = rank[slot];
+        const double nw = __dadd_rn(0.15, __dmul_rn(0.85, a.s));
+        rank[slot] = nw;
+        const uint32_t od = __ldg(f.outdeg + slot);
+        contrib_next[slot] = od ? __ddiv_rn(nw, (double)od) : 0.0;
+        if (nw != old) {
+            st.changed++;
+            st.max_stat = fmax(st.max_stat, fabs(nw - old));
+        }
+    }
+};
+
+__device__ __forceinline__ uint4 min4(uint4 a, uint4 b) {
+    return make_uint4(min(a.x, b.x), min(a.y, b.y), min(a.z, b.z), min(a.w, b.w));
+}
+__device__ __forceinline__ bool eq4(uint4 a, uint4 b) {
+    return a.x == b.x && a.y == b.y && a.z == b.z && a.w == b.w;
+}
+
+struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-122)
+    struct Acc {
+        uint4 m;
+        uint32_t has;
+    };
+    using Msg = uint4;
+    const uint4* dist_cur;
+    uint4* dist_next;
+    const uint32_t* active_cur;
+    FrontierView f;
+
+    __device__ static Acc identity() { return {make_uint4(kInf32, kInf32, kInf32, kInf32), 0u}; }
+    __device__ static Acc combine(Acc a, Acc b) { return {min4(a.m, b.m), a.has | b.has}; }
+    __device__ static Acc shfl(Acc a, int off) {
+        Acc r;
+        r.m.x = __shfl_xor_sync(kFull, a.m.x, off);
+        r.m.y = __shfl_xor_sync(kFull, a.m.y, off);
+        r.m.z = __shfl_xor_sync(kFull, a.m.z, off);
+        r.m.w = __shfl_xor_sync(kFull, a.m.w, off);
+        r.has = __shfl_xor_sync(kFull, a.has, off);
+        return r;
+    }
+    __device__ static void st_cg(Acc* p, Acc a) {
+        __stcg(&p->m, a.m);
+        __stcg(&p->has, a.has);
+    }
+    __device__ static Acc ld_cg(const Acc* p) { return {__ldcg(&p->m), __ldcg(&p->has)}; }
+    __device__ static bool has(const Acc& a) { return a.has != 0; }
+    // Gen: d + w per lane from an active source (102-105); inf stays inf
+    __device__ bool gen(uint32_t s, uint64_t e, const uint32_t* w, Msg& m) const {
+        if (!bit_test(active_cur, s)) return false;
+        const uint4 d = __ldg(dist_cur + s);
+        const uint32_t ww = w ? __ldg(w + e) : 1u;
+        m = make_uint4(sat_add(d.x, ww), sat_add(d.y, ww), sat_add(d.z, ww), sat_add(d.w, ww));
+        return true;
+    }
+    __device__ static void fold(Acc& a, Msg m) {
+        a.m = min4(a.m, m);
+        a.has = 1u;
+    }
+    // Apply: elementwise min, active iff changed (113-115)
+    __device__ void apply(uint32_t slot, Acc a, LocalStats& st) const {
+        if (!a.has) return;
+        st.targets++;
+        const uint4 o = dist_cur[slot];
+        const uint4 n = min4(o, a.m);
+        if (!eq4(n, o)) {
+            dist_next[slot] = n;
+            publish_changed(f, slot, st);
+        }
+    }
+};
+
+struct CcOps {  // min-label propagation
+    struct Acc {
+        uint32_t m;
+        uint32_t has;
+    };
+    using Msg = uint32_t;
+    const uint32_t* lab_cur;
+    uint32_t* lab_next;
+    const uint32_t* active_cur;
+    FrontierView f;
+
+    __device__ static Acc identity() { return {kInf32, 0u}; }
+    __device__ static Acc combine(Acc a, Acc b) { return {min(a.m, b.m), a.has | b.has}; }
+    __device__ static Acc shfl(Acc a, int off) {
+        return {__shfl_xor_sync(kFull, a.m, off), __shfl_xor_sync(kFull, a.has, off)};
+    }
+    __device__ static void st_cg(Acc* p, Acc a) {
+        __stcg(&p->m, a.m);
+        __stcg(&p->has, a.has);
+    }
+    __device__ static Acc ld_cg(const Acc* p) { return {__ldcg(&p->m), __ldcg(&p->has)}; }
+    __device__ static bool has(const Acc& a) { return a.has != 0; }
+    __device__ bool gen(uint32_t s, uint64_t, const uint32_t*, Msg& m) const {
+        if (!bit_test(active_cur, s)) return false;
+        m = __ldg(lab_cur + s);
+        return true;
+    }
+    __device__ static void fold(Acc& a, Msg m) {
+        a.m = min(a.m, m);
+        a.has = 1u;
+    }
+    __device__ void apply(uint32_t slot, Acc a, LocalStats& st) const {
+        if (!a.has) return;
+        st.targets++;
+        const uint32_t o = lab_cur[slot];
+        const uint32_t n = min(o, a.m);
+        if (n != o) {
+            lab_next[slot] = n;
+            publish_changed(f, slot, st);
+        }
+    }
+};
+
+// ======================================================================
+// policies: how an edge contributes to the accumulator, and what happens to
+// the folded value of a destination
+// ======================================================================
+
+template <class Ops>
+struct FusedPolicy {  // Gen∘Merge∘Apply
+    Ops ops;
+    const uint32_t* in_w;
+    using Acc = typename Ops::Acc;
+    __device__ void accumulate(Acc& a, uint32_t s, uint64_t e) const {
+        typename Ops::Msg m;
+        if (ops.gen(s, e, in_w, m)) Ops::fold(a, m);
+    }
+    __device__ void finish(uint32_t slot, Acc a, LocalStats& st) const { ops.apply(slot, a, st); }
+};
+
+template <class Ops>
+struct MergePolicy {  // MSGMerge over materialised messages
+    Ops ops;
+    const typename Ops::Msg* msg;
+    const uint8_t* valid;
+    typename Ops::Acc* merged;  // indexed by slot - lo
+    uint64_t lo;
+    using Acc = typename Ops::Acc;
+    __device__ void accumulate(Acc& a, uint32_t, uint64_t e) const {
+        if (valid[e]) Ops::fold(a, msg[e]);
+    }
+    __device__ void finish(uint32_t slot, Acc a, LocalStats&) const { merged[slot - lo] = a; }
+};
+
+// ======================================================================
+// the binned pull merge
+// ======================================================================
+
+struct PullLaunch {
+    uint64_t lo;           // owned slot base
+    const uint64_t* in_off;
+    const uint32_t* in_src;
+    // slot filter (relative), [flo, fhi)
+    uint64_t flo, fhi;
+    // chunk items
+    uint64_t num_items;
+    const uint32_t* item_slot;
+    const uint64_t* item_begin;
+    const uint32_t* item_first;
+    const uint32_t* item_count;
+    uint32_t* arrive;
+    void* partials;
+    unsigned chunk_blocks;
+    // group bins k = 5..0 (G = 1 << k): relative slot ranges and block counts
+    uint64_t bin_lo[kNumGroupBins], bin_hi[kNumGroupBins];
+    unsigned bin_blocks[kNumGroupBins];
+    StatStripe* stats;
+};
+
+template <class Pol>
+__device__ __forceinline__ void edge_loop(const Pol& p, const uint32_t* __restrict__ in_src,
+                                          typename Pol::Acc& acc, uint64_t e, uint64_t end,
+                                          int stride) {
+    // four independent index loads, then four gathers: MLP for the random reads
+    for (; e + 3ull * stride < end; e += 4ull * stride) {
+        const uint32_t s0 = __ldg(in_src + e);
+        const uint32_t s1 = __ldg(in_src + e + stride);
+        const uint32_t s2 = __ldg(in_src + e + 2ull * stride);
+        const uint32_t s3 = __ldg(in_src + e + 3ull * stride);
+        p.accumulate(acc, s0, e);
+        p.accumulate(acc, s1, e + stride);
+        p.accumulate(acc, s2, e + 2ull * stride);
+        p.accumulate(acc, s3, e + 3ull * stride);
+    }
+    for (; e < end; e += stride) p.accumulate(acc, __ldg(in_src + e), e);
+}
+
+template <int G, class Pol>
+__device__ __forceinline__ void run_group(const Pol& p, const PullLaunch& L, int k, unsigned b,
+                                          LocalStats& st) {
+    using Ops = decltype(p.ops);
+    constexpr int kPerBlock = kBlock / G;
+    const int grp = threadIdx.x / G;
+    const int gl = threadIdx.x % G;
+    const uint64_t rel = L.bin_lo[k] + (uint64_t)b * kPerBlock + grp;
+    const bool valid = rel < L.bin_hi[k] && rel >= L.flo && rel < L.fhi;
+    uint64_t beg = 0, end = 0;
+    if (valid) {
+        beg = __ldg(L.in_off + rel);
+        end = __ldg(L.in_off + rel + 1);
+    }
+    auto acc = Ops::identity();
+    edge_loop(p, L.in_src, acc, beg + gl, end, G);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc = Ops::combine(acc, Ops::shfl(acc, o));
+    if (valid && gl == 0) p.finish((uint32_t)(L.lo + rel), acc, st);
+}
+
+template <class Pol>
+__device__ __forceinline__ void run_item(const Pol& p, const PullLaunch& L, uint64_t item,
+                                         LocalStats& st) {
+    using Ops = decltype(p.ops);
+    using Acc = typename Ops::Acc;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rel = __ldg(L.item_slot + item);
+    const bool valid = rel >= L.flo && rel < L.fhi;
+    if (!valid) return;  // warp-uniform
+    const uint64_t beg = __ldg(L.item_begin + item);
+    const uint64_t seg_end = __ldg(L.in_off + rel + 1);
+    const uint64_t end = min(beg + (uint64_t)kChunkEdges, seg_end);
+    Acc acc = Ops::identity();
+    edge_loop(p, L.in_src, acc, beg + lane, end, 32);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = Ops::combine(acc, Ops::shfl(acc, o));
+    const uint32_t count = __ldg(L.item_count + item);
+    if (count == 1) {
+        if (lane == 0) p.finish((uint32_t)(L.lo + rel), acc, st);
+        return;
+    }
+    Acc* partials = reinterpret_cast<Acc*>(L.partials);
+    unsigned last = 0;
+    if (lane == 0) {
+        Ops::st_cg(partials + item, acc);
+        __threadfence();
+        last = (atomicAdd(L.arrive + rel, 1u) == count - 1) ? 1u : 0u;
+    }
+    last = __shfl_sync(kFull, last, 0);
+    if (!last) return;
+    __threadfence();
+    // the last warp folds the chunk partials of this slot in item order
+    const uint32_t first = __ldg(L.item_first + item);
+    Acc tot = Ops::identity();
+    for (uint32_t i = lane; i < count; i += 32) tot = Ops::combine(tot, Ops::ld_cg(partials + first + i));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot = Ops::combine(tot, Ops::shfl(tot, o));
+    if (lane == 0) {
+        L.arrive[rel] = 0u;  // reset for the next pass
+        p.finish((uint32_t)(L.lo + rel), tot, st);
+    }
+}
+
+template <class Pol>
+__global__ void __launch_bounds__(kBlock) k_pull(const Pol p, const PullLaunch L) {
+    LocalStats st;
+    unsigned b = blockIdx.x;
+    if (b < L.chunk_blocks) {
+        const uint64_t item = (uint64_t)b * (kBlock / 32) + (threadIdx.x >> 5);
+        if (item < L.num_items) run_item(p, L, item, st);
+    } else {
+        b -= L.chunk_blocks;
+        int k = kNumGroupBins - 1;
+        for (; k > 0; --k) {
+            if (b < L.bin_blocks[k]) break;
+            b -= L.bin_blocks[k];
+        }
+        switch (k) {
+            case 5: run_group<32>(p, L, 5, b, st); break;
+            case 4: run_group<16>(p, L, 4, b, st); break;
+            case 3: run_group<8>(p, L, 3, b, st); break;
+            case 2: run_group<4>(p, L, 2, b, st); break;
+            case 1: run_group<2>(p, L, 1, b, st); break;
+            default: run_group<1>(p, L, 0, b, st); break;
+        }
+    }
+    flush_stats(st, L.stats);
+}
+
+// ======================================================================
+// push (SSSP / CC): warp per frontier source over the CSR
+// ======================================================================
+
+struct PushLaunch {
+    uint64_t lo, hi;
+    const uint64_t* out_off;
+    const uint32_t* out_dst;
+    const uint32_t* out_w;
+    const uint32_t* frontier;
+    uint64_t nfront;
+    uint32_t* touched;  // bitmap over owned slots
+    uint32_t* list_next;
+    unsigned long long* count_next;
+};
+
+__global__ void __launch_bounds__(kBlock) k_push_sssp(const uint4* __restrict__ dist_cur, uint4* dist_next,
+                                                       const PushLaunch L) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
+    for (uint64_t f = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); f < L.nfront; f += nwarps) {
+        const uint32_t s = __ldg(L.frontier + f);
+        const uint64_t beg = __ldg(L.out_off + s), end = __ldg(L.out_off + s + 1);
+        const uint4 d = __ldg(dist_cur + s);
+        for (uint64_t e = beg + lane; e < end; e += 32) {
+            const uint32_t t = __ldg(L.out_dst + e);
+            const uint32_t w = L.out_w ? __ldg(L.out_w + e) : 1u;
+            const uint4 c = make_uint4(sat_add(d.x, w), sat_add(d.y, w), sat_add(d.z, w), sat_add(d.w, w));
+            uint4 cur = __ldcg(dist_next + t);
+            unsigned* p = reinterpret_cast<unsigned*>(dist_next + t);
+            bool lowered = false;
+            if (c.x < cur.x) lowered |= atomicMin(p + 0, c.x) > c.x;
+            if (c.y < cur.y) lowered |= atomicMin(p + 1, c.y) > c.y;
+            if (c.z < cur.z) lowered |= atomicMin(p + 2, c.z) > c.z;
+            if (c.w < cur.w) lowered |= atomicMin(p + 3, c.w) > c.w;
+            if (lowered && bit_set_atomic(L.touched, (uint32_t)(t - L.lo))) warp_append(L.list_next, L.count_next, t);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_push_cc(const uint32_t* __restrict__ lab_cur, uint32_t* lab_next,
+                                                     const PushLaunch L) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
+    for (uint64_t f = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); f < L.nfront; f += nwarps) {
+        const uint32_t s = __ldg(L.frontier + f);
+        const uint64_t beg = __ldg(L.out_off + s), end = __ldg(L.out_off + s + 1);
+        const uint32_t v = __ldg(lab_cur + s);
+        for (uint64_t e = beg + lane; e < end; e += 32) {
+            const uint32_t t = __ldg(L.out_dst + e);
+            if (v < __ldcg(lab_next + t) && atomicMin(lab_next + t, v) > v &&
+                bit_set_atomic(L.touched, (uint32_t)(t - L.lo)))
+                warp_append(L.list_next, L.count_next, t);
+        }
+    }
+}
+
+// commit the pushed changes: next -> cur, frontier bookkeeping, stats
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_push_apply(T* cur, const T* __restrict__ next,
+                                                        const uint32_t* __restrict__ list,
+                                                        const unsigned long long* count, FrontierView f,
+                                                        StatStripe* stats) {
+    LocalStats st;
+    const uint64_t n = *count;
+    for (uint64_t i = blockIdx.x * (uint64_t)kBlock + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kBlock) {
+        const uint32_t s = list[i];
+        cur[s] = next[s];
+        st.changed++;
+        st.targets++;
+        st.next_active++;
+        st.next_units += __ldg(f.outdeg + s);
+        if (bit_test(f.remote_src, s)) st.remote_active++;
+        atomicOr(f.active_next + (s >> 5), 1u << (s & 31));
+    }
+    flush_stats(st, stats);
+}
+
+// pull commit: cur[s] = next[s] for the changed slots
+template <typename T>
+__global__ void k_commit(T* cur, const T* __restrict__ next, const uint32_t* __restrict__ list,
+                         const unsigned long long* count) {
+    const uint64_t n = *count;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = list[i];
+        cur[s] = next[s];
+    }
+}
+
+// ======================================================================
+// request path kernels
+// ======================================================================
+
+template <class Ops>
+__global__ void k_gen(const Ops ops, const uint32_t* __restrict__ in_src, const uint32_t* __restrict__ in_w,
+                      uint64_t elo, uint64_t ehi, typename Ops::Msg* msg, uint8_t* valid) {
+    for (uint64_t e = elo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < ehi;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        typename Ops::Msg m;
+        const bool ok = ops.gen(__ldg(in_src + e), e, in_w, m);
+        if (ok) msg[e] = m;
+        valid[e] = ok ? 1 : 0;
+    }
+}
+
+template <class Ops>
+__global__ void __launch_bounds__(kBlock) k_apply(const Ops ops, const typename Ops::Acc* __restrict__ merged,
+                                                   uint64_t lo, uint64_t slo, uint64_t shi,
+                                                   StatStripe* stats) {
+    LocalStats st;
+    for (uint64_t s = slo + blockIdx.x * (uint64_t)kBlock + threadIdx.x; s < shi; s += (uint64_t)gridDim.x * kBlock)
+        ops.apply((uint32_t)s, merged[s - lo], st);
+    flush_stats(st, stats);
+}
+
+// ======================================================================
+// init / readback kernels
+// ======================================================================
+
+__global__ void k_pr_init(double* rank, double* contrib, const uint32_t* __restrict__ outdeg, uint64_t V) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < V; s += (uint64_t)gridDim.x * blockDim.x) {
+        rank[s] = 1.0;  // initial_attr (A/algorithms.py:141-142)
+        const uint32_t od = outdeg[s];
+        contrib[s] = od ? __ddiv_rn(1.0, (double)od) : 0.0;
+    }
+}
+
+__global__ void k_fill_u4(uint4* a, uint64_t n, uint4 v) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n; s += (uint64_t)gridDim.x * blockDim.x)
+        a[s] = v;
+}
+
+__global__ void k_iota_u32(uint32_t* a, uint64_t lo, uint64_t n) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n; s += (uint64_t)gridDim.x * blockDim.x)
+        a[s] = (uint32_t)(lo + s);
+}
+
+__global__ void k_bitmap_range(uint32_t* bm, uint64_t lo, uint64_t hi) {
+    for (uint64_t s = lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < hi; s += (uint64_t)gridDim.x * blockDim.x)
+        atomicOr(bm + (s >> 5), 1u << (s & 31));
+}
+
+__global__ void k_read_attrs(int algo, int arity, const uint32_t* __restrict__ d2s,
+                             uint64_t V, uint64_t lo, uint64_t hi, int owned_only, const double* rank,
+                             const uint4* dist, const uint32_t* lab, double* out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < V; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = d2s[i];
+        const bool mine = s >= lo && s < hi;
+        if (owned_only && !mine) {
+            for (int j = 0; j < arity; ++j) out[i * arity + j] = __longlong_as_double(0x7ff8000000000000ll);
+            continue;
+        }
+        if (algo == GXB_ALGO_PAGERANK) {
+            out[i] = rank[s];
+        } else if (algo == GXB_ALGO_SSSP) {
+            const uint4 d = dist[s];
+            const uint32_t l[4] = {d.x, d.y, d.z, d.w};
+            for (int j = 0; j < arity; ++j)
+                out[i * arity + j] = (l[j] == kInf32) ? __longlong_as_double(0x7ff0000000000000ll) : (double)l[j];
+        } else {
+            out[i] = (double)lab[s];
+        }
+    }
+}
+
+}  // namespace gxb
+
+using namespace gxb;
+
+// ======================================================================
+// host side
+// ======================================================================
+
+namespace {
+
+FrontierView frontier_view(gxb_state* s) {
+    const gxb_graph* g = s->g;
+    FrontierView f;
+    f.lo = g->lo;
+    f.outdeg = g->d_outdeg;
+    f.remote_src = g->d_remote_src;
+    f.active_next = s->d_active[1];
+    f.frontier_next = s->d_frontier[1];
+    f.frontier_count = s->d_fcount + 1;
+    return f;
+}
+
+PullLaunch pull_launch(gxb_state* s, uint64_t flo, uint64_t fhi) {
+    const gxb_graph* g = s->g;
+    const PullPlan& P = g->plan;
+    PullLaunch L;
+    std::memset(&L, 0, sizeof(L));
+    L.lo = g->lo;
+    L.in_off = g->d_in_off;
+    L.in_src = g->d_in_src;
+    L.flo = flo;
+    L.fhi = fhi;
+    L.num_items = P.num_items;
+    L.item_slot = P.d_item_slot;
+    L.item_begin = P.d_item_begin;
+    L.item_first = P.d_item_first;
+    L.item_count = P.d_item_count;
+    L.arrive = P.d_slot_arrive;
+    L.partials = s->d_partials;
+    L.chunk_blocks = (unsigned)((P.num_items + (kBlock / 32) - 1) / (kBlock / 32));
+    uint64_t prev = P.chunk_end;
+    for (int k = kNumGroupBins - 1; k >= 0; --k) {
+        L.bin_lo[k] = prev;
+        L.bin_hi[k] = std::max(prev, P.group_end[k]);
+        const uint64_t n = L.bin_hi[k] - L.bin_lo[k];
+        const uint64_t per = kBlock >> k;
+        L.bin_blocks[k] = (unsigned)((n + per - 1) / per);
+        prev = L.bin_hi[k];
+    }
+    L.stats = s->d_stats;
+    return L;
+}
+
+unsigned pull_grid(const PullLaunch& L) {
+    unsigned n = L.chunk_blocks;
+    for (int k = 0; k < kNumGroupBins; ++k) n += L.bin_blocks[k];
+    return n;
+}
+
+template <class Pol>
+int launch_pull(const Pol& p, const PullLaunch& L, cudaStream_t st) {
+    const unsigned grid = pull_grid(L);
+    if (grid) k_pull<Pol><<<grid, kBlock, 0, st>>>(p, L);
+    GXB_CUDA(cudaGetLastError());
+    return GXB_OK;
+}
+
+PrOps pr_ops(gxb_state* s) {
+    PrOps o;
+    o.contrib_cur = s->d_contrib[s->cur];
+    o.rank = s->d_rank;
+    o.contrib_next = s->d_contrib[s->cur ^ 1];
+    o.f = frontier_view(s);
+    return o;
+}
+SsspOps sssp_ops(gxb_state* s) {
+    SsspOps o;
+    o.dist_cur = s->d_dist_cur;
+    o.dist_next = s->d_dist_next;
+    o.active_cur = s->d_active[0];
+    o.f = frontier_view(s);
+    return o;
+}
+CcOps cc_ops(gxb_state* s) {
+    CcOps o;
+    o.lab_cur = s->d_lab_cur;
+    o.lab_next = s->d_lab_next;
+    o.active_cur = s->d_active[0];
+    o.f = frontier_view(s);
+    return o;
+}
+
+int begin_round(gxb_state* s, cudaStream_t st) {
+    if (s->stats_pending) {
+        GXB_CUDA(cudaEventSynchronize(s->stats_ready));
+        s->stats_pending = false;
+    }
+    GXB_CUDA(cudaMemsetAsync(s->d_stats, 0, sizeof(StatStripe) * kStripes, st));
+    GXB_CUDA(cudaMemsetAsync(s->d_fcount + 1, 0, sizeof(unsigned long long), st));
+    GXB_CUDA(cudaMemsetAsync(s->d_active[1], 0, 4 * s->words, st));
+    s->in_round = true;
+    return GXB_OK;
+}
+
+// close the round: commit values, rotate frontier buffers, snapshot stats
+int end_round(gxb_state* s, int direction, cudaStream_t st) {
+    gxb_graph* g = s->g;
+    if (s->algo == GXB_ALGO_PAGERANK) {
+        s->cur ^= 1;
+    } else if (direction == GXB_DIR_PULL) {
+        const unsigned grid = grid_for(g->hi - g->lo);
+        if (s->algo == GXB_ALGO_SSSP)
+            k_commit<uint4><<<grid, kBlock, 0, st>>>(s->d_dist_cur, s->d_dist_next, s->d_frontier[1], s->d_fcount + 1);
+        else
+            k_commit<uint32_t><<<grid, kBlock, 0, st>>>(s->d_lab_cur, s->d_lab_next, s->d_frontier[1], s->d_fcount + 1);
+        GXB_CUDA(cudaGetLastError());
+    }
+    if (s->algo != GXB_ALGO_PAGERANK) {
+        std::swap(s->d_active[0], s->d_active[1]);
+        std::swap(s->d_frontier[0], s->d_frontier[1]);
+        GXB_CUDA(cudaMemcpyAsync(s->d_fcount, s->d_fcount + 1, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+    }
+    GXB_CUDA(cudaMemcpyAsync(s->h_stats, s->d_stats, sizeof(StatStripe) * kStripes, cudaMemcpyDeviceToHost, st));
+    GXB_CUDA(cudaMemcpyAsync(s->h_fcount, s->d_fcount, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    GXB_CUDA(cudaEventRecord(s->stats_ready, st));
+    s->stats_pending = true;
+    s->in_round = false;
+    s->iteration++;
+    s->last_direction = direction;
+    return GXB_OK;
+}
+
+// host reduction of the stat stripes
+int collect_stats(gxb_state* s) {
+    if (s->stats_pending) {
+        GXB_CUDA(cudaEventSynchronize(s->stats_ready));
+        s->stats_pending = false;
+        gxb_iter_stats o;
+        std::memset(&o, 0, sizeof(o));
+        double m = 0.0;
+        for (int i = 0; i < kStripes; ++i) {
+            const StatStripe& t = s->h_stats[i];
+            o.changed += t.changed;
+            o.next_active += t.next_active;
+            o.next_units += t.next_units;
+            o.targets += t.targets;
+            o.remote_active += t.remote_active;
+            double x;
+            std::memcpy(&x, &t.max_stat_bits, 8);
+            m = std::max(m, x);
+        }
+        o.iteration = s->iteration;
+        o.units = s->units_cur;
+        o.max_stat = m;
+        o.direction = s->last_direction;
+        const gxb_graph* g = s->g;
+        if (s->algo == GXB_ALGO_PAGERANK) {
+            // every vertex stays active (A/algorithms.py:144-145, 159)
+            o.next_active = g->hi - g->lo;
+            o.next_units = s->owned_outdeg_sum;
+            o.targets = s->owned_targets;
+            o.voted = m < 1e-9 ? 1 : 0;  // PageRank.vote (164-165)
+            // all owned vertices are in the next frontier: count those with remote consumers
+            o.remote_active = s->last.remote_active;
+        } else {
+            o.voted = o.next_active == 0 ? 1 : 0;  // not next_active (70-72)
+        }
+        s->frontier_len = *s->h_fcount;
+        s->units_cur = o.next_units;
+        s->last = o;
+    }
+    return GXB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gxb_state_free(gxb_state* s);
+void gxb_lp_free(gxb_state* s);  // gxb_lp.cu
+
+int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, gxb_state** out) {
+    if (!g || !out) return fail(GXB_EINVAL, "gxb_state_create: null argument");
+    if (algo < GXB_ALGO_SSSP || algo > GXB_ALGO_CC) return fail(GXB_EINVAL, "unknown algorithm");
+    if (!g->ctx->alive) return fail(GXB_ESTATE, "gxb_state_create: daemon terminated");
+    GXB_CUDA(cudaSetDevice(g->ctx->device));
+    gxb_state* s = new gxb_state();
+    s->g = g;
+    s->algo = algo;
+    auto bail = [&](int rc) {
+        gxb_state_free(s);
+        return rc;
+    };
+    const uint64_t V = g->V, owned = g->hi - g->lo;
+    s->words = (V >> 5) + 1;
+    cudaStream_t st = 0;
+    // host copies of degrees for static counts
+    {
+        std::vector<uint32_t> od(V);
+        if (V && cudaMemcpy(od.data(), g->d_outdeg, 4 * V, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return bail(fail(GXB_ECUDA, "state_create: outdeg copy"));
+        for (uint64_t i = g->lo; i < g->hi; ++i) s->owned_outdeg_sum += od[i];
+        for (uint64_t i = 0; i < owned; ++i) s->owned_targets += g->h_indeg_sorted[i] > 0 ? 1 : 0;
+    }
+    int rc;
+    if ((rc = dalloc_t(&s->d_stats, kStripes)) != GXB_OK) return bail(rc);
+    if (cudaMallocHost(&s->h_stats, sizeof(StatStripe) * kStripes) != cudaSuccess ||
+        cudaMallocHost(&s->h_fcount, 64) != cudaSuccess)
+        return bail(fail(GXB_ENOMEM, "pinned stats"));
+    if (cudaEventCreateWithFlags(&s->stats_ready, cudaEventDisableTiming) != cudaSuccess)
+        return bail(fail(GXB_ECUDA, "event"));
+    if ((rc = dalloc_t(&s->d_fcount, 2)) != GXB_OK) return bail(rc);
+    for (int i = 0; i < 2; ++i) {
+        if ((rc = dalloc_t(&s->d_active[i], s->words)) != GXB_OK) return bail(rc);
+        if ((rc = dalloc_t(&s->d_frontier[i], V + 1)) != GXB_OK) return bail(rc);
+        cudaMemsetAsync(s->d_active[i], 0, 4 * s->words, st);
+    }
+    if ((rc = dalloc_t(&s->d_touched, (owned >> 5) + 1)) != GXB_OK) return bail(rc);
+    cudaMemsetAsync(s->d_touched, 0, 4 * ((owned >> 5) + 1), st);
+    // chunk partials: the largest accumulator is SsspOps::Acc (32 B with padding)
+    if ((rc = dalloc(&s->d_partials, 32 * (g->plan.num_items + 1))) != GXB_OK) return bail(rc);
+
+    const unsigned grid = grid_for(V);
+    uint64_t nfront = 0, units0 = 0;
+    if (algo == GXB_ALGO_PAGERANK) {
+        s->arity = 1;
+        if ((rc = dalloc_t(&s->d_rank, V)) != GXB_OK) return bail(rc);
+        for (int i = 0; i < 2; ++i)
+            if ((rc = dalloc_t(&s->d_contrib[i], V)) != GXB_OK) return bail(rc);
+        if (V) k_pr_init<<<grid, kBlock, 0, st>>>(s->d_rank, s->d_contrib[0], g->d_outdeg, V);
+        units0 = s->owned_outdeg_sum;
+    } else if (algo == GXB_ALGO_SSSP) {
+        if (nsrc < 0 || nsrc > 4) return bail(fail(GXB_EINVAL, "sssp supports 1..4 sources"));
+        std::vector<uint32_t> ids(V);
+        if (V && cudaMemcpy(ids.data(), g->d_slot2id, 4 * V, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return bail(fail(GXB_ECUDA, "state_create: id copy"));
+        std::vector<std::pair<uint32_t, uint32_t>> by_id(V);  // (id, slot)
+        for (uint64_t i = 0; i < V; ++i) by_id[i] = {ids[i], (uint32_t)i};
+        std::sort(by_id.begin(), by_id.end());
+        std::vector<uint32_t> src_ids;
+        if (sources && nsrc > 0) {
+            src_ids.assign(sources, sources + nsrc);
+        } else {
+            // sorted(vertex_ids)[:4] (A/algorithms.py:219-222)
+            for (uint64_t i = 0; i < V && i < 4; ++i) src_ids.push_back(by_id[i].first);
+        }
+        if (src_ids.empty()) return bail(fail(GXB_EINVAL, "sssp needs at least one source vertex"));
+        s->nsrc = (int)src_ids.size();
+        s->arity = s->nsrc;
+        if ((rc = dalloc_t(&s->d_dist_cur, V)) != GXB_OK) return bail(rc);
+        if ((rc = dalloc_t(&s->d_dist_next, V)) != GXB_OK) return bail(rc);
+        const uint4 inf = make_uint4(kInf32, kInf32, kInf32, kInf32);
+        if (V) k_fill_u4<<<grid, kBlock, 0, st>>>(s->d_dist_cur, V, inf);
+        std::vector<uint4> src_vals;
+        std::vector<uint32_t> front;
+        std::vector<uint32_t> h_od(V);
+        if (V) cudaMemcpy(h_od.data(), g->d_outdeg, 4 * V, cudaMemcpyDeviceToHost);
+        for (int j = 0; j < s->nsrc; ++j) {
+            auto it = std::lower_bound(by_id.begin(), by_id.end(), std::make_pair(src_ids[j], 0u));
+            if (it == by_id.end() || it->first != src_ids[j]) continue;  // absent source: all-inf lane
+            s->src_present[j] = true;
+            s->src_slot[j] = it->second;
+        }
+        // initial_attr: 0 on the own lane (96-97); initially_active: the sources (99-100)
+        std::vector<uint32_t> uniq;
+        for (int j = 0; j < s->nsrc; ++j)
+            if (s->src_present[j] && std::find(uniq.begin(), uniq.end(), s->src_slot[j]) == uniq.end())
+                uniq.push_back(s->src_slot[j]);
+        for (uint32_t slot : uniq) {
+            uint32_t l[4] = {kInf32, kInf32, kInf32, kInf32};
+            for (int j = 0; j < s->nsrc; ++j)
+                if (s->src_present[j] && s->src_slot[j] == slot) l[j] = 0;
+            const uint4 v = make_uint4(l[0], l[1], l[2], l[3]);
+            cudaMemcpyAsync(s->d_dist_cur + slot, &v, sizeof(uint4), cudaMemcpyHostToDevice, st);
+            cudaStreamSynchronize(st);
+            front.push_back(slot);
+            units0 += h_od[slot];
+        }
+        if (V) cudaMemcpyAsync(s->d_dist_next, s->d_dist_cur, sizeof(uint4) * V, cudaMemcpyDeviceToDevice, st);
+        std::vector<uint32_t> bm(s->words, 0);
+        for (uint32_t slot : front) bm[slot >> 5] |= 1u << (slot & 31);
+        cudaMemcpyAsync(s->d_active[0], bm.data(), 4 * s->words, cudaMemcpyHostToDevice, st);
+        if (!front.empty())
+            cudaMemcpyAsync(s->d_frontier[0], front.data(), 4 * front.size(), cudaMemcpyHostToDevice, st);
+        nfront = front.size();
+        cudaStreamSynchronize(st);
+    } else {
+        // LP / CC: label = vertex id, every vertex active (A/algorithms.py:179-183)
+        s->arity = 1;
+        if ((rc = dalloc_t(&s->d_lab_cur, V)) != GXB_OK) return bail(rc);
+        if ((rc = dalloc_t(&s->d_lab_next, V)) != GXB_OK) return bail(rc);
+        if (V) {
+            cudaMemcpyAsync(s->d_lab_cur, g->d_slot2id, 4 * V, cudaMemcpyDeviceToDevice, st);
+            cudaMemcpyAsync(s->d_lab_next, g->d_slot2id, 4 * V, cudaMemcpyDeviceToDevice, st);
+            k_bitmap_range<<<grid, kBlock, 0, st>>>(s->d_active[0], 0, V);
+            k_iota_u32<<<grid, kBlock, 0, st>>>(s->d_frontier[0], 0, V);
+        }
+        nfront = V;
+        std::vector<uint32_t> od(V);
+        if (V) cudaMemcpy(od.data(), g->d_outdeg, 4 * V, cudaMemcpyDeviceToHost);
+        for (uint64_t i = 0; i < V; ++i) units0 += od[i];
+    }
+    unsigned long long fc[2] = {nfront, 0};
+    cudaMemcpyAsync(s->d_fcount, fc, sizeof(fc), cudaMemcpyHostToDevice, st);
+    s->frontier_len = nfront;
+    s->units_cur = units0;
+    // the remote-active count of a PR round is static: every owned vertex is active
+    if (algo == GXB_ALGO_PAGERANK && g->nparts > 1) {
+        std::vector<uint32_t> rb(s->words);
+        cudaMemcpy(rb.data(), g->d_remote_src, 4 * ((V >> 5) + 1), cudaMemcpyDeviceToHost);
+        uint64_t c = 0;
+        for (uint64_t i = g->lo; i < g->hi; ++i) c += (rb[i >> 5] >> (i & 31)) & 1u;
+        s->last.remote_active = c;
+    }
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "gxb_state_create"));
+    *out = s;
+    return GXB_OK;
+}
+
+int gxb_state_free(gxb_state* s) {
+    if (!s) return GXB_OK;
+    dfree(s->d_rank);
+    dfree(s->d_contrib[0]);
+    dfree(s->d_contrib[1]);
+    dfree(s->d_dist_cur);
+    dfree(s->d_dist_next);
+    dfree(s->d_lab_cur);
+    dfree(s->d_lab_next);
+    for (int i = 0; i < 2; ++i) {
+        dfree(s->d_active[i]);
+        dfree(s->d_frontier[i]);
+    }
+    dfree(s->d_fcount);
+    dfree(s->d_touched);
+    dfree(s->d_stats);
+    if (s->h_stats) cudaFreeHost(s->h_stats);
+    if (s->h_fcount) cudaFreeHost(s->h_fcount);
+    if (s->stats_ready) cudaEventDestroy(s->stats_ready);
+    dfree(s->d_msg);
+    dfree(s->d_msg_valid);
+    dfree(s->d_merged);
+    dfree(s->d_partials);
+    gxb_lp_free(s);
+    dfree(s->d_send);
+    dfree(s->d_recv);
+    delete s;
+    return GXB_OK;
+}
+
+int gxb_state_arity(const gxb_state* s, int* out) {
+    if (!s || !out) return fail(GXB_EINVAL, "gxb_state_arity: null argument");
+    *out = s->arity;
+    return GXB_OK;
+}
+
+int gxb_lp_pull(gxb_state* s, cudaStream_t st);  // gxb_lp.cu
+
+int gxb_iterate(gxb_state* s, int direction, void* stream) {
+    if (!s) return fail(GXB_EINVAL, "gxb_iterate: null state");
+    if (s->in_round) return fail(GXB_ESTATE, "gxb_iterate: a request round is open (call gxb_commit)");
+    if (!s->g->ctx->alive) return fail(GXB_ESTATE, "gxb_iterate: daemon terminated");
+    cudaStream_t st = (cudaStream_t)stream;
+    gxb_graph* g = s->g;
+    GXB_CHECK(collect_stats(s));
+    GXB_CHECK(begin_round(s, st));
+    int dir = GXB_DIR_PULL;
+    if (s->algo == GXB_ALGO_SSSP || s->algo == GXB_ALGO_CC) {
+        if (direction == GXB_DIR_PUSH) dir = GXB_DIR_PUSH;
+        else if (direction == GXB_DIR_AUTO) dir = (s->units_cur * 20 < g->E) ? GXB_DIR_PUSH : GXB_DIR_PULL;
+        if (dir == GXB_DIR_PUSH && !g->has_csr) {
+            if (direction == GXB_DIR_PUSH) return fail(GXB_EINVAL, "push requested but the graph has no CSR");
+            dir = GXB_DIR_PULL;
+        }
+    }
+    const uint64_t owned = g->hi - g->lo;
+    if (dir == GXB_DIR_PULL) {
+        const PullLaunch L = pull_launch(s, 0, owned);
+        switch (s->algo) {
+            case GXB_ALGO_PAGERANK: {
+                FusedPolicy<PrOps> p{pr_ops(s), g->d_in_w};
+                GXB_CHECK(launch_pull(p, L, st));
+                break;
+            }
+            case GXB_ALGO_SSSP: {
+                FusedPolicy<SsspOps> p{sssp_ops(s), g->d_in_w};
+                GXB_CHECK(launch_pull(p, L, st));
+                break;
+            }
+            case GXB_ALGO_CC: {
+                FusedPolicy<CcOps> p{cc_ops(s), g->d_in_w};
+                GXB_CHECK(launch_pull(p, L, st));
+                break;
+            }
+            case GXB_ALGO_LP:
+                GXB_CHECK(gxb_lp_pull(s, st));
+                break;
+        }
+    } else {
+        PushLaunch P;
+        P.lo = g->lo;
+        P.hi = g->hi;
+        P.out_off = g->d_out_off;
+        P.out_dst = g->d_out_dst;
+        P.out_w = g->d_out_w;
+        P.frontier = s->d_frontier[0];
+        P.nfront = s->frontier_len;
+        P.touched = s->d_touched;
+        P.list_next = s->d_frontier[1];
+        P.count_next = s->d_fcount + 1;
+        const unsigned grid = grid_for(P.nfront * 32);
+        FrontierView f = frontier_view(s);
+        if (s->algo == GXB_ALGO_SSSP) {
+            if (P.nfront) k_push_sssp<<<grid, kBlock, 0, st>>>(s->d_dist_cur, s->d_dist_next, P);
+            k_push_apply<uint4><<<kNumSMs * 2, kBlock, 0, st>>>(s->d_dist_cur, s->d_dist_next, s->d_frontier[1],
+                                                                 s->d_fcount + 1, f, s->d_stats);
+        } else {
+            if (P.nfront) k_push_cc<<<grid, kBlock, 0, st>>>(s->d_lab_cur, s->d_lab_next, P);
+            k_push_apply<uint32_t><<<kNumSMs * 2, kBlock, 0, st>>>(s->d_lab_cur, s->d_lab_next, s->d_frontier[1],
+                                                                    s->d_fcount + 1, f, s->d_stats);
+        }
+        GXB_CUDA(cudaGetLastError());
+        GXB_CUDA(cudaMemsetAsync(s->d_touched, 0, 4 * ((owned >> 5) + 1), st));
+    }
+    return end_round(s, dir, st);
+}
+
+int gxb_request(gxb_state* s, int op, uint64_t lo, uint64_t hi, void* stream) {
+    if (!s) return fail(GXB_EINVAL, "gxb_request: null state");
+    if (!s->g->ctx->alive) return fail(GXB_ESTATE, "gxb_request: daemon terminated");
+    if (s->algo == GXB_ALGO_LP) return fail(GXB_EINVAL, "gxb_request: LP runs through gxb_iterate only");
+    cudaStream_t st = (cudaStream_t)stream;
+    gxb_graph* g = s->g;
+    const uint64_t owned = g->hi - g->lo;
+    if (lo > hi) return fail(GXB_EINVAL, "gxb_request: empty range with lo > hi");
+    // lazy message buffers: 16 B per owned edge covers every Msg type
+    if (!s->d_msg) {
+        GXB_CHECK(dalloc(&s->d_msg, 16 * (g->owned_edges + 1)));
+        GXB_CHECK(dalloc_t(&s->d_msg_valid, g->owned_edges + 1));
+        GXB_CHECK(dalloc(&s->d_merged, 32 * (owned + 1)));
+    }
+    if (!s->in_round) {
+        if (op != GXB_OP_GEN) return fail(GXB_ESTATE, "gxb_request: a round starts with GEN");
+        GXB_CHECK(collect_stats(s));
+        GXB_CHECK(begin_round(s, st));
+    }
+    if (op == GXB_OP_GEN) {
+        if (hi > g->owned_edges) return fail(GXB_EINVAL, "gxb_request(GEN): edge range outside the owned CSC");
+        const unsigned grid = grid_for(hi - lo);
+        if (hi > lo) {
+            switch (s->algo) {
+                case GXB_ALGO_PAGERANK:
+                    k_gen<PrOps><<<grid, kBlock, 0, st>>>(pr_ops(s), g->d_in_src, g->d_in_w, lo, hi,
+                                                         (double*)s->d_msg, s->d_msg_valid);
+                    break;
+                case GXB_ALGO_SSSP:
+                    k_gen<SsspOps><<<grid, kBlock, 0, st>>>(sssp_ops(s), g->d_in_src, g->d_in_w, lo, hi,
+                                                           (uint4*)s->d_msg, s->d_msg_valid);
+                    break;
+                case GXB_ALGO_CC:
+                    k_gen<CcOps><<<grid, kBlock, 0, st>>>(cc_ops(s), g->d_in_src, g->d_in_w, lo, hi,
+                                                         (uint32_t*)s->d_msg, s->d_msg_valid);
+                    break;
+            }
+        }
+        GXB_CUDA(cudaGetLastError());
+        return GXB_OK;
+    }
+    if (lo < g->lo || hi > g->hi)
+        return fail(GXB_ENOTOWNED, "apply targets vertex not owned by this node");
+    const uint64_t flo = lo - g->lo, fhi = hi - g->lo;
+    if (op == GXB_OP_MERGE) {
+        const PullLaunch L = pull_launch(s, flo, fhi);
+        switch (s->algo) {
+            case GXB_ALGO_PAGERANK: {
+                MergePolicy<PrOps> p{pr_ops(s), (const double*)s->d_msg, s->d_msg_valid,
+                                     (PrOps::Acc*)s->d_merged, g->lo};
+                GXB_CHECK(launch_pull(p, L, st));
+                break;
+            }
+            case GXB_ALGO_SSSP: {
+                MergePolicy<SsspOps> p{sssp_ops(s), (const uint4*)s->d_msg, s->d_msg_valid,
+                                       (SsspOps::Acc*)s->d_merged, g->lo};
+                GXB_CHECK(launch_pull(p, L, st));
+                break;
+            }
+            case GXB_ALGO_CC: {
+                MergePolicy<CcOps> p{cc_ops(s), (const uint32_t*)s->d_msg, s->d_msg_valid,
+                                     (CcOps::Acc*)s->d_merged, g->lo};
+                GXB_CHECK(launch_pull(p, L, st));
+                break;
+            }
+        }
+        return GXB_OK;
+    }
+    if (op == GXB_OP_APPLY) {
+        const unsigned grid = grid_for(hi - lo);
+        if (hi > lo) {
+            switch (s->algo) {
+                case GXB_ALGO_PAGERANK:
+                    k_apply<PrOps><<<grid, kBlock, 0, st>>>(pr_ops(s), (const PrOps::Acc*)s->d_merged, g->lo, lo, hi,
+                                                           s->d_stats);
+                    break;
+                case GXB_ALGO_SSSP:
+                    k_apply<SsspOps><<<grid, kBlock, 0, st>>>(sssp_ops(s), (const SsspOps::Acc*)s->d_merged, g->lo, lo,
+                                                             hi, s->d_stats);
+                    break;
+                case GXB_ALGO_CC:
+                    k_apply<CcOps><<<grid, kBlock, 0, st>>>(cc_ops(s), (const CcOps::Acc*)s->d_merged, g->lo, lo, hi,
+                                                           s->d_stats);
+                    break;
+            }
+        }
+        GXB_CUDA(cudaGetLastError());
+        return GXB_OK;
+    }
+    return fail(GXB_EINVAL, "unknown operation kind");
+}
+
+int gxb_commit(gxb_state* s, void* stream) {
+    if (!s) return fail(GXB_EINVAL, "gxb_commit: null state");
+    if (!s->in_round) return fail(GXB_ESTATE, "gxb_commit: no open round");
+    return end_round(s, GXB_DIR_PULL, (cudaStream_t)stream);
+}
+
+int gxb_stats(gxb_state* s, void* stream, gxb_iter_stats* out) {
+    if (!s || !out) return fail(GXB_EINVAL, "gxb_stats: null argument");
+    (void)stream;
+    GXB_CHECK(collect_stats(s));
+    *out = s->last;
+    return GXB_OK;
+}
+
+int gxb_read_attrs(gxb_state* s, double* host_out, int owned_only, void* stream) {
+    if (!s) return fail(GXB_EINVAL, "gxb_read_attrs: null state");
+    gxb_graph* g = s->g;
+    const uint64_t V = g->V;
+    if (!V) return GXB_OK;
+    if (!host_out) return fail(GXB_EINVAL, "gxb_read_attrs: null output");
+    cudaStream_t st = (cudaStream_t)stream;
+    double* tmp = nullptr;
+    GXB_CHECK(dalloc_t(&tmp, V * s->arity));
+    k_read_attrs<<<grid_for(V), kBlock, 0, st>>>(s->algo, s->arity, g->d_dense2slot, V, g->lo, g->hi,
+                                                 owned_only, s->d_rank, s->d_dist_cur, s->d_lab_cur, tmp);
+    cudaError_t e = cudaMemcpyAsync(host_out, tmp, 8 * V * s->arity, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    dfree(tmp);
+    if (e != cudaSuccess) return cuda_fail(e, "gxb_read_attrs");
+    return GXB_OK;
+}
+
+}  // extern "C"

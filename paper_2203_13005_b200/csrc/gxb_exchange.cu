@@ -1,0 +1,175 @@
+// gxb_exchange.cu — mirror-value exchange between destination partitions (K6).
+//
+// The reference's synchronisation round (A/engine.py:242-266) publishes the
+// next frontier's needs (gqq), uploads dirty-and-queried values (gdq,
+// A/agent.py:550-582) and installs them (A/agent.py:584-592); lazy uploading
+// keeps only changed values on the wire (A/sync.py:171-198) and the skip step
+// elides the whole round when no next-active vertex has a cross-partition
+// consumer (A/sync.py:201-208, A/agent.py:533-535).
+//
+// On B200 every rank holds a full-length replica of the source values its CSC
+// slice reads. The bytes move over NCCL (torch.distributed on NVLink) between
+// the device buffers exposed here:
+//   dense (PageRank): the owned slice of the contribution replica is
+//     all-gathered in place (every vertex changes every round);
+//   delta (SSSP / CC / LP): gxb_exchange_pack emits (slot, value) records of
+//     the owned vertices that changed (= the next frontier), the caller
+//     all-gathers them, and gxb_exchange_unpack installs peers' records into the
+//     replica, marks them active and appends them to the push frontier.
+#include <cstring>
+
+#include "gxb_state.cuh"
+
+namespace gxb {
+
+__device__ __forceinline__ int record_words(int algo) { return algo == GXB_ALGO_SSSP ? 5 : 2; }
+
+__global__ void k_pack(int algo, const uint32_t* __restrict__ list, const unsigned long long* count, uint64_t lo,
+                       uint64_t hi, const uint4* __restrict__ dist, const uint32_t* __restrict__ lab,
+                       uint32_t* out, unsigned long long* packed) {
+    const uint64_t n = *count;
+    const int W = record_words(algo);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = list[i];
+        // own changes only (received slots are appended after them)
+        if (s < lo || s >= hi) continue;
+        const unsigned long long k = atomicAdd(packed, 1ull);
+        uint32_t* r = out + k * W;
+        r[0] = s;
+        if (algo == GXB_ALGO_SSSP) {
+            const uint4 d = dist[s];
+            r[1] = d.x;
+            r[2] = d.y;
+            r[3] = d.z;
+            r[4] = d.w;
+        } else {
+            r[1] = lab[s];
+        }
+    }
+}
+
+__global__ void k_unpack(int algo, const uint32_t* __restrict__ rec, uint64_t n, uint64_t lo, uint64_t hi,
+                         uint4* dist_cur, uint4* dist_next, uint32_t* lab_cur, uint32_t* lab_next, uint32_t* active,
+                         uint32_t* list, unsigned long long* count, const uint32_t* __restrict__ outdeg,
+                         unsigned long long* units) {
+    const int W = record_words(algo);
+    unsigned long long u = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t* r = rec + i * W;
+        const uint32_t s = r[0];
+        if (s >= lo && s < hi) continue;  // own record echoed back by the all-gather
+        if (algo == GXB_ALGO_SSSP) {
+            const uint4 d = make_uint4(r[1], r[2], r[3], r[4]);
+            dist_cur[s] = d;
+            dist_next[s] = d;
+        } else {
+            lab_cur[s] = r[1];
+            lab_next[s] = r[1];
+        }
+        atomicOr(active + (s >> 5), 1u << (s & 31));
+        const unsigned long long k = atomicAdd(count, 1ull);
+        list[k] = s;
+        u += outdeg[s];
+    }
+    for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+    if ((threadIdx.x & 31) == 0 && u) atomicAdd(units, u);
+}
+
+}  // namespace gxb
+
+using namespace gxb;
+
+extern "C" {
+
+int gxb_exchange_buffer(gxb_state* s, int which, void** dev_ptr, uint64_t* bytes) {
+    if (!s || !dev_ptr || !bytes) return fail(GXB_EINVAL, "gxb_exchange_buffer: null argument");
+    gxb_graph* g = s->g;
+    const uint64_t V = g->V, owned = g->hi - g->lo;
+    const uint64_t rec = (s->algo == GXB_ALGO_SSSP) ? 20 : 8;
+    switch (which) {
+        case GXB_BUF_VALUES:
+            if (s->algo == GXB_ALGO_PAGERANK) {
+                *dev_ptr = s->d_contrib[s->cur];
+                *bytes = 8 * V;
+            } else if (s->algo == GXB_ALGO_SSSP) {
+                *dev_ptr = s->d_dist_cur;
+                *bytes = 16 * V;
+            } else {
+                *dev_ptr = s->d_lab_cur;
+                *bytes = 4 * V;
+            }
+            return GXB_OK;
+        case GXB_BUF_SEND:
+            if (!s->d_send) GXB_CHECK(dalloc(&s->d_send, rec * (owned + 1) + 16));
+            *dev_ptr = s->d_send;
+            *bytes = rec * (owned + 1);
+            return GXB_OK;
+        case GXB_BUF_RECV:
+            if (!s->d_recv) {
+                GXB_CHECK(dalloc(&s->d_recv, rec * (V + 1) + 16));
+                s->recv_cap = V + 1;
+            }
+            *dev_ptr = s->d_recv;
+            *bytes = rec * s->recv_cap;
+            return GXB_OK;
+        case GXB_BUF_RECORD_SIZE:
+            *dev_ptr = nullptr;
+            *bytes = rec;
+            return GXB_OK;
+    }
+    return fail(GXB_EINVAL, "gxb_exchange_buffer: unknown buffer");
+}
+
+int gxb_exchange_pack(gxb_state* s, void* stream, uint64_t* count_out) {
+    if (!s || !count_out) return fail(GXB_EINVAL, "gxb_exchange_pack: null argument");
+    if (s->algo == GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "gxb_exchange_pack: PageRank uses the dense exchange");
+    if (s->in_round) return fail(GXB_ESTATE, "gxb_exchange_pack: round still open");
+    void* p;
+    uint64_t b;
+    GXB_CHECK(gxb_exchange_buffer(s, GXB_BUF_SEND, &p, &b));
+    cudaStream_t st = (cudaStream_t)stream;
+    gxb_iter_stats tmp;
+    GXB_CHECK(gxb_stats(s, stream, &tmp));  // settles frontier_len
+    gxb_graph* g = s->g;
+    unsigned long long* d_cnt = reinterpret_cast<unsigned long long*>(s->d_fcount);  // scratch slot [1] is free now
+    GXB_CUDA(cudaMemsetAsync(d_cnt + 1, 0, 8, st));
+    if (s->frontier_len)
+        k_pack<<<grid_for(s->frontier_len), kBlock, 0, st>>>(s->algo, s->d_frontier[0], s->d_fcount, g->lo, g->hi,
+                                                             s->d_dist_cur, s->d_lab_cur, (uint32_t*)s->d_send,
+                                                             d_cnt + 1);
+    unsigned long long n = 0;
+    GXB_CUDA(cudaMemcpyAsync(&n, d_cnt + 1, 8, cudaMemcpyDeviceToHost, st));
+    GXB_CUDA(cudaStreamSynchronize(st));
+    *count_out = n;
+    return GXB_OK;
+}
+
+int gxb_exchange_unpack(gxb_state* s, const void* d_records, uint64_t count, void* stream) {
+    if (!s) return fail(GXB_EINVAL, "gxb_exchange_unpack: null state");
+    if (s->algo == GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "gxb_exchange_unpack: PageRank uses the dense exchange");
+    if (count == 0) return GXB_OK;
+    if (!d_records) return fail(GXB_EINVAL, "gxb_exchange_unpack: null records");
+    gxb_graph* g = s->g;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long* d_units = reinterpret_cast<unsigned long long*>(s->d_fcount) + 1;
+    GXB_CUDA(cudaMemsetAsync(d_units, 0, 8, st));
+    k_unpack<<<grid_for(count), kBlock, 0, st>>>(s->algo, (const uint32_t*)d_records, count, g->lo, g->hi,
+                                                 s->d_dist_cur, s->d_dist_next, s->d_lab_cur, s->d_lab_next,
+                                                 s->d_active[0], s->d_frontier[0], s->d_fcount, g->d_outdeg, d_units);
+    GXB_CUDA(cudaGetLastError());
+    unsigned long long u = 0, n = 0;
+    GXB_CUDA(cudaMemcpyAsync(&u, d_units, 8, cudaMemcpyDeviceToHost, st));
+    GXB_CUDA(cudaMemcpyAsync(&n, s->d_fcount, 8, cudaMemcpyDeviceToHost, st));
+    GXB_CUDA(cudaStreamSynchronize(st));
+    s->units_cur += u;
+    s->frontier_len = n;
+    return GXB_OK;
+}
+
+int gxb_exchange_finish(gxb_state* s, void* stream) {
+    if (!s) return fail(GXB_EINVAL, "gxb_exchange_finish: null state");
+    GXB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    return GXB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,133 @@
+// gxb_internal.cuh — shared internals of libgxb200.so (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/gxb.h"
+
+#if !defined(__CUDA_ARCH__) || __CUDA_ARCH__ >= 1000
+#else
+#error "libgxb200 is built for sm_100a only"
+#endif
+
+namespace gxb {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define GXB_CUDA(call)                                                      \
+    do {                                                                    \
+        cudaError_t _e = (call);                                            \
+        if (_e != cudaSuccess) return ::gxb::cuda_fail(_e, #call);          \
+    } while (0)
+
+#define GXB_CHECK(call)                                                     \
+    do {                                                                    \
+        int _rc = (call);                                                   \
+        if (_rc != GXB_OK) return _rc;                                      \
+    } while (0)
+
+constexpr uint32_t kInf32 = 0xFFFFFFFFu;  // SSSP "inf" lane / invalid label
+constexpr int kBlock = 256;               // threads per CTA for the vertex/edge kernels
+constexpr int kNumSMs = 148;
+
+// Degree bins of the pull merge (SURVEY.md §7 "workload balancing inside a GPU").
+// Slots are sorted by in-degree (descending), so every bin is a contiguous slot
+// range. Bin k < kNumGroupBins uses groups of (1 << k) lanes per destination;
+// destinations above kChunkMinDeg are split into chunks of kChunkEdges edges,
+// one warp per chunk, combined by the last-arriving warp.
+constexpr int kNumGroupBins = 6;            // G = 1, 2, 4, 8, 16, 32
+constexpr uint32_t kChunkMinDeg = 128;      // > this: chunked warps
+constexpr uint32_t kChunkEdges = 1024;      // edges per warp work item
+
+struct DeviceBuffer {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+
+// device allocation helper (cudaMalloc, tracked by the owner)
+int dalloc(void** p, size_t bytes);
+template <typename T>
+int dalloc_t(T** p, size_t n) {
+    return dalloc(reinterpret_cast<void**>(p), n * sizeof(T) + 16);
+}
+void dfree(void* p);
+
+struct PullPlan {
+    // slot boundaries (relative to owned_lo) of the bins; bins are in
+    // descending-degree order: [chunk | G32 | G16 | G8 | G4 | G2 | G1]
+    uint64_t chunk_end;                 // slots [0, chunk_end) are chunked
+    uint64_t group_end[kNumGroupBins];  // group bin k covers [prev_end, group_end[...]]
+    // chunk work items (one warp each)
+    uint64_t num_items;
+    uint32_t* d_item_slot = nullptr;    // owning slot (relative) per item
+    uint64_t* d_item_begin = nullptr;   // first edge of the item
+    uint32_t* d_item_first = nullptr;   // first item index of the same slot
+    uint32_t* d_item_count = nullptr;   // number of items of the same slot
+    uint32_t* d_slot_arrive = nullptr;  // per chunked slot arrival counters (chunk_end)
+};
+
+}  // namespace gxb
+
+struct gxb_ctx {
+    int device = 0;
+    int init_count = 0;
+    bool alive = false;
+    cudaDeviceProp prop{};
+};
+
+struct gxb_graph {
+    gxb_ctx* ctx = nullptr;
+    uint64_t V = 0, E = 0;
+    uint32_t max_id = 0;
+    uint32_t max_in_degree = 0;
+    int part = 0, nparts = 1;
+    uint64_t lo = 0, hi = 0;            // owned slot range
+    uint64_t owned_edges = 0, owned_out_edges = 0;
+    bool weighted = false, has_csr = false;
+    std::vector<uint64_t> bounds;       // nparts + 1 slot boundaries
+
+    uint32_t* d_slot2id = nullptr;      // V: original id per slot
+    uint32_t* d_dense2slot = nullptr;   // V: slot of the i-th smallest id
+    uint32_t* d_outdeg = nullptr;       // V: global out-degree per slot
+    uint32_t* d_remote_src = nullptr;   // bitmap over slots: has an out-edge into another part
+    uint64_t* d_in_off = nullptr;       // owned+1 offsets into d_in_src (0-based)
+    uint32_t* d_in_src = nullptr;       // source slot per owned in-edge (sorted by (dst, src))
+    uint32_t* d_in_w = nullptr;         // weight per owned in-edge (nullptr = unweighted)
+    uint64_t* d_out_off = nullptr;      // V+1: push CSR restricted to owned destinations
+    uint32_t* d_out_dst = nullptr;
+    uint32_t* d_out_w = nullptr;
+    std::vector<uint32_t> h_indeg_sorted;  // owned in-degrees (descending), host copy
+    gxb::PullPlan plan;
+};
+
+namespace gxb {
+
+// ---- bitmap helpers ----
+__device__ __forceinline__ bool bit_test(const uint32_t* bm, uint32_t i) {
+    return (__ldg(bm + (i >> 5)) >> (i & 31)) & 1u;
+}
+__device__ __forceinline__ bool bit_set_atomic(uint32_t* bm, uint32_t i) {
+    const uint32_t m = 1u << (i & 31);
+    return (atomicOr(bm + (i >> 5), m) & m) == 0u;  // true if newly set
+}
+
+__device__ __forceinline__ uint32_t sat_add(uint32_t d, uint32_t w) {
+    const uint32_t s = d + w;
+    return (s < d || d == kInf32) ? kInf32 : s;
+}
+
+inline unsigned grid_for(uint64_t n, int block = kBlock, uint64_t cap = 148ull * 64) {
+    uint64_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (unsigned)g;
+}
+
+int build_pull_plan(gxb_graph* g, cudaStream_t st);
+
+}  // namespace gxb

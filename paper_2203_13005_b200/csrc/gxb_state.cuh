@@ -1,0 +1,151 @@
+// gxb_state.cuh — algorithm state, statistics and the kernel-side views.
+#pragma once
+
+#include "gxb_internal.cuh"
+
+namespace gxb {
+
+constexpr int kStripes = 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+// striped device counters (one 64-byte stripe per blockIdx % kStripes keeps the
+// end-of-kernel atomics off a single L2 address)
+struct alignas(64) StatStripe {
+    unsigned long long changed;
+    unsigned long long next_active;
+    unsigned long long next_units;
+    unsigned long long targets;
+    unsigned long long remote_active;
+    unsigned long long max_stat_bits;  // non-negative double bits: u64 order == double order
+    unsigned long long pad[2];
+};
+
+struct LocalStats {
+    unsigned long long changed = 0, next_active = 0, next_units = 0, targets = 0, remote_active = 0;
+    double max_stat = 0.0;
+};
+
+// what every apply needs to publish a changed vertex (A/agent.py:404-417)
+struct FrontierView {
+    uint64_t lo;
+    const uint32_t* outdeg;        // per slot (global out-degree)
+    const uint32_t* remote_src;    // per-slot bitmap: has a consumer on another partition
+    uint32_t* active_next;         // per-slot bitmap
+    uint32_t* frontier_next;       // list of slots
+    unsigned long long* frontier_count;
+};
+
+__device__ __forceinline__ void warp_append(uint32_t* list, unsigned long long* count, uint32_t v) {
+    const unsigned mask = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(count, (unsigned long long)__popc(mask));
+    base = __shfl_sync(mask, base, leader);
+    list[base + __popc(mask & ((1u << lane) - 1u))] = v;
+}
+
+// a vertex changed and becomes active next iteration
+__device__ __forceinline__ void publish_changed(const FrontierView& f, uint32_t slot, LocalStats& st) {
+    st.changed++;
+    st.next_active++;
+    st.next_units += __ldg(f.outdeg + slot);
+    if (bit_test(f.remote_src, slot)) st.remote_active++;
+    atomicOr(f.active_next + (slot >> 5), 1u << (slot & 31));
+    warp_append(f.frontier_next, f.frontier_count, slot);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+// block-wide reduction of LocalStats into one stripe
+__device__ __forceinline__ void flush_stats(LocalStats st, StatStripe* stripes) {
+    __shared__ unsigned long long sh[kBlock / 32][6];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long v[5] = {st.changed, st.next_active, st.next_units, st.targets, st.remote_active};
+    double m = st.max_stat;
+    for (int i = 0; i < 5; ++i) v[i] = warp_sum(v[i]);
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(kFull, m, o));
+    if (lane == 0) {
+        for (int i = 0; i < 5; ++i) sh[warp][i] = v[i];
+        sh[warp][5] = (unsigned long long)__double_as_longlong(m);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t[5] = {0, 0, 0, 0, 0};
+        double mm = 0.0;
+        for (int w = 0; w < kBlock / 32; ++w) {
+            for (int i = 0; i < 5; ++i) t[i] += sh[w][i];
+            mm = fmax(mm, __longlong_as_double((long long)sh[w][5]));
+        }
+        StatStripe* s = stripes + (blockIdx.x % kStripes);
+        if (t[0]) atomicAdd(&s->changed, t[0]);
+        if (t[1]) atomicAdd(&s->next_active, t[1]);
+        if (t[2]) atomicAdd(&s->next_units, t[2]);
+        if (t[3]) atomicAdd(&s->targets, t[3]);
+        if (t[4]) atomicAdd(&s->remote_active, t[4]);
+        if (mm > 0.0) atomicMax(&s->max_stat_bits, (unsigned long long)__double_as_longlong(mm));
+    }
+}
+
+}  // namespace gxb
+
+struct gxb_state {
+    gxb_graph* g = nullptr;
+    int algo = 0;
+    int arity = 1;
+    int nsrc = 0;
+    uint32_t src_slot[4] = {0, 0, 0, 0};
+    bool src_present[4] = {false, false, false, false};
+    uint64_t iteration = 0;
+    uint64_t owned_outdeg_sum = 0;   // GEN units of a full frontier of owned vertices
+    uint64_t owned_targets = 0;      // owned slots with in-degree > 0 (PR targets)
+
+    // values (full-length replica over slots)
+    double* d_rank = nullptr;               // PR: rank per slot
+    double* d_contrib[2] = {nullptr, nullptr};  // PR: rank/outdeg, double-buffered
+    int cur = 0;
+    uint4* d_dist_cur = nullptr;            // SSSP: 4 lanes of u32 per slot
+    uint4* d_dist_next = nullptr;
+    uint32_t* d_lab_cur = nullptr;          // CC / LP labels
+    uint32_t* d_lab_next = nullptr;
+
+    // frontier
+    uint32_t* d_active[2] = {nullptr, nullptr};    // bitmaps over slots
+    uint32_t* d_frontier[2] = {nullptr, nullptr};  // slot lists
+    unsigned long long* d_fcount = nullptr;        // [2] counters
+    uint32_t* d_touched = nullptr;                 // push dedup bitmap over owned slots
+    uint64_t words = 0;                            // bitmap words over V
+    uint64_t frontier_len = 0;                     // host copy: length of the current frontier list
+    uint64_t units_cur = 0;                        // GEN units of the current frontier
+
+    // stats
+    gxb::StatStripe* d_stats = nullptr;
+    gxb::StatStripe* h_stats = nullptr;    // pinned
+    unsigned long long* h_fcount = nullptr; // pinned
+    cudaEvent_t stats_ready = nullptr;
+    bool stats_pending = false;
+    bool in_round = false;
+    int last_direction = GXB_DIR_PULL;
+    gxb_iter_stats last{};
+
+    // request path (materialised messages, lazily allocated)
+    void* d_msg = nullptr;
+    uint8_t* d_msg_valid = nullptr;
+    void* d_merged = nullptr;
+
+    // pull-merge partials (chunk items)
+    void* d_partials = nullptr;
+
+    // LP scratch
+    void* d_lp_scratch = nullptr;
+    size_t lp_scratch_bytes = 0;
+
+    // exchange
+    void* d_send = nullptr;
+    void* d_recv = nullptr;
+    uint64_t recv_cap = 0;
+};

@@ -1,0 +1,628 @@
+// gxb_store.cu — daemon lifecycle and the device-resident graph store (K0).
+//
+// Replaces `partition_graph` (A/graph.py:175-212), the per-partition
+// vertex/edge/ve_map tables (A/graph.py:93-106), the global out-degree table
+// (A/graph.py:203-210) and the static remote-destination index
+// (A/agent.py:156-166). Everything is built on the device:
+//   present-id bitmap -> popcount ranks (vertex set = ids present in edges,
+//   A/graph.py:163-164) -> in/out degrees (duplicates and self-loops count) ->
+//   degree-sorted slot order (in-degree descending, ties by id) -> relabelled
+//   edges -> destination-range partition balanced by in-edges (Lemma 2 with
+//   equal c_j, A/balancer.py:79-98) -> CSC of the owned destinations sorted by
+//   (dst, src) -> optional push CSR -> degree-bin plan of the pull merge.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "gxb_internal.cuh"
+
+namespace gxb {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+    return GXB_ECUDA;
+}
+
+int dalloc(void** p, size_t bytes) {
+    *p = nullptr;
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        return fail(GXB_ENOMEM, std::string("cudaMalloc(") + std::to_string(bytes) + "): " +
+                                    cudaGetErrorString(e));
+    }
+    return GXB_OK;
+}
+void dfree(void* p) {
+    if (p) cudaFree(p);
+}
+
+// ------------------------------------------------------------------ kernels
+
+__global__ void k_max_id(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, uint64_t n,
+                         uint32_t* out) {
+    uint32_t m = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        m = max(m, max(a[i], b[i]));
+    }
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+__global__ void k_mark_present(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                               uint64_t n, uint32_t* bm) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t x = a[i], y = b[i];
+        atomicOr(bm + (x >> 5), 1u << (x & 31));
+        atomicOr(bm + (y >> 5), 1u << (y & 31));
+    }
+}
+
+__global__ void k_word_popc(const uint32_t* __restrict__ bm, uint64_t words, uint32_t* cnt) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < words;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        cnt[i] = __popc(bm[i]);
+}
+
+// dense index (rank among present ids) of each present id; ids ascending
+__global__ void k_emit_ids(const uint32_t* __restrict__ bm, const uint32_t* __restrict__ prefix,
+                           uint64_t words, uint32_t* ids) {
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t bits = bm[w];
+        uint32_t r = prefix[w];
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            ids[r++] = (uint32_t)(w * 32 + b);
+            bits &= bits - 1;
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t rank_of(const uint32_t* bm, const uint32_t* prefix, uint32_t id) {
+    const uint32_t w = id >> 5;
+    const uint32_t below = bm[w] & ((1u << (id & 31)) - 1u);
+    return prefix[w] + __popc(below);
+}
+
+// edges -> dense indices in place, degrees
+__global__ void k_rank_edges(uint32_t* src, uint32_t* dst, uint64_t n, const uint32_t* __restrict__ bm,
+                             const uint32_t* __restrict__ prefix, uint32_t* outdeg, uint32_t* indeg) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = rank_of(bm, prefix, src[i]);
+        const uint32_t d = rank_of(bm, prefix, dst[i]);
+        src[i] = s;
+        dst[i] = d;
+        atomicAdd(outdeg + s, 1u);
+        atomicAdd(indeg + d, 1u);
+    }
+}
+
+__global__ void k_iota(uint32_t* a, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        a[i] = (uint32_t)i;
+}
+
+// slot order -> inverse map, per-slot id and out-degree
+__global__ void k_slot_tables(const uint32_t* __restrict__ slot2dense, uint64_t V,
+                              const uint32_t* __restrict__ ids_dense,
+                              const uint32_t* __restrict__ outdeg_dense, uint32_t* dense2slot,
+                              uint32_t* slot2id, uint32_t* outdeg_slot) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < V;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t d = slot2dense[s];
+        dense2slot[d] = (uint32_t)s;
+        slot2id[s] = ids_dense[d];
+        outdeg_slot[s] = outdeg_dense[d];
+    }
+}
+
+__global__ void k_relabel(uint32_t* src, uint32_t* dst, uint64_t n, const uint32_t* __restrict__ d2s) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        src[i] = d2s[src[i]];
+        dst[i] = d2s[dst[i]];
+    }
+}
+
+__device__ __forceinline__ int owner_of(const uint64_t* bounds, int nparts, uint32_t slot) {
+    int p = 0;
+    while (p + 1 < nparts && (uint64_t)slot >= bounds[p + 1]) ++p;
+    return p;
+}
+
+// remote-source bitmap and the CSC / CSR keys of the owned destinations
+__global__ void k_keys(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, uint64_t n,
+                       const uint64_t* __restrict__ bounds, int nparts, int part, uint64_t lo,
+                       uint64_t owned, uint64_t V, uint32_t* remote_bm, uint64_t* csc_key,
+                       uint64_t* csr_key) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = src[i], d = dst[i];
+        const int od = owner_of(bounds, nparts, d);
+        if (nparts > 1 && od != owner_of(bounds, nparts, s)) {
+            const uint32_t m = 1u << (s & 31);
+            if (!(remote_bm[s >> 5] & m)) atomicOr(remote_bm + (s >> 5), m);
+        }
+        const bool mine = (od == part);
+        csc_key[i] = mine ? ((uint64_t)(d - lo) << 32 | s) : (owned << 32);
+        if (csr_key) csr_key[i] = mine ? ((uint64_t)s << 32 | d) : ((uint64_t)V << 32);
+    }
+}
+
+// offsets of a key-sorted COO: off[k] = first index whose (key >> 32) >= k, k in [0, nseg]
+__global__ void k_offsets(const uint64_t* __restrict__ keys, uint64_t n, uint64_t nseg, uint64_t* off) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t cur = (i < n) ? (keys[i] >> 32) : nseg;
+        const uint64_t prev = (i == 0) ? 0 : ((keys[i - 1] >> 32) + 1);
+        const uint64_t stop = cur < nseg ? cur : nseg;
+        for (uint64_t k = prev; k <= stop; ++k) off[k] = i;
+    }
+}
+
+__global__ void k_low32(const uint64_t* __restrict__ keys, uint64_t n, uint32_t* out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = (uint32_t)keys[i];
+}
+
+static int bits_for(uint64_t v) {
+    int b = 0;
+    while (b < 64 && (v >> b) != 0) ++b;
+    return b;
+}
+
+static unsigned grid_e(uint64_t n) { return grid_for(n, kBlock, 148ull * 32); }
+
+// radix sort of 64-bit keys (and optional u32 values) over [0, end_bit)
+static int sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32_t* vals_alt,
+                      uint64_t n, int end_bit, cudaStream_t st, uint64_t** keys_out,
+                      uint32_t** vals_out) {
+    cub::DoubleBuffer<uint64_t> kb(keys, keys_alt);
+    cub::DoubleBuffer<uint32_t> vb(vals, vals_alt);
+    size_t temp = 0;
+    // CUB's num_items is int-typed for the legacy overload; use the 64-bit
+    // NumItemsT template parameter.
+    if (vals) {
+        GXB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, kb, vb, (int64_t)n, 0, end_bit, st));
+    } else {
+        GXB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, kb, (int64_t)n, 0, end_bit, st));
+    }
+    void* tmp = nullptr;
+    GXB_CHECK(dalloc(&tmp, temp));
+    cudaError_t e;
+    if (vals) e = cub::DeviceRadixSort::SortPairs(tmp, temp, kb, vb, (int64_t)n, 0, end_bit, st);
+    else e = cub::DeviceRadixSort::SortKeys(tmp, temp, kb, (int64_t)n, 0, end_bit, st);
+    cudaStreamSynchronize(st);
+    dfree(tmp);
+    if (e != cudaSuccess) return cuda_fail(e, "cub::DeviceRadixSort");
+    *keys_out = kb.Current();
+    *vals_out = vals ? vb.Current() : nullptr;
+    return GXB_OK;
+}
+
+template <typename T>
+static int exclusive_scan(const T* in, T* out, uint64_t n, cudaStream_t st) {
+    size_t temp = 0;
+    GXB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, in, out, (int64_t)n, st));
+    void* tmp = nullptr;
+    GXB_CHECK(dalloc(&tmp, temp));
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(tmp, temp, in, out, (int64_t)n, st);
+    cudaStreamSynchronize(st);
+    dfree(tmp);
+    if (e != cudaSuccess) return cuda_fail(e, "cub::DeviceScan");
+    return GXB_OK;
+}
+
+// RAII list of scratch buffers
+struct Scratch {
+    std::vector<void*> ptrs;
+    ~Scratch() {
+        for (void* p : ptrs) dfree(p);
+    }
+    template <typename T>
+    int get(T** p, size_t n) {
+        int rc = dalloc_t(p, n);
+        if (rc == GXB_OK) ptrs.push_back(*p);
+        return rc;
+    }
+};
+
+static void graph_release(gxb_graph* g) {
+    dfree(g->d_slot2id);
+    dfree(g->d_dense2slot);
+    dfree(g->d_outdeg);
+    dfree(g->d_remote_src);
+    dfree(g->d_in_off);
+    dfree(g->d_in_src);
+    dfree(g->d_in_w);
+    dfree(g->d_out_off);
+    dfree(g->d_out_dst);
+    dfree(g->d_out_w);
+    dfree(g->plan.d_item_slot);
+    dfree(g->plan.d_item_begin);
+    dfree(g->plan.d_item_first);
+    dfree(g->plan.d_item_count);
+    dfree(g->plan.d_slot_arrive);
+}
+
+// degree-bin plan of the pull merge (host side, from the owned in-degrees)
+int build_pull_plan(gxb_graph* g, cudaStream_t st) {
+    PullPlan& P = g->plan;
+    const uint64_t owned = g->hi - g->lo;
+    const std::vector<uint32_t>& deg = g->h_indeg_sorted;  // descending
+    // first slot with degree <= t
+    auto first_le = [&](uint64_t t) -> uint64_t {
+        return (uint64_t)(std::lower_bound(deg.begin(), deg.end(), (uint32_t)t,
+                                           [](uint32_t a, uint32_t b) { return a > b; }) -
+                          deg.begin());
+    };
+    P.chunk_end = first_le(kChunkMinDeg);
+    // group bin k (G = 1 << k) takes degrees in (2^(k+1), 2^(k+2)], k = 0 takes [0, 4]
+    for (int k = kNumGroupBins - 1; k >= 0; --k) {
+        const uint64_t lower = (k == 0) ? 0 : (1ull << (k + 1));
+        P.group_end[k] = (k == 0) ? owned : first_le(lower);
+    }
+    // chunk items
+    std::vector<uint32_t> islot, ifirst, icount;
+    std::vector<uint64_t> ibegin;
+    uint64_t off = 0;
+    for (uint64_t s = 0; s < P.chunk_end; ++s) {
+        const uint32_t d = deg[s];
+        const uint32_t n = (d + kChunkEdges - 1) / kChunkEdges;
+        const uint32_t first = (uint32_t)islot.size();
+        for (uint32_t k = 0; k < n; ++k) {
+            islot.push_back((uint32_t)s);
+            ibegin.push_back(off + (uint64_t)k * kChunkEdges);
+            ifirst.push_back(first);
+            icount.push_back(n);
+        }
+        off += d;
+    }
+    P.num_items = islot.size();
+    GXB_CHECK(dalloc_t(&P.d_item_slot, P.num_items));
+    GXB_CHECK(dalloc_t(&P.d_item_begin, P.num_items));
+    GXB_CHECK(dalloc_t(&P.d_item_first, P.num_items));
+    GXB_CHECK(dalloc_t(&P.d_item_count, P.num_items));
+    GXB_CHECK(dalloc_t(&P.d_slot_arrive, P.chunk_end));
+    if (P.num_items) {
+        GXB_CUDA(cudaMemcpyAsync(P.d_item_slot, islot.data(), 4 * P.num_items, cudaMemcpyHostToDevice, st));
+        GXB_CUDA(cudaMemcpyAsync(P.d_item_begin, ibegin.data(), 8 * P.num_items, cudaMemcpyHostToDevice, st));
+        GXB_CUDA(cudaMemcpyAsync(P.d_item_first, ifirst.data(), 4 * P.num_items, cudaMemcpyHostToDevice, st));
+        GXB_CUDA(cudaMemcpyAsync(P.d_item_count, icount.data(), 4 * P.num_items, cudaMemcpyHostToDevice, st));
+    }
+    GXB_CUDA(cudaMemsetAsync(P.d_slot_arrive, 0, 4 * (P.chunk_end + 1), st));
+    GXB_CUDA(cudaStreamSynchronize(st));
+    return GXB_OK;
+}
+
+static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t* dst_in,
+                            const uint32_t* w_in, uint64_t E, uint32_t flags, cudaStream_t st) {
+    Scratch S;
+    const bool host = flags & GXB_BUILD_HOST_INPUT;
+    const bool want_csr = !(flags & GXB_BUILD_NO_CSR);
+    g->E = E;
+    g->weighted = (w_in != nullptr);
+    // working copies (relabelled in place)
+    uint32_t *src = nullptr, *dst = nullptr, *w = nullptr;
+    GXB_CHECK(S.get(&src, E));
+    GXB_CHECK(S.get(&dst, E));
+    const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    GXB_CUDA(cudaMemcpyAsync(src, src_in, 4 * E, kind, st));
+    GXB_CUDA(cudaMemcpyAsync(dst, dst_in, 4 * E, kind, st));
+    if (w_in) {
+        GXB_CHECK(S.get(&w, E));
+        GXB_CUDA(cudaMemcpyAsync(w, w_in, 4 * E, kind, st));
+    }
+    // present ids
+    uint32_t* d_max = nullptr;
+    GXB_CHECK(S.get(&d_max, 1));
+    GXB_CUDA(cudaMemsetAsync(d_max, 0, 4, st));
+    if (E) k_max_id<<<grid_e(E), kBlock, 0, st>>>(src, dst, E, d_max);
+    uint32_t max_id = 0;
+    GXB_CUDA(cudaMemcpyAsync(&max_id, d_max, 4, cudaMemcpyDeviceToHost, st));
+    GXB_CUDA(cudaStreamSynchronize(st));
+    if (max_id == 0xFFFFFFFFu) return fail(GXB_ERANGE, "vertex id 4294967295 is reserved");
+    g->max_id = max_id;
+    const uint64_t words = E ? ((uint64_t)max_id >> 5) + 1 : 1;
+    uint32_t *bm = nullptr, *wcnt = nullptr, *wpre = nullptr;
+    GXB_CHECK(S.get(&bm, words));
+    GXB_CHECK(S.get(&wcnt, words + 1));
+    GXB_CHECK(S.get(&wpre, words + 1));
+    GXB_CUDA(cudaMemsetAsync(bm, 0, 4 * words, st));
+    GXB_CUDA(cudaMemsetAsync(wcnt, 0, 4 * (words + 1), st));
+    if (E) k_mark_present<<<grid_e(E), kBlock, 0, st>>>(src, dst, E, bm);
+    k_word_popc<<<grid_e(words), kBlock, 0, st>>>(bm, words, wcnt);
+    GXB_CHECK(exclusive_scan<uint32_t>(wcnt, wpre, words + 1, st));
+    uint32_t V32 = 0;
+    GXB_CUDA(cudaMemcpyAsync(&V32, wpre + words, 4, cudaMemcpyDeviceToHost, st));
+    GXB_CUDA(cudaStreamSynchronize(st));
+    const uint64_t V = E ? V32 : 0;
+    g->V = V;
+    uint32_t *ids_dense = nullptr, *outdeg_d = nullptr, *indeg_d = nullptr;
+    GXB_CHECK(S.get(&ids_dense, V));
+    GXB_CHECK(S.get(&outdeg_d, V));
+    GXB_CHECK(S.get(&indeg_d, V));
+    GXB_CUDA(cudaMemsetAsync(outdeg_d, 0, 4 * V + 4, st));
+    GXB_CUDA(cudaMemsetAsync(indeg_d, 0, 4 * V + 4, st));
+    if (E) {
+        k_emit_ids<<<grid_e(words), kBlock, 0, st>>>(bm, wpre, words, ids_dense);
+        k_rank_edges<<<grid_e(E), kBlock, 0, st>>>(src, dst, E, bm, wpre, outdeg_d, indeg_d);
+    }
+    // slot order: in-degree descending, ties by ascending id (stable sort)
+    uint32_t *iota = nullptr, *slot2dense = nullptr, *indeg_slot = nullptr;
+    GXB_CHECK(S.get(&iota, V));
+    GXB_CHECK(S.get(&slot2dense, V));
+    GXB_CHECK(S.get(&indeg_slot, V));
+    if (V) {
+        k_iota<<<grid_e(V), kBlock, 0, st>>>(iota, V);
+        size_t temp = 0;
+        GXB_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, temp, indeg_d, indeg_slot, iota,
+                                                           slot2dense, (int64_t)V, 0, 32, st));
+        void* tmp = nullptr;
+        GXB_CHECK(S.get(reinterpret_cast<uint8_t**>(&tmp), temp));
+        GXB_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, temp, indeg_d, indeg_slot, iota,
+                                                           slot2dense, (int64_t)V, 0, 32, st));
+    }
+    GXB_CHECK(dalloc_t(&g->d_dense2slot, V));
+    GXB_CHECK(dalloc_t(&g->d_slot2id, V));
+    GXB_CHECK(dalloc_t(&g->d_outdeg, V));
+    if (V)
+        k_slot_tables<<<grid_e(V), kBlock, 0, st>>>(slot2dense, V, ids_dense, outdeg_d, g->d_dense2slot,
+                                                      g->d_slot2id, g->d_outdeg);
+    if (E) k_relabel<<<grid_e(E), kBlock, 0, st>>>(src, dst, E, g->d_dense2slot);
+
+    // destination-range partition balanced by in-edge count
+    std::vector<uint32_t> h_indeg(V);
+    if (V) GXB_CUDA(cudaMemcpyAsync(h_indeg.data(), indeg_slot, 4 * V, cudaMemcpyDeviceToHost, st));
+    GXB_CUDA(cudaStreamSynchronize(st));
+    uint32_t maxin = 0;
+    for (uint64_t i = 0; i < V; ++i) maxin = std::max(maxin, h_indeg[i]);
+    g->max_in_degree = maxin;
+    g->bounds.assign(g->nparts + 1, 0);
+    g->bounds[g->nparts] = V;
+    {
+        // per-slot cost in pull bytes: 12 per in-edge + 32 per vertex;
+        // every rank computes the same bounds from the same edge list
+        auto cost = [&](uint64_t s) { return 12ull * h_indeg[s] + 32ull; };
+        uint64_t total = 0;
+        for (uint64_t s = 0; s < V; ++s) total += cost(s);
+        uint64_t acc = 0, s = 0;
+        for (int p = 1; p < g->nparts; ++p) {
+            const uint64_t target = (uint64_t)((long double)total * p / g->nparts);
+            while (s < V && acc < target) acc += cost(s++);
+            g->bounds[p] = s;
+        }
+    }
+    g->lo = g->bounds[g->part];
+    g->hi = g->bounds[g->part + 1];
+    const uint64_t owned = g->hi - g->lo;
+    g->h_indeg_sorted.assign(h_indeg.begin() + g->lo, h_indeg.begin() + g->hi);
+
+    uint64_t* d_bounds = nullptr;
+    GXB_CHECK(S.get(&d_bounds, g->nparts + 1));
+    GXB_CUDA(cudaMemcpyAsync(d_bounds, g->bounds.data(), 8 * (g->nparts + 1), cudaMemcpyHostToDevice, st));
+    const uint64_t rwords = (V >> 5) + 1;
+    GXB_CHECK(dalloc_t(&g->d_remote_src, rwords));
+    GXB_CUDA(cudaMemsetAsync(g->d_remote_src, 0, 4 * rwords, st));
+
+    uint64_t *csc_key = nullptr, *key_alt = nullptr, *csr_key = nullptr;
+    GXB_CHECK(S.get(&csc_key, E));
+    GXB_CHECK(S.get(&key_alt, E));
+    if (want_csr) GXB_CHECK(S.get(&csr_key, E));
+    if (E)
+        k_keys<<<grid_e(E), kBlock, 0, st>>>(src, dst, E, d_bounds, g->nparts, g->part, g->lo, owned, V,
+                                              g->d_remote_src, csc_key, csr_key);
+    // owned in-edge count
+    uint64_t owned_edges = 0;
+    for (uint64_t s = g->lo; s < g->hi; ++s) owned_edges += h_indeg[s];
+    g->owned_edges = owned_edges;
+
+    uint32_t* w_alt = nullptr;
+    if (w) GXB_CHECK(S.get(&w_alt, E));
+    // CSC
+    {
+        uint64_t* kout = nullptr;
+        uint32_t* vout = nullptr;
+        // keep a pristine copy of w for the CSR sort
+        uint32_t* w_csc = nullptr;
+        if (w && want_csr) {
+            GXB_CHECK(S.get(&w_csc, E));
+            GXB_CUDA(cudaMemcpyAsync(w_csc, w, 4 * E, cudaMemcpyDeviceToDevice, st));
+        } else {
+            w_csc = w;
+        }
+        if (E) GXB_CHECK(sort_pairs(csc_key, key_alt, w_csc, w_alt, E, 32 + bits_for(owned), st, &kout, &vout));
+        GXB_CHECK(dalloc_t(&g->d_in_off, owned + 1));
+        GXB_CHECK(dalloc_t(&g->d_in_src, owned_edges));
+        if (owned_edges) k_low32<<<grid_e(owned_edges), kBlock, 0, st>>>(kout, owned_edges, g->d_in_src);
+        k_offsets<<<grid_e(owned_edges + 1), kBlock, 0, st>>>(kout, owned_edges, owned, g->d_in_off);
+        if (w) {
+            GXB_CHECK(dalloc_t(&g->d_in_w, owned_edges));
+            if (owned_edges)
+                GXB_CUDA(cudaMemcpyAsync(g->d_in_w, vout, 4 * owned_edges, cudaMemcpyDeviceToDevice, st));
+        }
+        GXB_CUDA(cudaStreamSynchronize(st));
+    }
+    // push CSR (sources -> owned destinations)
+    if (want_csr) {
+        uint64_t* kout = nullptr;
+        uint32_t* vout = nullptr;
+        if (E) GXB_CHECK(sort_pairs(csr_key, key_alt, w, w_alt, E, 32 + bits_for(V), st, &kout, &vout));
+        GXB_CHECK(dalloc_t(&g->d_out_off, V + 1));
+        GXB_CHECK(dalloc_t(&g->d_out_dst, owned_edges));
+        if (owned_edges) k_low32<<<grid_e(owned_edges), kBlock, 0, st>>>(kout, owned_edges, g->d_out_dst);
+        k_offsets<<<grid_e(owned_edges + 1), kBlock, 0, st>>>(kout, owned_edges, V, g->d_out_off);
+        if (w) {
+            GXB_CHECK(dalloc_t(&g->d_out_w, owned_edges));
+            if (owned_edges)
+                GXB_CUDA(cudaMemcpyAsync(g->d_out_w, vout, 4 * owned_edges, cudaMemcpyDeviceToDevice, st));
+        }
+        g->has_csr = true;
+        g->owned_out_edges = owned_edges;
+        GXB_CUDA(cudaStreamSynchronize(st));
+    }
+    GXB_CUDA(cudaGetLastError());
+    GXB_CHECK(build_pull_plan(g, st));
+    return GXB_OK;
+}
+
+}  // namespace gxb
+
+using namespace gxb;
+
+// ------------------------------------------------------------------ C ABI
+
+extern "C" {
+
+const char* gxb_last_error(void) { return gxb::g_last_error.c_str(); }
+const char* gxb_version(void) { return "gxb200 0.1 sm_100a"; }
+
+int gxb_init(int device, gxb_ctx** out) {
+    if (!out) return fail(GXB_EINVAL, "gxb_init: null out");
+    int n = 0;
+    GXB_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) return fail(GXB_EINVAL, "gxb_init: device index out of range");
+    GXB_CUDA(cudaSetDevice(device));
+    gxb_ctx* c = new gxb_ctx();
+    c->device = device;
+    cudaError_t e = cudaGetDeviceProperties(&c->prop, device);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaGetDeviceProperties");
+    }
+    if (c->prop.major != 10) {
+        int maj = c->prop.major, min = c->prop.minor;
+        delete c;
+        return fail(GXB_ECUDA, "libgxb200 requires an sm_100 device, found sm_" + std::to_string(maj) +
+                                   std::to_string(min));
+    }
+    c->init_count = 1;  // Daemon.initialize runs exactly once (A/daemon.py:148-161)
+    c->alive = true;
+    *out = c;
+    return GXB_OK;
+}
+
+int gxb_reinit(gxb_ctx* ctx) {
+    if (!ctx) return fail(GXB_EINVAL, "gxb_reinit: null ctx");
+    return fail(GXB_EPROTO, std::string("daemon: re-initialization attempted in phase ") +
+                                (ctx->alive ? "ready" : "terminated"));
+}
+
+int gxb_init_count(const gxb_ctx* ctx, int* out) {
+    if (!ctx || !out) return fail(GXB_EINVAL, "gxb_init_count: null argument");
+    *out = ctx->init_count;
+    return GXB_OK;
+}
+
+int gxb_shutdown(gxb_ctx* ctx) {
+    if (!ctx) return GXB_OK;
+    if (ctx->alive) {
+        ctx->alive = false;
+        cudaDeviceSynchronize();
+    }
+    delete ctx;
+    return GXB_OK;
+}
+
+int gxb_graph_build(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint32_t* w,
+                    uint64_t num_edges, int part, int nparts, uint32_t flags, void* stream,
+                    gxb_graph** out) {
+    if (!ctx || !ctx->alive) return fail(GXB_ESTATE, "gxb_graph_build: daemon not initialised");
+    if (!out) return fail(GXB_EINVAL, "gxb_graph_build: null out");
+    if (num_edges && (!src || !dst)) return fail(GXB_EINVAL, "gxb_graph_build: null edge arrays");
+    if (nparts < 1 || nparts > 64 || part < 0 || part >= nparts)
+        return fail(GXB_EINVAL, "gxb_graph_build: bad partition index");
+    if (num_edges >= (1ull << 32)) return fail(GXB_ERANGE, "gxb_graph_build: more than 2^32-1 edges");
+    GXB_CUDA(cudaSetDevice(ctx->device));
+    gxb_graph* g = new gxb_graph();
+    g->ctx = ctx;
+    g->part = part;
+    g->nparts = nparts;
+    int rc = graph_build_impl(g, src, dst, w, num_edges, flags, (cudaStream_t)stream);
+    if (rc != GXB_OK) {
+        graph_release(g);
+        delete g;
+        return rc;
+    }
+    *out = g;
+    return GXB_OK;
+}
+
+int gxb_graph_get_info(const gxb_graph* g, gxb_graph_info* o) {
+    if (!g || !o) return fail(GXB_EINVAL, "gxb_graph_get_info: null argument");
+    std::memset(o, 0, sizeof(*o));
+    o->num_vertices = g->V;
+    o->num_edges = g->E;
+    o->owned_lo = g->lo;
+    o->owned_hi = g->hi;
+    o->owned_edges = g->owned_edges;
+    o->owned_out_edges = g->owned_out_edges;
+    o->max_id = g->max_id;
+    o->max_in_degree = g->max_in_degree;
+    o->part = g->part;
+    o->nparts = g->nparts;
+    o->weighted = g->weighted;
+    o->has_csr = g->has_csr;
+    return GXB_OK;
+}
+
+__global__ void k_gather_by_slot(const uint32_t* __restrict__ d2s, const uint32_t* __restrict__ vals,
+                                 uint64_t V, uint32_t* out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < V;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = vals[d2s[i]];
+}
+
+static int read_dense_u32(const gxb_graph* g, const uint32_t* per_slot, uint32_t* host_out) {
+    if (!g->V) return GXB_OK;
+    uint32_t* tmp = nullptr;
+    GXB_CHECK(dalloc_t(&tmp, g->V));
+    k_gather_by_slot<<<grid_e(g->V), kBlock>>>(g->d_dense2slot, per_slot, g->V, tmp);
+    cudaError_t e = cudaMemcpy(host_out, tmp, 4 * g->V, cudaMemcpyDeviceToHost);
+    dfree(tmp);
+    if (e != cudaSuccess) return cuda_fail(e, "read_dense_u32");
+    return GXB_OK;
+}
+
+int gxb_graph_ids(const gxb_graph* g, uint32_t* host_out) {
+    if (!g || (!host_out && g->V)) return fail(GXB_EINVAL, "gxb_graph_ids: null argument");
+    return read_dense_u32(g, g->d_slot2id, host_out);
+}
+
+int gxb_graph_out_degree(const gxb_graph* g, uint32_t* host_out) {
+    if (!g || (!host_out && g->V)) return fail(GXB_EINVAL, "gxb_graph_out_degree: null argument");
+    return read_dense_u32(g, g->d_outdeg, host_out);
+}
+
+int gxb_graph_part_bounds(const gxb_graph* g, uint64_t* host_out) {
+    if (!g || !host_out) return fail(GXB_EINVAL, "gxb_graph_part_bounds: null argument");
+    std::memcpy(host_out, g->bounds.data(), 8 * g->bounds.size());
+    return GXB_OK;
+}
+
+int gxb_graph_free(gxb_graph* g) {
+    if (!g) return GXB_OK;
+    graph_release(g);
+    delete g;
+    return GXB_OK;
+}
+
+}  // extern "C"

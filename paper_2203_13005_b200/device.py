@@ -1,0 +1,286 @@
+"""Python handles over the libgxb200 C ABI: daemon context, device graph store,
+algorithm state. Thin by design — every byte of per-iteration work runs in the
+sm_100a kernels; Python only sequences calls and reads the vote statistics."""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+ALGO_IDS = {"sssp": L.ALGO_SSSP, "pagerank": L.ALGO_PAGERANK, "lp": L.ALGO_LP, "cc": L.ALGO_CC}
+DIRECTIONS = {"auto": L.DIR_AUTO, "pull": L.DIR_PULL, "push": L.DIR_PUSH}
+U32_MAX = 0xFFFFFFFF
+
+
+def _vp(x) -> ctypes.c_void_p | None:
+    """Raw pointer of a numpy array, a torch tensor or an int."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return ctypes.c_void_p(x)
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data_as(ctypes.c_void_p)
+    if hasattr(x, "data_ptr"):
+        return ctypes.c_void_p(x.data_ptr())
+    raise TypeError(f"cannot take a device/host pointer of {type(x)!r}")
+
+
+def _stream_ptr(stream) -> ctypes.c_void_p | None:
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class DeviceContext:
+    """One initialised device daemon (Daemon.initialize runs once, A/daemon.py:148-161)."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = ctypes.c_void_p()
+        L.check(L.lib().gxb_init(device, ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise L.ProtocolError("daemon terminated")
+        return self._h
+
+    @property
+    def init_count(self) -> int:
+        out = ctypes.c_int()
+        L.check(L.lib().gxb_init_count(self.handle, ctypes.byref(out)))
+        return out.value
+
+    def reinit(self):
+        L.check(L.lib().gxb_reinit(self.handle))
+
+    def shutdown(self):
+        if self._h is not None:
+            L.check(L.lib().gxb_shutdown(self._h))
+            self._h = None
+
+    @property
+    def alive(self) -> bool:
+        return self._h is not None
+
+    def rmat(self, params, stream=None):
+        """Generate an R-MAT stream on the device (include/gxb_rmat.h); torch int32 tensors."""
+        import torch
+
+        m = params.num_edges
+        dev = torch.device("cuda", self.device)
+        src = torch.empty(m, dtype=torch.int32, device=dev)
+        dst = torch.empty(m, dtype=torch.int32, device=dev)
+        w = torch.empty(m, dtype=torch.int32, device=dev) if params.wmax else None
+        args = L.RmatArgs(*params.c_args())
+        st = _stream_ptr(stream if stream is not None else torch.cuda.current_stream(dev))
+        L.check(L.lib().gxb_rmat_generate(self.handle, ctypes.byref(args), _vp(src), _vp(dst), _vp(w), st))
+        return src, dst, w
+
+
+def validate_weights(w) -> np.ndarray | None:
+    """Device weights are u32 integers; float weights must be integral and non-negative
+    (negative weights are already rejected by the loader, A/graph.py:161-162)."""
+    if w is None:
+        return None
+    a = np.asarray(w)
+    if a.dtype.kind == "f":
+        if not np.all(np.isfinite(a)) or np.any(a < 0) or np.any(a != np.floor(a)) or np.any(a > U32_MAX - 1):
+            raise ValueError("device SSSP needs integral, non-negative edge weights below 2^32-1")
+        return a.astype(np.uint32)
+    if a.dtype.kind in "iu":
+        if a.size and (a.min() < 0 or a.max() > U32_MAX - 1):
+            raise ValueError("edge weights must be in [0, 2^32-2]")
+        return a.astype(np.uint32, copy=False)
+    raise ValueError(f"unsupported weight dtype {a.dtype}")
+
+
+class DeviceGraph:
+    """Device-resident CSC (+ push CSR) of one destination partition (A/graph.py:175-212)."""
+
+    def __init__(self, ctx: DeviceContext, src, dst, w=None, part: int = 0, nparts: int = 1,
+                 csr: bool = True, stream=None):
+        self.ctx = ctx
+        flags = 0 if csr else L.BUILD_NO_CSR
+        if hasattr(src, "is_cuda") and src.is_cuda:
+            n = int(src.numel())
+            keep = (src, dst, w)
+        else:
+            src = np.ascontiguousarray(src, dtype=np.uint32)
+            dst = np.ascontiguousarray(dst, dtype=np.uint32)
+            if src.shape != dst.shape:
+                raise ValueError("src/dst length mismatch")
+            w = validate_weights(w)
+            if w is not None:
+                w = np.ascontiguousarray(w, dtype=np.uint32)
+                if w.shape != src.shape:
+                    raise ValueError("weight length mismatch")
+            n = int(src.size)
+            flags |= L.BUILD_HOST_INPUT
+            keep = (src, dst, w)
+        self._keep = keep  # inputs must outlive the async copies
+        h = ctypes.c_void_p()
+        L.check(L.lib().gxb_graph_build(ctx.handle, _vp(src), _vp(dst), _vp(w), n, part, nparts, flags,
+                                        _stream_ptr(stream), ctypes.byref(h)))
+        self._h = h
+        self._keep = None
+        info = L.GraphInfo()
+        L.check(L.lib().gxb_graph_get_info(self._h, ctypes.byref(info)))
+        self.info = info
+        self.num_vertices = int(info.num_vertices)
+        self.num_edges = int(info.num_edges)
+        self.part, self.nparts = part, nparts
+        self.weighted = bool(info.weighted)
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def owned(self) -> tuple[int, int]:
+        return int(self.info.owned_lo), int(self.info.owned_hi)
+
+    def ids(self) -> np.ndarray:
+        out = np.empty(self.num_vertices, dtype=np.uint32)
+        L.check(L.lib().gxb_graph_ids(self._h, _vp(out)))
+        return out
+
+    def out_degree(self) -> np.ndarray:
+        out = np.empty(self.num_vertices, dtype=np.uint32)
+        L.check(L.lib().gxb_graph_out_degree(self._h, _vp(out)))
+        return out
+
+    def bounds(self) -> np.ndarray:
+        out = np.empty(self.nparts + 1, dtype=np.uint64)
+        L.check(L.lib().gxb_graph_part_bounds(self._h, _vp(out)))
+        return out
+
+    def free(self):
+        if getattr(self, "_h", None):
+            L.lib().gxb_graph_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class DeviceState:
+    """Algorithm values, frontier and statistics of one run on one partition."""
+
+    def __init__(self, graph: DeviceGraph, algo: str, sources=None, max_weight: int | None = None):
+        if algo not in ALGO_IDS:
+            raise ValueError(f"unknown algorithm {algo!r}")
+        self.graph = graph
+        self.algo = algo
+        srcs = None
+        nsrc = 0
+        if algo == "sssp":
+            if sources is not None:
+                srcs = np.ascontiguousarray(sources, dtype=np.uint32)
+                nsrc = int(srcs.size)
+                if nsrc == 0:
+                    raise ValueError("sssp needs at least one source vertex")
+                if nsrc > 4:
+                    raise ValueError("the device SSSP carries at most 4 sources per run")
+            # u32 distances are exact iff no shortest path can reach 2^32-1
+            if max_weight is not None and graph.num_vertices > 1 and \
+                    max_weight * (graph.num_vertices - 1) >= U32_MAX:
+                raise ValueError("edge weights too large for exact 32-bit distances")
+        h = ctypes.c_void_p()
+        L.check(L.lib().gxb_state_create(graph.handle, ALGO_IDS[algo], _vp(srcs), nsrc, ctypes.byref(h)))
+        self._h = h
+        ar = ctypes.c_int()
+        L.check(L.lib().gxb_state_arity(h, ctypes.byref(ar)))
+        self.arity = ar.value
+
+    @property
+    def handle(self):
+        return self._h
+
+    def iterate(self, direction: str = "auto", stream=None):
+        L.check(L.lib().gxb_iterate(self._h, DIRECTIONS[direction], _stream_ptr(stream)))
+
+    def request(self, op: int, lo: int, hi: int, stream=None):
+        L.check(L.lib().gxb_request(self._h, op, lo, hi, _stream_ptr(stream)))
+
+    def commit(self, stream=None):
+        L.check(L.lib().gxb_commit(self._h, _stream_ptr(stream)))
+
+    def stats(self, stream=None) -> dict:
+        st = L.IterStats()
+        L.check(L.lib().gxb_stats(self._h, _stream_ptr(stream), ctypes.byref(st)))
+        return st.as_dict()
+
+    def read_attrs(self, owned_only: bool = False, stream=None) -> np.ndarray:
+        V = self.graph.num_vertices
+        out = np.empty((V, self.arity), dtype=np.float64)
+        L.check(L.lib().gxb_read_attrs(self._h, _vp(out), int(owned_only), _stream_ptr(stream)))
+        return out
+
+    def buffer(self, which: int) -> tuple[int, int]:
+        p = ctypes.c_void_p()
+        b = ctypes.c_uint64()
+        L.check(L.lib().gxb_exchange_buffer(self._h, which, ctypes.byref(p), ctypes.byref(b)))
+        return int(p.value or 0), int(b.value)
+
+    def pack(self, stream=None) -> int:
+        n = ctypes.c_uint64()
+        L.check(L.lib().gxb_exchange_pack(self._h, _stream_ptr(stream), ctypes.byref(n)))
+        return int(n.value)
+
+    def unpack(self, ptr: int, count: int, stream=None):
+        L.check(L.lib().gxb_exchange_unpack(self._h, ctypes.c_void_p(ptr), count, _stream_ptr(stream)))
+
+    def free(self):
+        if getattr(self, "_h", None):
+            L.lib().gxb_state_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+@dataclass
+class DeviceRun:
+    """Result of a run_reference-equivalent loop on the device."""
+
+    ids: np.ndarray
+    attrs: np.ndarray
+    iterations: int
+    converged: bool
+    history: list = field(default_factory=list)
+
+
+def default_cap(algo: str, num_vertices: int) -> int:
+    """default_iteration_cap (A/algorithms.py:117-119, 167-168, 201-202; CC = |V|+1)."""
+    return {"sssp": num_vertices + 1, "pagerank": 100, "lp": 15, "cc": num_vertices + 1}[algo]
+
+
+def run_state(state: DeviceState, max_iterations: int | None = None, direction: str = "auto",
+              stream=None, keep_history: bool = False) -> tuple[int, bool, list]:
+    """Iterate like run_reference (A/algorithms.py:318-341): stop on the vote or the cap."""
+    cap = default_cap(state.algo, state.graph.num_vertices) if max_iterations is None else max_iterations
+    it, converged, hist = 0, False, []
+    while it < cap:
+        state.iterate(direction, stream)
+        st = state.stats(stream)
+        it += 1
+        if keep_history:
+            hist.append(st)
+        if st["voted"]:
+            converged = True
+            break
+    return it, converged, hist
