@@ -22,7 +22,9 @@
 // execute_request over a WorkItem (A/daemon.py:86-130) with range descriptors
 // instead of Python triplet blocks.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "gxb_state.cuh"
@@ -46,12 +48,13 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
     __device__ static Acc identity() { return {0.0}; }
     __device__ static Acc combine(Acc a, Acc b) { return {a.s + b.s}; }
     __device__ static Acc shfl(Acc a, int off) { return {__shfl_xor_sync(kFull, a.s, off)}; }
+    __device__ static Acc shfl_up(Acc a, int d) { return {__shfl_up_sync(kFull, a.s, d)}; }
     __device__ static void st_cg(Acc* p, Acc a) { __stcg(&p->s, a.s); }
     __device__ static Acc ld_cg(const Acc* p) { return {__ldcg(&p->s)}; }
     __device__ static bool has(const Acc&) { return true; }
     // Gen: rank / out_deg of the source (every vertex is active, 144-145)
     __device__ bool gen(uint32_t s, uint64_t, const uint32_t*, Msg& m) const {
-        m = __ldg(contrib_cur + s);
+        m = ld_keep_f64(contrib_cur + s, l2_evict_last());
         return true;
     }
     __device__ static void fold(Acc& a, Msg m) { a.s += m; }
@@ -99,6 +102,15 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
         r.has = __shfl_xor_sync(kFull, a.has, off);
         return r;
     }
+    __device__ static Acc shfl_up(Acc a, int d) {
+        Acc r;
+        r.m.x = __shfl_up_sync(kFull, a.m.x, d);
+        r.m.y = __shfl_up_sync(kFull, a.m.y, d);
+        r.m.z = __shfl_up_sync(kFull, a.m.z, d);
+        r.m.w = __shfl_up_sync(kFull, a.m.w, d);
+        r.has = __shfl_up_sync(kFull, a.has, d);
+        return r;
+    }
     __device__ static void st_cg(Acc* p, Acc a) {
         __stcg(&p->m, a.m);
         __stcg(&p->has, a.has);
@@ -108,8 +120,8 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
     // Gen: d + w per lane from an active source (102-105); inf stays inf
     __device__ bool gen(uint32_t s, uint64_t e, const uint32_t* w, Msg& m) const {
         if (!bit_test(active_cur, s)) return false;
-        const uint4 d = __ldg(dist_cur + s);
-        const uint32_t ww = w ? __ldg(w + e) : 1u;
+        const uint4 d = ld_keep_v4(dist_cur + s, l2_evict_last());
+        const uint32_t ww = w ? ld_stream_u32(w + e, l2_evict_first()) : 1u;
         m = make_uint4(sat_add(d.x, ww), sat_add(d.y, ww), sat_add(d.z, ww), sat_add(d.w, ww));
         return true;
     }
@@ -146,6 +158,9 @@ struct CcOps {  // min-label propagation
     __device__ static Acc shfl(Acc a, int off) {
         return {__shfl_xor_sync(kFull, a.m, off), __shfl_xor_sync(kFull, a.has, off)};
     }
+    __device__ static Acc shfl_up(Acc a, int d) {
+        return {__shfl_up_sync(kFull, a.m, d), __shfl_up_sync(kFull, a.has, d)};
+    }
     __device__ static void st_cg(Acc* p, Acc a) {
         __stcg(&p->m, a.m);
         __stcg(&p->has, a.has);
@@ -154,7 +169,7 @@ struct CcOps {  // min-label propagation
     __device__ static bool has(const Acc& a) { return a.has != 0; }
     __device__ bool gen(uint32_t s, uint64_t, const uint32_t*, Msg& m) const {
         if (!bit_test(active_cur, s)) return false;
-        m = __ldg(lab_cur + s);
+        m = ld_keep_u32(lab_cur + s, l2_evict_last());
         return true;
     }
     __device__ static void fold(Acc& a, Msg m) {
@@ -335,6 +350,173 @@ __global__ void __launch_bounds__(kBlock) k_pull(const Pol p, const PullLaunch L
         }
     }
     flush_stats(st, L.stats);
+}
+
+// ======================================================================
+// the edge-balanced pull merge ("warp tiles", merge-path style)
+//
+// Warp w owns CSC edges [kTileEdges * t, kTileEdges * (t + 1)); lane l owns
+// kTileK consecutive edges of it. A lane loads its source indices with two
+// 16-byte vector loads, issues kTileK independent gathers (Gen), and folds runs
+// of equal destination (Merge) using the offsets of at most kTileK + 1 slots.
+// Runs crossing lanes are combined by a segmented warp scan keyed by slot (the
+// keys are monotone); runs crossing tiles ("spans") publish a per-tile partial
+// and the last-arriving tile folds the partials in tile order, so the fold
+// order — and therefore the PageRank rounding — is deterministic.
+// ======================================================================
+
+struct TileLaunch {
+    uint64_t num_tiles;
+    uint64_t owned_edges;
+    const uint64_t* in_off;
+    const uint32_t* in_src;
+    const uint32_t* lane_slot;
+    const uint32_t* tile_head;
+    const uint32_t* tile_tail;
+    const uint32_t* span_first;
+    const uint32_t* span_count;
+    const uint64_t* span_pbase;
+    const uint32_t* span_slot;
+    uint32_t* span_arrive;
+    void* partials;
+    void* sums;   // per relative slot: folded accumulator
+};
+
+__device__ __forceinline__ uint4 ldg_v4(const uint32_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+
+template <class Pol>
+__device__ __forceinline__ void tile_emit(const Pol& p, const TileLaunch& L, uint64_t t, uint32_t head,
+                                          uint32_t tail, uint32_t key, typename Pol::Acc total) {
+    using Ops = decltype(p.ops);
+    using Acc = typename Ops::Acc;
+    uint32_t span = kNone;
+    if (head != kNone && key == __ldg(L.span_slot + head)) span = head;
+    else if (tail != kNone && key == __ldg(L.span_slot + tail)) span = tail;
+    if (span == kNone) {
+        reinterpret_cast<Acc*>(L.sums)[key] = total;
+    } else {
+        // folded by k_span_fold after the kernel boundary (no fences on the hot path)
+        reinterpret_cast<Acc*>(L.partials)[__ldg(L.span_pbase + span) + (t - __ldg(L.span_first + span))] = total;
+    }
+}
+
+template <class Pol>
+__global__ void __launch_bounds__(kBlock) k_tile(const Pol p, const TileLaunch L) {
+    using Ops = decltype(p.ops);
+    using Acc = typename Ops::Acc;
+    const int lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
+    const uint64_t pol = l2_evict_first();
+    uint64_t t = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+    // software pipeline: the next tile's index vectors are in flight while this tile gathers
+    uint4 na = make_uint4(0, 0, 0, 0), nb = na;
+    if (t < L.num_tiles) {
+        const uint64_t e = t * kTileEdges + (uint64_t)lane * kTileK;
+        na = ld_stream_v4(L.in_src + e, pol);
+        nb = ld_stream_v4(L.in_src + e + 4, pol);
+    }
+    for (; t < L.num_tiles; t += nwarps) {
+        const uint64_t e0 = t * kTileEdges + (uint64_t)lane * kTileK;
+        const bool live = e0 < L.owned_edges;
+        const uint32_t src[kTileK] = {na.x, na.y, na.z, na.w, nb.x, nb.y, nb.z, nb.w};
+        const uint32_t sa = live ? ld_stream_u32(L.lane_slot + t * 32 + lane, pol) : 0u;
+        const uint64_t tn = t + nwarps;
+        if (tn < L.num_tiles) {
+            const uint64_t e = tn * kTileEdges + (uint64_t)lane * kTileK;
+            na = ld_stream_v4(L.in_src + e, pol);
+            nb = ld_stream_v4(L.in_src + e + 4, pol);
+        }
+        // Gen: kTileK independent gathers
+        Acc v[kTileK];
+#pragma unroll
+        for (int j = 0; j < kTileK; ++j) {
+            v[j] = Ops::identity();
+            if (e0 + j < L.owned_edges) p.accumulate(v[j], src[j], e0 + j);
+        }
+        // run ends inside the lane: bit j set <=> a destination segment ends at edge e0 + j
+        uint32_t endmask = 0;
+#pragma unroll
+        for (int m = 0; m < kTileK; ++m) {
+            const uint64_t b = __ldg(L.in_off + sa + 1 + m);
+            const uint64_t r = b - e0;  // wraps for b < e0 (cannot happen: b > e0 for the slot of e0)
+            if (r >= 1 && r <= (uint64_t)kTileK) endmask |= 1u << (uint32_t)(r - 1);
+        }
+        const uint32_t nvalid = live ? (uint32_t)min((uint64_t)kTileK, L.owned_edges - e0) : 0u;
+        endmask &= (1u << nvalid) - 1u;          // ends past the valid edges do not exist
+        endmask &= ~(1u << (kTileK - 1));        // the final position is handled as the last run
+        uint32_t fkey = kNone, lkey = kNone;
+        Acc fval = Ops::identity(), lval = Ops::identity();
+        const bool multi = endmask != 0;
+        Acc acc = Ops::identity();
+        uint32_t key = sa;
+        bool first = true;
+#pragma unroll
+        for (int j = 0; j < kTileK; ++j) {
+            acc = Ops::combine(acc, v[j]);
+            if ((endmask >> j) & 1u) {
+                if (first) {
+                    fkey = key;
+                    fval = acc;
+                    first = false;
+                } else {
+                    reinterpret_cast<Acc*>(L.sums)[key] = acc;  // run wholly inside this lane
+                }
+                ++key;
+                acc = Ops::identity();
+            }
+        }
+        lkey = live ? key : kNone;
+        lval = acc;
+        if (!multi) {
+            fkey = lkey;
+            fval = lval;
+        }
+        // segmented inclusive scan of the lanes' last runs (keys are monotone)
+        Acc c = lval;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const Acc up = Ops::shfl_up(c, d);
+            const uint32_t k = __shfl_up_sync(kFull, lkey, d);
+            if (lane >= d && k == lkey) c = Ops::combine(up, c);
+        }
+        const uint32_t prev_key = __shfl_up_sync(kFull, lkey, 1);
+        const Acc prev_c = Ops::shfl_up(c, 1);
+        const uint32_t next_first = __shfl_down_sync(kFull, fkey, 1);
+        const uint32_t head = __ldg(L.tile_head + t), tail = __ldg(L.tile_tail + t);
+        if (multi && live) {
+            const Acc tot = (lane > 0 && prev_key == fkey) ? Ops::combine(prev_c, fval) : fval;
+            tile_emit(p, L, t, head, tail, fkey, tot);
+        }
+        if (lkey != kNone && (lane == 31 || next_first != lkey)) tile_emit(p, L, t, head, tail, lkey, c);
+    }
+}
+
+// fold the per-tile partials of every span in tile order (deterministic)
+template <class Ops>
+__global__ void k_span_fold(const uint32_t* __restrict__ span_slot, const uint32_t* __restrict__ span_count,
+                            const uint64_t* __restrict__ span_pbase, uint64_t num_spans,
+                            const typename Ops::Acc* __restrict__ partials, typename Ops::Acc* sums) {
+    using Acc = typename Ops::Acc;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < num_spans;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = span_pbase[k];
+        const uint32_t n = span_count[k];
+        Acc tot = Ops::identity();
+        for (uint32_t i = 0; i < n; ++i) tot = Ops::combine(tot, partials[b + i]);
+        sums[span_slot[k]] = tot;
+    }
+}
+
+// Apply over the folded sums of every owned slot (A/algorithms.py:327-338);
+// slots past nz_slots have no in-edge and fold the identity (merged.get(vid, zero)).
+template <class Ops>
+__global__ void __launch_bounds__(kBlock) k_apply_sums(const Ops ops, const typename Ops::Acc* __restrict__ sums,
+                                                        uint64_t lo, uint64_t owned, uint64_t nz,
+                                                        StatStripe* stats) {
+    LocalStats st;
+    for (uint64_t r = blockIdx.x * (uint64_t)kBlock + threadIdx.x; r < owned; r += (uint64_t)gridDim.x * kBlock)
+        ops.apply((uint32_t)(lo + r), r < nz ? sums[r] : Ops::identity(), st);
+    flush_stats(st, stats);
 }
 
 // ======================================================================
@@ -569,6 +751,64 @@ int launch_pull(const Pol& p, const PullLaunch& L, cudaStream_t st) {
     return GXB_OK;
 }
 
+TileLaunch tile_launch(gxb_state* s) {
+    const gxb_graph* g = s->g;
+    const TilePlan& T = g->tiles;
+    TileLaunch L;
+    L.num_tiles = T.num_tiles;
+    L.owned_edges = g->owned_edges;
+    L.in_off = g->d_in_off;
+    L.in_src = g->d_in_src;
+    L.lane_slot = T.d_lane_slot;
+    L.tile_head = T.d_tile_head;
+    L.tile_tail = T.d_tile_tail;
+    L.span_first = T.d_span_first;
+    L.span_count = T.d_span_count;
+    L.span_pbase = T.d_span_pbase;
+    L.span_slot = T.d_span_slot;
+    L.span_arrive = T.d_span_arrive;
+    L.partials = s->d_tile_partials;
+    L.sums = s->d_sums;
+    return L;
+}
+
+template <class Ops>
+int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st) {
+    const gxb_graph* g = s->g;
+    const TileLaunch L = tile_launch(s);
+    FusedPolicy<Ops> p{ops, g->d_in_w};
+    static int max_blocks = 0;
+    if (!max_blocks) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<FusedPolicy<Ops>>, kBlock, 0);
+        max_blocks = std::max(1, per_sm) * kNumSMs;
+    }
+    if (L.num_tiles) {
+        const uint64_t want = (L.num_tiles + (kBlock / 32) - 1) / (kBlock / 32);
+        const unsigned grid = (unsigned)std::min<uint64_t>(want, (uint64_t)max_blocks);
+        k_tile<FusedPolicy<Ops>><<<grid, kBlock, 0, st>>>(p, L);
+        const TilePlan& T = g->tiles;
+        if (T.num_spans)
+            k_span_fold<Ops><<<grid_for(T.num_spans), kBlock, 0, st>>>(
+                T.d_span_slot, T.d_span_count, T.d_span_pbase, T.num_spans,
+                (const typename Ops::Acc*)s->d_tile_partials, (typename Ops::Acc*)s->d_sums);
+    }
+    const uint64_t owned = g->hi - g->lo;
+    k_apply_sums<Ops><<<grid_for(owned), kBlock, 0, st>>>(ops, (const typename Ops::Acc*)s->d_sums, g->lo, owned,
+                                                          g->tiles.nz_slots, s->d_stats);
+    GXB_CUDA(cudaGetLastError());
+    return GXB_OK;
+}
+
+bool use_binned_pull() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("GXB_PULL_KERNEL");
+        v = (e && std::string(e) == "binned") ? 1 : 0;
+    }
+    return v == 1;
+}
+
 PrOps pr_ops(gxb_state* s) {
     PrOps o;
     o.contrib_cur = s->d_contrib[s->cur];
@@ -723,6 +963,8 @@ int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, 
     cudaMemsetAsync(s->d_touched, 0, 4 * ((owned >> 5) + 1), st);
     // chunk partials: the largest accumulator is SsspOps::Acc (32 B with padding)
     if ((rc = dalloc(&s->d_partials, 32 * (g->plan.num_items + 1))) != GXB_OK) return bail(rc);
+    if ((rc = dalloc(&s->d_tile_partials, 32 * (g->tiles.num_partials + 1))) != GXB_OK) return bail(rc);
+    if ((rc = dalloc(&s->d_sums, 32 * (owned + 1))) != GXB_OK) return bail(rc);
 
     const unsigned grid = grid_for(V);
     uint64_t nfront = 0, units0 = 0;
@@ -845,6 +1087,8 @@ int gxb_state_free(gxb_state* s) {
     dfree(s->d_msg_valid);
     dfree(s->d_merged);
     dfree(s->d_partials);
+    dfree(s->d_tile_partials);
+    dfree(s->d_sums);
     gxb_lp_free(s);
     dfree(s->d_send);
     dfree(s->d_recv);
@@ -878,7 +1122,13 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
         }
     }
     const uint64_t owned = g->hi - g->lo;
-    if (dir == GXB_DIR_PULL) {
+    if (dir == GXB_DIR_PULL && s->algo != GXB_ALGO_LP && !use_binned_pull()) {
+        switch (s->algo) {
+            case GXB_ALGO_PAGERANK: GXB_CHECK(launch_tile_and_apply(s, pr_ops(s), st)); break;
+            case GXB_ALGO_SSSP: GXB_CHECK(launch_tile_and_apply(s, sssp_ops(s), st)); break;
+            case GXB_ALGO_CC: GXB_CHECK(launch_tile_and_apply(s, cc_ops(s), st)); break;
+        }
+    } else if (dir == GXB_DIR_PULL) {
         const PullLaunch L = pull_launch(s, 0, owned);
         switch (s->algo) {
             case GXB_ALGO_PAGERANK: {

@@ -44,6 +44,28 @@ constexpr int kNumGroupBins = 6;            // G = 1, 2, 4, 8, 16, 32
 constexpr uint32_t kChunkMinDeg = 128;      // > this: chunked warps
 constexpr uint32_t kChunkEdges = 1024;      // edges per warp work item
 
+// Edge-balanced pull merge (the "warp tile" kernel): each warp owns kTileEdges
+// consecutive CSC edges, kTileK per lane, whatever the destination degrees.
+constexpr int kTileK = 8;
+constexpr uint64_t kTileEdges = 32 * kTileK;
+constexpr uint64_t kOffPad = 16;           // extra offset entries (= owned_edges) after the CSC offsets
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+struct TilePlan {
+    uint64_t nz_slots = 0;       // owned slots with in-degree > 0 (a prefix: slots are degree-sorted)
+    uint64_t num_tiles = 0;
+    uint64_t num_spans = 0;      // slots whose edges cross a tile boundary
+    uint64_t num_partials = 0;   // sum of tiles touched by spans
+    uint32_t* d_lane_slot = nullptr;   // per kTileK-edge lane chunk: slot of its first edge
+    uint32_t* d_tile_head = nullptr;   // per tile: span id of its first slot if that slot started earlier
+    uint32_t* d_tile_tail = nullptr;   // per tile: span id of its last slot if that slot continues
+    uint32_t* d_span_first = nullptr;  // per span: first tile
+    uint32_t* d_span_count = nullptr;  // per span: tiles touched
+    uint64_t* d_span_pbase = nullptr;  // per span: first partial index
+    uint32_t* d_span_slot = nullptr;   // per span: relative slot
+    uint32_t* d_span_arrive = nullptr; // per span: arrival counter (reset by the last arriver)
+};
+
 struct DeviceBuffer {
     void* ptr = nullptr;
     size_t bytes = 0;
@@ -103,6 +125,7 @@ struct gxb_graph {
     uint32_t* d_out_w = nullptr;
     std::vector<uint32_t> h_indeg_sorted;  // owned in-degrees (descending), host copy
     gxb::PullPlan plan;
+    gxb::TilePlan tiles;
 };
 
 namespace gxb {
@@ -114,6 +137,49 @@ __device__ __forceinline__ bool bit_test(const uint32_t* bm, uint32_t i) {
 __device__ __forceinline__ bool bit_set_atomic(uint32_t* bm, uint32_t i) {
     const uint32_t m = 1u << (i & 31);
     return (atomicOr(bm + (i >> 5), m) & m) == 0u;  // true if newly set
+}
+
+// ---- L2 eviction-priority hints (PTX createpolicy / ld ... L2::cache_hint) ----
+// The CSC index stream is touched once per round: evict it first so the hot,
+// degree-sorted prefix of the gathered value arrays stays resident in L2.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_last() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint4 ld_stream_v4(const void* ptr, uint64_t pol) {
+    uint4 r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+        : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_stream_u32(const void* ptr, uint64_t pol) {
+    uint32_t r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ld_keep_f64(const double* ptr, uint64_t pol) {
+    double r;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_keep_u32(const uint32_t* ptr, uint64_t pol) {
+    uint32_t r;
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint4 ld_keep_v4(const uint4* ptr, uint64_t pol) {
+    uint4 r;
+    asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+        : "l"(ptr), "l"(pol));
+    return r;
 }
 
 __device__ __forceinline__ uint32_t sat_add(uint32_t d, uint32_t w) {

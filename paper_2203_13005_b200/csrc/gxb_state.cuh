@@ -137,8 +137,10 @@ struct gxb_state {
     uint8_t* d_msg_valid = nullptr;
     void* d_merged = nullptr;
 
-    // pull-merge partials (chunk items)
+    // pull-merge partials (chunk items of the binned kernel, spans of the tile kernel)
     void* d_partials = nullptr;
+    void* d_tile_partials = nullptr;
+    void* d_sums = nullptr;  // per owned slot: folded accumulator of the tile kernel
 
     // LP scratch
     void* d_lp_scratch = nullptr;

@@ -177,6 +177,26 @@ __global__ void k_offsets(const uint64_t* __restrict__ keys, uint64_t n, uint64_
     }
 }
 
+__global__ void k_fill_u64(uint64_t* a, uint64_t n, uint64_t v) {
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) a[i] = v;
+}
+
+// lane-chunk table of the warp tiles: slot (relative) containing edge kTileK * c
+__global__ void k_lane_slot(const uint64_t* __restrict__ off, uint64_t nz, uint64_t nchunks, uint32_t* out) {
+    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nchunks;
+         c += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t e = c * kTileK;
+        uint64_t lo = 0, hi = nz;  // last s with off[s] <= e
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (off[mid] <= e) lo = mid; else hi = mid;
+        }
+        out[c] = (uint32_t)lo;
+    }
+}
+
+static uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
+
 __global__ void k_low32(const uint64_t* __restrict__ keys, uint64_t n, uint32_t* out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
@@ -261,6 +281,70 @@ static void graph_release(gxb_graph* g) {
     dfree(g->plan.d_item_first);
     dfree(g->plan.d_item_count);
     dfree(g->plan.d_slot_arrive);
+    dfree(g->tiles.d_lane_slot);
+    dfree(g->tiles.d_tile_head);
+    dfree(g->tiles.d_tile_tail);
+    dfree(g->tiles.d_span_first);
+    dfree(g->tiles.d_span_count);
+    dfree(g->tiles.d_span_pbase);
+    dfree(g->tiles.d_span_slot);
+    dfree(g->tiles.d_span_arrive);
+}
+
+// warp-tile plan of the edge-balanced pull merge: kTileEdges edges per warp;
+// slots crossing a tile boundary ("spans") combine per-tile partials
+static int build_tile_plan(gxb_graph* g, cudaStream_t st) {
+    TilePlan& T = g->tiles;
+    const std::vector<uint32_t>& deg = g->h_indeg_sorted;
+    const uint64_t owned = deg.size();
+    uint64_t nz = 0;
+    while (nz < owned && deg[nz] > 0) ++nz;
+    T.nz_slots = nz;
+    T.num_tiles = (g->owned_edges + kTileEdges - 1) / kTileEdges;
+    const uint64_t nchunks = T.num_tiles * 32;
+    GXB_CHECK(dalloc_t(&T.d_lane_slot, nchunks + 1));
+    if (nchunks) k_lane_slot<<<grid_e(nchunks), kBlock, 0, st>>>(g->d_in_off, nz, nchunks, T.d_lane_slot);
+    std::vector<uint32_t> head(T.num_tiles + 1, kNone), tail(T.num_tiles + 1, kNone);
+    std::vector<uint32_t> sfirst, scount, sslot;
+    std::vector<uint64_t> spbase;
+    uint64_t off = 0, pbase = 0;
+    for (uint64_t s = 0; s < nz; ++s) {
+        const uint64_t b = off, e = off + deg[s];
+        const uint64_t t0 = b / kTileEdges, t1 = (e - 1) / kTileEdges;
+        if (t0 != t1) {
+            const uint32_t k = (uint32_t)sfirst.size();
+            sfirst.push_back((uint32_t)t0);
+            scount.push_back((uint32_t)(t1 - t0 + 1));
+            sslot.push_back((uint32_t)s);
+            spbase.push_back(pbase);
+            pbase += t1 - t0 + 1;
+            tail[t0] = k;
+            for (uint64_t t = t0 + 1; t <= t1; ++t) head[t] = k;
+            for (uint64_t t = t0 + 1; t < t1; ++t) tail[t] = k;
+        }
+        off = e;
+    }
+    T.num_spans = sfirst.size();
+    T.num_partials = pbase;
+    int rc = GXB_OK;
+    auto up = [&](auto** d, const auto& h) {
+        if (rc != GXB_OK) return;
+        rc = dalloc_t(d, h.size() + 1);
+        if (rc == GXB_OK && !h.empty() &&
+            cudaMemcpyAsync(*d, h.data(), sizeof(h[0]) * h.size(), cudaMemcpyHostToDevice, st) != cudaSuccess)
+            rc = fail(GXB_ECUDA, "tile plan upload");
+    };
+    up(&T.d_tile_head, head);
+    up(&T.d_tile_tail, tail);
+    up(&T.d_span_first, sfirst);
+    up(&T.d_span_count, scount);
+    up(&T.d_span_pbase, spbase);
+    up(&T.d_span_slot, sslot);
+    GXB_CHECK(rc);
+    GXB_CHECK(dalloc_t(&T.d_span_arrive, T.num_spans + 1));
+    GXB_CUDA(cudaMemsetAsync(T.d_span_arrive, 0, 4 * (T.num_spans + 1), st));
+    GXB_CUDA(cudaStreamSynchronize(st));
+    return GXB_OK;
 }
 
 // degree-bin plan of the pull merge (host side, from the owned in-degrees)
@@ -450,12 +534,18 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
             w_csc = w;
         }
         if (E) GXB_CHECK(sort_pairs(csc_key, key_alt, w_csc, w_alt, E, 32 + bits_for(owned), st, &kout, &vout));
-        GXB_CHECK(dalloc_t(&g->d_in_off, owned + 1));
-        GXB_CHECK(dalloc_t(&g->d_in_src, owned_edges));
+        // offsets padded with kOffPad copies of owned_edges, edge arrays padded to whole
+        // warp tiles with zeros, so the tile kernel's vector loads never leave the buffers
+        const uint64_t padded = round_up(owned_edges, kTileEdges) + kTileEdges;
+        GXB_CHECK(dalloc_t(&g->d_in_off, owned + 1 + kOffPad));
+        GXB_CHECK(dalloc_t(&g->d_in_src, padded));
+        GXB_CUDA(cudaMemsetAsync(g->d_in_src, 0, 4 * padded, st));
         if (owned_edges) k_low32<<<grid_e(owned_edges), kBlock, 0, st>>>(kout, owned_edges, g->d_in_src);
         k_offsets<<<grid_e(owned_edges + 1), kBlock, 0, st>>>(kout, owned_edges, owned, g->d_in_off);
+        k_fill_u64<<<1, 32, 0, st>>>(g->d_in_off + owned + 1, kOffPad, owned_edges);
         if (w) {
-            GXB_CHECK(dalloc_t(&g->d_in_w, owned_edges));
+            GXB_CHECK(dalloc_t(&g->d_in_w, padded));
+            GXB_CUDA(cudaMemsetAsync(g->d_in_w, 0, 4 * padded, st));
             if (owned_edges)
                 GXB_CUDA(cudaMemcpyAsync(g->d_in_w, vout, 4 * owned_edges, cudaMemcpyDeviceToDevice, st));
         }
@@ -481,6 +571,7 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
     }
     GXB_CUDA(cudaGetLastError());
     GXB_CHECK(build_pull_plan(g, st));
+    GXB_CHECK(build_tile_plan(g, st));
     return GXB_OK;
 }
 
