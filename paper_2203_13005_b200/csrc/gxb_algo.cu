@@ -53,7 +53,8 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
     __device__ static Acc ld_cg(const Acc* p) { return {__ldcg(&p->s)}; }
     __device__ static bool has(const Acc&) { return true; }
     // Gen: rank / out_deg of the source (every vertex is active, 144-145)
-    __device__ bool gen(uint32_t s, uint64_t, const uint32_t*, Msg& m) const {
+    static constexpr bool kWeighted = false;
+    __device__ bool gen(uint32_t s, uint32_t, Msg& m) const {
         m = ld_keep_f64(contrib_cur + s, l2_evict_last());
         return true;
     }
@@ -81,57 +82,45 @@ __device__ __forceinline__ bool eq4(uint4 a, uint4 b) {
 }
 
 struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-122)
+    // The accumulator is the lane-wise min; "received a message" <=> some lane is
+    // finite: a message comes from an active source, which always holds a finite
+    // lane (it changed, or is a source at 0), and the host rejects weights for
+    // which d + w could saturate (max_w * |V| >= 2^32 - 1), so no finite sum
+    // ever reaches the INF sentinel.
     struct Acc {
         uint4 m;
-        uint32_t has;
     };
     using Msg = uint4;
     const uint4* dist_cur;
     uint4* dist_next;
     const uint32_t* active_cur;
     FrontierView f;
+    static constexpr bool kWeighted = true;
 
-    __device__ static Acc identity() { return {make_uint4(kInf32, kInf32, kInf32, kInf32), 0u}; }
-    __device__ static Acc combine(Acc a, Acc b) { return {min4(a.m, b.m), a.has | b.has}; }
+    __device__ static Acc identity() { return {make_uint4(kInf32, kInf32, kInf32, kInf32)}; }
+    __device__ static Acc combine(Acc a, Acc b) { return {min4(a.m, b.m)}; }
     __device__ static Acc shfl(Acc a, int off) {
-        Acc r;
-        r.m.x = __shfl_xor_sync(kFull, a.m.x, off);
-        r.m.y = __shfl_xor_sync(kFull, a.m.y, off);
-        r.m.z = __shfl_xor_sync(kFull, a.m.z, off);
-        r.m.w = __shfl_xor_sync(kFull, a.m.w, off);
-        r.has = __shfl_xor_sync(kFull, a.has, off);
-        return r;
+        return {make_uint4(__shfl_xor_sync(kFull, a.m.x, off), __shfl_xor_sync(kFull, a.m.y, off),
+                           __shfl_xor_sync(kFull, a.m.z, off), __shfl_xor_sync(kFull, a.m.w, off))};
     }
     __device__ static Acc shfl_up(Acc a, int d) {
-        Acc r;
-        r.m.x = __shfl_up_sync(kFull, a.m.x, d);
-        r.m.y = __shfl_up_sync(kFull, a.m.y, d);
-        r.m.z = __shfl_up_sync(kFull, a.m.z, d);
-        r.m.w = __shfl_up_sync(kFull, a.m.w, d);
-        r.has = __shfl_up_sync(kFull, a.has, d);
-        return r;
+        return {make_uint4(__shfl_up_sync(kFull, a.m.x, d), __shfl_up_sync(kFull, a.m.y, d),
+                           __shfl_up_sync(kFull, a.m.z, d), __shfl_up_sync(kFull, a.m.w, d))};
     }
-    __device__ static void st_cg(Acc* p, Acc a) {
-        __stcg(&p->m, a.m);
-        __stcg(&p->has, a.has);
-    }
-    __device__ static Acc ld_cg(const Acc* p) { return {__ldcg(&p->m), __ldcg(&p->has)}; }
-    __device__ static bool has(const Acc& a) { return a.has != 0; }
+    __device__ static void st_cg(Acc* p, Acc a) { __stcg(&p->m, a.m); }
+    __device__ static Acc ld_cg(const Acc* p) { return {__ldcg(&p->m)}; }
+    __device__ static bool has(const Acc& a) { return (a.m.x & a.m.y & a.m.z & a.m.w) != kInf32; }
     // Gen: d + w per lane from an active source (102-105); inf stays inf
-    __device__ bool gen(uint32_t s, uint64_t e, const uint32_t* w, Msg& m) const {
+    __device__ bool gen(uint32_t s, uint32_t w, Msg& m) const {
         if (!bit_test(active_cur, s)) return false;
         const uint4 d = ld_keep_v4(dist_cur + s, l2_evict_last());
-        const uint32_t ww = w ? ld_stream_u32(w + e, l2_evict_first()) : 1u;
-        m = make_uint4(sat_add(d.x, ww), sat_add(d.y, ww), sat_add(d.z, ww), sat_add(d.w, ww));
+        m = make_uint4(sat_add(d.x, w), sat_add(d.y, w), sat_add(d.z, w), sat_add(d.w, w));
         return true;
     }
-    __device__ static void fold(Acc& a, Msg m) {
-        a.m = min4(a.m, m);
-        a.has = 1u;
-    }
+    __device__ static void fold(Acc& a, Msg m) { a.m = min4(a.m, m); }
     // Apply: elementwise min, active iff changed (113-115)
     __device__ void apply(uint32_t slot, Acc a, LocalStats& st) const {
-        if (!a.has) return;
+        if (!has(a)) return;
         st.targets++;
         const uint4 o = dist_cur[slot];
         const uint4 n = min4(o, a.m);
@@ -142,42 +131,32 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
     }
 };
 
-struct CcOps {  // min-label propagation
+struct CcOps {  // min-label propagation; labels < 0xFFFFFFFF
     struct Acc {
         uint32_t m;
-        uint32_t has;
     };
     using Msg = uint32_t;
     const uint32_t* lab_cur;
     uint32_t* lab_next;
     const uint32_t* active_cur;
     FrontierView f;
+    static constexpr bool kWeighted = false;
 
-    __device__ static Acc identity() { return {kInf32, 0u}; }
-    __device__ static Acc combine(Acc a, Acc b) { return {min(a.m, b.m), a.has | b.has}; }
-    __device__ static Acc shfl(Acc a, int off) {
-        return {__shfl_xor_sync(kFull, a.m, off), __shfl_xor_sync(kFull, a.has, off)};
-    }
-    __device__ static Acc shfl_up(Acc a, int d) {
-        return {__shfl_up_sync(kFull, a.m, d), __shfl_up_sync(kFull, a.has, d)};
-    }
-    __device__ static void st_cg(Acc* p, Acc a) {
-        __stcg(&p->m, a.m);
-        __stcg(&p->has, a.has);
-    }
-    __device__ static Acc ld_cg(const Acc* p) { return {__ldcg(&p->m), __ldcg(&p->has)}; }
-    __device__ static bool has(const Acc& a) { return a.has != 0; }
-    __device__ bool gen(uint32_t s, uint64_t, const uint32_t*, Msg& m) const {
+    __device__ static Acc identity() { return {kInf32}; }
+    __device__ static Acc combine(Acc a, Acc b) { return {min(a.m, b.m)}; }
+    __device__ static Acc shfl(Acc a, int off) { return {__shfl_xor_sync(kFull, a.m, off)}; }
+    __device__ static Acc shfl_up(Acc a, int d) { return {__shfl_up_sync(kFull, a.m, d)}; }
+    __device__ static void st_cg(Acc* p, Acc a) { __stcg(&p->m, a.m); }
+    __device__ static Acc ld_cg(const Acc* p) { return {__ldcg(&p->m)}; }
+    __device__ static bool has(const Acc& a) { return a.m != kInf32; }
+    __device__ bool gen(uint32_t s, uint32_t, Msg& m) const {
         if (!bit_test(active_cur, s)) return false;
         m = ld_keep_u32(lab_cur + s, l2_evict_last());
         return true;
     }
-    __device__ static void fold(Acc& a, Msg m) {
-        a.m = min(a.m, m);
-        a.has = 1u;
-    }
+    __device__ static void fold(Acc& a, Msg m) { a.m = min(a.m, m); }
     __device__ void apply(uint32_t slot, Acc a, LocalStats& st) const {
-        if (!a.has) return;
+        if (!has(a)) return;
         st.targets++;
         const uint32_t o = lab_cur[slot];
         const uint32_t n = min(o, a.m);
@@ -200,7 +179,12 @@ struct FusedPolicy {  // Gen∘Merge∘Apply
     using Acc = typename Ops::Acc;
     __device__ void accumulate(Acc& a, uint32_t s, uint64_t e) const {
         typename Ops::Msg m;
-        if (ops.gen(s, e, in_w, m)) Ops::fold(a, m);
+        const uint32_t w = (Ops::kWeighted && in_w) ? __ldg(in_w + e) : 1u;
+        if (ops.gen(s, w, m)) Ops::fold(a, m);
+    }
+    __device__ void accumulate_w(Acc& a, uint32_t s, uint32_t w) const {
+        typename Ops::Msg m;
+        if (ops.gen(s, w, m)) Ops::fold(a, m);
     }
     __device__ void finish(uint32_t slot, Acc a, LocalStats& st) const { ops.apply(slot, a, st); }
 };
@@ -371,6 +355,8 @@ struct TileLaunch {
     const uint64_t* in_off;
     const uint32_t* in_src;
     const uint32_t* lane_slot;
+    const uint8_t* lane_mask;
+    const uint32_t* in_w;
     const uint32_t* tile_head;
     const uint32_t* tile_tail;
     const uint32_t* span_first;
@@ -400,52 +386,58 @@ __device__ __forceinline__ void tile_emit(const Pol& p, const TileLaunch& L, uin
     }
 }
 
+__device__ __forceinline__ uint8_t ld_stream_u8(const uint8_t* ptr, uint64_t pol) {
+    uint16_t r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(r) : "l"(ptr), "l"(pol));
+    return (uint8_t)r;
+}
+
 template <class Pol>
 __global__ void __launch_bounds__(kBlock) k_tile(const Pol p, const TileLaunch L) {
     using Ops = decltype(p.ops);
     using Acc = typename Ops::Acc;
+    constexpr bool kW = Ops::kWeighted;
     const int lane = threadIdx.x & 31;
     const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
     const uint64_t pol = l2_evict_first();
+    const bool weighted = kW && L.in_w != nullptr;
     uint64_t t = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
-    // software pipeline: the next tile's index vectors are in flight while this tile gathers
-    uint4 na = make_uint4(0, 0, 0, 0), nb = na;
-    if (t < L.num_tiles) {
-        const uint64_t e = t * kTileEdges + (uint64_t)lane * kTileK;
+    // software pipeline: the next tile's streams (indices, weights, lane tables)
+    // are in flight while this tile gathers
+    uint4 na = make_uint4(0, 0, 0, 0), nb = na, wa = make_uint4(1, 1, 1, 1), wb = wa;
+    uint32_t nsa = 0, nmask = 0;
+    auto prefetch = [&](uint64_t tt) {
+        const uint64_t e = tt * kTileEdges + (uint64_t)lane * kTileK;
         na = ld_stream_v4(L.in_src + e, pol);
         nb = ld_stream_v4(L.in_src + e + 4, pol);
-    }
+        if (weighted) {
+            wa = ld_stream_v4(L.in_w + e, pol);
+            wb = ld_stream_v4(L.in_w + e + 4, pol);
+        }
+        nsa = ld_stream_u32(L.lane_slot + tt * 32 + lane, pol);
+        nmask = ld_stream_u8(L.lane_mask + tt * 32 + lane, pol);
+    };
+    if (t < L.num_tiles) prefetch(t);
     for (; t < L.num_tiles; t += nwarps) {
         const uint64_t e0 = t * kTileEdges + (uint64_t)lane * kTileK;
         const bool live = e0 < L.owned_edges;
         const uint32_t src[kTileK] = {na.x, na.y, na.z, na.w, nb.x, nb.y, nb.z, nb.w};
-        const uint32_t sa = live ? ld_stream_u32(L.lane_slot + t * 32 + lane, pol) : 0u;
-        const uint64_t tn = t + nwarps;
-        if (tn < L.num_tiles) {
-            const uint64_t e = tn * kTileEdges + (uint64_t)lane * kTileK;
-            na = ld_stream_v4(L.in_src + e, pol);
-            nb = ld_stream_v4(L.in_src + e + 4, pol);
-        }
+        const uint32_t wgt[kTileK] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+        const uint32_t sa = nsa;
+        uint32_t endmask = nmask;
+        if (t + nwarps < L.num_tiles) prefetch(t + nwarps);
         // Gen: kTileK independent gathers
         Acc v[kTileK];
 #pragma unroll
         for (int j = 0; j < kTileK; ++j) {
             v[j] = Ops::identity();
-            if (e0 + j < L.owned_edges) p.accumulate(v[j], src[j], e0 + j);
-        }
-        // run ends inside the lane: bit j set <=> a destination segment ends at edge e0 + j
-        uint32_t endmask = 0;
-#pragma unroll
-        for (int m = 0; m < kTileK; ++m) {
-            const uint64_t b = __ldg(L.in_off + sa + 1 + m);
-            const uint64_t r = b - e0;  // wraps for b < e0 (cannot happen: b > e0 for the slot of e0)
-            if (r >= 1 && r <= (uint64_t)kTileK) endmask |= 1u << (uint32_t)(r - 1);
+            if (e0 + j < L.owned_edges) p.accumulate_w(v[j], src[j], wgt[j]);
         }
         const uint32_t nvalid = live ? (uint32_t)min((uint64_t)kTileK, L.owned_edges - e0) : 0u;
-        endmask &= (1u << nvalid) - 1u;          // ends past the valid edges do not exist
-        endmask &= ~(1u << (kTileK - 1));        // the final position is handled as the last run
-        uint32_t fkey = kNone, lkey = kNone;
-        Acc fval = Ops::identity(), lval = Ops::identity();
+        endmask &= (1u << nvalid) - 1u;      // no segment ends past the valid edges
+        endmask &= ~(1u << (kTileK - 1));    // the final position is handled as the last run
+        uint32_t fkey = kNone;
+        Acc fval = Ops::identity();
         const bool multi = endmask != 0;
         Acc acc = Ops::identity();
         uint32_t key = sa;
@@ -465,8 +457,8 @@ __global__ void __launch_bounds__(kBlock) k_tile(const Pol p, const TileLaunch L
                 acc = Ops::identity();
             }
         }
-        lkey = live ? key : kNone;
-        lval = acc;
+        const uint32_t lkey = live ? key : kNone;
+        const Acc lval = acc;
         if (!multi) {
             fkey = lkey;
             fval = lval;
@@ -482,12 +474,12 @@ __global__ void __launch_bounds__(kBlock) k_tile(const Pol p, const TileLaunch L
         const uint32_t prev_key = __shfl_up_sync(kFull, lkey, 1);
         const Acc prev_c = Ops::shfl_up(c, 1);
         const uint32_t next_first = __shfl_down_sync(kFull, fkey, 1);
-        const uint32_t head = __ldg(L.tile_head + t), tail = __ldg(L.tile_tail + t);
         if (multi && live) {
             const Acc tot = (lane > 0 && prev_key == fkey) ? Ops::combine(prev_c, fval) : fval;
-            tile_emit(p, L, t, head, tail, fkey, tot);
+            tile_emit(p, L, t, __ldg(L.tile_head + t), __ldg(L.tile_tail + t), fkey, tot);
         }
-        if (lkey != kNone && (lane == 31 || next_first != lkey)) tile_emit(p, L, t, head, tail, lkey, c);
+        if (lkey != kNone && (lane == 31 || next_first != lkey))
+            tile_emit(p, L, t, __ldg(L.tile_head + t), __ldg(L.tile_tail + t), lkey, c);
     }
 }
 
@@ -618,7 +610,8 @@ __global__ void k_gen(const Ops ops, const uint32_t* __restrict__ in_src, const 
     for (uint64_t e = elo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < ehi;
          e += (uint64_t)gridDim.x * blockDim.x) {
         typename Ops::Msg m;
-        const bool ok = ops.gen(__ldg(in_src + e), e, in_w, m);
+        const uint32_t w = (Ops::kWeighted && in_w) ? __ldg(in_w + e) : 1u;
+        const bool ok = ops.gen(__ldg(in_src + e), w, m);
         if (ok) msg[e] = m;
         valid[e] = ok ? 1 : 0;
     }
@@ -760,6 +753,8 @@ TileLaunch tile_launch(gxb_state* s) {
     L.in_off = g->d_in_off;
     L.in_src = g->d_in_src;
     L.lane_slot = T.d_lane_slot;
+    L.lane_mask = T.d_lane_mask;
+    L.in_w = g->d_in_w;
     L.tile_head = T.d_tile_head;
     L.tile_tail = T.d_tile_tail;
     L.span_first = T.d_span_first;
@@ -991,6 +986,9 @@ int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, 
             for (uint64_t i = 0; i < V && i < 4; ++i) src_ids.push_back(by_id[i].first);
         }
         if (src_ids.empty()) return bail(fail(GXB_EINVAL, "sssp needs at least one source vertex"));
+        // exact u32 arithmetic: no message d + w may reach the INF sentinel
+        if ((unsigned __int128)g->max_w * V >= 0xFFFFFFFFull)
+            return bail(fail(GXB_ERANGE, "edge weights too large for exact 32-bit distances (max_w * |V| >= 2^32-1)"));
         s->nsrc = (int)src_ids.size();
         s->arity = s->nsrc;
         if ((rc = dalloc_t(&s->d_dist_cur, V)) != GXB_OK) return bail(rc);

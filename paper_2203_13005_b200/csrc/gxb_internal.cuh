@@ -57,6 +57,7 @@ struct TilePlan {
     uint64_t num_spans = 0;      // slots whose edges cross a tile boundary
     uint64_t num_partials = 0;   // sum of tiles touched by spans
     uint32_t* d_lane_slot = nullptr;   // per kTileK-edge lane chunk: slot of its first edge
+    uint8_t* d_lane_mask = nullptr;    // per lane chunk: bit j <=> edge kTileK*c + j closes its segment
     uint32_t* d_tile_head = nullptr;   // per tile: span id of its first slot if that slot started earlier
     uint32_t* d_tile_tail = nullptr;   // per tile: span id of its last slot if that slot continues
     uint32_t* d_span_first = nullptr;  // per span: first tile
@@ -107,6 +108,7 @@ struct gxb_graph {
     uint64_t V = 0, E = 0;
     uint32_t max_id = 0;
     uint32_t max_in_degree = 0;
+    uint32_t max_w = 0;                 // largest edge weight (1 when unweighted)
     int part = 0, nparts = 1;
     uint64_t lo = 0, hi = 0;            // owned slot range
     uint64_t owned_edges = 0, owned_out_edges = 0;

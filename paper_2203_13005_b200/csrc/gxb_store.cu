@@ -181,8 +181,10 @@ __global__ void k_fill_u64(uint64_t* a, uint64_t n, uint64_t v) {
     for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) a[i] = v;
 }
 
-// lane-chunk table of the warp tiles: slot (relative) containing edge kTileK * c
-__global__ void k_lane_slot(const uint64_t* __restrict__ off, uint64_t nz, uint64_t nchunks, uint32_t* out) {
+// lane-chunk tables of the warp tiles: slot (relative) containing edge kTileK * c,
+// and the bitmask of the chunk's positions that close a destination segment
+__global__ void k_lane_slot(const uint64_t* __restrict__ off, uint64_t nz, uint64_t nchunks, uint32_t* out,
+                            uint8_t* mask) {
     for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nchunks;
          c += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t e = c * kTileK;
@@ -192,6 +194,12 @@ __global__ void k_lane_slot(const uint64_t* __restrict__ off, uint64_t nz, uint6
             if (off[mid] <= e) lo = mid; else hi = mid;
         }
         out[c] = (uint32_t)lo;
+        uint32_t m = 0;
+        for (int k = 1; k <= kTileK; ++k) {  // every in-degree >= 1 here: at most kTileK ends
+            const uint64_t b = (lo + k <= nz) ? off[lo + k] : ~0ull;
+            if (b > e && b <= e + kTileK) m |= 1u << (uint32_t)(b - e - 1);
+        }
+        mask[c] = (uint8_t)m;
     }
 }
 
@@ -282,6 +290,7 @@ static void graph_release(gxb_graph* g) {
     dfree(g->plan.d_item_count);
     dfree(g->plan.d_slot_arrive);
     dfree(g->tiles.d_lane_slot);
+    dfree(g->tiles.d_lane_mask);
     dfree(g->tiles.d_tile_head);
     dfree(g->tiles.d_tile_tail);
     dfree(g->tiles.d_span_first);
@@ -302,8 +311,10 @@ static int build_tile_plan(gxb_graph* g, cudaStream_t st) {
     T.nz_slots = nz;
     T.num_tiles = (g->owned_edges + kTileEdges - 1) / kTileEdges;
     const uint64_t nchunks = T.num_tiles * 32;
-    GXB_CHECK(dalloc_t(&T.d_lane_slot, nchunks + 1));
-    if (nchunks) k_lane_slot<<<grid_e(nchunks), kBlock, 0, st>>>(g->d_in_off, nz, nchunks, T.d_lane_slot);
+    GXB_CHECK(dalloc_t(&T.d_lane_slot, nchunks + 32));
+    GXB_CHECK(dalloc_t(&T.d_lane_mask, nchunks + 32));
+    if (nchunks)
+        k_lane_slot<<<grid_e(nchunks), kBlock, 0, st>>>(g->d_in_off, nz, nchunks, T.d_lane_slot, T.d_lane_mask);
     std::vector<uint32_t> head(T.num_tiles + 1, kNone), tail(T.num_tiles + 1, kNone);
     std::vector<uint32_t> sfirst, scount, sslot;
     std::vector<uint64_t> spbase;
@@ -414,6 +425,16 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
     if (w_in) {
         GXB_CHECK(S.get(&w, E));
         GXB_CUDA(cudaMemcpyAsync(w, w_in, 4 * E, kind, st));
+    }
+    // largest weight (the SSSP state checks max_w * |V| < 2^32 - 1 for exact u32 sums)
+    if (w && E) {
+        uint32_t* d_wmax = nullptr;
+        GXB_CHECK(S.get(&d_wmax, 1));
+        GXB_CUDA(cudaMemsetAsync(d_wmax, 0, 4, st));
+        k_max_id<<<grid_e(E), kBlock, 0, st>>>(w, w, E, d_wmax);
+        GXB_CUDA(cudaMemcpyAsync(&g->max_w, d_wmax, 4, cudaMemcpyDeviceToHost, st));
+    } else {
+        g->max_w = E ? 1u : 0u;
     }
     // present ids
     uint32_t* d_max = nullptr;

@@ -192,9 +192,9 @@ class DeviceState:
                     raise ValueError("sssp needs at least one source vertex")
                 if nsrc > 4:
                     raise ValueError("the device SSSP carries at most 4 sources per run")
-            # u32 distances are exact iff no shortest path can reach 2^32-1
-            if max_weight is not None and graph.num_vertices > 1 and \
-                    max_weight * (graph.num_vertices - 1) >= U32_MAX:
+            # u32 distances are exact iff no message d + w can reach 2^32-1 (the
+            # library re-checks this against the stored weights)
+            if max_weight is not None and max_weight * graph.num_vertices >= U32_MAX:
                 raise ValueError("edge weights too large for exact 32-bit distances")
         h = ctypes.c_void_p()
         L.check(L.lib().gxb_state_create(graph.handle, ALGO_IDS[algo], _vp(srcs), nsrc, ctypes.byref(h)))
