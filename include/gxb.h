@@ -121,6 +121,12 @@ int gxb_reinit(gxb_ctx* ctx);                       /* always GXB_EPROTO (A/daem
 int gxb_init_count(const gxb_ctx* ctx, int* out);
 int gxb_shutdown(gxb_ctx* ctx);                     /* idempotent (A/daemon.py:163-168) */
 
+/* ---- tuning knobs (process-wide): "tile_minblocks" (0/4/6/8), "l2_hot_mb",
+ * "push_alpha" (push when frontier out-edges * alpha < |E|), "pull_kernel"
+ * (0 = edge-balanced warp tiles, 1 = degree-binned groups) ---- */
+int gxb_set_option(const char* name, int64_t value);
+int gxb_get_option(const char* name, int64_t* value);
+
 /* ---- device R-MAT ingest ---- */
 /* Fills device arrays src/dst[/w] (num = gxb_rmat_num_edges) on `stream`. */
 int gxb_rmat_generate(gxb_ctx* ctx, const gxb_rmat_args* args, uint32_t* d_src,

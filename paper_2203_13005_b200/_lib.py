@@ -73,6 +73,8 @@ def _sig(L):
         "gxb_reinit": (I, [P]),
         "gxb_init_count": (I, [P, ctypes.POINTER(I)]),
         "gxb_shutdown": (I, [P]),
+        "gxb_set_option": (I, [ctypes.c_char_p, ctypes.c_int64]),
+        "gxb_get_option": (I, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64)]),
         "gxb_rmat_generate": (I, [P, ctypes.POINTER(RmatArgs), P, P, P, P]),
         "gxb_graph_build": (I, [P, P, P, P, U64, I, I, U32, P, PP]),
         "gxb_graph_get_info": (I, [P, ctypes.POINTER(GraphInfo)]),
@@ -115,6 +117,16 @@ def lib():
         _sig(L)
         _lib = L
     return _lib
+
+
+def set_option(name: str, value: int) -> None:
+    check(lib().gxb_set_option(name.encode(), int(value)))
+
+
+def get_option(name: str) -> int:
+    v = ctypes.c_int64()
+    check(lib().gxb_get_option(name.encode(), ctypes.byref(v)))
+    return v.value
 
 
 def check(rc: int) -> int:

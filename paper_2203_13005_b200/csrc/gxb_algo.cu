@@ -44,6 +44,8 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
     double* rank;
     double* contrib_next;
     FrontierView f;
+    uint32_t hot;  // slots [0, hot) keep L2 priority (degree-sorted: the most-gathered sources)
+    uint32_t hot1; // slots [0, hot1) also allocate in L1; the rest bypass L1
 
     __device__ static Acc identity() { return {0.0}; }
     __device__ static Acc combine(Acc a, Acc b) { return {a.s + b.s}; }
@@ -55,7 +57,8 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
     // Gen: rank / out_deg of the source (every vertex is active, 144-145)
     static constexpr bool kWeighted = false;
     __device__ bool gen(uint32_t s, uint32_t, Msg& m) const {
-        m = ld_keep_f64(contrib_cur + s, l2_evict_last());
+        const uint64_t pol = s < hot ? l2_evict_last() : l2_evict_first();
+        m = s < hot1 ? ld_l1_f64(contrib_cur + s, pol) : ld_nol1_f64(contrib_cur + s, pol);
         return true;
     }
     __device__ static void fold(Acc& a, Msg m) { a.s += m; }
@@ -95,6 +98,7 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
     uint4* dist_next;
     const uint32_t* active_cur;
     FrontierView f;
+    uint32_t hot, hot1;
     static constexpr bool kWeighted = true;
 
     __device__ static Acc identity() { return {make_uint4(kInf32, kInf32, kInf32, kInf32)}; }
@@ -113,7 +117,8 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
     // Gen: d + w per lane from an active source (102-105); inf stays inf
     __device__ bool gen(uint32_t s, uint32_t w, Msg& m) const {
         if (!bit_test(active_cur, s)) return false;
-        const uint4 d = ld_keep_v4(dist_cur + s, l2_evict_last());
+        const uint64_t pol = s < hot ? l2_evict_last() : l2_evict_first();
+        const uint4 d = s < hot1 ? ld_l1_v4(dist_cur + s, pol) : ld_nol1_v4(dist_cur + s, pol);
         m = make_uint4(sat_add(d.x, w), sat_add(d.y, w), sat_add(d.z, w), sat_add(d.w, w));
         return true;
     }
@@ -140,6 +145,7 @@ struct CcOps {  // min-label propagation; labels < 0xFFFF
     uint32_t* lab_next;
     const uint32_t* active_cur;
     FrontierView f;
+    uint32_t hot, hot1;
     static constexpr bool kWeighted = false;
 
     __device__ static Acc identity() { return {kInf32}; }
@@ -151,7 +157,8 @@ struct CcOps {  // min-label propagation; labels < 0xFFFF
     __device__ static bool has(const Acc& a) { return a.m != kInf32; }
     __device__ bool gen(uint32_t s, uint32_t, Msg& m) const {
         if (!bit_test(active_cur, s)) return false;
-        m = ld_keep_u32(lab_cur + s, l2_evict_last());
+        const uint64_t pol = s < hot ? l2_evict_last() : l2_evict_first();
+        m = s < hot1 ? ld_l1_u32(lab_cur + s, pol) : ld_nol1_u32(lab_cur + s, pol);
         return true;
     }
     __device__ static void fold(Acc& a, Msg m) { a.m = min(a.m, m); }
@@ -392,8 +399,8 @@ __device__ __forceinline__ uint8_t ld_stream_u8(const uint8_t* ptr, uint64_t pol
     return (uint8_t)r;
 }
 
-template <class Pol>
-__global__ void __launch_bounds__(kBlock) k_tile(const Pol p, const TileLaunch L) {
+template <class Pol, int kMinBlocks>
+__global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile(const Pol p, const TileLaunch L) {
     using Ops = decltype(p.ops);
     using Acc = typename Ops::Acc;
     constexpr bool kW = Ops::kWeighted;
@@ -464,6 +471,120 @@ __global__ void __launch_bounds__(kBlock) k_tile(const Pol p, const TileLaunch L
             fval = lval;
         }
         // segmented inclusive scan of the lanes' last runs (keys are monotone)
+        Acc c = lval;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const Acc up = Ops::shfl_up(c, d);
+            const uint32_t k = __shfl_up_sync(kFull, lkey, d);
+            if (lane >= d && k == lkey) c = Ops::combine(up, c);
+        }
+        const uint32_t prev_key = __shfl_up_sync(kFull, lkey, 1);
+        const Acc prev_c = Ops::shfl_up(c, 1);
+        const uint32_t next_first = __shfl_down_sync(kFull, fkey, 1);
+        if (multi && live) {
+            const Acc tot = (lane > 0 && prev_key == fkey) ? Ops::combine(prev_c, fval) : fval;
+            tile_emit(p, L, t, __ldg(L.tile_head + t), __ldg(L.tile_tail + t), fkey, tot);
+        }
+        if (lkey != kNone && (lane == 31 || next_first != lkey))
+            tile_emit(p, L, t, __ldg(L.tile_head + t), __ldg(L.tile_tail + t), lkey, c);
+    }
+}
+
+// Transposed variant: lane l gathers edges e_tile + 32 j + l (j < kTileK), so one
+// gather instruction covers 32 CONSECUTIVE edges. Inside a high-degree segment the
+// sources are sorted, and in the degree-sorted hot prefix consecutive sources sit
+// in the same 32-byte sectors: L1 merges those lanes into one L2 request. The
+// values are transposed through shared memory (row padding 1 per kTileK keeps
+// both sides bank-friendly) and then folded by the same per-lane run logic.
+__device__ __forceinline__ uint32_t tpos(uint32_t p) { return p + (p >> 3); }
+
+template <class Pol, int kMinBlocks>
+__global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_t(const Pol p, const TileLaunch L) {
+    using Ops = decltype(p.ops);
+    using Acc = typename Ops::Acc;
+    constexpr bool kW = Ops::kWeighted;
+    constexpr uint32_t kRow = kTileEdges + kTileEdges / kTileK;
+    __shared__ Acc sbuf[kBlock / 32][kRow];
+    const int lane = threadIdx.x & 31;
+    Acc* buf = sbuf[threadIdx.x >> 5];
+    const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
+    const uint64_t pol = l2_evict_first();
+    const bool weighted = kW && L.in_w != nullptr;
+    uint64_t t = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+    uint32_t nidx[kTileK], nw[kTileK];
+    uint32_t nsa = 0, nmask = 0;
+#pragma unroll
+    for (int j = 0; j < kTileK; ++j) {
+        nidx[j] = 0;
+        nw[j] = 1;
+    }
+    auto prefetch = [&](uint64_t tt) {
+        const uint64_t e = tt * kTileEdges + (uint64_t)lane;
+#pragma unroll
+        for (int j = 0; j < kTileK; ++j) nidx[j] = ld_stream_u32(L.in_src + e + 32 * j, pol);
+        if (weighted) {
+#pragma unroll
+            for (int j = 0; j < kTileK; ++j) nw[j] = ld_stream_u32(L.in_w + e + 32 * j, pol);
+        }
+        nsa = ld_stream_u32(L.lane_slot + tt * 32 + lane, pol);
+        nmask = ld_stream_u8(L.lane_mask + tt * 32 + lane, pol);
+    };
+    if (t < L.num_tiles) prefetch(t);
+    for (; t < L.num_tiles; t += nwarps) {
+        const uint64_t et = t * kTileEdges;
+        uint32_t idx[kTileK], wgt[kTileK];
+#pragma unroll
+        for (int j = 0; j < kTileK; ++j) {
+            idx[j] = nidx[j];
+            wgt[j] = nw[j];
+        }
+        const uint32_t sa = nsa;
+        uint32_t endmask = nmask;
+        if (t + nwarps < L.num_tiles) prefetch(t + nwarps);
+        // Gen: coalesced gathers of 32 consecutive edges per instruction
+#pragma unroll
+        for (int j = 0; j < kTileK; ++j) {
+            Acc v = Ops::identity();
+            if (et + 32 * j + lane < L.owned_edges) p.accumulate_w(v, idx[j], wgt[j]);
+            buf[tpos(32 * j + lane)] = v;
+        }
+        __syncwarp();
+        const uint64_t e0 = et + (uint64_t)lane * kTileK;
+        const bool live = e0 < L.owned_edges;
+        Acc v[kTileK];
+#pragma unroll
+        for (int j = 0; j < kTileK; ++j) v[j] = buf[tpos(kTileK * lane + j)];
+        __syncwarp();
+        const uint32_t nvalid = live ? (uint32_t)min((uint64_t)kTileK, L.owned_edges - e0) : 0u;
+        endmask &= (1u << nvalid) - 1u;
+        endmask &= ~(1u << (kTileK - 1));
+        uint32_t fkey = kNone;
+        Acc fval = Ops::identity();
+        const bool multi = endmask != 0;
+        Acc acc = Ops::identity();
+        uint32_t key = sa;
+        bool first = true;
+#pragma unroll
+        for (int j = 0; j < kTileK; ++j) {
+            acc = Ops::combine(acc, v[j]);
+            if ((endmask >> j) & 1u) {
+                if (first) {
+                    fkey = key;
+                    fval = acc;
+                    first = false;
+                } else {
+                    reinterpret_cast<Acc*>(L.sums)[key] = acc;
+                }
+                ++key;
+                acc = Ops::identity();
+            }
+        }
+        const uint32_t lkey = live ? key : kNone;
+        const Acc lval = acc;
+        if (!multi) {
+            fkey = lkey;
+            fval = lval;
+        }
         Acc c = lval;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -772,16 +893,22 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st) {
     const gxb_graph* g = s->g;
     const TileLaunch L = tile_launch(s);
     FusedPolicy<Ops> p{ops, g->d_in_w};
-    static int max_blocks = 0;
-    if (!max_blocks) {
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<FusedPolicy<Ops>>, kBlock, 0);
-        max_blocks = std::max(1, per_sm) * kNumSMs;
-    }
+    const int variant = (int)options().tile_minblocks;
+    using Pol = FusedPolicy<Ops>;
+    void (*kern)(const Pol, const TileLaunch);
+    if (options().tile_layout == 1)
+        kern = (variant == 8) ? k_tile<Pol, 8> : (variant == 6) ? k_tile<Pol, 6>
+             : (variant == 4) ? k_tile<Pol, 4> : k_tile<Pol, 1>;
+    else
+        kern = (variant == 8) ? k_tile_t<Pol, 8> : (variant == 6) ? k_tile_t<Pol, 6>
+             : (variant == 4) ? k_tile_t<Pol, 4> : k_tile_t<Pol, 1>;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, 0);
+    const int max_blocks = std::max(1, per_sm) * kNumSMs;
     if (L.num_tiles) {
         const uint64_t want = (L.num_tiles + (kBlock / 32) - 1) / (kBlock / 32);
         const unsigned grid = (unsigned)std::min<uint64_t>(want, (uint64_t)max_blocks);
-        k_tile<FusedPolicy<Ops>><<<grid, kBlock, 0, st>>>(p, L);
+        kern<<<grid, kBlock, 0, st>>>(p, L);
         const TilePlan& T = g->tiles;
         if (T.num_spans)
             k_span_fold<Ops><<<grid_for(T.num_spans), kBlock, 0, st>>>(
@@ -795,13 +922,17 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st) {
     return GXB_OK;
 }
 
-bool use_binned_pull() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("GXB_PULL_KERNEL");
-        v = (e && std::string(e) == "binned") ? 1 : 0;
-    }
-    return v == 1;
+bool use_binned_pull() { return options().pull_kernel == 1; }
+
+// L2 budget for the gathered value prefix (GXB_L2_HOT_MB, default 64 of the 126 MB)
+uint32_t hot_slots(const gxb_state* s, size_t bytes_per_slot) {
+    const uint64_t n = ((uint64_t)options().l2_hot_mb << 20) / bytes_per_slot;
+    return (uint32_t)std::min<uint64_t>(n, s->g->V);
+}
+
+uint32_t hot_l1_slots(const gxb_state* s, size_t bytes_per_slot) {
+    const uint64_t n = ((uint64_t)options().l1_hot_kb << 10) / bytes_per_slot;
+    return (uint32_t)std::min<uint64_t>(n, s->g->V);
 }
 
 PrOps pr_ops(gxb_state* s) {
@@ -810,6 +941,8 @@ PrOps pr_ops(gxb_state* s) {
     o.rank = s->d_rank;
     o.contrib_next = s->d_contrib[s->cur ^ 1];
     o.f = frontier_view(s);
+    o.hot = hot_slots(s, sizeof(double));
+    o.hot1 = hot_l1_slots(s, sizeof(double));
     return o;
 }
 SsspOps sssp_ops(gxb_state* s) {
@@ -818,6 +951,8 @@ SsspOps sssp_ops(gxb_state* s) {
     o.dist_next = s->d_dist_next;
     o.active_cur = s->d_active[0];
     o.f = frontier_view(s);
+    o.hot = hot_slots(s, sizeof(uint4));
+    o.hot1 = hot_l1_slots(s, sizeof(uint4));
     return o;
 }
 CcOps cc_ops(gxb_state* s) {
@@ -826,6 +961,8 @@ CcOps cc_ops(gxb_state* s) {
     o.lab_next = s->d_lab_next;
     o.active_cur = s->d_active[0];
     o.f = frontier_view(s);
+    o.hot = hot_slots(s, sizeof(uint32_t));
+    o.hot1 = hot_l1_slots(s, sizeof(uint32_t));
     return o;
 }
 
@@ -1113,7 +1250,7 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
     int dir = GXB_DIR_PULL;
     if (s->algo == GXB_ALGO_SSSP || s->algo == GXB_ALGO_CC) {
         if (direction == GXB_DIR_PUSH) dir = GXB_DIR_PUSH;
-        else if (direction == GXB_DIR_AUTO) dir = (s->units_cur * 20 < g->E) ? GXB_DIR_PUSH : GXB_DIR_PULL;
+        else if (direction == GXB_DIR_AUTO) dir = (s->units_cur * (uint64_t)options().push_alpha < g->E) ? GXB_DIR_PUSH : GXB_DIR_PULL;
         if (dir == GXB_DIR_PUSH && !g->has_csr) {
             if (direction == GXB_DIR_PUSH) return fail(GXB_EINVAL, "push requested but the graph has no CSR");
             dir = GXB_DIR_PULL;

@@ -184,6 +184,40 @@ __device__ __forceinline__ uint4 ld_keep_v4(const uint4* ptr, uint64_t pol) {
     return r;
 }
 
+// hottest prefix: keep in L1 as well (evict_last); the rest bypasses L1
+__device__ __forceinline__ double ld_l1_f64(const double* ptr, uint64_t pol) {
+    double r;
+    asm("ld.global.nc.L1::evict_last.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ld_nol1_f64(const double* ptr, uint64_t pol) {
+    double r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint4 ld_l1_v4(const uint4* ptr, uint64_t pol) {
+    uint4 r;
+    asm("ld.global.nc.L1::evict_last.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint4 ld_nol1_v4(const uint4* ptr, uint64_t pol) {
+    uint4 r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_l1_u32(const uint32_t* ptr, uint64_t pol) {
+    uint32_t r;
+    asm("ld.global.nc.L1::evict_last.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_nol1_u32(const uint32_t* ptr, uint64_t pol) {
+    uint32_t r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t sat_add(uint32_t d, uint32_t w) {
     const uint32_t s = d + w;
     return (s < d || d == kInf32) ? kInf32 : s;
@@ -197,5 +231,16 @@ inline unsigned grid_for(uint64_t n, int block = kBlock, uint64_t cap = 148ull *
 }
 
 int build_pull_plan(gxb_graph* g, cudaStream_t st);
+
+// runtime tuning knobs (gxb_set_option); defaults are the measured best on B200
+struct Options {
+    int64_t tile_minblocks = 0;   // __launch_bounds__ min-blocks variant of the tile kernel (0/4/6/8)
+    int64_t l2_hot_mb = 64;       // L2 budget (MB) of the evict-last prefix of gathered values
+    int64_t l1_hot_kb = 160;      // L1 budget (KB) of the L1-allocating prefix (others bypass L1)
+    int64_t push_alpha = 20;      // push when frontier out-edges * alpha < |E|
+    int64_t pull_kernel = 0;      // 0 = warp tiles, 1 = degree-binned groups
+    int64_t tile_layout = 0;      // 0 = transposed (coalesced gathers), 1 = lane-contiguous
+};
+Options& options();
 
 }  // namespace gxb

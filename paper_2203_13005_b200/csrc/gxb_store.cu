@@ -23,6 +23,19 @@ namespace gxb {
 
 static thread_local std::string g_last_error;
 
+Options& options() {
+    static Options o;
+    static bool init = false;
+    if (!init) {
+        init = true;
+        if (const char* e = getenv("GXB_TILE_MINBLOCKS")) o.tile_minblocks = atol(e);
+        if (const char* e = getenv("GXB_L2_HOT_MB")) o.l2_hot_mb = atol(e);
+        if (const char* e = getenv("GXB_PUSH_ALPHA")) o.push_alpha = atol(e);
+        if (const char* e = getenv("GXB_PULL_KERNEL")) o.pull_kernel = std::string(e) == "binned" ? 1 : 0;
+    }
+    return o;
+}
+
 void set_error(const std::string& msg) { g_last_error = msg; }
 int fail(int code, const std::string& msg) {
     g_last_error = msg;
@@ -629,6 +642,48 @@ int gxb_init(int device, gxb_ctx** out) {
     c->init_count = 1;  // Daemon.initialize runs exactly once (A/daemon.py:148-161)
     c->alive = true;
     *out = c;
+    return GXB_OK;
+}
+
+int gxb_set_option(const char* name, int64_t value) {
+    if (!name) return fail(GXB_EINVAL, "gxb_set_option: null name");
+    Options& o = options();
+    const std::string n(name);
+    if (n == "tile_minblocks") {
+        if (value != 0 && value != 4 && value != 6 && value != 8) return fail(GXB_EINVAL, "tile_minblocks: 0/4/6/8");
+        o.tile_minblocks = value;
+    } else if (n == "l2_hot_mb") {
+        if (value < 0) return fail(GXB_EINVAL, "l2_hot_mb must be >= 0");
+        o.l2_hot_mb = value;
+    } else if (n == "push_alpha") {
+        if (value < 0) return fail(GXB_EINVAL, "push_alpha must be >= 0");
+        o.push_alpha = value;
+    } else if (n == "l1_hot_kb") {
+        if (value < 0) return fail(GXB_EINVAL, "l1_hot_kb must be >= 0");
+        o.l1_hot_kb = value;
+    } else if (n == "tile_layout") {
+        if (value != 0 && value != 1) return fail(GXB_EINVAL, "tile_layout: 0 = transposed, 1 = contiguous");
+        o.tile_layout = value;
+    } else if (n == "pull_kernel") {
+        if (value != 0 && value != 1) return fail(GXB_EINVAL, "pull_kernel: 0 = tiles, 1 = binned");
+        o.pull_kernel = value;
+    } else {
+        return fail(GXB_EINVAL, "unknown option " + n);
+    }
+    return GXB_OK;
+}
+
+int gxb_get_option(const char* name, int64_t* value) {
+    if (!name || !value) return fail(GXB_EINVAL, "gxb_get_option: null argument");
+    Options& o = options();
+    const std::string n(name);
+    if (n == "tile_minblocks") *value = o.tile_minblocks;
+    else if (n == "l2_hot_mb") *value = o.l2_hot_mb;
+    else if (n == "push_alpha") *value = o.push_alpha;
+    else if (n == "pull_kernel") *value = o.pull_kernel;
+    else if (n == "tile_layout") *value = o.tile_layout;
+    else if (n == "l1_hot_kb") *value = o.l1_hot_kb;
+    else return fail(GXB_EINVAL, "unknown option " + n);
     return GXB_OK;
 }
 
