@@ -1,0 +1,436 @@
+"""Benchmark: GTEPS per BSP iteration of GX-Plug's MSGGen -> MSGMerge -> MSGApply
+path (+ mirror exchange) on synthetic R-MAT graphs, on N B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload pr-s26]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference        # CPU restatement of the reference path
+
+One step = one BSP iteration over the whole graph: Gen∘Merge∘Apply on every
+partition, the skip vote, the mirror exchange and the convergence verdict.
+value = edges processed per second by the whole job (GTEPS_E = E * K / time),
+timed with CUDA events on the launching stream, max over ranks. The graph
+(R-MAT, Graph500 parameters, edge factor 16, scrambled ids) is generated on the
+device from a fixed seed; its CSC (4.3 GB at scale 26) is far larger than L2,
+so no L2 flush is needed between steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "GTEPS/iteration (PageRank, SSSP, R-MAT) at 1/2/4/8 B200; % of HBM roofline"
+
+WORKLOADS = {
+    # name: (algo, scale, rmat overrides, iterations-per-run cap, config text)
+    "pr-s26": ("pagerank", 26, {}, None, "PageRank on R-MAT scale-26 (~1B edges) edge-partitioned over N B200"),
+    "sssp-s26": ("sssp", 26, {"wmax": 63}, None, "SSSP (Bellman-Ford, int weights 1..63) on R-MAT scale-26"),
+    "sssp-s22": ("sssp", 22, {"wmax": 63}, None, "SSSP (Bellman-Ford, int weights) on R-MAT scale-22 on 1 B200"),
+    "cc-s24": ("cc", 24, {"symmetric": True}, None, "Connected components (min-label) on R-MAT scale-24"),
+    "lp-s22": ("lp", 22, {"a": 0.65, "b": 0.15, "c": 0.15}, 15, "Label propagation on skewed R-MAT (a=0.65)"),
+    "pr-s16": ("pagerank", 16, {}, 10, "PageRank 10 iters on R-MAT scale-16 (config 1)"),
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def wait_first(self, timeout=10.0):
+        t = time.perf_counter()
+        while self.proc is not None and not self.lines and time.perf_counter() - t < timeout:
+            time.sleep(0.01)
+
+    def mark(self, start: bool):
+        if start:
+            self.t0 = time.perf_counter()
+        else:
+            self.t1 = time.perf_counter()
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", float("inf"))
+        inside = [ln for ts, ln in self.lines if t0 - 0.025 <= ts <= t1 + 0.025]
+        if not inside and self.lines:  # region shorter than the sampling period: nearest sample
+            mid = 0.5 * (t0 + t1)
+            inside = [min(self.lines, key=lambda x: abs(x[0] - mid))[1]]
+        for ln in inside:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------------------- CPU arm
+
+_CPU_GRAPHS = {}
+
+
+def cpu_graph(algo, scale, over, seed=1):
+    """R-MAT sample graph for the CPU restatement (cached per process)."""
+    key = (algo, scale, tuple(sorted(over.items())), seed)
+    if key not in _CPU_GRAPHS:
+        from oracle import oracle
+        from paper_2203_13005_b200.rmat import RmatParams
+        p = RmatParams(scale=scale, seed=seed, **over)
+        src, dst, w = oracle.rmat(p.scale, p.edge_factor, p.seed, p.a, p.b, p.c, p.wmax, p.scramble, p.symmetric)
+        _CPU_GRAPHS[key] = oracle.OracleGraph(src, dst, None if w is None else w.astype("float64"))
+    return _CPU_GRAPHS[key]
+
+
+def cpu_sample(algo, scale, over, iters, threads=0, seed=1):
+    """Time the CPU restatement of run_reference (oracle/, OpenMP, all host threads)."""
+    from oracle import oracle
+    g = cpu_graph(algo, scale, over, seed)
+    t = time.perf_counter()
+    r = g.run(algo, max_iterations=iters, nthreads=threads)
+    dt = time.perf_counter() - t
+    units = int(r.units.sum())
+    return dict(seconds=dt, iterations=r.iterations, edges=g.num_edges, units=units,
+                gteps=g.num_edges * r.iterations / dt / 1e9, threads=threads or oracle.max_threads(),
+                result=r, graph=g)
+
+
+def run_reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    algo, scale, over, _, text = WORKLOADS[args.workload]
+    from oracle import oracle
+    threads = oracle.max_threads()
+    sample_scale = min(scale, args.cpu_scale)
+    vals = []
+    for _ in range(args.warmup):
+        cpu_sample(algo, sample_scale, over, 1)
+    t_total = 0.0
+    edges = 0
+    for _ in range(args.steps):
+        r = cpu_sample(algo, sample_scale, over, 1)
+        vals.append(r["gteps"])
+        t_total += r["seconds"]
+        edges += r["edges"]
+    v = edges / t_total / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GTEPS",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * t_total / args.steps, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64" if algo == "pagerank" else "u32",
+        "data": "synthetic",
+        "config": {"workload": args.workload, "description": text, "rmat_scale": sample_scale,
+                   "edge_factor": 16, "seed": 1, "parallelism": "cpu"},
+        "cpu_baseline": {"value": round(v, 4), "unit": "GTEPS", "cores": threads, "kind": "port",
+                         "sample": f"one {algo} BSP iteration per step on R-MAT scale-{sample_scale} "
+                                   f"(same generator/seed; scale-{scale} does not fit a bounded CPU run); "
+                                   "oracle/gx_oracle.c = C restatement of run_reference (A/algorithms.py:298-342), "
+                                   "the reference itself is pure Python and GIL-bound"},
+        "e2e": {"value": round(v, 4), "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU arm
+
+def algorithmic_bytes(algo, E, V, units=None, nz=None):
+    """PR 12E + 32V; SSSP 24 E_scanned + 36V; CC/LP 8 E_scanned + 12V."""
+    if algo == "pagerank":
+        return 12 * E + 32 * V
+    if algo == "sssp":
+        return 24 * (units if units is not None else E) + 36 * V
+    return 8 * (units if units is not None else E) + 12 * V
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gxb", choices=["gxb", "reference"])
+    ap.add_argument("--workload", default="pr-s26", choices=sorted(WORKLOADS))
+    ap.add_argument("--scale", type=int, default=None, help="override the R-MAT scale")
+    ap.add_argument("--cpu-scale", type=int, default=22)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2203_13005_b200 import _lib as L
+    from paper_2203_13005_b200.device import DeviceContext, DeviceGraph, DeviceState
+    from paper_2203_13005_b200.dist import Collective, PartitionedRun
+    from paper_2203_13005_b200.rmat import RmatParams
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    comm = Collective()
+    algo, scale, over, cap, text = WORKLOADS[args.workload]
+    if args.scale:
+        scale = args.scale
+    params = RmatParams(scale=scale, seed=1, **over)
+    ctx = DeviceContext(local)
+    stream = torch.cuda.current_stream(dev)
+
+    # graph: same device-generated edge stream on every rank, own destination range kept
+    src, dst, w = ctx.rmat(params, stream)
+    graph = DeviceGraph(ctx, src, dst, w, part=rank, nparts=world, csr=algo in ("sssp", "cc"), stream=stream)
+    del src, dst, w
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    E, V = graph.num_edges, graph.num_vertices
+    bounds = graph.bounds()
+
+    def new_run():
+        st = DeviceState(graph, algo)
+        return PartitionedRun(st, bounds, comm, enable_skip=True, device=dev)
+
+    # ---- device-timed steps ----
+    clocks = ClockSampler(local).__enter__()
+    run = new_run()
+    run.state.profile(enable=True, reset=True)
+    for _ in range(args.warmup):
+        run.step()
+    if algo != "pagerank":
+        # frontier algorithms: time whole runs (a step = one iteration of a fresh run)
+        run = new_run()
+        run.state.profile(enable=True, reset=True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    run.state.profile(reset=True)
+    launches = 0
+    step_ms = []
+    units = 0
+    clocks.wait_first()
+    clocks.mark(True)
+    t_wall = time.perf_counter()
+    for _ in range(args.steps):
+        ev0.record(stream)
+        rec = run.step()
+        ev1.record(stream)
+        ev1.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+        units += rec.units
+        if rec.converged and algo != "pagerank":
+            launches += run.state.profile()["kernels_launched"]
+            run = new_run()
+            run.state.profile(enable=True, reset=True)
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall
+    clocks.mark(False)
+    time.sleep(0.05)
+    clocks.__exit__(None, None, None)
+    prof = run.state.profile()
+    launches += prof["kernels_launched"]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    gteps = E * args.steps / (total_ms * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (the fused warp-tile Gen∘Merge) ----
+    peak, peak_kind = load_peaks()
+    lo, hi = graph.owned
+    owned_E = int(graph.info.owned_edges)
+    kern_ms = prof["main_kernel_ms"] / max(1, prof["main_kernel_launches"])
+    if algo == "pagerank":
+        kbytes = 12 * owned_E + 8 * (hi - lo)          # idx + gathered contribution per edge, sums out
+    elif algo == "sssp":
+        kbytes = 24 * owned_E + 16 * (hi - lo)
+    else:
+        kbytes = 8 * owned_E + 4 * (hi - lo)
+    achieved = kbytes / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else None
+    it_bytes = algorithmic_bytes(algo, E, V)
+    roofline = {
+        "bound": "hbm", "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
+        "frac": round(achieved / peak, 4) if achieved else None, "traffic": None,
+        "kernel": "k_tile_t (fused MSGGen+MSGMerge warp tiles)", "kernel_ms": round(kern_ms, 4),
+        "algorithmic_bytes_per_launch": kbytes, "peak_kind": peak_kind,
+        "iteration_frac": round(it_bytes * world / (ms_per_step * 1e-3) / 1e9 / (peak * world), 4)
+        if algo == "pagerank" else None,
+    }
+
+    # ---- e2e through the public API with host buffers (agent pull/push per step) ----
+    e2e = None
+    if not args.no_e2e:
+        import numpy as np
+        st = run.state
+        arity = st.arity
+        host_in = torch.empty(V * arity, dtype=torch.float64, pin_memory=True)
+        host_out = torch.empty(V * arity, dtype=torch.float64, pin_memory=True)
+        st.read_attrs_into(host_in.numpy().reshape(V, arity))
+        e2e_run = PartitionedRun(st, bounds, comm, enable_skip=True, device=dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            st.write_attrs(host_in, stream)            # update("pull_from_upper")
+            e2e_run.step()                             # requestGen/Merge/Apply + sync round
+            st.read_attrs_into(host_out.numpy().reshape(V, arity), owned_only=False, stream=stream)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": round(E * args.steps / e2e_s / 1e9, 3), "unit": "GTEPS",
+               "h2d_bytes_per_step": 8 * V * arity, "d2h_bytes_per_step": 8 * V * arity,
+               "path": "DeviceState.write_attrs (pull_from_upper) -> gxb_iterate + sync round -> "
+                       "gxb_read_attrs (push_to_upper), pinned host buffers"}
+
+    # ---- secondary workload (SSSP on the same scale) and CPU baseline, rank 0 / N = 1 ----
+    skipped_rounds = run.skipped_rounds
+    secondary = None
+    if world == 1 and not args.no_secondary and algo == "pagerank":
+        del run
+        graph.free()
+        torch.cuda.empty_cache()
+        p2 = RmatParams(scale=scale, seed=1, wmax=63)
+        s2, d2, w2 = ctx.rmat(p2, stream)
+        g2 = DeviceGraph(ctx, s2, d2, w2, csr=True, stream=stream)
+        del s2, d2, w2
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        for _rep in range(2):  # the first run warms allocations; the second is timed
+            st2 = DeviceState(g2, "sssp")
+            r2 = PartitionedRun(st2, g2.bounds(), comm, device=dev)
+            per_iter = []
+            ev0.record(stream)
+            while r2.iteration < g2.num_vertices + 1:
+                e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e_a.record(stream)
+                rr = r2.step()
+                e_b.record(stream)
+                per_iter.append((e_a, e_b, rr))
+                if rr.converged:
+                    break
+            ev1.record(stream)
+            ev1.synchronize()
+            it2, conv2 = r2.iteration, r2.records[-1].converged
+            ms2 = ev0.elapsed_time(ev1)
+        scanned = sum(r.units for r in r2.records)
+        secondary = {"workload": f"sssp-s{scale}", "iterations": it2, "converged": conv2,
+                     "total_ms": round(ms2, 3), "gteps_e": round(g2.num_edges * it2 / (ms2 * 1e-3) / 1e9, 2),
+                     "gteps_ref": round(scanned / (ms2 * 1e-3) / 1e9, 2),
+                     "iteration_ms": [round(a.elapsed_time(b), 3) for a, b, _ in per_iter],
+                     "directions": ["push" if r.direction == 2 else "pull" for _, _, r in per_iter],
+                     "note": "GTEPS_ref counts the reference's GEN units (out-edges of active vertices)"}
+        g2.free()
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            r = cpu_sample(algo, min(scale, args.cpu_scale), over, 1)
+            cpu = {"value": round(r["gteps"], 4), "unit": "GTEPS", "cores": r["threads"], "kind": "port",
+                   "sample": f"one {algo} iteration on R-MAT scale-{min(scale, args.cpu_scale)} "
+                             f"({r['edges']} edges, {r['seconds']:.2f} s), oracle/gx_oracle.c OpenMP restatement"}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": "GTEPS", "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(gteps, 3), "unit": "GTEPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if algo == "pagerank" else "u32", "data": "synthetic",
+            "config": {"workload": args.workload, "description": text, "rmat_scale": scale,
+                       "rmat_abc": [params.a, params.b, params.c], "edge_factor": 16, "seed": 1,
+                       "scramble": True, "num_edges": E, "num_vertices": V,
+                       "parallelism": f"dst-range partition x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (CSC 4 B/edge), no flush"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(), "wall_s": round(t_wall, 3),
+            "skipped_rounds": skipped_rounds,
+        }
+        if secondary:
+            line["secondary"] = secondary
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

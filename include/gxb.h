@@ -202,6 +202,24 @@ int gxb_exchange_finish(gxb_state* s, void* stream);
  * writes NaN elsewhere). */
 int gxb_read_attrs(gxb_state* s, double* host_out, int owned_only, void* stream);
 
+/* install attribute values from the host (ascending original-id order, same
+ * encoding as gxb_read_attrs) — the agent's update("pull_from_upper")
+ * (A/agent.py:224-232, 433-443). Does not change the active frontier.
+ * SSSP distances / labels must be non-negative integers < 2^32-1 (+inf allowed
+ * for distances), else GXB_ERANGE. */
+int gxb_write_attrs(gxb_state* s, const double* host_in, void* stream);
+
+/* ---- profiling: CUDA events around the main merge kernel of every fused
+ * iteration, and a count of every kernel the library launched ---- */
+typedef struct gxb_profile {
+    double   main_kernel_ms;       /* summed device time of the main merge kernel */
+    uint64_t main_kernel_launches;
+    uint64_t kernels_launched;     /* all kernels launched by gxb_iterate since the last reset */
+    uint64_t iterations;
+} gxb_profile;
+int gxb_profile_enable(gxb_state* s, int on);
+int gxb_profile_read(gxb_state* s, gxb_profile* out, int reset);
+
 #ifdef __cplusplus
 }
 #endif

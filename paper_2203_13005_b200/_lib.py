@@ -51,6 +51,16 @@ class IterStats(ctypes.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_}
 
 
+class Profile(ctypes.Structure):
+    _fields_ = [
+        ("main_kernel_ms", ctypes.c_double), ("main_kernel_launches", ctypes.c_uint64),
+        ("kernels_launched", ctypes.c_uint64), ("iterations", ctypes.c_uint64),
+    ]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
 class RmatArgs(ctypes.Structure):
     _fields_ = [
         ("scale", ctypes.c_uint32), ("edge_factor", ctypes.c_uint32), ("seed", ctypes.c_uint64),
@@ -94,6 +104,9 @@ def _sig(L):
         "gxb_exchange_unpack": (I, [P, P, U64, P]),
         "gxb_exchange_finish": (I, [P, P]),
         "gxb_read_attrs": (I, [P, P, I, P]),
+        "gxb_write_attrs": (I, [P, P, P]),
+        "gxb_profile_enable": (I, [P, I]),
+        "gxb_profile_read": (I, [P, ctypes.POINTER(Profile), I]),
     }
     for name, (res, args) in table.items():
         f = getattr(L, name)

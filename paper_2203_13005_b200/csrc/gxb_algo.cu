@@ -27,6 +27,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "gxb_state.cuh"
 
 namespace gxb {
@@ -648,42 +650,72 @@ struct PushLaunch {
     unsigned long long* count_next;
 };
 
-__global__ void __launch_bounds__(kBlock) k_push_sssp(const uint4* __restrict__ dist_cur, uint4* dist_next,
-                                                       const PushLaunch L) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
-    for (uint64_t f = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); f < L.nfront; f += nwarps) {
-        const uint32_t s = __ldg(L.frontier + f);
-        const uint64_t beg = __ldg(L.out_off + s), end = __ldg(L.out_off + s + 1);
-        const uint4 d = __ldg(dist_cur + s);
-        for (uint64_t e = beg + lane; e < end; e += 32) {
-            const uint32_t t = __ldg(L.out_dst + e);
-            const uint32_t w = L.out_w ? __ldg(L.out_w + e) : 1u;
-            const uint4 c = make_uint4(sat_add(d.x, w), sat_add(d.y, w), sat_add(d.z, w), sat_add(d.w, w));
-            uint4 cur = __ldcg(dist_next + t);
-            unsigned* p = reinterpret_cast<unsigned*>(dist_next + t);
-            bool lowered = false;
-            if (c.x < cur.x) lowered |= atomicMin(p + 0, c.x) > c.x;
-            if (c.y < cur.y) lowered |= atomicMin(p + 1, c.y) > c.y;
-            if (c.z < cur.z) lowered |= atomicMin(p + 2, c.z) > c.z;
-            if (c.w < cur.w) lowered |= atomicMin(p + 3, c.w) > c.w;
-            if (lowered && bit_set_atomic(L.touched, (uint32_t)(t - L.lo))) warp_append(L.list_next, L.count_next, t);
-        }
+// Edge-balanced push: every frontier source is cut into kPushChunk-edge chunks
+// (an inclusive scan of chunk counts maps a global chunk id back to its source),
+// so a hub with a million out-edges is spread over thousands of warps instead of
+// serialising one warp. Each edge relaxes the destination with atomicMin and a
+// touched bitmap deduplicates the next frontier.
+constexpr uint32_t kPushChunk = 256;
+
+__global__ void k_push_counts(const uint32_t* __restrict__ frontier, uint64_t n, const uint64_t* __restrict__ out_off,
+                              uint32_t* counts) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = frontier[i];
+        const uint64_t d = out_off[s + 1] - out_off[s];
+        counts[i] = (uint32_t)((d + kPushChunk - 1) / kPushChunk);
     }
 }
 
-__global__ void __launch_bounds__(kBlock) k_push_cc(const uint32_t* __restrict__ lab_cur, uint32_t* lab_next,
-                                                     const PushLaunch L) {
+struct SsspPush {
+    const uint4* dist_cur;
+    uint4* dist_next;
+    using Val = uint4;
+    __device__ Val load(uint32_t s) const { return __ldg(dist_cur + s); }
+    __device__ bool relax(Val d, uint32_t t, uint32_t w) const {
+        const uint4 c = make_uint4(sat_add(d.x, w), sat_add(d.y, w), sat_add(d.z, w), sat_add(d.w, w));
+        const uint4 cur = __ldcg(dist_next + t);
+        unsigned* p = reinterpret_cast<unsigned*>(dist_next + t);
+        bool lowered = false;
+        if (c.x < cur.x) lowered |= atomicMin(p + 0, c.x) > c.x;
+        if (c.y < cur.y) lowered |= atomicMin(p + 1, c.y) > c.y;
+        if (c.z < cur.z) lowered |= atomicMin(p + 2, c.z) > c.z;
+        if (c.w < cur.w) lowered |= atomicMin(p + 3, c.w) > c.w;
+        return lowered;
+    }
+};
+
+struct CcPush {
+    const uint32_t* lab_cur;
+    uint32_t* lab_next;
+    using Val = uint32_t;
+    __device__ Val load(uint32_t s) const { return __ldg(lab_cur + s); }
+    __device__ bool relax(Val v, uint32_t t, uint32_t) const {
+        return v < __ldcg(lab_next + t) && atomicMin(lab_next + t, v) > v;
+    }
+};
+
+template <class Op>
+__global__ void __launch_bounds__(kBlock) k_push(const Op op, const PushLaunch L, const uint32_t* __restrict__ cpre) {
     const int lane = threadIdx.x & 31;
+    if (L.nfront == 0) return;
+    const uint64_t total = cpre[L.nfront - 1];
     const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
-    for (uint64_t f = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); f < L.nfront; f += nwarps) {
-        const uint32_t s = __ldg(L.frontier + f);
-        const uint64_t beg = __ldg(L.out_off + s), end = __ldg(L.out_off + s + 1);
-        const uint32_t v = __ldg(lab_cur + s);
+    for (uint64_t c = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); c < total; c += nwarps) {
+        // first f with cpre[f] > c
+        uint64_t lo = 0, hi = L.nfront - 1;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (__ldg(cpre + mid) > c) hi = mid; else lo = mid + 1;
+        }
+        const uint64_t k = c - (lo ? __ldg(cpre + lo - 1) : 0);
+        const uint32_t s = __ldg(L.frontier + lo);
+        const uint64_t beg = __ldg(L.out_off + s) + k * kPushChunk;
+        const uint64_t end = min(beg + kPushChunk, __ldg(L.out_off + s + 1));
+        const typename Op::Val v = op.load(s);
         for (uint64_t e = beg + lane; e < end; e += 32) {
             const uint32_t t = __ldg(L.out_dst + e);
-            if (v < __ldcg(lab_next + t) && atomicMin(lab_next + t, v) > v &&
-                bit_set_atomic(L.touched, (uint32_t)(t - L.lo)))
+            const uint32_t w = L.out_w ? __ldg(L.out_w + e) : 1u;
+            if (op.relax(v, t, w) && bit_set_atomic(L.touched, (uint32_t)(t - L.lo)))
                 warp_append(L.list_next, L.count_next, t);
         }
     }
@@ -798,6 +830,41 @@ __global__ void k_read_attrs(int algo, int arity, const uint32_t* __restrict__ d
     }
 }
 
+// attributes in ascending-id order -> slots (the agent's pull_from_upper)
+__global__ void k_write_attrs(int algo, int arity, const uint32_t* __restrict__ d2s, uint64_t V,
+                              const uint32_t* __restrict__ outdeg, const double* __restrict__ in, double* rank,
+                              double* contrib, uint4* dist_cur, uint4* dist_next, uint32_t* lab_cur,
+                              uint32_t* lab_next, uint32_t* bad) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < V; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = d2s[i];
+        if (algo == GXB_ALGO_PAGERANK) {
+            const double r = in[i];
+            rank[s] = r;
+            const uint32_t od = outdeg[s];
+            contrib[s] = od ? __ddiv_rn(r, (double)od) : 0.0;
+        } else if (algo == GXB_ALGO_SSSP) {
+            uint32_t l[4] = {kInf32, kInf32, kInf32, kInf32};
+            for (int j = 0; j < arity; ++j) {
+                const double x = in[i * arity + j];
+                if (isinf(x) && x > 0) continue;
+                if (!(x >= 0.0 && x < 4294967295.0 && x == floor(x))) atomicOr(bad, 1u);
+                else l[j] = (uint32_t)x;
+            }
+            const uint4 v = make_uint4(l[0], l[1], l[2], l[3]);
+            dist_cur[s] = v;
+            dist_next[s] = v;
+        } else {
+            const double x = in[i];
+            if (!(x >= 0.0 && x < 4294967295.0 && x == floor(x))) {
+                atomicOr(bad, 1u);
+            } else {
+                lab_cur[s] = (uint32_t)x;
+                lab_next[s] = (uint32_t)x;
+            }
+        }
+    }
+}
+
 }  // namespace gxb
 
 using namespace gxb;
@@ -893,7 +960,9 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st) {
     const gxb_graph* g = s->g;
     const TileLaunch L = tile_launch(s);
     FusedPolicy<Ops> p{ops, g->d_in_w};
-    const int variant = (int)options().tile_minblocks;
+    // measured best min-blocks per accumulator width (PR/CC 6, SSSP 4); 0 = auto
+    int variant = (int)options().tile_minblocks;
+    if (variant == 0) variant = (sizeof(typename Ops::Acc) >= 16) ? 4 : 6;
     using Pol = FusedPolicy<Ops>;
     void (*kern)(const Pol, const TileLaunch);
     if (options().tile_layout == 1)
@@ -908,16 +977,25 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st) {
     if (L.num_tiles) {
         const uint64_t want = (L.num_tiles + (kBlock / 32) - 1) / (kBlock / 32);
         const unsigned grid = (unsigned)std::min<uint64_t>(want, (uint64_t)max_blocks);
+        if (s->timing) GXB_CUDA(cudaEventRecord(s->kev[0], st));
         kern<<<grid, kBlock, 0, st>>>(p, L);
+        if (s->timing) {
+            GXB_CUDA(cudaEventRecord(s->kev[1], st));
+            s->timing_pending = true;
+        }
+        s->launches++;
         const TilePlan& T = g->tiles;
-        if (T.num_spans)
+        if (T.num_spans) {
             k_span_fold<Ops><<<grid_for(T.num_spans), kBlock, 0, st>>>(
                 T.d_span_slot, T.d_span_count, T.d_span_pbase, T.num_spans,
                 (const typename Ops::Acc*)s->d_tile_partials, (typename Ops::Acc*)s->d_sums);
+            s->launches++;
+        }
     }
     const uint64_t owned = g->hi - g->lo;
     k_apply_sums<Ops><<<grid_for(owned), kBlock, 0, st>>>(ops, (const typename Ops::Acc*)s->d_sums, g->lo, owned,
                                                           g->tiles.nz_slots, s->d_stats);
+    s->launches++;
     GXB_CUDA(cudaGetLastError());
     return GXB_OK;
 }
@@ -989,6 +1067,7 @@ int end_round(gxb_state* s, int direction, cudaStream_t st) {
             k_commit<uint4><<<grid, kBlock, 0, st>>>(s->d_dist_cur, s->d_dist_next, s->d_frontier[1], s->d_fcount + 1);
         else
             k_commit<uint32_t><<<grid, kBlock, 0, st>>>(s->d_lab_cur, s->d_lab_next, s->d_frontier[1], s->d_fcount + 1);
+        s->launches++;
         GXB_CUDA(cudaGetLastError());
     }
     if (s->algo != GXB_ALGO_PAGERANK) {
@@ -1044,6 +1123,14 @@ int collect_stats(gxb_state* s) {
         s->frontier_len = *s->h_fcount;
         s->units_cur = o.next_units;
         s->last = o;
+    }
+    if (s->timing_pending) {
+        float ms = 0.f;
+        GXB_CUDA(cudaEventSynchronize(s->kev[1]));
+        GXB_CUDA(cudaEventElapsedTime(&ms, s->kev[0], s->kev[1]));
+        s->kernel_ms += ms;
+        s->kernel_launches++;
+        s->timing_pending = false;
     }
     return GXB_OK;
 }
@@ -1222,6 +1309,12 @@ int gxb_state_free(gxb_state* s) {
     dfree(s->d_msg_valid);
     dfree(s->d_merged);
     dfree(s->d_partials);
+    dfree(s->d_stage);
+    if (s->kev[0]) cudaEventDestroy(s->kev[0]);
+    if (s->kev[1]) cudaEventDestroy(s->kev[1]);
+    dfree(s->d_push_counts);
+    dfree(s->d_push_cpre);
+    dfree(s->d_push_tmp);
     dfree(s->d_tile_partials);
     dfree(s->d_sums);
     gxb_lp_free(s);
@@ -1283,8 +1376,10 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
             }
             case GXB_ALGO_LP:
                 GXB_CHECK(gxb_lp_pull(s, st));
+                s->launches += 3;
                 break;
         }
+        if (s->algo != GXB_ALGO_LP) s->launches++;
     } else {
         PushLaunch P;
         P.lo = g->lo;
@@ -1297,17 +1392,34 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
         P.touched = s->d_touched;
         P.list_next = s->d_frontier[1];
         P.count_next = s->d_fcount + 1;
-        const unsigned grid = grid_for(P.nfront * 32);
         FrontierView f = frontier_view(s);
-        if (s->algo == GXB_ALGO_SSSP) {
-            if (P.nfront) k_push_sssp<<<grid, kBlock, 0, st>>>(s->d_dist_cur, s->d_dist_next, P);
+        if (!s->d_push_counts) {
+            GXB_CHECK(dalloc_t(&s->d_push_counts, g->V + 1));
+            GXB_CHECK(dalloc_t(&s->d_push_cpre, g->V + 1));
+            size_t tb = 0;
+            GXB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, s->d_push_counts, s->d_push_cpre, (int64_t)(g->V + 1), st));
+            s->push_tmp_bytes = tb;
+            GXB_CHECK(dalloc(&s->d_push_tmp, tb));
+        }
+        if (P.nfront) {
+            s->launches += 3;  // counts, scan, push
+            k_push_counts<<<grid_for(P.nfront), kBlock, 0, st>>>(P.frontier, P.nfront, P.out_off, s->d_push_counts);
+            size_t tb = s->push_tmp_bytes;
+            GXB_CUDA(cub::DeviceScan::InclusiveSum(s->d_push_tmp, tb, s->d_push_counts, s->d_push_cpre,
+                                                   (int64_t)P.nfront, st));
+            const unsigned grid = grid_for((s->units_cur / kPushChunk + P.nfront) * 32, kBlock, 148ull * 16);
+            if (s->algo == GXB_ALGO_SSSP)
+                k_push<SsspPush><<<grid, kBlock, 0, st>>>(SsspPush{s->d_dist_cur, s->d_dist_next}, P, s->d_push_cpre);
+            else
+                k_push<CcPush><<<grid, kBlock, 0, st>>>(CcPush{s->d_lab_cur, s->d_lab_next}, P, s->d_push_cpre);
+        }
+        s->launches++;
+        if (s->algo == GXB_ALGO_SSSP)
             k_push_apply<uint4><<<kNumSMs * 2, kBlock, 0, st>>>(s->d_dist_cur, s->d_dist_next, s->d_frontier[1],
                                                                  s->d_fcount + 1, f, s->d_stats);
-        } else {
-            if (P.nfront) k_push_cc<<<grid, kBlock, 0, st>>>(s->d_lab_cur, s->d_lab_next, P);
+        else
             k_push_apply<uint32_t><<<kNumSMs * 2, kBlock, 0, st>>>(s->d_lab_cur, s->d_lab_next, s->d_frontier[1],
                                                                     s->d_fcount + 1, f, s->d_stats);
-        }
         GXB_CUDA(cudaGetLastError());
         GXB_CUDA(cudaMemsetAsync(s->d_touched, 0, 4 * ((owned >> 5) + 1), st));
     }
@@ -1420,6 +1532,11 @@ int gxb_stats(gxb_state* s, void* stream, gxb_iter_stats* out) {
     return GXB_OK;
 }
 
+static int stage(gxb_state* s) {
+    if (!s->d_stage) GXB_CHECK(dalloc_t(&s->d_stage, s->g->V * s->arity + 1));
+    return GXB_OK;
+}
+
 int gxb_read_attrs(gxb_state* s, double* host_out, int owned_only, void* stream) {
     if (!s) return fail(GXB_EINVAL, "gxb_read_attrs: null state");
     gxb_graph* g = s->g;
@@ -1427,14 +1544,59 @@ int gxb_read_attrs(gxb_state* s, double* host_out, int owned_only, void* stream)
     if (!V) return GXB_OK;
     if (!host_out) return fail(GXB_EINVAL, "gxb_read_attrs: null output");
     cudaStream_t st = (cudaStream_t)stream;
-    double* tmp = nullptr;
-    GXB_CHECK(dalloc_t(&tmp, V * s->arity));
+    GXB_CHECK(stage(s));
     k_read_attrs<<<grid_for(V), kBlock, 0, st>>>(s->algo, s->arity, g->d_dense2slot, V, g->lo, g->hi,
-                                                 owned_only, s->d_rank, s->d_dist_cur, s->d_lab_cur, tmp);
-    cudaError_t e = cudaMemcpyAsync(host_out, tmp, 8 * V * s->arity, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    dfree(tmp);
-    if (e != cudaSuccess) return cuda_fail(e, "gxb_read_attrs");
+                                                 owned_only, s->d_rank, s->d_dist_cur, s->d_lab_cur, s->d_stage);
+    GXB_CUDA(cudaMemcpyAsync(host_out, s->d_stage, 8 * V * s->arity, cudaMemcpyDeviceToHost, st));
+    GXB_CUDA(cudaStreamSynchronize(st));
+    return GXB_OK;
+}
+
+int gxb_write_attrs(gxb_state* s, const double* host_in, void* stream) {
+    if (!s) return fail(GXB_EINVAL, "gxb_write_attrs: null state");
+    if (s->in_round) return fail(GXB_ESTATE, "gxb_write_attrs: a round is open");
+    gxb_graph* g = s->g;
+    const uint64_t V = g->V;
+    if (!V) return GXB_OK;
+    if (!host_in) return fail(GXB_EINVAL, "gxb_write_attrs: null input");
+    cudaStream_t st = (cudaStream_t)stream;
+    GXB_CHECK(collect_stats(s));
+    GXB_CHECK(stage(s));
+    GXB_CUDA(cudaMemcpyAsync(s->d_stage, host_in, 8 * V * s->arity, cudaMemcpyHostToDevice, st));
+    uint32_t* d_bad = reinterpret_cast<uint32_t*>(s->d_fcount) + 2;  // scratch word of counter [1]
+    GXB_CUDA(cudaMemsetAsync(d_bad, 0, 4, st));
+    k_write_attrs<<<grid_for(V), kBlock, 0, st>>>(s->algo, s->arity, g->d_dense2slot, V, g->d_outdeg, s->d_stage,
+                                                  s->d_rank, s->d_contrib[s->cur], s->d_dist_cur, s->d_dist_next,
+                                                  s->d_lab_cur, s->d_lab_next, d_bad);
+    uint32_t bad = 0;
+    GXB_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
+    GXB_CUDA(cudaStreamSynchronize(st));
+    if (bad) return fail(GXB_ERANGE, "gxb_write_attrs: value not representable on the device");
+    return GXB_OK;
+}
+
+int gxb_profile_enable(gxb_state* s, int on) {
+    if (!s) return fail(GXB_EINVAL, "gxb_profile_enable: null state");
+    if (on && !s->kev[0]) {
+        GXB_CUDA(cudaEventCreate(&s->kev[0]));
+        GXB_CUDA(cudaEventCreate(&s->kev[1]));
+    }
+    s->timing = on != 0;
+    return GXB_OK;
+}
+
+int gxb_profile_read(gxb_state* s, gxb_profile* out, int reset) {
+    if (!s || !out) return fail(GXB_EINVAL, "gxb_profile_read: null argument");
+    GXB_CHECK(collect_stats(s));
+    out->main_kernel_ms = s->kernel_ms;
+    out->main_kernel_launches = s->kernel_launches;
+    out->kernels_launched = s->launches;
+    out->iterations = s->iteration;
+    if (reset) {
+        s->kernel_ms = 0.0;
+        s->kernel_launches = 0;
+        s->launches = 0;
+    }
     return GXB_OK;
 }
 

@@ -142,9 +142,26 @@ struct gxb_state {
     void* d_tile_partials = nullptr;
     void* d_sums = nullptr;  // per owned slot: folded accumulator of the tile kernel
 
+    // push scheduling (chunk counts, their inclusive scan, CUB scratch)
+    uint32_t* d_push_counts = nullptr;
+    uint32_t* d_push_cpre = nullptr;
+    void* d_push_tmp = nullptr;
+    size_t push_tmp_bytes = 0;
+
     // LP scratch
     void* d_lp_scratch = nullptr;
     size_t lp_scratch_bytes = 0;
+
+    // host<->device attribute staging (ascending-id order)
+    double* d_stage = nullptr;
+
+    // profiling: events around the main merge kernel, launch counter
+    bool timing = false;
+    bool timing_pending = false;
+    cudaEvent_t kev[2] = {nullptr, nullptr};
+    double kernel_ms = 0.0;
+    uint64_t kernel_launches = 0;
+    uint64_t launches = 0;
 
     // exchange
     void* d_send = nullptr;

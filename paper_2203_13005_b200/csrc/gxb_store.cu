@@ -650,7 +650,8 @@ int gxb_set_option(const char* name, int64_t value) {
     Options& o = options();
     const std::string n(name);
     if (n == "tile_minblocks") {
-        if (value != 0 && value != 4 && value != 6 && value != 8) return fail(GXB_EINVAL, "tile_minblocks: 0/4/6/8");
+        if (value != 0 && value != 1 && value != 4 && value != 6 && value != 8)
+            return fail(GXB_EINVAL, "tile_minblocks: 0 (auto) / 1 / 4 / 6 / 8");
         o.tile_minblocks = value;
     } else if (n == "l2_hot_mb") {
         if (value < 0) return fail(GXB_EINVAL, "l2_hot_mb must be >= 0");

@@ -227,6 +227,28 @@ class DeviceState:
         L.check(L.lib().gxb_read_attrs(self._h, _vp(out), int(owned_only), _stream_ptr(stream)))
         return out
 
+    def read_attrs_into(self, out: np.ndarray, owned_only: bool = False, stream=None) -> np.ndarray:
+        """Like read_attrs into a caller-provided (e.g. pinned) host array."""
+        L.check(L.lib().gxb_read_attrs(self._h, _vp(out), int(owned_only), _stream_ptr(stream)))
+        return out
+
+    def write_attrs(self, values, stream=None):
+        """Install attributes (ascending-id order) from the host: the agent's pull_from_upper."""
+        if isinstance(values, np.ndarray):
+            a = np.ascontiguousarray(values, dtype=np.float64)
+            if a.size != self.graph.num_vertices * self.arity:
+                raise ValueError("attribute array has the wrong length")
+            L.check(L.lib().gxb_write_attrs(self._h, _vp(a), _stream_ptr(stream)))
+        else:  # pinned torch tensor
+            L.check(L.lib().gxb_write_attrs(self._h, _vp(values), _stream_ptr(stream)))
+
+    def profile(self, enable: bool | None = None, reset: bool = False) -> dict:
+        if enable is not None:
+            L.check(L.lib().gxb_profile_enable(self._h, int(enable)))
+        p = L.Profile()
+        L.check(L.lib().gxb_profile_read(self._h, ctypes.byref(p), int(reset)))
+        return p.as_dict()
+
     def buffer(self, which: int) -> tuple[int, int]:
         p = ctypes.c_void_p()
         b = ctypes.c_uint64()

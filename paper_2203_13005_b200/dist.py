@@ -1,0 +1,189 @@
+"""Multi-GPU driver: one process per GPU, destination-range partitions, mirror
+exchange over torch.distributed (NCCL on NVLink; gloo for the CPU tests).
+
+Mirrors the reference's barrier schedule for one iteration (A/engine.py:226-294,
+298-331): compute (Gen/Merge/Apply on the own partition) -> skip decision
+(1-bit AND of partition-closedness, A/engine.py:242-246, A/sync.py:201-208) ->
+sync round (only the changed values that a peer consumes travel: the lazy upload
+of A/sync.py:171-198, realised as a delta all-gather of (slot, value) records, or
+a dense all-gather of the contribution slices for PageRank where every vertex
+changes) -> verdict (AND of the local votes, A/engine.py:131-136, 267-285).
+
+The collectives are plain NCCL calls issued by torch.distributed on library-owned
+device buffers (zero-copy views through __cuda_array_interface__); the per-vertex
+work of packing and installing records runs in libgxb200 kernels.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+
+class _CAI:
+    """Zero-copy __cuda_array_interface__ wrapper of a library device buffer."""
+
+    def __init__(self, ptr: int, nbytes: int, typestr: str = "|u1"):
+        itemsize = int(typestr[2:])
+        self.__cuda_array_interface__ = {
+            "shape": (nbytes // itemsize,), "typestr": typestr, "data": (ptr, False), "version": 3,
+            "strides": None,
+        }
+
+
+def device_view(ptr: int, nbytes: int, dtype: str = "u1"):
+    import torch
+    typestr = {"u1": "|u1", "f8": "<f8", "u4": "<u4", "i8": "<i8"}[dtype]
+    return torch.as_tensor(_CAI(ptr, nbytes, typestr), device="cuda")
+
+
+@dataclass
+class StepRecord:
+    """Per-iteration record in the spirit of IterationRecord (A/engine.py:63-85)."""
+
+    iteration: int
+    changed: int
+    next_active: int
+    units: int
+    remote_active: int
+    max_stat: float
+    skipped: bool
+    converged: bool
+    exchanged_bytes: int = 0
+    direction: int = 1
+
+    def to_line(self, model: str = "bsp") -> str:
+        return (f"iter={self.iteration} model={model} changed={self.changed} active={self.next_active} "
+                f"units={self.units} skipped={str(self.skipped).lower()} "
+                f"uploads={self.exchanged_bytes} converged={str(self.converged).lower()}")
+
+
+class Collective:
+    """The few collectives of one iteration, over an optional torch process group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+
+    def vote(self, counts: list[int], max_stat: float, device) -> tuple[list[int], float]:
+        """SUM of counters and MAX of the convergence statistic over ranks."""
+        import torch
+        if self.world == 1:
+            return counts, max_stat
+        c = torch.tensor(counts, dtype=torch.int64, device=device)
+        m = torch.tensor([max_stat], dtype=torch.float64, device=device)
+        self.dist.all_reduce(c, group=self.group)
+        self.dist.all_reduce(m, op=self.dist.ReduceOp.MAX, group=self.group)
+        return [int(x) for x in c.tolist()], float(m.item())
+
+    def allgatherv(self, out_views, my_view):
+        """All-gather with uneven sizes into caller-provided views (grouped P2P)."""
+        if self.world == 1:
+            return
+        ops = []
+        for peer in range(self.world):
+            if peer == self.rank:
+                continue
+            if my_view.numel():
+                ops.append(self.dist.P2POp(self.dist.isend, my_view, peer, self.group))
+            if out_views[peer].numel():
+                ops.append(self.dist.P2POp(self.dist.irecv, out_views[peer], peer, self.group))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def gather_counts(self, n: int, device) -> list[int]:
+        import torch
+        if self.world == 1:
+            return [n]
+        t = torch.tensor([n], dtype=torch.int64, device=device)
+        out = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [int(x.item()) for x in out]
+
+
+@dataclass
+class PartitionedRun:
+    """One rank's share of a partitioned BSP run."""
+
+    state: object                      # DeviceState (or a test double with the same surface)
+    bounds: np.ndarray                 # slot boundaries of the partitions (world + 1)
+    comm: Collective
+    enable_skip: bool = True
+    records: list = field(default_factory=list)
+    device: object = None
+
+    def __post_init__(self):
+        self.algo = self.state.algo
+        self.iteration = 0
+        self.skipped_rounds = 0
+
+    # ---- the sync round ---------------------------------------------------
+    def _exchange_dense(self) -> int:
+        """PageRank: every vertex changes, so all-gather each owner's contribution slice."""
+        ptr, nbytes = self.state.buffer(L.BUF_VALUES)
+        values = self._view(ptr, nbytes, "f8")
+        views = [values[int(self.bounds[r]):int(self.bounds[r + 1])] for r in range(self.comm.world)]
+        self.comm.allgatherv(views, views[self.comm.rank])
+        return 8 * int(self.bounds[-1] - (self.bounds[self.comm.rank + 1] - self.bounds[self.comm.rank]))
+
+    def _exchange_delta(self) -> int:
+        """SSSP / CC / LP: only changed owned values travel, as (slot, value) records."""
+        rec = self.state.buffer(L.BUF_RECORD_SIZE)[1]
+        n = self.state.pack()
+        counts = self.comm.gather_counts(n, self.device)
+        sptr, sbytes = self.state.buffer(L.BUF_SEND)
+        rptr, rbytes = self.state.buffer(L.BUF_RECV)
+        send = self._view(sptr, sbytes, "u1")[: n * rec]
+        recv = self._view(rptr, rbytes, "u1")
+        offs = np.concatenate([[0], np.cumsum(counts)]) * rec
+        views = [recv[int(offs[r]):int(offs[r + 1])] for r in range(self.comm.world)]
+        views[self.comm.rank].copy_(send)
+        self.comm.allgatherv(views, send)
+        total = int(sum(counts))
+        self.state.unpack(rptr, total)
+        return (total - n) * rec
+
+    def _view(self, ptr, nbytes, dtype):
+        if hasattr(self.state, "view"):
+            return self.state.view(ptr, nbytes, dtype)
+        return device_view(ptr, nbytes, dtype)
+
+    # ---- one iteration ----------------------------------------------------
+    def step(self, direction: str = "auto") -> StepRecord:
+        self.state.iterate(direction)
+        st = self.state.stats()
+        counts, max_stat = self.comm.vote(
+            [st["changed"], st["next_active"], st["next_units"], st["remote_active"]], st["max_stat"],
+            self.device)
+        changed, next_active, next_units, remote_active = counts
+        self.iteration += 1
+        # skip iff no next-active vertex anywhere has a consumer on another partition
+        skip = self.comm.world == 1 or (self.enable_skip and remote_active == 0)
+        moved = 0
+        if not skip:
+            moved = self._exchange_dense() if self.algo == "pagerank" else self._exchange_delta()
+        if self.algo == "pagerank":
+            converged = max_stat < 1e-9           # PageRank.vote (A/algorithms.py:164-165)
+        else:
+            converged = next_active == 0          # not next_active (A/algorithms.py:70-72)
+        if skip and self.comm.world > 1 and not converged:
+            self.skipped_rounds += 1
+        rec = StepRecord(self.iteration, changed, next_active, st["units"], remote_active, max_stat,
+                         skip and self.comm.world > 1, converged, moved, st["direction"])
+        self.records.append(rec)
+        return rec
+
+    def run(self, max_iterations: int, direction: str = "auto") -> tuple[int, bool]:
+        converged = False
+        while self.iteration < max_iterations:
+            if self.step(direction).converged:
+                converged = True
+                break
+        return self.iteration, converged

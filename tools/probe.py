@@ -51,7 +51,10 @@ def main():
         if st["voted"]:
             break
     E = g.num_edges
-    out = dict(scale=args.scale, algo=args.algo, V=g.num_vertices, E=E, gen_s=t1 - t0, build_s=t2 - t1,
+    import subprocess
+    clk = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
+                          "--format=csv,noheader"], capture_output=True, text=True).stdout.strip()
+    out = dict(clocks=clk, scale=args.scale, algo=args.algo, V=g.num_vertices, E=E, gen_s=t1 - t0, build_s=t2 - t1,
                iters=it, ms=[round(x, 4) for x in times], hist=hist[:40],
                gteps_e=[round(E / (x * 1e-3) / 1e9, 2) for x in times][:12])
     print(json.dumps(out))
