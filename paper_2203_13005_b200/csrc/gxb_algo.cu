@@ -395,103 +395,6 @@ __device__ __forceinline__ void tile_emit(const Pol& p, const TileLaunch& L, uin
     }
 }
 
-__device__ __forceinline__ uint8_t ld_stream_u8(const uint8_t* ptr, uint64_t pol) {
-    uint16_t r;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(r) : "l"(ptr), "l"(pol));
-    return (uint8_t)r;
-}
-
-template <class Pol, int kMinBlocks>
-__global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile(const Pol p, const TileLaunch L) {
-    using Ops = decltype(p.ops);
-    using Acc = typename Ops::Acc;
-    constexpr bool kW = Ops::kWeighted;
-    const int lane = threadIdx.x & 31;
-    const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
-    const uint64_t pol = l2_evict_first();
-    const bool weighted = kW && L.in_w != nullptr;
-    uint64_t t = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
-    // software pipeline: the next tile's streams (indices, weights, lane tables)
-    // are in flight while this tile gathers
-    uint4 na = make_uint4(0, 0, 0, 0), nb = na, wa = make_uint4(1, 1, 1, 1), wb = wa;
-    uint32_t nsa = 0, nmask = 0;
-    auto prefetch = [&](uint64_t tt) {
-        const uint64_t e = tt * kTileEdges + (uint64_t)lane * kTileK;
-        na = ld_stream_v4(L.in_src + e, pol);
-        nb = ld_stream_v4(L.in_src + e + 4, pol);
-        if (weighted) {
-            wa = ld_stream_v4(L.in_w + e, pol);
-            wb = ld_stream_v4(L.in_w + e + 4, pol);
-        }
-        nsa = ld_stream_u32(L.lane_slot + tt * 32 + lane, pol);
-        nmask = ld_stream_u8(L.lane_mask + tt * 32 + lane, pol);
-    };
-    if (t < L.num_tiles) prefetch(t);
-    for (; t < L.num_tiles; t += nwarps) {
-        const uint64_t e0 = t * kTileEdges + (uint64_t)lane * kTileK;
-        const bool live = e0 < L.owned_edges;
-        const uint32_t src[kTileK] = {na.x, na.y, na.z, na.w, nb.x, nb.y, nb.z, nb.w};
-        const uint32_t wgt[kTileK] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
-        const uint32_t sa = nsa;
-        uint32_t endmask = nmask;
-        if (t + nwarps < L.num_tiles) prefetch(t + nwarps);
-        // Gen: kTileK independent gathers
-        Acc v[kTileK];
-#pragma unroll
-        for (int j = 0; j < kTileK; ++j) {
-            v[j] = Ops::identity();
-            if (e0 + j < L.owned_edges) p.accumulate_w(v[j], src[j], wgt[j]);
-        }
-        const uint32_t nvalid = live ? (uint32_t)min((uint64_t)kTileK, L.owned_edges - e0) : 0u;
-        endmask &= (1u << nvalid) - 1u;      // no segment ends past the valid edges
-        endmask &= ~(1u << (kTileK - 1));    // the final position is handled as the last run
-        uint32_t fkey = kNone;
-        Acc fval = Ops::identity();
-        const bool multi = endmask != 0;
-        Acc acc = Ops::identity();
-        uint32_t key = sa;
-        bool first = true;
-#pragma unroll
-        for (int j = 0; j < kTileK; ++j) {
-            acc = Ops::combine(acc, v[j]);
-            if ((endmask >> j) & 1u) {
-                if (first) {
-                    fkey = key;
-                    fval = acc;
-                    first = false;
-                } else {
-                    reinterpret_cast<Acc*>(L.sums)[key] = acc;  // run wholly inside this lane
-                }
-                ++key;
-                acc = Ops::identity();
-            }
-        }
-        const uint32_t lkey = live ? key : kNone;
-        const Acc lval = acc;
-        if (!multi) {
-            fkey = lkey;
-            fval = lval;
-        }
-        // segmented inclusive scan of the lanes' last runs (keys are monotone)
-        Acc c = lval;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const Acc up = Ops::shfl_up(c, d);
-            const uint32_t k = __shfl_up_sync(kFull, lkey, d);
-            if (lane >= d && k == lkey) c = Ops::combine(up, c);
-        }
-        const uint32_t prev_key = __shfl_up_sync(kFull, lkey, 1);
-        const Acc prev_c = Ops::shfl_up(c, 1);
-        const uint32_t next_first = __shfl_down_sync(kFull, fkey, 1);
-        if (multi && live) {
-            const Acc tot = (lane > 0 && prev_key == fkey) ? Ops::combine(prev_c, fval) : fval;
-            tile_emit(p, L, t, __ldg(L.tile_head + t), __ldg(L.tile_tail + t), fkey, tot);
-        }
-        if (lkey != kNone && (lane == 31 || next_first != lkey))
-            tile_emit(p, L, t, __ldg(L.tile_head + t), __ldg(L.tile_tail + t), lkey, c);
-    }
-}
-
 // Transposed variant: lane l gathers edges e_tile + 32 j + l (j < kTileK), so one
 // gather instruction covers 32 CONSECUTIVE edges. Inside a high-degree segment the
 // sources are sorted, and in the degree-sorted hot prefix consecutive sources sit
@@ -964,12 +867,7 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st) {
     int variant = (int)options().tile_minblocks;
     if (variant == 0) variant = (sizeof(typename Ops::Acc) >= 16) ? 4 : 6;
     using Pol = FusedPolicy<Ops>;
-    void (*kern)(const Pol, const TileLaunch);
-    if (options().tile_layout == 1)
-        kern = (variant == 8) ? k_tile<Pol, 8> : (variant == 6) ? k_tile<Pol, 6>
-             : (variant == 4) ? k_tile<Pol, 4> : k_tile<Pol, 1>;
-    else
-        kern = (variant == 8) ? k_tile_t<Pol, 8> : (variant == 6) ? k_tile_t<Pol, 6>
+    void (*kern)(const Pol, const TileLaunch) = (variant == 8) ? k_tile_t<Pol, 8> : (variant == 6) ? k_tile_t<Pol, 6>
              : (variant == 4) ? k_tile_t<Pol, 4> : k_tile_t<Pol, 1>;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, 0);

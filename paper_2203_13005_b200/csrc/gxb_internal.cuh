@@ -166,6 +166,11 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const void* ptr, uint64_t pol)
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
     return r;
 }
+__device__ __forceinline__ uint8_t ld_stream_u8(const uint8_t* ptr, uint64_t pol) {
+    uint16_t r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(r) : "l"(ptr), "l"(pol));
+    return (uint8_t)r;
+}
 __device__ __forceinline__ double ld_keep_f64(const double* ptr, uint64_t pol) {
     double r;
     asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
@@ -239,7 +244,6 @@ struct Options {
     int64_t l1_hot_kb = 160;      // L1 budget (KB) of the L1-allocating prefix (others bypass L1)
     int64_t push_alpha = 20;      // push when frontier out-edges * alpha < |E|
     int64_t pull_kernel = 0;      // 0 = warp tiles, 1 = degree-binned groups
-    int64_t tile_layout = 0;      // 0 = transposed (coalesced gathers), 1 = lane-contiguous
 };
 Options& options();
 

@@ -662,9 +662,6 @@ int gxb_set_option(const char* name, int64_t value) {
     } else if (n == "l1_hot_kb") {
         if (value < 0) return fail(GXB_EINVAL, "l1_hot_kb must be >= 0");
         o.l1_hot_kb = value;
-    } else if (n == "tile_layout") {
-        if (value != 0 && value != 1) return fail(GXB_EINVAL, "tile_layout: 0 = transposed, 1 = contiguous");
-        o.tile_layout = value;
     } else if (n == "pull_kernel") {
         if (value != 0 && value != 1) return fail(GXB_EINVAL, "pull_kernel: 0 = tiles, 1 = binned");
         o.pull_kernel = value;
@@ -682,7 +679,6 @@ int gxb_get_option(const char* name, int64_t* value) {
     else if (n == "l2_hot_mb") *value = o.l2_hot_mb;
     else if (n == "push_alpha") *value = o.push_alpha;
     else if (n == "pull_kernel") *value = o.pull_kernel;
-    else if (n == "tile_layout") *value = o.tile_layout;
     else if (n == "l1_hot_kb") *value = o.l1_hot_kb;
     else return fail(GXB_EINVAL, "unknown option " + n);
     return GXB_OK;
