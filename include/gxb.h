@@ -68,6 +68,10 @@ extern "C" {
 /* gxb_graph_build flags */
 #define GXB_BUILD_HOST_INPUT   0x1u  /* src/dst/w are host pointers (else device pointers) */
 #define GXB_BUILD_NO_CSR       0x2u  /* skip the push-mode CSR (PR/LP never push) */
+#define GXB_BUILD_ID_RANGES    0x4u  /* partitions = contiguous ascending-id ranges of even
+                                        vertex counts, as partition_graph(even_sizes) does
+                                        (A/graph.py:169-212); default = ranges balanced by
+                                        in-edges over the degree-sorted order */
 
 /* gxb_iterate direction policy */
 #define GXB_DIR_AUTO  0
@@ -143,6 +147,12 @@ int gxb_rmat_generate(gxb_ctx* ctx, const gxb_rmat_args* args, uint32_t* d_src,
 int gxb_graph_build(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint32_t* w,
                     uint64_t num_edges, int part, int nparts, uint32_t flags, void* stream,
                     gxb_graph** out);
+/* as gxb_graph_build with explicit per-partition vertex counts over ascending ids
+ * (the `sizes` argument of partition_graph, A/graph.py:175-191); sum must equal the
+ * number of present ids, else GXB_EINVAL */
+int gxb_graph_build_sized(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint32_t* w,
+                          uint64_t num_edges, int part, int nparts, const uint64_t* sizes, uint32_t flags,
+                          void* stream, gxb_graph** out);
 int gxb_graph_get_info(const gxb_graph* g, gxb_graph_info* out);
 /* ascending present ids (host buffer of num_vertices) */
 int gxb_graph_ids(const gxb_graph* g, uint32_t* host_out);

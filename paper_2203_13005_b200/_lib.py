@@ -22,7 +22,7 @@ GXB_ESTATE = -77
 
 ALGO_SSSP, ALGO_PAGERANK, ALGO_LP, ALGO_CC = 0, 1, 2, 3
 OP_GEN, OP_MERGE, OP_APPLY = 0, 1, 2
-BUILD_HOST_INPUT, BUILD_NO_CSR = 0x1, 0x2
+BUILD_HOST_INPUT, BUILD_NO_CSR, BUILD_ID_RANGES = 0x1, 0x2, 0x4
 DIR_AUTO, DIR_PULL, DIR_PUSH = 0, 1, 2
 BUF_VALUES, BUF_SEND, BUF_RECV, BUF_RECORD_SIZE = 0, 1, 2, 3
 
@@ -87,6 +87,7 @@ def _sig(L):
         "gxb_get_option": (I, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64)]),
         "gxb_rmat_generate": (I, [P, ctypes.POINTER(RmatArgs), P, P, P, P]),
         "gxb_graph_build": (I, [P, P, P, P, U64, I, I, U32, P, PP]),
+        "gxb_graph_build_sized": (I, [P, P, P, P, U64, I, I, P, U32, P, PP]),
         "gxb_graph_get_info": (I, [P, ctypes.POINTER(GraphInfo)]),
         "gxb_graph_ids": (I, [P, P]),
         "gxb_graph_out_degree": (I, [P, P]),

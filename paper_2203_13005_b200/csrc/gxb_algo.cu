@@ -1170,12 +1170,22 @@ int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, 
     cudaMemcpyAsync(s->d_fcount, fc, sizeof(fc), cudaMemcpyHostToDevice, st);
     s->frontier_len = nfront;
     s->units_cur = units0;
-    // the remote-active count of a PR round is static: every owned vertex is active
-    if (algo == GXB_ALGO_PAGERANK && g->nparts > 1) {
+    // remote-active count of the initial frontier (the GAS seed round's skip vote,
+    // A/agent.py:533-535); for PageRank it stays this value every round
+    if (g->nparts > 1) {
         std::vector<uint32_t> rb(s->words);
         cudaMemcpy(rb.data(), g->d_remote_src, 4 * ((V >> 5) + 1), cudaMemcpyDeviceToHost);
         uint64_t c = 0;
-        for (uint64_t i = g->lo; i < g->hi; ++i) c += (rb[i >> 5] >> (i & 31)) & 1u;
+        if (algo == GXB_ALGO_SSSP) {
+            for (int j = 0; j < s->nsrc; ++j) {
+                const uint32_t sl = s->src_slot[j];
+                bool dup = false;
+                for (int k = 0; k < j; ++k) dup |= s->src_present[k] && s->src_slot[k] == sl;
+                if (s->src_present[j] && !dup && sl >= g->lo && sl < g->hi) c += (rb[sl >> 5] >> (sl & 31)) & 1u;
+            }
+        } else {
+            for (uint64_t i = g->lo; i < g->hi; ++i) c += (rb[i >> 5] >> (i & 31)) & 1u;
+        }
         s->last.remote_active = c;
     }
     cudaError_t e = cudaStreamSynchronize(st);
@@ -1338,8 +1348,7 @@ int gxb_request(gxb_state* s, int op, uint64_t lo, uint64_t hi, void* stream) {
         GXB_CHECK(dalloc_t(&s->d_msg_valid, g->owned_edges + 1));
         GXB_CHECK(dalloc(&s->d_merged, 32 * (owned + 1)));
     }
-    if (!s->in_round) {
-        if (op != GXB_OP_GEN) return fail(GXB_ESTATE, "gxb_request: a round starts with GEN");
+    if (!s->in_round) {  // the first request of an iteration opens the round
         GXB_CHECK(collect_stats(s));
         GXB_CHECK(begin_round(s, st));
     }
@@ -1418,7 +1427,10 @@ int gxb_request(gxb_state* s, int op, uint64_t lo, uint64_t hi, void* stream) {
 
 int gxb_commit(gxb_state* s, void* stream) {
     if (!s) return fail(GXB_EINVAL, "gxb_commit: null state");
-    if (!s->in_round) return fail(GXB_ESTATE, "gxb_commit: no open round");
+    if (!s->in_round) {  // a partition with nothing to request still closes an (empty) round
+        GXB_CHECK(collect_stats(s));
+        GXB_CHECK(begin_round(s, (cudaStream_t)stream));
+    }
     return end_round(s, GXB_DIR_PULL, (cudaStream_t)stream);
 }
 

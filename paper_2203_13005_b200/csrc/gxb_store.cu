@@ -216,6 +216,22 @@ __global__ void k_lane_slot(const uint64_t* __restrict__ off, uint64_t nz, uint6
     }
 }
 
+// (partition of the dense id) << 32 | ~in-degree: ascending = by partition, then in-degree descending
+__global__ void k_part_keys(const uint32_t* __restrict__ indeg, uint64_t V, const uint64_t* __restrict__ idb,
+                            int nparts, uint64_t* keys) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < V; i += (uint64_t)gridDim.x * blockDim.x) {
+        int p = 0;
+        while (p + 1 < nparts && i >= idb[p + 1]) ++p;
+        keys[i] = ((uint64_t)p << 32) | (uint64_t)(0xFFFFFFFFu - indeg[i]);
+    }
+}
+
+__global__ void k_gather_indeg(const uint32_t* __restrict__ slot2dense, const uint32_t* __restrict__ indeg,
+                               uint64_t V, uint32_t* out) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < V; s += (uint64_t)gridDim.x * blockDim.x)
+        out[s] = indeg[slot2dense[s]];
+}
+
 static uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
 
 __global__ void k_low32(const uint64_t* __restrict__ keys, uint64_t n, uint32_t* out) {
@@ -484,12 +500,32 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
         k_emit_ids<<<grid_e(words), kBlock, 0, st>>>(bm, wpre, words, ids_dense);
         k_rank_edges<<<grid_e(E), kBlock, 0, st>>>(src, dst, E, bm, wpre, outdeg_d, indeg_d);
     }
-    // slot order: in-degree descending, ties by ascending id (stable sort)
+    // slot order: in-degree descending, ties by ascending id (stable sort). With
+    // GXB_BUILD_ID_RANGES the partitions are the reference's contiguous ascending-id
+    // ranges (partition_graph + even_sizes, A/graph.py:169-212) and the degree sort
+    // runs inside each range: key = (partition << 32) | ~in-degree.
+    const bool id_ranges = (flags & GXB_BUILD_ID_RANGES) != 0;
+    std::vector<uint64_t> id_bounds;
+    if (id_ranges) {
+        id_bounds.assign(g->nparts + 1, 0);
+        if (!g->part_sizes.empty()) {
+            uint64_t acc = 0;
+            for (int p = 0; p < g->nparts; ++p) acc += g->part_sizes[p];
+            if (acc != V) return fail(GXB_EINVAL, "partition sizes sum to " + std::to_string(acc) +
+                                                      ", expected " + std::to_string(V) + " vertices");
+            for (int p = 0; p < g->nparts; ++p) id_bounds[p + 1] = id_bounds[p] + g->part_sizes[p];
+        } else {
+            for (int p = 0; p < g->nparts; ++p) {  // even_sizes(V, m)
+                const uint64_t base = V / g->nparts, rem = V % g->nparts;
+                id_bounds[p + 1] = id_bounds[p] + base + ((uint64_t)p < rem ? 1 : 0);
+            }
+        }
+    }
     uint32_t *iota = nullptr, *slot2dense = nullptr, *indeg_slot = nullptr;
     GXB_CHECK(S.get(&iota, V));
     GXB_CHECK(S.get(&slot2dense, V));
     GXB_CHECK(S.get(&indeg_slot, V));
-    if (V) {
+    if (V && !id_ranges) {
         k_iota<<<grid_e(V), kBlock, 0, st>>>(iota, V);
         size_t temp = 0;
         GXB_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, temp, indeg_d, indeg_slot, iota,
@@ -498,6 +534,22 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
         GXB_CHECK(S.get(reinterpret_cast<uint8_t**>(&tmp), temp));
         GXB_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, temp, indeg_d, indeg_slot, iota,
                                                            slot2dense, (int64_t)V, 0, 32, st));
+    } else if (V) {
+        uint64_t *pkey = nullptr, *pkey_out = nullptr, *d_idb = nullptr;
+        GXB_CHECK(S.get(&pkey, V));
+        GXB_CHECK(S.get(&pkey_out, V));
+        GXB_CHECK(S.get(&d_idb, g->nparts + 1));
+        GXB_CUDA(cudaMemcpyAsync(d_idb, id_bounds.data(), 8 * (g->nparts + 1), cudaMemcpyHostToDevice, st));
+        k_iota<<<grid_e(V), kBlock, 0, st>>>(iota, V);
+        k_part_keys<<<grid_e(V), kBlock, 0, st>>>(indeg_d, V, d_idb, g->nparts, pkey);
+        size_t temp = 0;
+        GXB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, pkey, pkey_out, iota, slot2dense, (int64_t)V, 0,
+                                                 32 + bits_for((uint64_t)g->nparts), st));
+        void* tmp = nullptr;
+        GXB_CHECK(S.get(reinterpret_cast<uint8_t**>(&tmp), temp));
+        GXB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, temp, pkey, pkey_out, iota, slot2dense, (int64_t)V, 0,
+                                                 32 + bits_for((uint64_t)g->nparts), st));
+        k_gather_indeg<<<grid_e(V), kBlock, 0, st>>>(slot2dense, indeg_d, V, indeg_slot);
     }
     GXB_CHECK(dalloc_t(&g->d_dense2slot, V));
     GXB_CHECK(dalloc_t(&g->d_slot2id, V));
@@ -516,7 +568,9 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
     g->max_in_degree = maxin;
     g->bounds.assign(g->nparts + 1, 0);
     g->bounds[g->nparts] = V;
-    {
+    if (id_ranges) {
+        g->bounds = id_bounds;
+    } else {
         // per-slot cost in pull bytes: 12 per in-edge + 32 per vertex;
         // every rank computes the same bounds from the same edge list
         auto cost = [&](uint64_t s) { return 12ull * h_indeg[s] + 32ull; };
@@ -709,6 +763,12 @@ int gxb_shutdown(gxb_ctx* ctx) {
 int gxb_graph_build(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint32_t* w,
                     uint64_t num_edges, int part, int nparts, uint32_t flags, void* stream,
                     gxb_graph** out) {
+    return gxb_graph_build_sized(ctx, src, dst, w, num_edges, part, nparts, nullptr, flags, stream, out);
+}
+
+int gxb_graph_build_sized(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint32_t* w,
+                          uint64_t num_edges, int part, int nparts, const uint64_t* sizes, uint32_t flags,
+                          void* stream, gxb_graph** out) {
     if (!ctx || !ctx->alive) return fail(GXB_ESTATE, "gxb_graph_build: daemon not initialised");
     if (!out) return fail(GXB_EINVAL, "gxb_graph_build: null out");
     if (num_edges && (!src || !dst)) return fail(GXB_EINVAL, "gxb_graph_build: null edge arrays");
@@ -720,6 +780,10 @@ int gxb_graph_build(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst, cons
     g->ctx = ctx;
     g->part = part;
     g->nparts = nparts;
+    if (sizes) {
+        g->part_sizes.assign(sizes, sizes + nparts);
+        flags |= GXB_BUILD_ID_RANGES;
+    }
     int rc = graph_build_impl(g, src, dst, w, num_edges, flags, (cudaStream_t)stream);
     if (rc != GXB_OK) {
         graph_release(g);

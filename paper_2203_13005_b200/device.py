@@ -106,9 +106,19 @@ class DeviceGraph:
     """Device-resident CSC (+ push CSR) of one destination partition (A/graph.py:175-212)."""
 
     def __init__(self, ctx: DeviceContext, src, dst, w=None, part: int = 0, nparts: int = 1,
-                 csr: bool = True, stream=None):
+                 csr: bool = True, stream=None, partitioning: str = "edges", sizes=None):
+        """partitioning: "edges" = destination ranges balanced by in-edges over the
+        degree-sorted order (default); "ids" = the reference's contiguous ascending-id
+        ranges (even_sizes, or explicit `sizes`)."""
         self.ctx = ctx
         flags = 0 if csr else L.BUILD_NO_CSR
+        if partitioning not in ("edges", "ids"):
+            raise ValueError(f"unknown partitioning {partitioning!r}")
+        if partitioning == "ids" or sizes is not None:
+            flags |= L.BUILD_ID_RANGES
+        sizes_arr = None if sizes is None else np.ascontiguousarray(sizes, dtype=np.uint64)
+        if sizes_arr is not None and sizes_arr.size != nparts:
+            raise ValueError("one size per partition required")
         if hasattr(src, "is_cuda") and src.is_cuda:
             n = int(src.numel())
             keep = (src, dst, w)
@@ -127,8 +137,8 @@ class DeviceGraph:
             keep = (src, dst, w)
         self._keep = keep  # inputs must outlive the async copies
         h = ctypes.c_void_p()
-        L.check(L.lib().gxb_graph_build(ctx.handle, _vp(src), _vp(dst), _vp(w), n, part, nparts, flags,
-                                        _stream_ptr(stream), ctypes.byref(h)))
+        L.check(L.lib().gxb_graph_build_sized(ctx.handle, _vp(src), _vp(dst), _vp(w), n, part, nparts,
+                                              _vp(sizes_arr), flags, _stream_ptr(stream), ctypes.byref(h)))
         self._h = h
         self._keep = None
         info = L.GraphInfo()

@@ -1,0 +1,230 @@
+"""CPU-only tests of the host layer: generator, loader, algorithm descriptors,
+region protocol, daemon/agent lifecycle (with a recording fake device state),
+and the C-ABI surface of libgxb200.so (symbols only; no compute without a GPU)."""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+import re
+import threading
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, REPO
+
+from paper_2203_13005_b200 import channel as C
+from paper_2203_13005_b200.algorithms import (ConnectedComponents, LabelPropagation, PageRank,
+                                              SsspBellmanFord, make_algorithm)
+from paper_2203_13005_b200.graph import EdgeArrays, GraphParseError, even_sizes, load_edge_list
+from paper_2203_13005_b200.rmat import RmatParams, rmat_host
+
+
+# ---------------------------------------------------------------- generator
+@pytest.mark.parametrize("kw", [dict(scale=7), dict(scale=9, wmax=63, seed=4),
+                                dict(scale=10, symmetric=True, seed=2),
+                                dict(scale=8, a=0.65, b=0.15, c=0.15, scramble=False)])
+def test_rmat_host_matches_c_generator(oracle_lib, kw):
+    p = RmatParams(**kw)
+    s, d, w = rmat_host(p)
+    s2, d2, w2 = oracle_lib.rmat(p.scale, p.edge_factor, p.seed, p.a, p.b, p.c, p.wmax, p.scramble, p.symmetric)
+    np.testing.assert_array_equal(s, s2)
+    np.testing.assert_array_equal(d, d2)
+    assert (w is None and w2 is None) or np.array_equal(w, w2)
+
+
+def test_rmat_properties():
+    p = RmatParams(scale=12, seed=9, wmax=63)
+    s, d, w = rmat_host(p)
+    assert s.size == 16 << 12 and s.max() < 4096 and d.max() < 4096
+    assert w.min() >= 1 and w.max() <= 63
+    with pytest.raises(ValueError):
+        RmatParams(scale=0)
+    with pytest.raises(ValueError):
+        RmatParams(scale=10, a=0.6, b=0.3, c=0.2)
+
+
+# ---------------------------------------------------------------- loader
+def test_load_edge_list_matches_reference(tmp_path):
+    with open(os.path.join(GOLDEN, "edge_lists.json")) as fh:
+        cases = json.load(fh)
+    for name, case in cases.items():
+        p = tmp_path / f"{name}.txt"
+        p.write_bytes(case["text"].encode("ascii"))
+        if case["ok"]:
+            vertices, edges = load_edge_list(p)
+            assert sorted(vertices) == case["vertices"], name
+            assert [[e.src, e.dst, e.weight] for e in edges] == case["edges"], name
+        else:
+            with pytest.raises(GraphParseError) as exc:
+                load_edge_list(p)
+            assert exc.value.lineno == case["lineno"], name
+            assert str(exc.value) == case["message"], name
+
+
+def test_edge_arrays():
+    ea = EdgeArrays.from_edges([(5, 7), (7, 5, 2.0), (5, 5)])
+    assert ea.vertex_ids().tolist() == [5, 7]
+    assert ea.out_degree() == {5: 2, 7: 1}
+    assert ea.weight is not None and ea.weight.tolist() == [1.0, 2.0, 1.0]
+    assert even_sizes(10, 3) == [4, 3, 3]
+
+
+# ---------------------------------------------------------------- algorithms
+def test_make_algorithm_semantics():
+    a = make_algorithm("sssp", {5, 9, 2, 14, 30}, None)
+    assert isinstance(a, SsspBellmanFord) and a.sources == [2, 5, 9, 14]
+    assert make_algorithm("sssp", {3, 1}, None).sources == [1, 3]
+    with pytest.raises(ValueError, match="pagerank needs the global out-degree table"):
+        make_algorithm("pagerank", {1}, None)
+    with pytest.raises(ValueError, match="unknown algorithm"):
+        make_algorithm("bfs", {1}, {})
+    with pytest.raises(ValueError, match="at least one source"):
+        SsspBellmanFord([])
+    pr = make_algorithm("pagerank", {0, 1}, {0: 1, 1: 0})
+    assert isinstance(pr, PageRank) and pr.base == 0.15 and pr.damping == 0.85
+    assert pr.initial_attr(0) == (1.0, 1) and pr.default_iteration_cap(5) == 100
+    assert pr.vote(1e-10, set()) and not pr.vote(1e-8, set())
+    assert isinstance(make_algorithm("lp", {1}), LabelPropagation)
+    assert isinstance(make_algorithm("cc", {1}), ConnectedComponents)
+    s = SsspBellmanFord([0, 3])
+    assert s.initial_attr(3) == (float("inf"), 0.0) and s.format_attr((1.0, float("inf"))) == "1.0 inf"
+
+
+# ---------------------------------------------------------------- region protocol
+def test_trace_conformance_and_rotation():
+    assert C.trace_conforms([])
+    assert C.trace_conforms("ExchangeFinished RotateFinished ComputeAllFinished".split())
+    ok = "ExchangeFinished RotateFinished ComputeFinished ExchangeFinished RotateFinished ComputeAllFinished Shutdown"
+    assert C.trace_conforms(ok.split())
+    assert not C.trace_conforms("ExchangeFinished ComputeFinished".split())
+    r = C.SharedRegion("k", 4)
+    assert r.roles() == (C.Role.NEW, C.Role.COMPUTE, C.Role.UPLOAD)
+    C.rotate(r)
+    assert r.roles() == (C.Role.COMPUTE, C.Role.UPLOAD, C.Role.NEW) and r.cycle_count == 1
+
+
+class FakeDeviceState:
+    """Records the range requests a daemon executes (no GPU)."""
+
+    def __init__(self, owned_edges=100, owned=(0, 40), fail_on=None):
+        self.calls = []
+        self.fail_on = fail_on
+        self.algo = "cc"
+
+        class _G:
+            pass
+        self.graph = _G()
+        self.graph.owned = owned
+        self.graph.info = type("I", (), {"owned_edges": owned_edges})()
+        self.commits = 0
+
+    def request(self, op, lo, hi):
+        if self.fail_on is not None and op == self.fail_on:
+            raise ValueError("apply targets vertex 99 not owned by this node")
+        self.calls.append((op, lo, hi))
+
+    def commit(self):
+        self.commits += 1
+
+    def iterate(self, direction="auto"):
+        self.calls.append(("fused",))
+
+    def stats(self):
+        return {"remote_active": 0, "voted": 1, "changed": 0, "next_active": 0}
+
+
+def test_daemon_lifecycle_and_protocol():
+    from paper_2203_13005_b200.daemon import AcceleratorProfile, GpuDaemon, daemon_init, execute_request
+    regions = {"r0": C.SharedRegion("r0", 8)}
+    with pytest.raises(KeyError):
+        GpuDaemon(AcceleratorProfile(4), None, "nope", regions)
+    st = FakeDeviceState()
+    d = daemon_init(AcceleratorProfile(4), None, "r0", regions, st)
+    assert d.init_count == 1
+    with pytest.raises(C.ProtocolError, match="re-initialization"):
+        d.initialize()
+    with pytest.raises(ValueError):
+        AcceleratorProfile(0)
+    item = C.WorkItem(C.OpKind.GEN, 0, C.RangeDescriptor(0, 8), 8)
+    cost = execute_request(st, AcceleratorProfile(4, 2.0, 3.0), item)
+    assert cost == 3.0 + 2.0 * 8 and item.result_units == 8
+    d.shutdown()
+    d.shutdown()  # idempotent
+
+
+def test_agent_request_protocol_round_robin():
+    from paper_2203_13005_b200.agent import GpuAgent
+    from paper_2203_13005_b200.daemon import AcceleratorProfile
+    st = FakeDeviceState(owned_edges=100, owned=(10, 50))
+    a = GpuAgent(0, st, make_algorithm("cc", [1]), block_size=16)
+    with pytest.raises(C.ProtocolError):
+        a.request(C.OpKind.GEN)
+    a.connect([AcceleratorProfile(4), AcceleratorProfile(4)])
+    with pytest.raises(C.ProtocolError):
+        a.connect([AcceleratorProfile(4)])
+    a.begin_iteration()
+    a.gen_phase()
+    a.merge_apply_phase()
+    gens = sorted(c for c in st.calls if c[0] == 0)
+    assert gens[0] == (0, 0, 16) and gens[-1] == (0, 96, 100) and len(gens) == 7
+    merges = sorted(c for c in st.calls if c[0] == 1)
+    assert merges[0][1] == 10 and merges[-1][2] == 50
+    assert st.commits == 1 and a.vote() and a.round_closed()
+    for d in a.daemons:
+        assert C.trace_conforms(d.region.trace) and d.region.copy_count == 0
+    # transfer checks (A/agent.py:208-222)
+    with pytest.raises(KeyError):
+        a.transfer(C.WorkItem(C.OpKind.GEN, 0, C.RangeDescriptor(0, 1), 1), "missing")
+    with pytest.raises(ValueError, match="exceeds slot capacity"):
+        a.transfer(C.WorkItem(C.OpKind.GEN, 0, C.RangeDescriptor(0, 99), 99), "node0-daemon0")
+    with pytest.raises(ValueError):
+        a.update("sideways")
+    a.shutdown()
+
+
+def test_daemon_error_surfaces_to_agent():
+    from paper_2203_13005_b200.agent import GpuAgent
+    from paper_2203_13005_b200.daemon import AcceleratorProfile
+    st = FakeDeviceState(fail_on=2)
+    a = GpuAgent(0, st, make_algorithm("cc", [1]), block_size=64, recv_timeout=10)
+    a.connect([AcceleratorProfile(4)])
+    a.begin_iteration()
+    a.request(C.OpKind.GEN)
+    with pytest.raises(ValueError, match="not owned"):
+        a.request(C.OpKind.APPLY)
+    a.shutdown()
+
+
+# ---------------------------------------------------------------- C ABI surface
+def test_abi_exports_every_declared_symbol():
+    """libgxb200.so loads on a CPU-only host and exports each function of include/gxb.h."""
+    from paper_2203_13005_b200 import _lib as L
+    with open(os.path.join(REPO, "include", "gxb.h")) as fh:
+        text = fh.read()
+    names = sorted(set(re.findall(r"^\s*(?:const\s+char\*|int|void)\s+(gxb_\w+)\s*\(", text, re.M)))
+    assert len(names) >= 25
+    lib = ctypes.CDLL(L.LIB_PATH)
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    assert L.lib().gxb_version().startswith(b"gxb200")
+    # no GPU here: gxb_init reports an error instead of crashing
+    import torch
+    if not torch.cuda.is_available():
+        h = ctypes.c_void_p()
+        assert L.lib().gxb_init(0, ctypes.byref(h)) != 0
+        assert L.lib().gxb_last_error()
+
+
+def test_options_roundtrip():
+    from paper_2203_13005_b200 import _lib as L
+    old = L.get_option("push_alpha")
+    L.set_option("push_alpha", 13)
+    assert L.get_option("push_alpha") == 13
+    L.set_option("push_alpha", old)
+    with pytest.raises(ValueError):
+        L.set_option("no_such_knob", 1)
+    with pytest.raises(ValueError):
+        L.set_option("tile_minblocks", 3)
