@@ -66,11 +66,17 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
     __device__ static void fold(Acc& a, Msg m) { a.s += m; }
     // Apply: 0.15 + 0.85 * sum with two roundings (157-159; no FMA contraction),
     // convergence_stat |new - old| (161-162), always active.
-    __device__ void apply(uint32_t slot, Acc a, LocalStats& st) const {
-        const double old = rank[slot];
+    struct Pre {
+        double old;
+        uint32_t od;
+    };
+    __device__ Pre preload(uint32_t slot) const { return {rank[slot], __ldg(f.outdeg + slot)}; }
+    __device__ void apply(uint32_t slot, Acc a, LocalStats& st) const { apply_pre(slot, a, preload(slot), st); }
+    __device__ void apply_pre(uint32_t slot, Acc a, Pre p, LocalStats& st) const {
+        const double old = p.old;
         const double nw = __dadd_rn(0.15, __dmul_rn(0.85, a.s));
         rank[slot] = nw;
-        const uint32_t od = __ldg(f.outdeg + slot);
+        const uint32_t od = p.od;
         contrib_next[slot] = od ? __ddiv_rn(nw, (double)od) : 0.0;
         if (nw != old) {
             st.changed++;
@@ -126,10 +132,18 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
     }
     __device__ static void fold(Acc& a, Msg m) { a.m = min4(a.m, m); }
     // Apply: elementwise min, active iff changed (113-115)
+    struct Pre {
+        uint4 o;
+    };
+    __device__ Pre preload(uint32_t slot) const { return {dist_cur[slot]}; }
     __device__ void apply(uint32_t slot, Acc a, LocalStats& st) const {
         if (!has(a)) return;
+        apply_pre(slot, a, preload(slot), st);
+    }
+    __device__ void apply_pre(uint32_t slot, Acc a, Pre p, LocalStats& st) const {
+        if (!has(a)) return;
         st.targets++;
-        const uint4 o = dist_cur[slot];
+        const uint4 o = p.o;
         const uint4 n = min4(o, a.m);
         if (!eq4(n, o)) {
             dist_next[slot] = n;
@@ -164,10 +178,18 @@ struct CcOps {  // min-label propagation; labels < 0xFFFF
         return true;
     }
     __device__ static void fold(Acc& a, Msg m) { a.m = min(a.m, m); }
+    struct Pre {
+        uint32_t o;
+    };
+    __device__ Pre preload(uint32_t slot) const { return {lab_cur[slot]}; }
     __device__ void apply(uint32_t slot, Acc a, LocalStats& st) const {
         if (!has(a)) return;
+        apply_pre(slot, a, preload(slot), st);
+    }
+    __device__ void apply_pre(uint32_t slot, Acc a, Pre p, LocalStats& st) const {
+        if (!has(a)) return;
         st.targets++;
-        const uint32_t o = lab_cur[slot];
+        const uint32_t o = p.o;
         const uint32_t n = min(o, a.m);
         if (n != o) {
             lab_next[slot] = n;
@@ -363,6 +385,7 @@ struct TileLaunch {
     uint64_t owned_edges;
     const uint64_t* in_off;
     const uint32_t* in_src;
+    const uint64_t* tile_start;
     const uint32_t* lane_slot;
     const uint8_t* lane_mask;
     const uint32_t* in_w;
@@ -418,13 +441,16 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_t(const Pol p, cons
     uint64_t t = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
     uint32_t nidx[kTileK], nw[kTileK];
     uint32_t nsa = 0, nmask = 0;
+    uint64_t nbeg = 0, nend = 0;
 #pragma unroll
     for (int j = 0; j < kTileK; ++j) {
         nidx[j] = 0;
         nw[j] = 1;
     }
     auto prefetch = [&](uint64_t tt) {
-        const uint64_t e = tt * kTileEdges + (uint64_t)lane;
+        nbeg = tt * kTileEdges;  // fixed tiles (tile_start[t] == t * kTileEdges)
+        nend = min(nbeg + kTileEdges, L.owned_edges);
+        const uint64_t e = nbeg + (uint64_t)lane;
 #pragma unroll
         for (int j = 0; j < kTileK; ++j) nidx[j] = ld_stream_u32(L.in_src + e + 32 * j, pol);
         if (weighted) {
@@ -436,7 +462,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_t(const Pol p, cons
     };
     if (t < L.num_tiles) prefetch(t);
     for (; t < L.num_tiles; t += nwarps) {
-        const uint64_t et = t * kTileEdges;
+        const uint64_t et = nbeg, tend = nend;
         uint32_t idx[kTileK], wgt[kTileK];
 #pragma unroll
         for (int j = 0; j < kTileK; ++j) {
@@ -450,19 +476,21 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_t(const Pol p, cons
 #pragma unroll
         for (int j = 0; j < kTileK; ++j) {
             Acc v = Ops::identity();
-            if (et + 32 * j + lane < L.owned_edges) p.accumulate_w(v, idx[j], wgt[j]);
+            if (et + 32 * j + lane < tend) p.accumulate_w(v, idx[j], wgt[j]);
             buf[tpos(32 * j + lane)] = v;
         }
         __syncwarp();
         const uint64_t e0 = et + (uint64_t)lane * kTileK;
-        const bool live = e0 < L.owned_edges;
+        const bool live = e0 < tend;
         Acc v[kTileK];
 #pragma unroll
         for (int j = 0; j < kTileK; ++j) v[j] = buf[tpos(kTileK * lane + j)];
         __syncwarp();
-        const uint32_t nvalid = live ? (uint32_t)min((uint64_t)kTileK, L.owned_edges - e0) : 0u;
+        const uint32_t nvalid = live ? (uint32_t)min((uint64_t)kTileK, tend - e0) : 0u;
+        // the run holding the last valid edge is the lane's last run (it may continue into the
+        // next lane); ends past the valid edges do not exist
         endmask &= (1u << nvalid) - 1u;
-        endmask &= ~(1u << (kTileK - 1));
+        if (nvalid) endmask &= ~(1u << (nvalid - 1));
         uint32_t fkey = kNone;
         Acc fval = Ops::identity();
         const bool multi = endmask != 0;
@@ -531,9 +559,25 @@ template <class Ops>
 __global__ void __launch_bounds__(kBlock) k_apply_sums(const Ops ops, const typename Ops::Acc* __restrict__ sums,
                                                         uint64_t lo, uint64_t owned, uint64_t nz,
                                                         StatStripe* stats) {
+    // four independent slots per step: all loads are issued before any store
+    constexpr int kU = 4;
     LocalStats st;
-    for (uint64_t r = blockIdx.x * (uint64_t)kBlock + threadIdx.x; r < owned; r += (uint64_t)gridDim.x * kBlock)
-        ops.apply((uint32_t)(lo + r), r < nz ? sums[r] : Ops::identity(), st);
+    const uint64_t stride = (uint64_t)gridDim.x * kBlock;
+    for (uint64_t r0 = blockIdx.x * (uint64_t)kBlock + threadIdx.x; r0 < owned; r0 += kU * stride) {
+        typename Ops::Acc a[kU];
+        typename Ops::Pre pre[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint64_t r = r0 + u * stride;
+            a[u] = (r < nz) ? sums[r] : Ops::identity();
+            if (r < owned) pre[u] = ops.preload((uint32_t)(lo + r));
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint64_t r = r0 + u * stride;
+            if (r < owned) ops.apply_pre((uint32_t)(lo + r), a[u], pre[u], st);
+        }
+    }
     flush_stats(st, stats);
 }
 
@@ -843,6 +887,7 @@ TileLaunch tile_launch(gxb_state* s) {
     L.owned_edges = g->owned_edges;
     L.in_off = g->d_in_off;
     L.in_src = g->d_in_src;
+    L.tile_start = T.d_tile_start;
     L.lane_slot = T.d_lane_slot;
     L.lane_mask = T.d_lane_mask;
     L.in_w = g->d_in_w;

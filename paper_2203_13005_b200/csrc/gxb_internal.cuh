@@ -56,6 +56,7 @@ struct TilePlan {
     uint64_t num_tiles = 0;
     uint64_t num_spans = 0;      // slots whose edges cross a tile boundary
     uint64_t num_partials = 0;   // sum of tiles touched by spans
+    uint64_t* d_tile_start = nullptr;  // num_tiles + 1 tile boundaries (edge offsets, slot-aligned)
     uint32_t* d_lane_slot = nullptr;   // per kTileK-edge lane chunk: slot of its first edge
     uint8_t* d_lane_mask = nullptr;    // per lane chunk: bit j <=> edge kTileK*c + j closes its segment
     uint32_t* d_tile_head = nullptr;   // per tile: span id of its first slot if that slot started earlier

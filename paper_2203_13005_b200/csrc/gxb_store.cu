@@ -194,13 +194,21 @@ __global__ void k_fill_u64(uint64_t* a, uint64_t n, uint64_t v) {
     for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) a[i] = v;
 }
 
-// lane-chunk tables of the warp tiles: slot (relative) containing edge kTileK * c,
-// and the bitmask of the chunk's positions that close a destination segment
-__global__ void k_lane_slot(const uint64_t* __restrict__ off, uint64_t nz, uint64_t nchunks, uint32_t* out,
-                            uint8_t* mask) {
+// lane-chunk tables of the warp tiles: lane l of tile t covers edges
+// [start_t + kTileK l, start_t + kTileK (l + 1)) clipped to the tile; its slot
+// (relative) is the one containing the first edge, and bit j of its mask marks a
+// position that closes a destination segment
+__global__ void k_lane_slot(const uint64_t* __restrict__ off, uint64_t nz, const uint64_t* __restrict__ tstart,
+                            uint64_t nchunks, uint32_t* out, uint8_t* mask) {
     for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nchunks;
          c += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t e = c * kTileK;
+        const uint64_t t = c >> 5, l = c & 31;
+        const uint64_t e = tstart[t] + l * kTileK, tend = tstart[t + 1];
+        if (e >= tend) {
+            out[c] = 0;
+            mask[c] = 0;
+            continue;
+        }
         uint64_t lo = 0, hi = nz;  // last s with off[s] <= e
         while (hi - lo > 1) {
             const uint64_t mid = (lo + hi) >> 1;
@@ -210,7 +218,7 @@ __global__ void k_lane_slot(const uint64_t* __restrict__ off, uint64_t nz, uint6
         uint32_t m = 0;
         for (int k = 1; k <= kTileK; ++k) {  // every in-degree >= 1 here: at most kTileK ends
             const uint64_t b = (lo + k <= nz) ? off[lo + k] : ~0ull;
-            if (b > e && b <= e + kTileK) m |= 1u << (uint32_t)(b - e - 1);
+            if (b > e && b <= e + kTileK && b <= tend) m |= 1u << (uint32_t)(b - e - 1);
         }
         mask[c] = (uint8_t)m;
     }
@@ -319,6 +327,7 @@ static void graph_release(gxb_graph* g) {
     dfree(g->plan.d_item_count);
     dfree(g->plan.d_slot_arrive);
     dfree(g->tiles.d_lane_slot);
+    dfree(g->tiles.d_tile_start);
     dfree(g->tiles.d_lane_mask);
     dfree(g->tiles.d_tile_head);
     dfree(g->tiles.d_tile_tail);
@@ -338,31 +347,38 @@ static int build_tile_plan(gxb_graph* g, cudaStream_t st) {
     uint64_t nz = 0;
     while (nz < owned && deg[nz] > 0) ++nz;
     T.nz_slots = nz;
-    T.num_tiles = (g->owned_edges + kTileEdges - 1) / kTileEdges;
-    const uint64_t nchunks = T.num_tiles * 32;
-    GXB_CHECK(dalloc_t(&T.d_lane_slot, nchunks + 32));
-    GXB_CHECK(dalloc_t(&T.d_lane_mask, nchunks + 32));
-    if (nchunks)
-        k_lane_slot<<<grid_e(nchunks), kBlock, 0, st>>>(g->d_in_off, nz, nchunks, T.d_lane_slot, T.d_lane_mask);
+    // Fixed tiles of kTileEdges edges (measured faster than slot-aligned variable tiles:
+    // those leave lanes idle at every cut); slots crossing a tile boundary become spans
+    // whose per-tile partials are folded by k_span_fold.
+    std::vector<uint64_t> off(nz + 1, 0);
+    for (uint64_t s = 0; s < nz; ++s) off[s + 1] = off[s] + deg[s];
+    const uint64_t E = off[nz];
+    std::vector<uint64_t> starts;
+    starts.reserve(E / kTileEdges + 2);
+    for (uint64_t pos = 0; pos < E; pos += kTileEdges) starts.push_back(pos);
+    T.num_tiles = starts.size();
+    starts.push_back(E);
+    // span table: slots crossing a tile boundary (hubs)
     std::vector<uint32_t> head(T.num_tiles + 1, kNone), tail(T.num_tiles + 1, kNone);
     std::vector<uint32_t> sfirst, scount, sslot;
     std::vector<uint64_t> spbase;
-    uint64_t off = 0, pbase = 0;
+    uint64_t pbase = 0, t = 0;
     for (uint64_t s = 0; s < nz; ++s) {
-        const uint64_t b = off, e = off + deg[s];
-        const uint64_t t0 = b / kTileEdges, t1 = (e - 1) / kTileEdges;
-        if (t0 != t1) {
-            const uint32_t k = (uint32_t)sfirst.size();
-            sfirst.push_back((uint32_t)t0);
-            scount.push_back((uint32_t)(t1 - t0 + 1));
-            sslot.push_back((uint32_t)s);
-            spbase.push_back(pbase);
-            pbase += t1 - t0 + 1;
-            tail[t0] = k;
-            for (uint64_t t = t0 + 1; t <= t1; ++t) head[t] = k;
-            for (uint64_t t = t0 + 1; t < t1; ++t) tail[t] = k;
-        }
-        off = e;
+        if (off[s] / kTileEdges == (off[s + 1] - 1) / kTileEdges) continue;  // inside one tile
+        while (t + 1 < T.num_tiles && starts[t + 1] <= off[s]) ++t;
+        uint64_t t1 = t;
+        while (t1 + 1 < T.num_tiles && starts[t1 + 1] < off[s + 1]) ++t1;
+        if (t1 == t) continue;
+        const uint32_t k = (uint32_t)sfirst.size();
+        sfirst.push_back((uint32_t)t);
+        scount.push_back((uint32_t)(t1 - t + 1));
+        sslot.push_back((uint32_t)s);
+        spbase.push_back(pbase);
+        pbase += t1 - t + 1;
+        tail[t] = k;
+        for (uint64_t u = t + 1; u <= t1; ++u) head[u] = k;
+        for (uint64_t u = t + 1; u < t1; ++u) tail[u] = k;
+        t = t1;
     }
     T.num_spans = sfirst.size();
     T.num_partials = pbase;
@@ -374,6 +390,7 @@ static int build_tile_plan(gxb_graph* g, cudaStream_t st) {
             cudaMemcpyAsync(*d, h.data(), sizeof(h[0]) * h.size(), cudaMemcpyHostToDevice, st) != cudaSuccess)
             rc = fail(GXB_ECUDA, "tile plan upload");
     };
+    up(&T.d_tile_start, starts);
     up(&T.d_tile_head, head);
     up(&T.d_tile_tail, tail);
     up(&T.d_span_first, sfirst);
@@ -381,6 +398,12 @@ static int build_tile_plan(gxb_graph* g, cudaStream_t st) {
     up(&T.d_span_pbase, spbase);
     up(&T.d_span_slot, sslot);
     GXB_CHECK(rc);
+    const uint64_t nchunks = T.num_tiles * 32;
+    GXB_CHECK(dalloc_t(&T.d_lane_slot, nchunks + 32));
+    GXB_CHECK(dalloc_t(&T.d_lane_mask, nchunks + 32));
+    if (nchunks)
+        k_lane_slot<<<grid_e(nchunks), kBlock, 0, st>>>(g->d_in_off, nz, T.d_tile_start, nchunks, T.d_lane_slot,
+                                                         T.d_lane_mask);
     GXB_CHECK(dalloc_t(&T.d_span_arrive, T.num_spans + 1));
     GXB_CUDA(cudaMemsetAsync(T.d_span_arrive, 0, 4 * (T.num_spans + 1), st));
     GXB_CUDA(cudaStreamSynchronize(st));
@@ -571,9 +594,10 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
     if (id_ranges) {
         g->bounds = id_bounds;
     } else {
-        // per-slot cost in pull bytes: 12 per in-edge + 32 per vertex;
+        // per-slot cost: 12 B per in-edge (index + gathered value) and 64 B-equivalent per
+        // vertex (apply, stats, span folding measured at ~5 edges' worth on B200);
         // every rank computes the same bounds from the same edge list
-        auto cost = [&](uint64_t s) { return 12ull * h_indeg[s] + 32ull; };
+        auto cost = [&](uint64_t s) { return 12ull * h_indeg[s] + 64ull; };
         uint64_t total = 0;
         for (uint64_t s = 0; s < V; ++s) total += cost(s);
         uint64_t acc = 0, s = 0;

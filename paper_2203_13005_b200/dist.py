@@ -118,6 +118,7 @@ class PartitionedRun:
     enable_skip: bool = True
     records: list = field(default_factory=list)
     device: object = None
+    phase_times: dict | None = None   # per-phase seconds when profiling (adds a sync per phase)
 
     def __post_init__(self):
         self.algo = self.state.algo
@@ -156,12 +157,27 @@ class PartitionedRun:
         return device_view(ptr, nbytes, dtype)
 
     # ---- one iteration ----------------------------------------------------
+    def _tick(self, name, t0):
+        if self.phase_times is not None:
+            import time
+            import torch
+            if self.device is not None:
+                torch.cuda.synchronize(self.device)
+            t = time.perf_counter()
+            self.phase_times[name] = self.phase_times.get(name, 0.0) + (t - t0)
+            return t
+        return t0
+
     def step(self, direction: str = "auto") -> StepRecord:
+        import time
+        t0 = time.perf_counter() if self.phase_times is not None else 0.0
         self.state.iterate(direction)
         st = self.state.stats()
+        t0 = self._tick("compute", t0)
         counts, max_stat = self.comm.vote(
             [st["changed"], st["next_active"], st["next_units"], st["remote_active"]], st["max_stat"],
             self.device)
+        t0 = self._tick("vote", t0)
         changed, next_active, next_units, remote_active = counts
         self.iteration += 1
         # skip iff no next-active vertex anywhere has a consumer on another partition
@@ -169,6 +185,7 @@ class PartitionedRun:
         moved = 0
         if not skip:
             moved = self._exchange_dense() if self.algo == "pagerank" else self._exchange_delta()
+        t0 = self._tick("exchange", t0)
         if self.algo == "pagerank":
             converged = max_stat < 1e-9           # PageRank.vote (A/algorithms.py:164-165)
         else:
