@@ -150,3 +150,22 @@ def test_write_attrs_round_trip(ctx):
             bad[0, 0] = 0.5
             with pytest.raises(ValueError):
                 s2.write_attrs(bad)
+
+
+def test_compat_drop_in_with_reference_shaped_objects():
+    """compat.run_partitioned takes reference-shaped Algorithm / RunConfig / PartitionedGraph."""
+    from types import SimpleNamespace
+    from paper_2203_13005_b200 import compat
+    from paper_2203_13005_b200.graph import Edge
+    edges = [Edge(0, 1, 2.0), Edge(1, 2, 3.0), Edge(2, 0, 1.0), Edge(3, 2, 1.0)]
+    parts = [SimpleNamespace(vertices={0: None, 1: None}, edges=edges[:2]),
+             SimpleNamespace(vertices={2: None, 3: None}, edges=edges[2:])]
+    graph = SimpleNamespace(partitions=parts)
+    algo = SimpleNamespace(name="sssp", sources=[0, 3])
+    cfg = SimpleNamespace(partitions=2, daemons_per_node=1, block_size=256, enable_cache=False, cache_capacity=8,
+                          cache_decay=0.5, cache_boost=1.0, enable_skip=False, io_cost=0.01, seed=0,
+                          max_iterations=None, barrier_timeout=60.0)
+    attrs, metrics = compat.run_partitioned(graph, algo, SimpleNamespace(value="bsp"), cfg)
+    inf = float("inf")
+    assert attrs == {0: (0.0, 2.0), 1: (2.0, 4.0), 2: (5.0, 1.0), 3: (inf, 0.0)}
+    assert metrics.converged and metrics.protocol_conformant()
