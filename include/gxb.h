@@ -72,6 +72,9 @@ extern "C" {
                                         vertex counts, as partition_graph(even_sizes) does
                                         (A/graph.py:169-212); default = ranges balanced by
                                         in-edges over the degree-sorted order */
+#define GXB_BUILD_RANGES       0x8u  /* contiguous degree-sorted ranges balanced by in-edge
+                                        cost instead of the default round-robin deal of the
+                                        degree-sorted order (nparts > 1) */
 
 /* gxb_iterate direction policy */
 #define GXB_DIR_AUTO  0
@@ -138,6 +141,9 @@ int gxb_rmat_generate(gxb_ctx* ctx, const gxb_rmat_args* args, uint32_t* d_src,
 
 /* ---- graph store (A/graph.py:175-212) ----
  * Builds the device store from E edges (src[i] -> dst[i], weight w[i] or 1).
+ * Default partitioning for nparts > 1: the in-degree-sorted order is dealt
+ * round-robin (each partition gets every nparts-th vertex, hence the same share of
+ * hubs and of the tail) and each partition's share is one contiguous slot range.
  * Weights are non-negative integers (u32); the float64 reference weights are
  * accepted by the Python layer only when integral.
  * nparts/part: destination-range partition (part in [0, nparts)); every rank

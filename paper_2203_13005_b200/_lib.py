@@ -22,7 +22,7 @@ GXB_ESTATE = -77
 
 ALGO_SSSP, ALGO_PAGERANK, ALGO_LP, ALGO_CC = 0, 1, 2, 3
 OP_GEN, OP_MERGE, OP_APPLY = 0, 1, 2
-BUILD_HOST_INPUT, BUILD_NO_CSR, BUILD_ID_RANGES = 0x1, 0x2, 0x4
+BUILD_HOST_INPUT, BUILD_NO_CSR, BUILD_ID_RANGES, BUILD_RANGES = 0x1, 0x2, 0x4, 0x8
 DIR_AUTO, DIR_PULL, DIR_PUSH = 0, 1, 2
 BUF_VALUES, BUF_SEND, BUF_RECV, BUF_RECORD_SIZE = 0, 1, 2, 3
 

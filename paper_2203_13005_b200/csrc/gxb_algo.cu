@@ -37,6 +37,15 @@ namespace gxb {
 // algorithm semantics
 // ======================================================================
 
+// Degree rank of a slot within its partition block. Slots are in-degree-sorted per
+// partition (a dealt multi-GPU layout starts every block with its hubs); the rank
+// selects the L1/L2 residency hint, so an approximate block index is fine:
+// q = umulhi(s, magic) ~ s / block, rank = s - q * block.
+struct HotPrefix {
+    uint32_t block = 0xFFFFFFFFu, magic = 0;
+    __device__ __forceinline__ uint32_t rank(uint32_t s) const { return s - __umulhi(s, magic) * block; }
+};
+
 struct PrOps {  // PageRank (A/algorithms.py:125-171)
     struct Acc {
         double s;
@@ -46,8 +55,9 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
     double* rank;
     double* contrib_next;
     FrontierView f;
-    uint32_t hot;  // slots [0, hot) keep L2 priority (degree-sorted: the most-gathered sources)
-    uint32_t hot1; // slots [0, hot1) also allocate in L1; the rest bypass L1
+    HotPrefix hp;  // degree rank of a slot inside its partition block
+    uint32_t hot;  // ranks [0, hot) keep L2 priority (degree-sorted: the most-gathered sources)
+    uint32_t hot1; // ranks [0, hot1) also allocate in L1; the rest bypass L1
 
     __device__ static Acc identity() { return {0.0}; }
     __device__ static Acc combine(Acc a, Acc b) { return {a.s + b.s}; }
@@ -59,8 +69,9 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
     // Gen: rank / out_deg of the source (every vertex is active, 144-145)
     static constexpr bool kWeighted = false;
     __device__ bool gen(uint32_t s, uint32_t, Msg& m) const {
-        const uint64_t pol = s < hot ? l2_evict_last() : l2_evict_first();
-        m = s < hot1 ? ld_l1_f64(contrib_cur + s, pol) : ld_nol1_f64(contrib_cur + s, pol);
+        const uint32_t r = hp.rank(s);
+        const uint64_t pol = r < hot ? l2_evict_last() : l2_evict_first();
+        m = r < hot1 ? ld_l1_f64(contrib_cur + s, pol) : ld_nol1_f64(contrib_cur + s, pol);
         return true;
     }
     __device__ static void fold(Acc& a, Msg m) { a.s += m; }
@@ -106,6 +117,7 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
     uint4* dist_next;
     const uint32_t* active_cur;
     FrontierView f;
+    HotPrefix hp;
     uint32_t hot, hot1;
     static constexpr bool kWeighted = true;
 
@@ -125,8 +137,9 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
     // Gen: d + w per lane from an active source (102-105); inf stays inf
     __device__ bool gen(uint32_t s, uint32_t w, Msg& m) const {
         if (!bit_test(active_cur, s)) return false;
-        const uint64_t pol = s < hot ? l2_evict_last() : l2_evict_first();
-        const uint4 d = s < hot1 ? ld_l1_v4(dist_cur + s, pol) : ld_nol1_v4(dist_cur + s, pol);
+        const uint32_t r = hp.rank(s);
+        const uint64_t pol = r < hot ? l2_evict_last() : l2_evict_first();
+        const uint4 d = r < hot1 ? ld_l1_v4(dist_cur + s, pol) : ld_nol1_v4(dist_cur + s, pol);
         m = make_uint4(sat_add(d.x, w), sat_add(d.y, w), sat_add(d.z, w), sat_add(d.w, w));
         return true;
     }
@@ -161,6 +174,7 @@ struct CcOps {  // min-label propagation; labels < 0xFFFF
     uint32_t* lab_next;
     const uint32_t* active_cur;
     FrontierView f;
+    HotPrefix hp;
     uint32_t hot, hot1;
     static constexpr bool kWeighted = false;
 
@@ -173,8 +187,9 @@ struct CcOps {  // min-label propagation; labels < 0xFFFF
     __device__ static bool has(const Acc& a) { return a.m != kInf32; }
     __device__ bool gen(uint32_t s, uint32_t, Msg& m) const {
         if (!bit_test(active_cur, s)) return false;
-        const uint64_t pol = s < hot ? l2_evict_last() : l2_evict_first();
-        m = s < hot1 ? ld_l1_u32(lab_cur + s, pol) : ld_nol1_u32(lab_cur + s, pol);
+        const uint32_t r = hp.rank(s);
+        const uint64_t pol = r < hot ? l2_evict_last() : l2_evict_first();
+        m = r < hot1 ? ld_l1_u32(lab_cur + s, pol) : ld_nol1_u32(lab_cur + s, pol);
         return true;
     }
     __device__ static void fold(Acc& a, Msg m) { a.m = min(a.m, m); }
@@ -946,6 +961,17 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st) {
 bool use_binned_pull() { return options().pull_kernel == 1; }
 
 // L2 budget for the gathered value prefix (GXB_L2_HOT_MB, default 64 of the 126 MB)
+HotPrefix hot_prefix(const gxb_state* s) {
+    HotPrefix h;
+    const gxb_graph* g = s->g;
+    if (g->nparts > 1 && g->V) {
+        const uint64_t blk = (g->V + g->nparts - 1) / g->nparts;
+        h.block = (uint32_t)blk;
+        h.magic = (uint32_t)((1ull << 32) / blk + 1);
+    }
+    return h;
+}
+
 uint32_t hot_slots(const gxb_state* s, size_t bytes_per_slot) {
     const uint64_t n = ((uint64_t)options().l2_hot_mb << 20) / bytes_per_slot;
     return (uint32_t)std::min<uint64_t>(n, s->g->V);
@@ -962,7 +988,8 @@ PrOps pr_ops(gxb_state* s) {
     o.rank = s->d_rank;
     o.contrib_next = s->d_contrib[s->cur ^ 1];
     o.f = frontier_view(s);
-    o.hot = hot_slots(s, sizeof(double));
+    o.hp = hot_prefix(s);
+    o.hot = hot_slots(s, sizeof(double)) / s->g->nparts;
     o.hot1 = hot_l1_slots(s, sizeof(double));
     return o;
 }
@@ -972,7 +999,8 @@ SsspOps sssp_ops(gxb_state* s) {
     o.dist_next = s->d_dist_next;
     o.active_cur = s->d_active[0];
     o.f = frontier_view(s);
-    o.hot = hot_slots(s, sizeof(uint4));
+    o.hp = hot_prefix(s);
+    o.hot = hot_slots(s, sizeof(uint4)) / s->g->nparts;
     o.hot1 = hot_l1_slots(s, sizeof(uint4));
     return o;
 }
@@ -982,7 +1010,8 @@ CcOps cc_ops(gxb_state* s) {
     o.lab_next = s->d_lab_next;
     o.active_cur = s->d_active[0];
     o.f = frontier_view(s);
-    o.hot = hot_slots(s, sizeof(uint32_t));
+    o.hp = hot_prefix(s);
+    o.hot = hot_slots(s, sizeof(uint32_t)) / s->g->nparts;
     o.hot1 = hot_l1_slots(s, sizeof(uint32_t));
     return o;
 }

@@ -240,6 +240,16 @@ __global__ void k_gather_indeg(const uint32_t* __restrict__ slot2dense, const ui
         out[s] = indeg[slot2dense[s]];
 }
 
+// round-robin deal of the degree-sorted order: position i -> partition i % n, rank i / n
+__global__ void k_deal(const uint32_t* __restrict__ s2d, const uint32_t* __restrict__ indeg, uint64_t V, int n,
+                       const uint64_t* __restrict__ bounds, uint32_t* s2d_out, uint32_t* indeg_out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < V; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t pos = bounds[i % n] + i / n;
+        s2d_out[pos] = s2d[i];
+        indeg_out[pos] = indeg[i];
+    }
+}
+
 static uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
 
 __global__ void k_low32(const uint64_t* __restrict__ keys, uint64_t n, uint32_t* out) {
@@ -574,6 +584,26 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
                                                  32 + bits_for((uint64_t)g->nparts), st));
         k_gather_indeg<<<grid_e(V), kBlock, 0, st>>>(slot2dense, indeg_d, V, indeg_slot);
     }
+    // GXB_BUILD_RANGES keeps contiguous degree-sorted ranges balanced by cost; the default
+    // for nparts > 1 deals the degree-sorted order round-robin (position i -> partition
+    // i mod nparts), so every partition gets 1/nparts of the hubs AND of the low-degree
+    // tail: balanced edges, balanced vertices and a balanced dense exchange
+    const bool dealt = !id_ranges && g->nparts > 1 && !(flags & GXB_BUILD_RANGES);
+    std::vector<uint64_t> deal_bounds;
+    if (dealt && V) {
+        deal_bounds.assign(g->nparts + 1, 0);
+        for (int p = 0; p < g->nparts; ++p)
+            deal_bounds[p + 1] = deal_bounds[p] + (V - p + g->nparts - 1) / g->nparts;
+        uint32_t *s2d = nullptr, *ind = nullptr;
+        GXB_CHECK(S.get(&s2d, V));
+        GXB_CHECK(S.get(&ind, V));
+        uint64_t* d_db = nullptr;
+        GXB_CHECK(S.get(&d_db, g->nparts + 1));
+        GXB_CUDA(cudaMemcpyAsync(d_db, deal_bounds.data(), 8 * (g->nparts + 1), cudaMemcpyHostToDevice, st));
+        k_deal<<<grid_e(V), kBlock, 0, st>>>(slot2dense, indeg_slot, V, g->nparts, d_db, s2d, ind);
+        slot2dense = s2d;
+        indeg_slot = ind;
+    }
     GXB_CHECK(dalloc_t(&g->d_dense2slot, V));
     GXB_CHECK(dalloc_t(&g->d_slot2id, V));
     GXB_CHECK(dalloc_t(&g->d_outdeg, V));
@@ -593,6 +623,8 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
     g->bounds[g->nparts] = V;
     if (id_ranges) {
         g->bounds = id_bounds;
+    } else if (dealt) {
+        g->bounds = deal_bounds;
     } else {
         // per-slot cost: 12 B per in-edge (index + gathered value) and 64 B-equivalent per
         // vertex (apply, stats, span folding measured at ~5 edges' worth on B200);

@@ -107,13 +107,16 @@ class DeviceGraph:
 
     def __init__(self, ctx: DeviceContext, src, dst, w=None, part: int = 0, nparts: int = 1,
                  csr: bool = True, stream=None, partitioning: str = "edges", sizes=None):
-        """partitioning: "edges" = destination ranges balanced by in-edges over the
-        degree-sorted order (default); "ids" = the reference's contiguous ascending-id
-        ranges (even_sizes, or explicit `sizes`)."""
+        """partitioning: "edges" = the degree-sorted order dealt round-robin to the
+        partitions (balanced edges, vertices and exchange; default); "ranges" = contiguous
+        degree-sorted ranges balanced by in-edge cost; "ids" = the reference's contiguous
+        ascending-id ranges (even_sizes, or explicit `sizes`)."""
         self.ctx = ctx
         flags = 0 if csr else L.BUILD_NO_CSR
-        if partitioning not in ("edges", "ids"):
+        if partitioning not in ("edges", "ranges", "ids"):
             raise ValueError(f"unknown partitioning {partitioning!r}")
+        if partitioning == "ranges":
+            flags |= L.BUILD_RANGES
         if partitioning == "ids" or sizes is not None:
             flags |= L.BUILD_ID_RANGES
         sizes_arr = None if sizes is None else np.ascontiguousarray(sizes, dtype=np.uint64)
