@@ -98,6 +98,9 @@ typedef struct gxb_graph_info {
     int32_t  nparts;
     int32_t  weighted;
     int32_t  has_csr;
+    uint64_t num_slots;        /* device slot space: num_vertices, or padded to equal
+                                  partition blocks (dealt layout); value buffers are
+                                  num_slots long */
 } gxb_graph_info;
 
 typedef struct gxb_iter_stats {

@@ -35,6 +35,7 @@ class GraphInfo(ctypes.Structure):
         ("max_id", ctypes.c_uint32), ("max_in_degree", ctypes.c_uint32),
         ("part", ctypes.c_int32), ("nparts", ctypes.c_int32),
         ("weighted", ctypes.c_int32), ("has_csr", ctypes.c_int32),
+        ("num_slots", ctypes.c_uint64),
     ]
 
 

@@ -746,9 +746,11 @@ __global__ void __launch_bounds__(kBlock) k_apply(const Ops ops, const typename 
 // init / readback kernels
 // ======================================================================
 
-__global__ void k_pr_init(double* rank, double* contrib, const uint32_t* __restrict__ outdeg, uint64_t V) {
+__global__ void k_pr_init(double* rank, double* contrib, const uint32_t* __restrict__ outdeg,
+                          const uint32_t* __restrict__ slot2id, uint64_t V) {
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < V; s += (uint64_t)gridDim.x * blockDim.x) {
-        rank[s] = 1.0;  // initial_attr (A/algorithms.py:141-142)
+        // initial_attr (A/algorithms.py:141-142); a padding slot starts at its fixed point 0.15
+        rank[s] = slot2id[s] == kInf32 ? 0.15 : 1.0;
         const uint32_t od = outdeg[s];
         contrib[s] = od ? __ddiv_rn(1.0, (double)od) : 0.0;
     }
@@ -964,8 +966,8 @@ bool use_binned_pull() { return options().pull_kernel == 1; }
 HotPrefix hot_prefix(const gxb_state* s) {
     HotPrefix h;
     const gxb_graph* g = s->g;
-    if (g->nparts > 1 && g->V) {
-        const uint64_t blk = (g->V + g->nparts - 1) / g->nparts;
+    if (g->nparts > 1 && g->S) {
+        const uint64_t blk = (g->S + g->nparts - 1) / g->nparts;
         h.block = (uint32_t)blk;
         h.magic = (uint32_t)((1ull << 32) / blk + 1);
     }
@@ -974,12 +976,12 @@ HotPrefix hot_prefix(const gxb_state* s) {
 
 uint32_t hot_slots(const gxb_state* s, size_t bytes_per_slot) {
     const uint64_t n = ((uint64_t)options().l2_hot_mb << 20) / bytes_per_slot;
-    return (uint32_t)std::min<uint64_t>(n, s->g->V);
+    return (uint32_t)std::min<uint64_t>(n, s->g->S);
 }
 
 uint32_t hot_l1_slots(const gxb_state* s, size_t bytes_per_slot) {
     const uint64_t n = ((uint64_t)options().l1_hot_kb << 10) / bytes_per_slot;
-    return (uint32_t)std::min<uint64_t>(n, s->g->V);
+    return (uint32_t)std::min<uint64_t>(n, s->g->S);
 }
 
 PrOps pr_ops(gxb_state* s) {
@@ -1126,7 +1128,8 @@ int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, 
         gxb_state_free(s);
         return rc;
     };
-    const uint64_t V = g->V, owned = g->hi - g->lo;
+    // slot arrays span the slot space S (= V, or padded to equal partition blocks)
+    const uint64_t V = g->S, owned = g->hi - g->lo;
     s->words = (V >> 5) + 1;
     cudaStream_t st = 0;
     // host copies of degrees for static counts
@@ -1164,7 +1167,7 @@ int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, 
         if ((rc = dalloc_t(&s->d_rank, V)) != GXB_OK) return bail(rc);
         for (int i = 0; i < 2; ++i)
             if ((rc = dalloc_t(&s->d_contrib[i], V)) != GXB_OK) return bail(rc);
-        if (V) k_pr_init<<<grid, kBlock, 0, st>>>(s->d_rank, s->d_contrib[0], g->d_outdeg, V);
+        if (V) k_pr_init<<<grid, kBlock, 0, st>>>(s->d_rank, s->d_contrib[0], g->d_outdeg, g->d_slot2id, V);
         units0 = s->owned_outdeg_sum;
     } else if (algo == GXB_ALGO_SSSP) {
         if (nsrc < 0 || nsrc > 4) return bail(fail(GXB_EINVAL, "sssp supports 1..4 sources"));
@@ -1174,12 +1177,13 @@ int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, 
         std::vector<std::pair<uint32_t, uint32_t>> by_id(V);  // (id, slot)
         for (uint64_t i = 0; i < V; ++i) by_id[i] = {ids[i], (uint32_t)i};
         std::sort(by_id.begin(), by_id.end());
+        by_id.resize(g->V);  // padding slots (id 0xFFFFFFFF) sort last and are not vertices
         std::vector<uint32_t> src_ids;
         if (sources && nsrc > 0) {
             src_ids.assign(sources, sources + nsrc);
         } else {
             // sorted(vertex_ids)[:4] (A/algorithms.py:219-222)
-            for (uint64_t i = 0; i < V && i < 4; ++i) src_ids.push_back(by_id[i].first);
+            for (uint64_t i = 0; i < g->V && i < 4; ++i) src_ids.push_back(by_id[i].first);
         }
         if (src_ids.empty()) return bail(fail(GXB_EINVAL, "sssp needs at least one source vertex"));
         // exact u32 arithmetic: no message d + w may reach the INF sentinel
@@ -1376,10 +1380,10 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
         P.count_next = s->d_fcount + 1;
         FrontierView f = frontier_view(s);
         if (!s->d_push_counts) {
-            GXB_CHECK(dalloc_t(&s->d_push_counts, g->V + 1));
-            GXB_CHECK(dalloc_t(&s->d_push_cpre, g->V + 1));
+            GXB_CHECK(dalloc_t(&s->d_push_counts, g->S + 1));
+            GXB_CHECK(dalloc_t(&s->d_push_cpre, g->S + 1));
             size_t tb = 0;
-            GXB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, s->d_push_counts, s->d_push_cpre, (int64_t)(g->V + 1), st));
+            GXB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, s->d_push_counts, s->d_push_cpre, (int64_t)(g->S + 1), st));
             s->push_tmp_bytes = tb;
             GXB_CHECK(dalloc(&s->d_push_tmp, tb));
         }

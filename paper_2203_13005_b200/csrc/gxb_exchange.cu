@@ -84,7 +84,7 @@ extern "C" {
 int gxb_exchange_buffer(gxb_state* s, int which, void** dev_ptr, uint64_t* bytes) {
     if (!s || !dev_ptr || !bytes) return fail(GXB_EINVAL, "gxb_exchange_buffer: null argument");
     gxb_graph* g = s->g;
-    const uint64_t V = g->V, owned = g->hi - g->lo;
+    const uint64_t V = g->S, owned = g->hi - g->lo;  // value replicas span the slot space
     const uint64_t rec = (s->algo == GXB_ALGO_SSSP) ? 20 : 8;
     switch (which) {
         case GXB_BUF_VALUES:

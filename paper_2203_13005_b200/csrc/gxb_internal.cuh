@@ -107,6 +107,7 @@ struct gxb_ctx {
 struct gxb_graph {
     gxb_ctx* ctx = nullptr;
     uint64_t V = 0, E = 0;
+    uint64_t S = 0;                     // slot count: V, or nparts * ceil(V / nparts) when dealt (padding slots)
     uint32_t max_id = 0;
     uint32_t max_in_degree = 0;
     uint32_t max_w = 0;                 // largest edge weight (1 when unweighted)

@@ -132,14 +132,19 @@ __global__ void k_iota(uint32_t* a, uint64_t n) {
         a[i] = (uint32_t)i;
 }
 
-// slot order -> inverse map, per-slot id and out-degree
-__global__ void k_slot_tables(const uint32_t* __restrict__ slot2dense, uint64_t V,
+// slot order -> inverse map, per-slot id and out-degree (padding slots: id kNone, degree 0)
+__global__ void k_slot_tables(const uint32_t* __restrict__ slot2dense, uint64_t S,
                               const uint32_t* __restrict__ ids_dense,
                               const uint32_t* __restrict__ outdeg_dense, uint32_t* dense2slot,
                               uint32_t* slot2id, uint32_t* outdeg_slot) {
-    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < V;
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < S;
          s += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t d = slot2dense[s];
+        if (d == 0xFFFFFFFFu) {
+            slot2id[s] = 0xFFFFFFFFu;
+            outdeg_slot[s] = 0;
+            continue;
+        }
         dense2slot[d] = (uint32_t)s;
         slot2id[s] = ids_dense[d];
         outdeg_slot[s] = outdeg_dense[d];
@@ -240,11 +245,12 @@ __global__ void k_gather_indeg(const uint32_t* __restrict__ slot2dense, const ui
         out[s] = indeg[slot2dense[s]];
 }
 
-// round-robin deal of the degree-sorted order: position i -> partition i % n, rank i / n
+// round-robin deal of the degree-sorted order: position i -> block i % n, rank i / n
+// (blocks of equal size B; the unfilled tail slot of a block stays a padding slot)
 __global__ void k_deal(const uint32_t* __restrict__ s2d, const uint32_t* __restrict__ indeg, uint64_t V, int n,
-                       const uint64_t* __restrict__ bounds, uint32_t* s2d_out, uint32_t* indeg_out) {
+                       uint64_t B, uint32_t* s2d_out, uint32_t* indeg_out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < V; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t pos = bounds[i % n] + i / n;
+        const uint64_t pos = (i % n) * B + i / n;
         s2d_out[pos] = s2d[i];
         indeg_out[pos] = indeg[i];
     }
@@ -590,37 +596,40 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
     // tail: balanced edges, balanced vertices and a balanced dense exchange
     const bool dealt = !id_ranges && g->nparts > 1 && !(flags & GXB_BUILD_RANGES);
     std::vector<uint64_t> deal_bounds;
+    uint64_t SL = V;  // slot count; dealt blocks are padded to equal size B = ceil(V / nparts)
     if (dealt && V) {
+        const uint64_t B = (V + g->nparts - 1) / g->nparts;
+        SL = B * g->nparts;
         deal_bounds.assign(g->nparts + 1, 0);
-        for (int p = 0; p < g->nparts; ++p)
-            deal_bounds[p + 1] = deal_bounds[p] + (V - p + g->nparts - 1) / g->nparts;
+        for (int p = 0; p <= g->nparts; ++p) deal_bounds[p] = B * p;
         uint32_t *s2d = nullptr, *ind = nullptr;
-        GXB_CHECK(S.get(&s2d, V));
-        GXB_CHECK(S.get(&ind, V));
-        uint64_t* d_db = nullptr;
-        GXB_CHECK(S.get(&d_db, g->nparts + 1));
-        GXB_CUDA(cudaMemcpyAsync(d_db, deal_bounds.data(), 8 * (g->nparts + 1), cudaMemcpyHostToDevice, st));
-        k_deal<<<grid_e(V), kBlock, 0, st>>>(slot2dense, indeg_slot, V, g->nparts, d_db, s2d, ind);
+        GXB_CHECK(S.get(&s2d, SL));
+        GXB_CHECK(S.get(&ind, SL));
+        // padding slots (one at the end of some blocks): no id, no edges
+        GXB_CUDA(cudaMemsetAsync(s2d, 0xFF, 4 * SL, st));
+        GXB_CUDA(cudaMemsetAsync(ind, 0, 4 * SL, st));
+        k_deal<<<grid_e(V), kBlock, 0, st>>>(slot2dense, indeg_slot, V, g->nparts, B, s2d, ind);
         slot2dense = s2d;
         indeg_slot = ind;
     }
+    g->S = SL;
     GXB_CHECK(dalloc_t(&g->d_dense2slot, V));
-    GXB_CHECK(dalloc_t(&g->d_slot2id, V));
-    GXB_CHECK(dalloc_t(&g->d_outdeg, V));
-    if (V)
-        k_slot_tables<<<grid_e(V), kBlock, 0, st>>>(slot2dense, V, ids_dense, outdeg_d, g->d_dense2slot,
+    GXB_CHECK(dalloc_t(&g->d_slot2id, SL));
+    GXB_CHECK(dalloc_t(&g->d_outdeg, SL));
+    if (SL)
+        k_slot_tables<<<grid_e(SL), kBlock, 0, st>>>(slot2dense, SL, ids_dense, outdeg_d, g->d_dense2slot,
                                                       g->d_slot2id, g->d_outdeg);
     if (E) k_relabel<<<grid_e(E), kBlock, 0, st>>>(src, dst, E, g->d_dense2slot);
 
     // destination-range partition balanced by in-edge count
-    std::vector<uint32_t> h_indeg(V);
-    if (V) GXB_CUDA(cudaMemcpyAsync(h_indeg.data(), indeg_slot, 4 * V, cudaMemcpyDeviceToHost, st));
+    std::vector<uint32_t> h_indeg(SL);
+    if (SL) GXB_CUDA(cudaMemcpyAsync(h_indeg.data(), indeg_slot, 4 * SL, cudaMemcpyDeviceToHost, st));
     GXB_CUDA(cudaStreamSynchronize(st));
     uint32_t maxin = 0;
-    for (uint64_t i = 0; i < V; ++i) maxin = std::max(maxin, h_indeg[i]);
+    for (uint64_t i = 0; i < SL; ++i) maxin = std::max(maxin, h_indeg[i]);
     g->max_in_degree = maxin;
     g->bounds.assign(g->nparts + 1, 0);
-    g->bounds[g->nparts] = V;
+    g->bounds[g->nparts] = SL;
     if (id_ranges) {
         g->bounds = id_bounds;
     } else if (dealt) {
@@ -647,7 +656,7 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
     uint64_t* d_bounds = nullptr;
     GXB_CHECK(S.get(&d_bounds, g->nparts + 1));
     GXB_CUDA(cudaMemcpyAsync(d_bounds, g->bounds.data(), 8 * (g->nparts + 1), cudaMemcpyHostToDevice, st));
-    const uint64_t rwords = (V >> 5) + 1;
+    const uint64_t rwords = (SL >> 5) + 1;
     GXB_CHECK(dalloc_t(&g->d_remote_src, rwords));
     GXB_CUDA(cudaMemsetAsync(g->d_remote_src, 0, 4 * rwords, st));
 
@@ -656,7 +665,7 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
     GXB_CHECK(S.get(&key_alt, E));
     if (want_csr) GXB_CHECK(S.get(&csr_key, E));
     if (E)
-        k_keys<<<grid_e(E), kBlock, 0, st>>>(src, dst, E, d_bounds, g->nparts, g->part, g->lo, owned, V,
+        k_keys<<<grid_e(E), kBlock, 0, st>>>(src, dst, E, d_bounds, g->nparts, g->part, g->lo, owned, SL,
                                               g->d_remote_src, csc_key, csr_key);
     // owned in-edge count
     uint64_t owned_edges = 0;
@@ -699,11 +708,11 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
     if (want_csr) {
         uint64_t* kout = nullptr;
         uint32_t* vout = nullptr;
-        if (E) GXB_CHECK(sort_pairs(csr_key, key_alt, w, w_alt, E, 32 + bits_for(V), st, &kout, &vout));
-        GXB_CHECK(dalloc_t(&g->d_out_off, V + 1));
+        if (E) GXB_CHECK(sort_pairs(csr_key, key_alt, w, w_alt, E, 32 + bits_for(SL), st, &kout, &vout));
+        GXB_CHECK(dalloc_t(&g->d_out_off, SL + 1));
         GXB_CHECK(dalloc_t(&g->d_out_dst, owned_edges));
         if (owned_edges) k_low32<<<grid_e(owned_edges), kBlock, 0, st>>>(kout, owned_edges, g->d_out_dst);
-        k_offsets<<<grid_e(owned_edges + 1), kBlock, 0, st>>>(kout, owned_edges, V, g->d_out_off);
+        k_offsets<<<grid_e(owned_edges + 1), kBlock, 0, st>>>(kout, owned_edges, SL, g->d_out_off);
         if (w) {
             GXB_CHECK(dalloc_t(&g->d_out_w, owned_edges));
             if (owned_edges)
@@ -854,6 +863,7 @@ int gxb_graph_get_info(const gxb_graph* g, gxb_graph_info* o) {
     if (!g || !o) return fail(GXB_EINVAL, "gxb_graph_get_info: null argument");
     std::memset(o, 0, sizeof(*o));
     o->num_vertices = g->V;
+    o->num_slots = g->S;
     o->num_edges = g->E;
     o->owned_lo = g->lo;
     o->owned_hi = g->hi;

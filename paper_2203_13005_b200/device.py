@@ -148,6 +148,7 @@ class DeviceGraph:
         L.check(L.lib().gxb_graph_get_info(self._h, ctypes.byref(info)))
         self.info = info
         self.num_vertices = int(info.num_vertices)
+        self.num_slots = int(info.num_slots)
         self.num_edges = int(info.num_edges)
         self.part, self.nparts = part, nparts
         self.weighted = bool(info.weighted)

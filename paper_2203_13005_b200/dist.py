@@ -71,16 +71,26 @@ class Collective:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
 
-    def vote(self, counts: list[int], max_stat: float, device) -> tuple[list[int], float]:
-        """SUM of counters and MAX of the convergence statistic over ranks."""
+    def vote_start(self, counts: list[int], max_stat: float, device):
+        """Launch the vote: one all-gather of every rank's (counters, max statistic)."""
         import torch
         if self.world == 1:
-            return counts, max_stat
-        c = torch.tensor(counts, dtype=torch.int64, device=device)
-        m = torch.tensor([max_stat], dtype=torch.float64, device=device)
-        self.dist.all_reduce(c, group=self.group)
-        self.dist.all_reduce(m, op=self.dist.ReduceOp.MAX, group=self.group)
-        return [int(x) for x in c.tolist()], float(m.item())
+            return (counts, max_stat)
+        mine = torch.tensor([float(c) for c in counts] + [max_stat], dtype=torch.float64, device=device)
+        out = torch.empty(self.world * mine.numel(), dtype=torch.float64, device=device)
+        self.dist.all_gather_into_tensor(out, mine, group=self.group)
+        return out
+
+    def vote_finish(self, handle) -> tuple[list[int], float]:
+        """SUM of the counters (exact below 2^53) and MAX of the statistic over ranks."""
+        if isinstance(handle, tuple):
+            return handle
+        rows = handle.view(self.world, -1).cpu().tolist()
+        counts = [int(sum(r[i] for r in rows)) for i in range(len(rows[0]) - 1)]
+        return counts, max(r[-1] for r in rows)
+
+    def vote(self, counts: list[int], max_stat: float, device) -> tuple[list[int], float]:
+        return self.vote_finish(self.vote_start(counts, max_stat, device))
 
     def allgatherv(self, out_views, my_view):
         """All-gather with uneven sizes into caller-provided views (grouped P2P)."""
@@ -97,6 +107,12 @@ class Collective:
         if ops:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
+
+    def allgather_inplace(self, out, mine):
+        """Equal-size all-gather where `mine` is this rank's block of `out` (NCCL in place)."""
+        if self.world == 1:
+            return
+        self.dist.all_gather_into_tensor(out, mine, group=self.group)
 
     def gather_counts(self, n: int, device) -> list[int]:
         import torch
@@ -124,15 +140,26 @@ class PartitionedRun:
         self.algo = self.state.algo
         self.iteration = 0
         self.skipped_rounds = 0
+        self._pr_remote = None
 
     # ---- the sync round ---------------------------------------------------
     def _exchange_dense(self) -> int:
-        """PageRank: every vertex changes, so all-gather each owner's contribution slice."""
+        """PageRank: every vertex changes, so all-gather each owner's contribution slice.
+
+        The dealt layout pads every partition block to the same size, so this is one
+        in-place NCCL all-gather over the replica (ring / NVLS); other layouts fall back
+        to a grouped send/recv all-gather-v."""
         ptr, nbytes = self.state.buffer(L.BUF_VALUES)
         values = self._view(ptr, nbytes, "f8")
-        views = [values[int(self.bounds[r]):int(self.bounds[r + 1])] for r in range(self.comm.world)]
-        self.comm.allgatherv(views, views[self.comm.rank])
-        return 8 * int(self.bounds[-1] - (self.bounds[self.comm.rank + 1] - self.bounds[self.comm.rank]))
+        sizes = np.diff(self.bounds.astype(np.int64))
+        r = self.comm.rank
+        if (sizes == sizes[0]).all() and hasattr(self.comm, "allgather_inplace"):
+            blk = int(sizes[0])
+            self.comm.allgather_inplace(values[: blk * self.comm.world], values[r * blk:(r + 1) * blk])
+        else:
+            views = [values[int(self.bounds[q]):int(self.bounds[q + 1])] for q in range(self.comm.world)]
+            self.comm.allgatherv(views, views[r])
+        return 8 * int(self.bounds[-1] - sizes[r])
 
     def _exchange_delta(self) -> int:
         """SSSP / CC / LP: only changed owned values travel, as (slot, value) records."""
@@ -174,16 +201,26 @@ class PartitionedRun:
         self.state.iterate(direction)
         st = self.state.stats()
         t0 = self._tick("compute", t0)
-        counts, max_stat = self.comm.vote(
+        handle = self.comm.vote_start(
             [st["changed"], st["next_active"], st["next_units"], st["remote_active"]], st["max_stat"],
             self.device)
+        moved = 0
+        early = False
+        if self.algo == "pagerank" and self._pr_remote is not None and self.comm.world > 1:
+            # every PageRank vertex is active every round, so the skip vote is the same each
+            # round: start the dense exchange behind the vote without waiting for its result
+            early = not (self.enable_skip and self._pr_remote == 0)
+            if early:
+                moved = self._exchange_dense()
+        counts, max_stat = self.comm.vote_finish(handle)
         t0 = self._tick("vote", t0)
         changed, next_active, next_units, remote_active = counts
+        if self.algo == "pagerank":
+            self._pr_remote = remote_active
         self.iteration += 1
         # skip iff no next-active vertex anywhere has a consumer on another partition
         skip = self.comm.world == 1 or (self.enable_skip and remote_active == 0)
-        moved = 0
-        if not skip:
+        if not skip and not early:
             moved = self._exchange_dense() if self.algo == "pagerank" else self._exchange_delta()
         t0 = self._tick("exchange", t0)
         if self.algo == "pagerank":
