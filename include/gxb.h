@@ -235,6 +235,7 @@ typedef struct gxb_profile {
     uint64_t main_kernel_launches;
     uint64_t kernels_launched;     /* all kernels launched by gxb_iterate since the last reset */
     uint64_t iterations;
+    double   rest_ms;              /* device time of the round after the main kernel (apply, folds, commit) */
 } gxb_profile;
 int gxb_profile_enable(gxb_state* s, int on);
 int gxb_profile_read(gxb_state* s, gxb_profile* out, int reset);

@@ -56,6 +56,7 @@ class Profile(ctypes.Structure):
     _fields_ = [
         ("main_kernel_ms", ctypes.c_double), ("main_kernel_launches", ctypes.c_uint64),
         ("kernels_launched", ctypes.c_uint64), ("iterations", ctypes.c_uint64),
+        ("rest_ms", ctypes.c_double),
     ]
 
     def as_dict(self):

@@ -1049,6 +1049,7 @@ int end_round(gxb_state* s, int direction, cudaStream_t st) {
         std::swap(s->d_frontier[0], s->d_frontier[1]);
         GXB_CUDA(cudaMemcpyAsync(s->d_fcount, s->d_fcount + 1, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
     }
+    if (s->timing_pending) GXB_CUDA(cudaEventRecord(s->kev[2], st));  // end of the round's kernels
     GXB_CUDA(cudaMemcpyAsync(s->h_stats, s->d_stats, sizeof(StatStripe) * kStripes, cudaMemcpyDeviceToHost, st));
     GXB_CUDA(cudaMemcpyAsync(s->h_fcount, s->d_fcount, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     GXB_CUDA(cudaEventRecord(s->stats_ready, st));
@@ -1100,9 +1101,11 @@ int collect_stats(gxb_state* s) {
     }
     if (s->timing_pending) {
         float ms = 0.f;
-        GXB_CUDA(cudaEventSynchronize(s->kev[1]));
+        GXB_CUDA(cudaEventSynchronize(s->kev[2]));
         GXB_CUDA(cudaEventElapsedTime(&ms, s->kev[0], s->kev[1]));
         s->kernel_ms += ms;
+        GXB_CUDA(cudaEventElapsedTime(&ms, s->kev[1], s->kev[2]));
+        s->rest_ms += ms;
         s->kernel_launches++;
         s->timing_pending = false;
     }
@@ -1296,8 +1299,8 @@ int gxb_state_free(gxb_state* s) {
     dfree(s->d_merged);
     dfree(s->d_partials);
     dfree(s->d_stage);
-    if (s->kev[0]) cudaEventDestroy(s->kev[0]);
-    if (s->kev[1]) cudaEventDestroy(s->kev[1]);
+    for (int i = 0; i < 3; ++i)
+        if (s->kev[i]) cudaEventDestroy(s->kev[i]);
     dfree(s->d_push_counts);
     dfree(s->d_push_cpre);
     dfree(s->d_push_tmp);
@@ -1566,8 +1569,7 @@ int gxb_write_attrs(gxb_state* s, const double* host_in, void* stream) {
 int gxb_profile_enable(gxb_state* s, int on) {
     if (!s) return fail(GXB_EINVAL, "gxb_profile_enable: null state");
     if (on && !s->kev[0]) {
-        GXB_CUDA(cudaEventCreate(&s->kev[0]));
-        GXB_CUDA(cudaEventCreate(&s->kev[1]));
+        for (int i = 0; i < 3; ++i) GXB_CUDA(cudaEventCreate(&s->kev[i]));
     }
     s->timing = on != 0;
     return GXB_OK;
@@ -1577,11 +1579,13 @@ int gxb_profile_read(gxb_state* s, gxb_profile* out, int reset) {
     if (!s || !out) return fail(GXB_EINVAL, "gxb_profile_read: null argument");
     GXB_CHECK(collect_stats(s));
     out->main_kernel_ms = s->kernel_ms;
+    out->rest_ms = s->rest_ms;
     out->main_kernel_launches = s->kernel_launches;
     out->kernels_launched = s->launches;
     out->iterations = s->iteration;
     if (reset) {
         s->kernel_ms = 0.0;
+        s->rest_ms = 0.0;
         s->kernel_launches = 0;
         s->launches = 0;
     }

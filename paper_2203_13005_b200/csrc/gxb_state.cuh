@@ -158,8 +158,9 @@ struct gxb_state {
     // profiling: events around the main merge kernel, launch counter
     bool timing = false;
     bool timing_pending = false;
-    cudaEvent_t kev[2] = {nullptr, nullptr};
+    cudaEvent_t kev[3] = {nullptr, nullptr, nullptr};
     double kernel_ms = 0.0;
+    double rest_ms = 0.0;  // device time after the main kernel until the round closes
     uint64_t kernel_launches = 0;
     uint64_t launches = 0;
 

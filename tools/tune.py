@@ -46,6 +46,7 @@ def main():
     keys = list(grid)
     combos = list(itertools.product(*[grid[k] for k in keys]))
     res = {c: [] for c in combos}
+    kern = {}
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     print("clocks before:", smi(), flush=True)
     for _ in range(args.rounds):
@@ -58,17 +59,23 @@ def main():
                 for _ in range(3):
                     s.iterate("auto")
                     s.stats()
+            s.profile(enable=True, reset=True)
             for _ in range(args.iters):
                 ev[0].record()
                 s.iterate(args.direction)
                 ev[1].record()
                 s.stats()
                 res[c].append(ev[0].elapsed_time(ev[1]))
+            pr = s.profile()
+            kern.setdefault(c, []).append((pr["main_kernel_ms"] / max(1, pr["main_kernel_launches"]),
+                                           pr["rest_ms"] / max(1, pr["main_kernel_launches"])))
             s.free()
     print("clocks after:", smi(), flush=True)
     for c in combos:
         print(json.dumps({"opts": dict(zip(keys, c)), "median_ms": round(statistics.median(res[c]), 4),
-                          "min_ms": round(min(res[c]), 4)}))
+                          "min_ms": round(min(res[c]), 4),
+                          "kernel_ms": round(statistics.median(k for k, _ in kern.get(c, [(0, 0)])), 4),
+                          "rest_ms": round(statistics.median(r for _, r in kern.get(c, [(0, 0)])), 4)}))
 
 
 if __name__ == "__main__":
