@@ -55,6 +55,7 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
     double* rank;
     double* contrib_next;
     FrontierView f;
+    bool msg32;    // messages (rank / out_deg) stored and gathered as float32 (option pr_message_bits = 32)
     HotPrefix hp;  // degree rank of a slot inside its partition block
     uint32_t hot;  // ranks [0, hot) keep L2 priority (degree-sorted: the most-gathered sources)
     uint32_t hot1; // ranks [0, hot1) also allocate in L1; the rest bypass L1
@@ -71,7 +72,12 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
     __device__ bool gen(uint32_t s, uint32_t, Msg& m) const {
         const uint32_t r = hp.rank(s);
         const uint64_t pol = r < hot ? l2_evict_last() : l2_evict_first();
-        m = r < hot1 ? ld_l1_f64(contrib_cur + s, pol) : ld_nol1_f64(contrib_cur + s, pol);
+        if (msg32) {
+            const float* c = reinterpret_cast<const float*>(contrib_cur) + s;
+            m = (double)(r < hot1 ? ld_l1_f32(c, pol) : ld_nol1_f32(c, pol));
+        } else {
+            m = r < hot1 ? ld_l1_f64(contrib_cur + s, pol) : ld_nol1_f64(contrib_cur + s, pol);
+        }
         return true;
     }
     __device__ static void fold(Acc& a, Msg m) { a.s += m; }
@@ -88,7 +94,9 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
         const double nw = __dadd_rn(0.15, __dmul_rn(0.85, a.s));
         rank[slot] = nw;
         const uint32_t od = p.od;
-        contrib_next[slot] = od ? __ddiv_rn(nw, (double)od) : 0.0;
+        const double c = od ? __ddiv_rn(nw, (double)od) : 0.0;
+        if (msg32) reinterpret_cast<float*>(contrib_next)[slot] = __double2float_rn(c);
+        else contrib_next[slot] = c;
         if (nw != old) {
             st.changed++;
             st.max_stat = fmax(st.max_stat, fabs(nw - old));
@@ -747,12 +755,14 @@ __global__ void __launch_bounds__(kBlock) k_apply(const Ops ops, const typename 
 // ======================================================================
 
 __global__ void k_pr_init(double* rank, double* contrib, const uint32_t* __restrict__ outdeg,
-                          const uint32_t* __restrict__ slot2id, uint64_t V) {
+                          const uint32_t* __restrict__ slot2id, uint64_t V, bool msg32) {
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < V; s += (uint64_t)gridDim.x * blockDim.x) {
         // initial_attr (A/algorithms.py:141-142); a padding slot starts at its fixed point 0.15
         rank[s] = slot2id[s] == kInf32 ? 0.15 : 1.0;
         const uint32_t od = outdeg[s];
-        contrib[s] = od ? __ddiv_rn(1.0, (double)od) : 0.0;
+        const double c = od ? __ddiv_rn(1.0, (double)od) : 0.0;
+        if (msg32) reinterpret_cast<float*>(contrib)[s] = __double2float_rn(c);
+        else contrib[s] = c;
     }
 }
 
@@ -798,14 +808,16 @@ __global__ void k_read_attrs(int algo, int arity, const uint32_t* __restrict__ d
 __global__ void k_write_attrs(int algo, int arity, const uint32_t* __restrict__ d2s, uint64_t V,
                               const uint32_t* __restrict__ outdeg, const double* __restrict__ in, double* rank,
                               double* contrib, uint4* dist_cur, uint4* dist_next, uint32_t* lab_cur,
-                              uint32_t* lab_next, uint32_t* bad) {
+                              uint32_t* lab_next, uint32_t* bad, bool msg32) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < V; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t s = d2s[i];
         if (algo == GXB_ALGO_PAGERANK) {
             const double r = in[i];
             rank[s] = r;
             const uint32_t od = outdeg[s];
-            contrib[s] = od ? __ddiv_rn(r, (double)od) : 0.0;
+            const double c = od ? __ddiv_rn(r, (double)od) : 0.0;
+            if (msg32) reinterpret_cast<float*>(contrib)[s] = __double2float_rn(c);
+            else contrib[s] = c;
         } else if (algo == GXB_ALGO_SSSP) {
             uint32_t l[4] = {kInf32, kInf32, kInf32, kInf32};
             for (int j = 0; j < arity; ++j) {
@@ -989,6 +1001,7 @@ PrOps pr_ops(gxb_state* s) {
     o.contrib_cur = s->d_contrib[s->cur];
     o.rank = s->d_rank;
     o.contrib_next = s->d_contrib[s->cur ^ 1];
+    o.msg32 = s->msg32;
     o.f = frontier_view(s);
     o.hp = hot_prefix(s);
     o.hot = hot_slots(s, sizeof(double)) / s->g->nparts;
@@ -1170,7 +1183,8 @@ int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, 
         if ((rc = dalloc_t(&s->d_rank, V)) != GXB_OK) return bail(rc);
         for (int i = 0; i < 2; ++i)
             if ((rc = dalloc_t(&s->d_contrib[i], V)) != GXB_OK) return bail(rc);
-        if (V) k_pr_init<<<grid, kBlock, 0, st>>>(s->d_rank, s->d_contrib[0], g->d_outdeg, g->d_slot2id, V);
+        s->msg32 = options().pr_message_bits == 32;
+        if (V) k_pr_init<<<grid, kBlock, 0, st>>>(s->d_rank, s->d_contrib[0], g->d_outdeg, g->d_slot2id, V, s->msg32);
         units0 = s->owned_outdeg_sum;
     } else if (algo == GXB_ALGO_SSSP) {
         if (nsrc < 0 || nsrc > 4) return bail(fail(GXB_EINVAL, "sssp supports 1..4 sources"));
@@ -1558,7 +1572,7 @@ int gxb_write_attrs(gxb_state* s, const double* host_in, void* stream) {
     GXB_CUDA(cudaMemsetAsync(d_bad, 0, 4, st));
     k_write_attrs<<<grid_for(V), kBlock, 0, st>>>(s->algo, s->arity, g->d_dense2slot, V, g->d_outdeg, s->d_stage,
                                                   s->d_rank, s->d_contrib[s->cur], s->d_dist_cur, s->d_dist_next,
-                                                  s->d_lab_cur, s->d_lab_next, d_bad);
+                                                  s->d_lab_cur, s->d_lab_next, d_bad, s->msg32);
     uint32_t bad = 0;
     GXB_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
     GXB_CUDA(cudaStreamSynchronize(st));

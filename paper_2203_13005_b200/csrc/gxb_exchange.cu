@@ -90,7 +90,7 @@ int gxb_exchange_buffer(gxb_state* s, int which, void** dev_ptr, uint64_t* bytes
         case GXB_BUF_VALUES:
             if (s->algo == GXB_ALGO_PAGERANK) {
                 *dev_ptr = s->d_contrib[s->cur];
-                *bytes = 8 * V;
+                *bytes = (s->msg32 ? 4 : 8) * V;
             } else if (s->algo == GXB_ALGO_SSSP) {
                 *dev_ptr = s->d_dist_cur;
                 *bytes = 16 * V;

@@ -226,6 +226,17 @@ __device__ __forceinline__ uint32_t ld_nol1_u32(const uint32_t* ptr, uint64_t po
     return r;
 }
 
+__device__ __forceinline__ float ld_l1_f32(const float* ptr, uint64_t pol) {
+    float r;
+    asm("ld.global.nc.L1::evict_last.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ float ld_nol1_f32(const float* ptr, uint64_t pol) {
+    float r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t sat_add(uint32_t d, uint32_t w) {
     const uint32_t s = d + w;
     return (s < d || d == kInf32) ? kInf32 : s;
@@ -247,6 +258,7 @@ struct Options {
     int64_t l1_hot_kb = 160;      // L1 budget (KB) of the L1-allocating prefix (others bypass L1)
     int64_t push_alpha = 20;      // push when frontier out-edges * alpha < |E|
     int64_t pull_kernel = 0;      // 0 = warp tiles, 1 = degree-binned groups
+    int64_t pr_message_bits = 64; // PageRank message (rank / out_deg) precision: 64 or 32 (f64 accumulation)
 };
 Options& options();
 

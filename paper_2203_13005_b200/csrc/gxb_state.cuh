@@ -108,6 +108,7 @@ struct gxb_state {
     double* d_rank = nullptr;               // PR: rank per slot
     double* d_contrib[2] = {nullptr, nullptr};  // PR: rank/outdeg, double-buffered
     int cur = 0;
+    bool msg32 = false;                     // PR messages in float32 (gathered / exchanged at 4 B)
     uint4* d_dist_cur = nullptr;            // SSSP: 4 lanes of u32 per slot
     uint4* d_dist_next = nullptr;
     uint32_t* d_lab_cur = nullptr;          // CC / LP labels

@@ -32,6 +32,7 @@ Options& options() {
         if (const char* e = getenv("GXB_L2_HOT_MB")) o.l2_hot_mb = atol(e);
         if (const char* e = getenv("GXB_PUSH_ALPHA")) o.push_alpha = atol(e);
         if (const char* e = getenv("GXB_PULL_KERNEL")) o.pull_kernel = std::string(e) == "binned" ? 1 : 0;
+        if (const char* e = getenv("GXB_PR_MESSAGE_BITS")) o.pr_message_bits = atol(e) == 32 ? 32 : 64;
     }
     return o;
 }
@@ -781,6 +782,9 @@ int gxb_set_option(const char* name, int64_t value) {
     } else if (n == "l1_hot_kb") {
         if (value < 0) return fail(GXB_EINVAL, "l1_hot_kb must be >= 0");
         o.l1_hot_kb = value;
+    } else if (n == "pr_message_bits") {
+        if (value != 32 && value != 64) return fail(GXB_EINVAL, "pr_message_bits: 32 or 64");
+        o.pr_message_bits = value;
     } else if (n == "pull_kernel") {
         if (value != 0 && value != 1) return fail(GXB_EINVAL, "pull_kernel: 0 = tiles, 1 = binned");
         o.pull_kernel = value;
@@ -798,6 +802,7 @@ int gxb_get_option(const char* name, int64_t* value) {
     else if (n == "l2_hot_mb") *value = o.l2_hot_mb;
     else if (n == "push_alpha") *value = o.push_alpha;
     else if (n == "pull_kernel") *value = o.pull_kernel;
+    else if (n == "pr_message_bits") *value = o.pr_message_bits;
     else if (n == "l1_hot_kb") *value = o.l1_hot_kb;
     else return fail(GXB_EINVAL, "unknown option " + n);
     return GXB_OK;

@@ -36,7 +36,7 @@ class _CAI:
 
 def device_view(ptr: int, nbytes: int, dtype: str = "u1"):
     import torch
-    typestr = {"u1": "|u1", "f8": "<f8", "u4": "<u4", "i8": "<i8"}[dtype]
+    typestr = {"u1": "|u1", "f8": "<f8", "f4": "<f4", "u4": "<u4", "i8": "<i8"}[dtype]
     return torch.as_tensor(_CAI(ptr, nbytes, typestr), device="cuda")
 
 
@@ -150,7 +150,8 @@ class PartitionedRun:
         in-place NCCL all-gather over the replica (ring / NVLS); other layouts fall back
         to a grouped send/recv all-gather-v."""
         ptr, nbytes = self.state.buffer(L.BUF_VALUES)
-        values = self._view(ptr, nbytes, "f8")
+        width = nbytes // max(1, int(self.bounds[-1]))   # 8 (f64 messages) or 4 (pr_message_bits = 32)
+        values = self._view(ptr, nbytes, "f8" if width == 8 else "f4")
         sizes = np.diff(self.bounds.astype(np.int64))
         r = self.comm.rank
         if (sizes == sizes[0]).all() and hasattr(self.comm, "allgather_inplace"):
@@ -159,7 +160,7 @@ class PartitionedRun:
         else:
             views = [values[int(self.bounds[q]):int(self.bounds[q + 1])] for q in range(self.comm.world)]
             self.comm.allgatherv(views, views[r])
-        return 8 * int(self.bounds[-1] - sizes[r])
+        return width * int(self.bounds[-1] - sizes[r])
 
     def _exchange_delta(self) -> int:
         """SSSP / CC / LP: only changed owned values travel, as (slot, value) records."""

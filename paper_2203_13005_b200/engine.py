@@ -152,13 +152,14 @@ def exchange_local(states, bounds) -> int:
         return 0
     moved = 0
     if states[0].algo == "pagerank":
-        views = [device_view(*s.buffer(L.BUF_VALUES), "f8") for s in states]
+        width = states[0].buffer(L.BUF_VALUES)[1] // max(1, int(bounds[-1]))
+        views = [device_view(*s.buffer(L.BUF_VALUES), "f8" if width == 8 else "f4") for s in states]
         for j in range(m):
             lo, hi = int(bounds[j]), int(bounds[j + 1])
             for k in range(m):
                 if k != j and hi > lo:
                     views[k][lo:hi].copy_(views[j][lo:hi])
-                    moved += 8 * (hi - lo)
+                    moved += width * (hi - lo)
         return moved
     rec = states[0].buffer(L.BUF_RECORD_SIZE)[1]
     counts = [s.pack() for s in states]

@@ -140,3 +140,21 @@ def test_device_rmat_matches_host(ctx):
         np.testing.assert_array_equal(d.cpu().numpy().view(np.uint32), hd)
         if hw is not None:
             np.testing.assert_array_equal(w.cpu().numpy().view(np.uint32), hw)
+
+
+@pytest.mark.parametrize("scale", [10, 14])
+def test_pagerank_f32_messages_within_north_star(ctx, oracle_lib, scale):
+    """Option pr_message_bits = 32: messages gathered/exchanged as float32, accumulated in
+    float64. The north-star bar (PR within 1e-5 relative per vertex) holds."""
+    from paper_2203_13005_b200 import _lib as L
+    from paper_2203_13005_b200.rmat import RmatParams, rmat_host
+    src, dst, _ = rmat_host(RmatParams(scale=scale, seed=61))
+    L.set_option("pr_message_bits", 32)
+    try:
+        g, s, attrs, it, conv, _ = device_run(ctx, src, dst, None, "pagerank", 20)
+    finally:
+        L.set_option("pr_message_bits", 64)
+    ref = oracle_lib.OracleGraph(src, dst).run("pagerank", max_iterations=20)
+    err = np.abs(attrs - ref.attrs) / np.maximum(1.0, np.abs(ref.attrs))
+    assert float(err.max()) <= 1e-5, float(err.max())
+    assert float(err.max()) > 0.0  # really the float32 message path
