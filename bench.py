@@ -206,6 +206,49 @@ def algorithmic_bytes(algo, E, V, units=None, nz=None):
     return 8 * (units if units is not None else E) + 12 * V
 
 
+def time_frontier_run(ctx, comm, dev, stream, name, algo, params, cap):
+    """One full run (to convergence or cap) of a frontier algorithm; the first run warms
+    allocations, the second is timed per iteration with CUDA events."""
+    import torch
+    from paper_2203_13005_b200.device import DeviceGraph, DeviceState
+    from paper_2203_13005_b200.dist import PartitionedRun
+    s, d, w = ctx.rmat(params, stream)
+    g = DeviceGraph(ctx, s, d, w, csr=algo in ("sssp", "cc"), stream=stream)
+    del s, d, w
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    limit = cap if cap is not None else g.num_vertices + 1
+    for _rep in range(2):
+        st = DeviceState(g, algo)
+        r = PartitionedRun(st, g.bounds(), comm, device=dev)
+        per_iter = []
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        while r.iteration < limit:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            rec = r.step()
+            b.record(stream)
+            per_iter.append((a, b, rec))
+            if rec.converged:
+                break
+        t1.record(stream)
+        t1.synchronize()
+        ms = t0.elapsed_time(t1)
+        st.free()
+    scanned = sum(x.units for x in r.records)
+    out = {"workload": name, "num_edges": g.num_edges, "num_vertices": g.num_vertices,
+           "iterations": r.iteration, "converged": r.records[-1].converged, "total_ms": round(ms, 3),
+           "gteps_e": round(g.num_edges * r.iteration / (ms * 1e-3) / 1e9, 2),
+           "gteps_ref": round(scanned / (ms * 1e-3) / 1e9, 2),
+           "iteration_ms": [round(a.elapsed_time(b), 3) for a, b, _ in per_iter],
+           "directions": ["push" if x.direction == 2 else "pull" for _, _, x in per_iter],
+           "note": "GTEPS_ref counts the reference's GEN units (out-edges of active vertices)"}
+    g.free()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -373,37 +416,13 @@ def main():
         del run
         graph.free()
         torch.cuda.empty_cache()
-        p2 = RmatParams(scale=scale, seed=1, wmax=63)
-        s2, d2, w2 = ctx.rmat(p2, stream)
-        g2 = DeviceGraph(ctx, s2, d2, w2, csr=True, stream=stream)
-        del s2, d2, w2
-        torch.cuda.synchronize()
-        torch.cuda.empty_cache()
-        for _rep in range(2):  # the first run warms allocations; the second is timed
-            st2 = DeviceState(g2, "sssp")
-            r2 = PartitionedRun(st2, g2.bounds(), comm, device=dev)
-            per_iter = []
-            ev0.record(stream)
-            while r2.iteration < g2.num_vertices + 1:
-                e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e_a.record(stream)
-                rr = r2.step()
-                e_b.record(stream)
-                per_iter.append((e_a, e_b, rr))
-                if rr.converged:
-                    break
-            ev1.record(stream)
-            ev1.synchronize()
-            it2, conv2 = r2.iteration, r2.records[-1].converged
-            ms2 = ev0.elapsed_time(ev1)
-        scanned = sum(r.units for r in r2.records)
-        secondary = {"workload": f"sssp-s{scale}", "iterations": it2, "converged": conv2,
-                     "total_ms": round(ms2, 3), "gteps_e": round(g2.num_edges * it2 / (ms2 * 1e-3) / 1e9, 2),
-                     "gteps_ref": round(scanned / (ms2 * 1e-3) / 1e9, 2),
-                     "iteration_ms": [round(a.elapsed_time(b), 3) for a, b, _ in per_iter],
-                     "directions": ["push" if r.direction == 2 else "pull" for _, _, r in per_iter],
-                     "note": "GTEPS_ref counts the reference's GEN units (out-edges of active vertices)"}
-        g2.free()
+        secondary = []
+        for wname, walgo, wparams, wcap in (
+                ("sssp-s26", "sssp", RmatParams(scale=scale, seed=1, wmax=63), None),
+                ("cc-s24", "cc", RmatParams(scale=min(scale, 24), seed=1, symmetric=True), None),
+                ("lp-s24-a65", "lp", RmatParams(scale=min(scale, 24), seed=1, a=0.65, b=0.15, c=0.15), 15)):
+            secondary.append(time_frontier_run(ctx, comm, dev, stream, wname, walgo, wparams, wcap))
+            torch.cuda.empty_cache()
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

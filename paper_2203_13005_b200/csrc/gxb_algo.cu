@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -125,6 +126,7 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
     uint4* dist_next;
     const uint32_t* active_cur;
     FrontierView f;
+    bool commit_inline;  // apply runs in its own kernel after every gather: write cur too, no commit pass
     HotPrefix hp;
     uint32_t hot, hot1;
     static constexpr bool kWeighted = true;
@@ -168,6 +170,7 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
         const uint4 n = min4(o, a.m);
         if (!eq4(n, o)) {
             dist_next[slot] = n;
+            if (commit_inline) const_cast<uint4*>(dist_cur)[slot] = n;
             publish_changed(f, slot, st);
         }
     }
@@ -182,6 +185,7 @@ struct CcOps {  // min-label propagation; labels < 0xFFFF
     uint32_t* lab_next;
     const uint32_t* active_cur;
     FrontierView f;
+    bool commit_inline;
     HotPrefix hp;
     uint32_t hot, hot1;
     static constexpr bool kWeighted = false;
@@ -216,6 +220,7 @@ struct CcOps {  // min-label propagation; labels < 0xFFFF
         const uint32_t n = min(o, a.m);
         if (n != o) {
             lab_next[slot] = n;
+            if (commit_inline) const_cast<uint32_t*>(lab_cur)[slot] = n;
             publish_changed(f, slot, st);
         }
     }
@@ -965,7 +970,12 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st) {
         }
     }
     const uint64_t owned = g->hi - g->lo;
-    k_apply_sums<Ops><<<grid_for(owned), kBlock, 0, st>>>(ops, (const typename Ops::Acc*)s->d_sums, g->lo, owned,
+    Ops aops = ops;
+    if constexpr (!std::is_same<Ops, PrOps>::value) {
+        aops.commit_inline = true;  // every gather of the round is done: commit changes in place
+        s->committed_inline = true;
+    }
+    k_apply_sums<Ops><<<grid_for(owned), kBlock, 0, st>>>(aops, (const typename Ops::Acc*)s->d_sums, g->lo, owned,
                                                           g->tiles.nz_slots, s->d_stats);
     s->launches++;
     GXB_CUDA(cudaGetLastError());
@@ -1014,6 +1024,7 @@ SsspOps sssp_ops(gxb_state* s) {
     o.dist_next = s->d_dist_next;
     o.active_cur = s->d_active[0];
     o.f = frontier_view(s);
+    o.commit_inline = false;
     o.hp = hot_prefix(s);
     o.hot = hot_slots(s, sizeof(uint4)) / s->g->nparts;
     o.hot1 = hot_l1_slots(s, sizeof(uint4));
@@ -1025,6 +1036,7 @@ CcOps cc_ops(gxb_state* s) {
     o.lab_next = s->d_lab_next;
     o.active_cur = s->d_active[0];
     o.f = frontier_view(s);
+    o.commit_inline = false;
     o.hp = hot_prefix(s);
     o.hot = hot_slots(s, sizeof(uint32_t)) / s->g->nparts;
     o.hot1 = hot_l1_slots(s, sizeof(uint32_t));
@@ -1040,6 +1052,7 @@ int begin_round(gxb_state* s, cudaStream_t st) {
     GXB_CUDA(cudaMemsetAsync(s->d_fcount + 1, 0, sizeof(unsigned long long), st));
     GXB_CUDA(cudaMemsetAsync(s->d_active[1], 0, 4 * s->words, st));
     s->in_round = true;
+    s->committed_inline = false;
     return GXB_OK;
 }
 
@@ -1048,7 +1061,7 @@ int end_round(gxb_state* s, int direction, cudaStream_t st) {
     gxb_graph* g = s->g;
     if (s->algo == GXB_ALGO_PAGERANK) {
         s->cur ^= 1;
-    } else if (direction == GXB_DIR_PULL) {
+    } else if (direction == GXB_DIR_PULL && !s->committed_inline) {
         const unsigned grid = grid_for(g->hi - g->lo);
         if (s->algo == GXB_ALGO_SSSP)
             k_commit<uint4><<<grid, kBlock, 0, st>>>(s->d_dist_cur, s->d_dist_next, s->d_frontier[1], s->d_fcount + 1);
@@ -1127,10 +1140,23 @@ int collect_stats(gxb_state* s) {
 
 }  // namespace
 
+// push scheduling buffers, allocated with the state so no iteration pays for cudaMalloc
+static int alloc_push(gxb_state* s) {
+    const gxb_graph* g = s->g;
+    GXB_CHECK(dalloc_t(&s->d_push_counts, g->S + 1));
+    GXB_CHECK(dalloc_t(&s->d_push_cpre, g->S + 1));
+    size_t tb = 0;
+    GXB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, s->d_push_counts, s->d_push_cpre, (int64_t)(g->S + 1)));
+    s->push_tmp_bytes = tb;
+    GXB_CHECK(dalloc(&s->d_push_tmp, tb));
+    return GXB_OK;
+}
+
 extern "C" {
 
 int gxb_state_free(gxb_state* s);
-void gxb_lp_free(gxb_state* s);  // gxb_lp.cu
+void gxb_lp_free(gxb_state* s);                     // gxb_lp.cu
+int gxb_lp_prepare(gxb_state* s, cudaStream_t st);  // gxb_lp.cu
 
 int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, gxb_state** out) {
     if (!g || !out) return fail(GXB_EINVAL, "gxb_state_create: null argument");
@@ -1283,6 +1309,9 @@ int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, 
         }
         s->last.remote_active = c;
     }
+    if ((algo == GXB_ALGO_SSSP || algo == GXB_ALGO_CC) && g->has_csr && (rc = alloc_push(s)) != GXB_OK)
+        return bail(rc);
+    if (algo == GXB_ALGO_LP && (rc = gxb_lp_prepare(s, st)) != GXB_OK) return bail(rc);
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return bail(cuda_fail(e, "gxb_state_create"));
     *out = s;
@@ -1333,7 +1362,8 @@ int gxb_state_arity(const gxb_state* s, int* out) {
     return GXB_OK;
 }
 
-int gxb_lp_pull(gxb_state* s, cudaStream_t st);  // gxb_lp.cu
+int gxb_lp_pull(gxb_state* s, cudaStream_t st);     // gxb_lp.cu
+
 
 int gxb_iterate(gxb_state* s, int direction, void* stream) {
     if (!s) return fail(GXB_EINVAL, "gxb_iterate: null state");
@@ -1396,14 +1426,7 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
         P.list_next = s->d_frontier[1];
         P.count_next = s->d_fcount + 1;
         FrontierView f = frontier_view(s);
-        if (!s->d_push_counts) {
-            GXB_CHECK(dalloc_t(&s->d_push_counts, g->S + 1));
-            GXB_CHECK(dalloc_t(&s->d_push_cpre, g->S + 1));
-            size_t tb = 0;
-            GXB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, s->d_push_counts, s->d_push_cpre, (int64_t)(g->S + 1), st));
-            s->push_tmp_bytes = tb;
-            GXB_CHECK(dalloc(&s->d_push_tmp, tb));
-        }
+        if (!s->d_push_counts) GXB_CHECK(alloc_push(s));
         if (P.nfront) {
             s->launches += 3;  // counts, scan, push
             k_push_counts<<<grid_for(P.nfront), kBlock, 0, st>>>(P.frontier, P.nfront, P.out_off, s->d_push_counts);

@@ -13,8 +13,9 @@
 //  * in-degree > kChunkMinDeg: warps stream kChunkEdges-edge chunks, pre-merge
 //    equal labels inside the warp with __match_any_sync, and fold (label, count)
 //    into a per-destination open-addressing table in global memory (L2
-//    atomics). A tiled scan then reduces every table to its packed argmax and
-//    clears it for the next round; a last pass applies.
+//    atomics); every update also raises the destination's running packed
+//    argmax (count << 32 | ~label) with atomicMax, so no table scan is needed;
+//    a last pass applies and the tables are reset with memsets.
 #include <algorithm>
 #include <vector>
 
@@ -23,7 +24,6 @@
 namespace gxb {
 
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
-constexpr uint32_t kTile = 2048;  // table entries per argmax block
 
 struct LpHub {
     uint64_t* tab_off;   // per chunked slot: first entry
@@ -31,10 +31,6 @@ struct LpHub {
     uint32_t* keys;
     uint32_t* counts;
     unsigned long long* best;  // per chunked slot: packed (count << 32 | ~label), 0 = no message
-    uint32_t* tile_slot;       // per tile: chunked slot
-    uint64_t* tile_begin;      // per tile: first entry
-    uint32_t* tile_len;
-    uint64_t num_tiles;
     uint64_t entries;
 };
 
@@ -52,8 +48,9 @@ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
     return x;
 }
 
-__device__ __forceinline__ void table_add(uint32_t* keys, uint32_t* counts, uint64_t base, uint32_t mask,
-                                          uint32_t label, uint32_t c) {
+// fold (label, c) into a destination's table; returns the label's new count
+__device__ __forceinline__ uint32_t table_add(uint32_t* keys, uint32_t* counts, uint64_t base, uint32_t mask,
+                                              uint32_t label, uint32_t c) {
     uint32_t i = mix32(label) & mask;
     while (true) {
         const uint64_t at = base + i;
@@ -62,10 +59,7 @@ __device__ __forceinline__ void table_add(uint32_t* keys, uint32_t* counts, uint
             k = atomicCAS(keys + at, kEmpty, label);
             if (k == kEmpty) k = label;
         }
-        if (k == label) {
-            atomicAdd(counts + at, c);
-            return;
-        }
+        if (k == label) return atomicAdd(counts + at, c) + c;
         i = (i + 1) & mask;
     }
 }
@@ -159,7 +153,13 @@ __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item) {
         }
         const unsigned long long key = ok ? (unsigned long long)lab : (0x100000000ull | (unsigned)lane);
         const unsigned m = __match_any_sync(kFull, key);
-        if (ok && lane == __ffs(m) - 1) table_add(L.hub.keys, L.hub.counts, base, mask, lab, __popc(m));
+        if (ok && lane == __ffs(m) - 1) {
+            // the running argmax: a label's packed (count, ~label) only grows, so the max over
+            // every update equals the max over final counts
+            const uint32_t nc = table_add(L.hub.keys, L.hub.counts, base, mask, lab, __popc(m));
+            const unsigned long long pk = ((unsigned long long)nc << 32) | (unsigned long long)(~lab);
+            if (pk > __ldcg(L.hub.best + rel)) atomicMax(L.hub.best + rel, pk);
+        }
     }
 }
 
@@ -189,30 +189,6 @@ __global__ void __launch_bounds__(kBlock) k_lp_pull(const LpLaunch L) {
     flush_stats(st, L.stats);
 }
 
-// per tile of a hub table: packed argmax -> best[slot]; clear the entries
-__global__ void __launch_bounds__(kBlock) k_lp_hub_argmax(const LpHub H) {
-    const uint64_t t = blockIdx.x;
-    if (t >= H.num_tiles) return;
-    const uint32_t slot = H.tile_slot[t];
-    const uint64_t b0 = H.tile_begin[t];
-    const uint32_t n = H.tile_len[t];
-    unsigned long long best = 0ull;
-    for (uint32_t i = threadIdx.x; i < n; i += kBlock) {
-        const uint32_t k = H.keys[b0 + i];
-        if (k != kEmpty) {
-            const unsigned long long p = ((unsigned long long)H.counts[b0 + i] << 32) | (unsigned long long)(~k);
-            best = p > best ? p : best;
-            H.keys[b0 + i] = kEmpty;
-            H.counts[b0 + i] = 0u;
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long q = __shfl_xor_sync(kFull, best, o);
-        best = q > best ? q : best;
-    }
-    if ((threadIdx.x & 31) == 0 && best) atomicMax(H.best + slot, best);
-}
-
 __global__ void __launch_bounds__(kBlock) k_lp_hub_apply(const LpLaunch L, uint64_t chunk_end) {
     LocalStats st;
     for (uint64_t rel = blockIdx.x * (uint64_t)kBlock + threadIdx.x; rel < chunk_end; rel += (uint64_t)gridDim.x * kBlock) {
@@ -237,9 +213,6 @@ static void lp_free(LpScratch* S) {
     dfree(H.keys);
     dfree(H.counts);
     dfree(H.best);
-    dfree(H.tile_slot);
-    dfree(H.tile_begin);
-    dfree(H.tile_len);
     delete S;
 }
 
@@ -251,23 +224,14 @@ static int lp_setup(gxb_state* s, cudaStream_t st) {
     LpHub& H = S->hub;
     std::vector<uint64_t> off(P.chunk_end + 1);
     std::vector<uint32_t> mask(P.chunk_end + 1);
-    std::vector<uint32_t> tslot;
-    std::vector<uint64_t> tbeg;
-    std::vector<uint32_t> tlen;
     uint64_t acc = 0;
     for (uint64_t r = 0; r < P.chunk_end; ++r) {
         const uint64_t size = std::max<uint64_t>(256, next_pow2(2ull * g->h_indeg_sorted[r]));
         off[r] = acc;
         mask[r] = (uint32_t)(size - 1);
-        for (uint64_t b = 0; b < size; b += kTile) {
-            tslot.push_back((uint32_t)r);
-            tbeg.push_back(acc + b);
-            tlen.push_back((uint32_t)std::min<uint64_t>(kTile, size - b));
-        }
         acc += size;
     }
     H.entries = acc;
-    H.num_tiles = tslot.size();
     int rc = GXB_OK;
     auto up = [&](auto** d, const auto& h) {
         if (rc != GXB_OK) return;
@@ -278,9 +242,6 @@ static int lp_setup(gxb_state* s, cudaStream_t st) {
     };
     up(&H.tab_off, off);
     up(&H.tab_mask, mask);
-    up(&H.tile_slot, tslot);
-    up(&H.tile_begin, tbeg);
-    up(&H.tile_len, tlen);
     if (rc == GXB_OK) rc = dalloc_t(&H.keys, acc + 1);
     if (rc == GXB_OK) rc = dalloc_t(&H.counts, acc + 1);
     if (rc == GXB_OK) rc = dalloc_t(&H.best, P.chunk_end + 1);
@@ -307,6 +268,11 @@ extern "C" void gxb_lp_free(gxb_state* s) {
         lp_free(reinterpret_cast<LpScratch*>(s->d_lp_scratch));
         s->d_lp_scratch = nullptr;
     }
+}
+
+extern "C" int gxb_lp_prepare(gxb_state* s, cudaStream_t st) {
+    if (!s->d_lp_scratch) GXB_CHECK(lp_setup(s, st));
+    return GXB_OK;
 }
 
 extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
@@ -344,9 +310,11 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
     }
     L.hub = S->hub;
     if (grid) k_lp_pull<<<grid, kBlock, 0, st>>>(L);
-    if (S->hub.num_tiles) {
-        k_lp_hub_argmax<<<(unsigned)S->hub.num_tiles, kBlock, 0, st>>>(S->hub);
+    if (S->chunk_end) {
         k_lp_hub_apply<<<grid_for(S->chunk_end), kBlock, 0, st>>>(L, S->chunk_end);
+        // empty the tables for the next round (plain memsets: no read-back of the tables)
+        GXB_CUDA(cudaMemsetAsync(S->hub.keys, 0xFF, 4 * S->hub.entries, st));
+        GXB_CUDA(cudaMemsetAsync(S->hub.counts, 0, 4 * S->hub.entries, st));
     }
     GXB_CUDA(cudaGetLastError());
     return GXB_OK;

@@ -130,6 +130,7 @@ struct gxb_state {
     cudaEvent_t stats_ready = nullptr;
     bool stats_pending = false;
     bool in_round = false;
+    bool committed_inline = false;  // the round's apply already wrote the current values
     int last_direction = GXB_DIR_PULL;
     gxb_iter_stats last{};
 
