@@ -214,6 +214,30 @@ int gxb_exchange_finish(gxb_state* s, void* stream);
 #define GXB_BUF_SEND        1   /* packed (slot, value) records of this rank */
 #define GXB_BUF_RECV        2   /* receive area for peers' records */
 #define GXB_BUF_RECORD_SIZE 3   /* bytes per record in *bytes */
+#define GXB_BUF_VALUES_NEXT 4   /* PageRank: the contribution array the open round writes */
+#define GXB_BUF_SPARSE_SEND 5   /* PageRank needed-only exchange: my values, grouped by peer */
+#define GXB_BUF_SPARSE_RECV 6   /* PageRank needed-only exchange: peers' values, grouped by peer */
+
+/* Needed-only dense exchange (PageRank, nparts > 1): peer q receives exactly my owned
+ * slots that are sources of edges into q's destinations (static lists built with the
+ * graph, sorted by slot on both sides). pack: values -> GXB_BUF_SPARSE_SEND grouped by
+ * peer (send_counts); the caller runs an all-to-all into GXB_BUF_SPARSE_RECV
+ * (recv_counts); unpack scatters them into the replica. */
+int gxb_exchange_sparse_counts(const gxb_state* s, uint64_t* send_counts, uint64_t* recv_counts);
+int gxb_exchange_sparse_pack(gxb_state* s, void* stream);
+int gxb_exchange_sparse_unpack(gxb_state* s, void* stream);
+
+/* ---- pipeline shuffle (Alg. 1-2 realised as stream overlap) ----
+ * A PageRank pull round split into K exchange chunks of the owned slots (chunk k =
+ * relative slots [b[k], b[k+1]), b from gxb_graph_xchunks; every rank cuts its block
+ * with b[k] = owned * k^2 / K^2, so chunk 0 holds the hubs). After gxb_iterate_chunk(k)
+ * the chunk's new contributions (GXB_BUF_VALUES_NEXT) are final and can be sent while
+ * later chunks compute; gxb_iterate_end closes the round (stats, buffer rotation).
+ * Equivalent to gxb_iterate when all chunks are run. */
+int gxb_graph_xchunks(const gxb_graph* g, int* K, uint64_t* host_bounds);
+int gxb_iterate_begin(gxb_state* s, void* stream);
+int gxb_iterate_chunk(gxb_state* s, int k, void* stream);
+int gxb_iterate_end(gxb_state* s, void* stream);
 
 /* attributes in ascending original-id order (host buffer num_vertices * arity;
  * SSSP: float64 distances, +inf unreachable; PR: float64 rank; LP/CC: float64 label).

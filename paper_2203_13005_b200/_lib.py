@@ -24,7 +24,8 @@ ALGO_SSSP, ALGO_PAGERANK, ALGO_LP, ALGO_CC = 0, 1, 2, 3
 OP_GEN, OP_MERGE, OP_APPLY = 0, 1, 2
 BUILD_HOST_INPUT, BUILD_NO_CSR, BUILD_ID_RANGES, BUILD_RANGES = 0x1, 0x2, 0x4, 0x8
 DIR_AUTO, DIR_PULL, DIR_PUSH = 0, 1, 2
-BUF_VALUES, BUF_SEND, BUF_RECV, BUF_RECORD_SIZE = 0, 1, 2, 3
+BUF_VALUES, BUF_SEND, BUF_RECV, BUF_RECORD_SIZE, BUF_VALUES_NEXT = 0, 1, 2, 3, 4
+BUF_SPARSE_SEND, BUF_SPARSE_RECV = 5, 6
 
 
 class GraphInfo(ctypes.Structure):
@@ -95,6 +96,10 @@ def _sig(L):
         "gxb_graph_out_degree": (I, [P, P]),
         "gxb_graph_part_bounds": (I, [P, P]),
         "gxb_graph_free": (I, [P]),
+        "gxb_graph_xchunks": (I, [P, ctypes.POINTER(I), P]),
+        "gxb_iterate_begin": (I, [P, P]),
+        "gxb_iterate_chunk": (I, [P, I, P]),
+        "gxb_iterate_end": (I, [P, P]),
         "gxb_state_create": (I, [P, I, P, I, PP]),
         "gxb_state_free": (I, [P]),
         "gxb_state_arity": (I, [P, ctypes.POINTER(I)]),
@@ -106,6 +111,9 @@ def _sig(L):
         "gxb_exchange_pack": (I, [P, P, ctypes.POINTER(U64)]),
         "gxb_exchange_unpack": (I, [P, P, U64, P]),
         "gxb_exchange_finish": (I, [P, P]),
+        "gxb_exchange_sparse_counts": (I, [P, P, P]),
+        "gxb_exchange_sparse_pack": (I, [P, P]),
+        "gxb_exchange_sparse_unpack": (I, [P, P]),
         "gxb_read_attrs": (I, [P, P, I, P]),
         "gxb_write_attrs": (I, [P, P, P]),
         "gxb_profile_enable": (I, [P, I]),

@@ -409,7 +409,8 @@ __global__ void __launch_bounds__(kBlock) k_pull(const Pol p, const PullLaunch L
 // ======================================================================
 
 struct TileLaunch {
-    uint64_t num_tiles;
+    uint64_t num_tiles;   // end of the tile range of this launch
+    uint64_t tile_begin;  // first tile of this launch (an exchange chunk)
     uint64_t owned_edges;
     const uint64_t* in_off;
     const uint32_t* in_src;
@@ -466,7 +467,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_t(const Pol p, cons
     const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
     const uint64_t pol = l2_evict_first();
     const bool weighted = kW && L.in_w != nullptr;
-    uint64_t t = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+    uint64_t t = L.tile_begin + (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
     uint32_t nidx[kTileK], nw[kTileK];
     uint32_t nsa = 0, nmask = 0;
     uint64_t nbeg = 0, nend = 0;
@@ -476,8 +477,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_t(const Pol p, cons
         nw[j] = 1;
     }
     auto prefetch = [&](uint64_t tt) {
-        nbeg = tt * kTileEdges;  // fixed tiles (tile_start[t] == t * kTileEdges)
-        nend = min(nbeg + kTileEdges, L.owned_edges);
+        nbeg = __ldg(L.tile_start + tt);  // tiles restart at every exchange chunk
+        nend = __ldg(L.tile_start + tt + 1);
         const uint64_t e = nbeg + (uint64_t)lane;
 #pragma unroll
         for (int j = 0; j < kTileK; ++j) nidx[j] = ld_stream_u32(L.in_src + e + 32 * j, pol);
@@ -568,10 +569,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_t(const Pol p, cons
 // fold the per-tile partials of every span in tile order (deterministic)
 template <class Ops>
 __global__ void k_span_fold(const uint32_t* __restrict__ span_slot, const uint32_t* __restrict__ span_count,
-                            const uint64_t* __restrict__ span_pbase, uint64_t num_spans,
+                            const uint64_t* __restrict__ span_pbase, uint64_t span_lo, uint64_t span_hi,
                             const typename Ops::Acc* __restrict__ partials, typename Ops::Acc* sums) {
     using Acc = typename Ops::Acc;
-    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < num_spans;
+    for (uint64_t k = span_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < span_hi;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t b = span_pbase[k];
         const uint32_t n = span_count[k];
@@ -585,13 +586,13 @@ __global__ void k_span_fold(const uint32_t* __restrict__ span_slot, const uint32
 // slots past nz_slots have no in-edge and fold the identity (merged.get(vid, zero)).
 template <class Ops>
 __global__ void __launch_bounds__(kBlock) k_apply_sums(const Ops ops, const typename Ops::Acc* __restrict__ sums,
-                                                        uint64_t lo, uint64_t owned, uint64_t nz,
+                                                        uint64_t lo, uint64_t rlo, uint64_t owned, uint64_t nz,
                                                         StatStripe* stats) {
-    // four independent slots per step: all loads are issued before any store
+    // relative slots [rlo, owned); four independent slots per step: all loads before any store
     constexpr int kU = 4;
     LocalStats st;
     const uint64_t stride = (uint64_t)gridDim.x * kBlock;
-    for (uint64_t r0 = blockIdx.x * (uint64_t)kBlock + threadIdx.x; r0 < owned; r0 += kU * stride) {
+    for (uint64_t r0 = rlo + blockIdx.x * (uint64_t)kBlock + threadIdx.x; r0 < owned; r0 += kU * stride) {
         typename Ops::Acc a[kU];
         typename Ops::Pre pre[kU];
 #pragma unroll
@@ -918,6 +919,7 @@ TileLaunch tile_launch(gxb_state* s) {
     const TilePlan& T = g->tiles;
     TileLaunch L;
     L.num_tiles = T.num_tiles;
+    L.tile_begin = 0;
     L.owned_edges = g->owned_edges;
     L.in_off = g->d_in_off;
     L.in_src = g->d_in_src;
@@ -937,10 +939,18 @@ TileLaunch tile_launch(gxb_state* s) {
     return L;
 }
 
+// one exchange chunk (or all of them for k < 0): Gen∘Merge tiles, span folds, Apply
 template <class Ops>
-int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st) {
+int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st, int chunk = -1) {
     const gxb_graph* g = s->g;
-    const TileLaunch L = tile_launch(s);
+    const TilePlan& T = g->tiles;
+    const int K = T.num_xchunks;
+    const int k0 = chunk < 0 ? 0 : chunk, k1 = chunk < 0 ? K : chunk + 1;
+    TileLaunch L = tile_launch(s);
+    L.tile_begin = T.xchunk_tile[k0];
+    L.num_tiles = T.xchunk_tile[k1];
+    const uint64_t span_lo = T.xchunk_span[k0], span_hi = T.xchunk_span[k1];
+    const uint64_t r_lo = T.xchunk_slot[k0], r_hi = T.xchunk_slot[k1];
     FusedPolicy<Ops> p{ops, g->d_in_w};
     // measured best min-blocks per accumulator width (PR/CC 6, SSSP 4); 0 = auto
     int variant = (int)options().tile_minblocks;
@@ -948,36 +958,41 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st) {
     using Pol = FusedPolicy<Ops>;
     void (*kern)(const Pol, const TileLaunch) = (variant == 8) ? k_tile_t<Pol, 8> : (variant == 6) ? k_tile_t<Pol, 6>
              : (variant == 4) ? k_tile_t<Pol, 4> : k_tile_t<Pol, 1>;
+    if (options().carveout >= 0)  // shared-memory carveout (% of max): the rest of the 256 KB is L1
+        GXB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)options().carveout));
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, 0);
-    const int max_blocks = std::max(1, per_sm) * kNumSMs;
-    if (L.num_tiles) {
-        const uint64_t want = (L.num_tiles + (kBlock / 32) - 1) / (kBlock / 32);
+    // chunked rounds leave SMs free for the NCCL kernels of the overlapped exchange
+    const int sms = chunk >= 0 ? std::max(1, kNumSMs - (int)options().overlap_reserve_sms) : kNumSMs;
+    const int max_blocks = std::max(1, per_sm) * sms;
+    const uint64_t ntiles = L.num_tiles - L.tile_begin;
+    if (ntiles) {
+        const uint64_t want = (ntiles + (kBlock / 32) - 1) / (kBlock / 32);
         const unsigned grid = (unsigned)std::min<uint64_t>(want, (uint64_t)max_blocks);
-        if (s->timing) GXB_CUDA(cudaEventRecord(s->kev[0], st));
+        if (s->timing && chunk <= 0) GXB_CUDA(cudaEventRecord(s->kev[0], st));
         kern<<<grid, kBlock, 0, st>>>(p, L);
-        if (s->timing) {
+        if (s->timing && (chunk < 0 || chunk == K - 1)) {
             GXB_CUDA(cudaEventRecord(s->kev[1], st));
             s->timing_pending = true;
         }
         s->launches++;
-        const TilePlan& T = g->tiles;
-        if (T.num_spans) {
-            k_span_fold<Ops><<<grid_for(T.num_spans), kBlock, 0, st>>>(
-                T.d_span_slot, T.d_span_count, T.d_span_pbase, T.num_spans,
+        if (span_hi > span_lo) {
+            k_span_fold<Ops><<<grid_for(span_hi - span_lo), kBlock, 0, st>>>(
+                T.d_span_slot, T.d_span_count, T.d_span_pbase, span_lo, span_hi,
                 (const typename Ops::Acc*)s->d_tile_partials, (typename Ops::Acc*)s->d_sums);
             s->launches++;
         }
     }
-    const uint64_t owned = g->hi - g->lo;
     Ops aops = ops;
     if constexpr (!std::is_same<Ops, PrOps>::value) {
         aops.commit_inline = true;  // every gather of the round is done: commit changes in place
         s->committed_inline = true;
     }
-    k_apply_sums<Ops><<<grid_for(owned), kBlock, 0, st>>>(aops, (const typename Ops::Acc*)s->d_sums, g->lo, owned,
-                                                          g->tiles.nz_slots, s->d_stats);
-    s->launches++;
+    if (r_hi > r_lo) {
+        k_apply_sums<Ops><<<grid_for(r_hi - r_lo), kBlock, 0, st>>>(aops, (const typename Ops::Acc*)s->d_sums,
+                                                                     g->lo, r_lo, r_hi, T.nz_slots, s->d_stats);
+        s->launches++;
+    }
     GXB_CUDA(cudaGetLastError());
     return GXB_OK;
 }
@@ -1351,6 +1366,8 @@ int gxb_state_free(gxb_state* s) {
     dfree(s->d_sums);
     gxb_lp_free(s);
     dfree(s->d_send);
+    dfree(s->d_xsend);
+    dfree(s->d_xrecv);
     dfree(s->d_recv);
     delete s;
     return GXB_OK;
@@ -1450,6 +1467,30 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
         GXB_CUDA(cudaMemsetAsync(s->d_touched, 0, 4 * ((owned >> 5) + 1), st));
     }
     return end_round(s, dir, st);
+}
+
+// Pipeline shuffle (multi-GPU): a PageRank pull round split into exchange chunks so the
+// caller can send chunk k's new contributions while chunk k+1 computes.
+int gxb_iterate_begin(gxb_state* s, void* stream) {
+    if (!s) return fail(GXB_EINVAL, "gxb_iterate_begin: null state");
+    if (s->algo != GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "chunked rounds are for PageRank (dense exchange)");
+    if (options().pull_kernel == 1) return fail(GXB_EINVAL, "chunked rounds need the warp-tile pull kernel");
+    if (s->in_round) return fail(GXB_ESTATE, "gxb_iterate_begin: a round is open");
+    GXB_CHECK(collect_stats(s));
+    return begin_round(s, (cudaStream_t)stream);
+}
+
+int gxb_iterate_chunk(gxb_state* s, int k, void* stream) {
+    if (!s) return fail(GXB_EINVAL, "gxb_iterate_chunk: null state");
+    if (!s->in_round) return fail(GXB_ESTATE, "gxb_iterate_chunk: no open round");
+    if (k < 0 || k >= s->g->tiles.num_xchunks) return fail(GXB_EINVAL, "gxb_iterate_chunk: chunk out of range");
+    return launch_tile_and_apply(s, pr_ops(s), (cudaStream_t)stream, k);
+}
+
+int gxb_iterate_end(gxb_state* s, void* stream) {
+    if (!s) return fail(GXB_EINVAL, "gxb_iterate_end: null state");
+    if (!s->in_round) return fail(GXB_ESTATE, "gxb_iterate_end: no open round");
+    return end_round(s, GXB_DIR_PULL, (cudaStream_t)stream);
 }
 
 int gxb_request(gxb_state* s, int op, uint64_t lo, uint64_t hi, void* stream) {

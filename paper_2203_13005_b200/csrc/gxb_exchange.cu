@@ -75,6 +75,19 @@ __global__ void k_unpack(int algo, const uint32_t* __restrict__ rec, uint64_t n,
     if ((threadIdx.x & 31) == 0 && u) atomicAdd(units, u);
 }
 
+// needed-only dense exchange (PageRank): gather my values for every peer / scatter theirs
+template <typename T>
+__global__ void k_sparse_pack(const T* __restrict__ values, const uint32_t* __restrict__ idx, uint64_t n, T* out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = values[idx[i]];
+}
+
+template <typename T>
+__global__ void k_sparse_unpack(T* values, const uint32_t* __restrict__ idx, uint64_t n, const T* __restrict__ in) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        values[idx[i]] = in[i];
+}
+
 }  // namespace gxb
 
 using namespace gxb;
@@ -99,6 +112,24 @@ int gxb_exchange_buffer(gxb_state* s, int which, void** dev_ptr, uint64_t* bytes
                 *bytes = 4 * V;
             }
             return GXB_OK;
+        case GXB_BUF_VALUES_NEXT:  // PR: the contributions being written by the open round
+            if (s->algo != GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "GXB_BUF_VALUES_NEXT is PageRank-only");
+            *dev_ptr = s->d_contrib[s->cur ^ 1];
+            *bytes = (s->msg32 ? 4 : 8) * V;
+            return GXB_OK;
+        case GXB_BUF_SPARSE_SEND:
+        case GXB_BUF_SPARSE_RECV: {
+            if (s->algo != GXB_ALGO_PAGERANK || g->nparts < 2)
+                return fail(GXB_EINVAL, "sparse exchange buffers: PageRank on a partitioned graph only");
+            const uint64_t w = s->msg32 ? 4 : 8;
+            const bool snd = which == GXB_BUF_SPARSE_SEND;
+            const uint64_t n = snd ? g->xsend_off[g->nparts] : g->xrecv_off[g->nparts];
+            void** slot = snd ? &s->d_xsend : &s->d_xrecv;
+            if (!*slot) GXB_CHECK(dalloc(slot, w * (n + 1)));
+            *dev_ptr = *slot;
+            *bytes = w * n;
+            return GXB_OK;
+        }
         case GXB_BUF_SEND:
             if (!s->d_send) GXB_CHECK(dalloc(&s->d_send, rec * (owned + 1) + 16));
             *dev_ptr = s->d_send;
@@ -163,6 +194,57 @@ int gxb_exchange_unpack(gxb_state* s, const void* d_records, uint64_t count, voi
     GXB_CUDA(cudaStreamSynchronize(st));
     s->units_cur += u;
     s->frontier_len = n;
+    return GXB_OK;
+}
+
+int gxb_exchange_sparse_counts(const gxb_state* s, uint64_t* send_counts, uint64_t* recv_counts) {
+    if (!s || !send_counts || !recv_counts) return fail(GXB_EINVAL, "gxb_exchange_sparse_counts: null argument");
+    const gxb_graph* g = s->g;
+    if (g->nparts < 2 || g->xsend_off.empty()) return fail(GXB_EINVAL, "no needed-only exchange lists (nparts < 2)");
+    for (int q = 0; q < g->nparts; ++q) {
+        send_counts[q] = g->xsend_off[q + 1] - g->xsend_off[q];
+        recv_counts[q] = g->xrecv_off[q + 1] - g->xrecv_off[q];
+    }
+    return GXB_OK;
+}
+
+int gxb_exchange_sparse_pack(gxb_state* s, void* stream) {
+    if (!s) return fail(GXB_EINVAL, "gxb_exchange_sparse_pack: null state");
+    if (s->in_round) return fail(GXB_ESTATE, "gxb_exchange_sparse_pack: round still open");
+    void* buf;
+    uint64_t bytes;
+    GXB_CHECK(gxb_exchange_buffer(s, GXB_BUF_SPARSE_SEND, &buf, &bytes));
+    const gxb_graph* g = s->g;
+    const uint64_t n = g->xsend_off[g->nparts];
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n) {
+        if (s->msg32)
+            k_sparse_pack<float><<<grid_for(n), kBlock, 0, st>>>((const float*)s->d_contrib[s->cur], g->d_xsend_idx, n,
+                                                              (float*)buf);
+        else
+            k_sparse_pack<double><<<grid_for(n), kBlock, 0, st>>>(s->d_contrib[s->cur], g->d_xsend_idx, n, (double*)buf);
+    }
+    GXB_CUDA(cudaGetLastError());
+    return GXB_OK;
+}
+
+int gxb_exchange_sparse_unpack(gxb_state* s, void* stream) {
+    if (!s) return fail(GXB_EINVAL, "gxb_exchange_sparse_unpack: null state");
+    void* buf;
+    uint64_t bytes;
+    GXB_CHECK(gxb_exchange_buffer(s, GXB_BUF_SPARSE_RECV, &buf, &bytes));
+    const gxb_graph* g = s->g;
+    const uint64_t n = g->xrecv_off[g->nparts];
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n) {
+        if (s->msg32)
+            k_sparse_unpack<float><<<grid_for(n), kBlock, 0, st>>>((float*)s->d_contrib[s->cur], g->d_xrecv_idx, n,
+                                                                (const float*)buf);
+        else
+            k_sparse_unpack<double><<<grid_for(n), kBlock, 0, st>>>(s->d_contrib[s->cur], g->d_xrecv_idx, n,
+                                                                 (const double*)buf);
+    }
+    GXB_CUDA(cudaGetLastError());
     return GXB_OK;
 }
 

@@ -56,6 +56,10 @@ struct TilePlan {
     uint64_t num_tiles = 0;
     uint64_t num_spans = 0;      // slots whose edges cross a tile boundary
     uint64_t num_partials = 0;   // sum of tiles touched by spans
+    int num_xchunks = 1;         // exchange chunks of the owned slots (pipeline shuffle)
+    std::vector<uint64_t> xchunk_slot;  // K+1 relative slot bounds
+    std::vector<uint64_t> xchunk_tile;  // K+1 tile bounds
+    std::vector<uint64_t> xchunk_span;  // K+1 span bounds
     uint64_t* d_tile_start = nullptr;  // num_tiles + 1 tile boundaries (edge offsets, slot-aligned)
     uint32_t* d_lane_slot = nullptr;   // per kTileK-edge lane chunk: slot of its first edge
     uint8_t* d_lane_mask = nullptr;    // per lane chunk: bit j <=> edge kTileK*c + j closes its segment
@@ -129,6 +133,10 @@ struct gxb_graph {
     uint32_t* d_out_dst = nullptr;
     uint32_t* d_out_w = nullptr;
     std::vector<uint32_t> h_indeg_sorted;  // owned in-degrees (descending), host copy
+    // needed-only exchange (nparts > 1): sorted slot lists per peer, segment offsets on host
+    uint32_t* d_xsend_idx = nullptr;    // my owned slots needed by peer q: [xsend_off[q], xsend_off[q+1])
+    uint32_t* d_xrecv_idx = nullptr;    // peer p's slots my CSC reads:      [xrecv_off[p], xrecv_off[p+1])
+    std::vector<uint64_t> xsend_off, xrecv_off;
     gxb::PullPlan plan;
     gxb::TilePlan tiles;
 };
@@ -250,6 +258,7 @@ inline unsigned grid_for(uint64_t n, int block = kBlock, uint64_t cap = 148ull *
 }
 
 int build_pull_plan(gxb_graph* g, cudaStream_t st);
+uint64_t xchunk_bound(uint64_t owned, int k, int K);  // relative slot bound k of K exchange chunks
 
 // runtime tuning knobs (gxb_set_option); defaults are the measured best on B200
 struct Options {
@@ -258,6 +267,9 @@ struct Options {
     int64_t l1_hot_kb = 160;      // L1 budget (KB) of the L1-allocating prefix (others bypass L1)
     int64_t push_alpha = 20;      // push when frontier out-edges * alpha < |E|
     int64_t pull_kernel = 0;      // 0 = warp tiles, 1 = degree-binned groups
+    int64_t carveout = -1;        // tile kernel shared-memory carveout in % (-1 = driver default)
+    int64_t exchange_chunks = 1;  // multi-GPU: chunks of the dense exchange overlapped with compute
+    int64_t overlap_reserve_sms = 8;  // SMs left to NCCL while a chunked round computes
     int64_t pr_message_bits = 64; // PageRank message (rank / out_deg) precision: 64 or 32 (f64 accumulation)
 };
 Options& options();

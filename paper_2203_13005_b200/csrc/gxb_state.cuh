@@ -167,6 +167,8 @@ struct gxb_state {
     uint64_t launches = 0;
 
     // exchange
+    void* d_xsend = nullptr;  // needed-only PR exchange: packed values per peer
+    void* d_xrecv = nullptr;
     void* d_send = nullptr;
     void* d_recv = nullptr;
     uint64_t recv_cap = 0;

@@ -344,6 +344,8 @@ static void graph_release(gxb_graph* g) {
     dfree(g->plan.d_item_count);
     dfree(g->plan.d_slot_arrive);
     dfree(g->tiles.d_lane_slot);
+    dfree(g->d_xsend_idx);
+    dfree(g->d_xrecv_idx);
     dfree(g->tiles.d_tile_start);
     dfree(g->tiles.d_lane_mask);
     dfree(g->tiles.d_tile_head);
@@ -357,6 +359,10 @@ static void graph_release(gxb_graph* g) {
 
 // warp-tile plan of the edge-balanced pull merge: kTileEdges edges per warp;
 // slots crossing a tile boundary ("spans") combine per-tile partials
+uint64_t xchunk_bound(uint64_t owned, int k, int K) {
+    return owned * (uint64_t)k * (uint64_t)k / ((uint64_t)K * (uint64_t)K);  // exact: peers recompute it
+}
+
 static int build_tile_plan(gxb_graph* g, cudaStream_t st) {
     TilePlan& T = g->tiles;
     const std::vector<uint32_t>& deg = g->h_indeg_sorted;
@@ -364,24 +370,41 @@ static int build_tile_plan(gxb_graph* g, cudaStream_t st) {
     uint64_t nz = 0;
     while (nz < owned && deg[nz] > 0) ++nz;
     T.nz_slots = nz;
-    // Fixed tiles of kTileEdges edges (measured faster than slot-aligned variable tiles:
-    // those leave lanes idle at every cut); slots crossing a tile boundary become spans
-    // whose per-tile partials are folded by k_span_fold.
+    // Exchange chunks (multi-GPU pipeline shuffle): the owned slots are cut into K chunks
+    // at quadratic fractions (k/K)^2 of the owned count, so chunk 0 holds the few hub slots
+    // (most of the edges) and the last chunk the many tail slots. Every rank cuts its own
+    // block with the same formula, so peers know each other's chunk ranges.
+    const int K = std::max(1, g->nparts > 1 ? (int)options().exchange_chunks : 1);
+    T.num_xchunks = K;
+    T.xchunk_slot.assign(K + 1, 0);
+    for (int k = 0; k <= K; ++k) T.xchunk_slot[k] = xchunk_bound(owned, k, K);
+    // Fixed tiles of kTileEdges edges restarting at every chunk (measured faster than
+    // slot-aligned variable tiles: those leave lanes idle at every cut); slots crossing a
+    // tile boundary become spans whose per-tile partials are folded by k_span_fold.
     std::vector<uint64_t> off(nz + 1, 0);
     for (uint64_t s = 0; s < nz; ++s) off[s + 1] = off[s] + deg[s];
     const uint64_t E = off[nz];
     std::vector<uint64_t> starts;
-    starts.reserve(E / kTileEdges + 2);
-    for (uint64_t pos = 0; pos < E; pos += kTileEdges) starts.push_back(pos);
+    starts.reserve(E / kTileEdges + K + 2);
+    T.xchunk_tile.assign(K + 1, 0);
+    for (int k = 0; k < K; ++k) {
+        T.xchunk_tile[k] = starts.size();
+        const uint64_t e0 = off[std::min<uint64_t>(T.xchunk_slot[k], nz)];
+        const uint64_t e1 = off[std::min<uint64_t>(T.xchunk_slot[k + 1], nz)];
+        for (uint64_t pos = e0; pos < e1; pos += kTileEdges) starts.push_back(pos);
+    }
     T.num_tiles = starts.size();
+    T.xchunk_tile[K] = T.num_tiles;
     starts.push_back(E);
-    // span table: slots crossing a tile boundary (hubs)
+    // span table: slots crossing a tile boundary (hubs); never across chunks
     std::vector<uint32_t> head(T.num_tiles + 1, kNone), tail(T.num_tiles + 1, kNone);
     std::vector<uint32_t> sfirst, scount, sslot;
     std::vector<uint64_t> spbase;
+    T.xchunk_span.assign(K + 1, 0);
     uint64_t pbase = 0, t = 0;
+    int kc = 0;
     for (uint64_t s = 0; s < nz; ++s) {
-        if (off[s] / kTileEdges == (off[s + 1] - 1) / kTileEdges) continue;  // inside one tile
+        while (kc < K && s >= T.xchunk_slot[kc + 1]) T.xchunk_span[++kc] = sfirst.size();
         while (t + 1 < T.num_tiles && starts[t + 1] <= off[s]) ++t;
         uint64_t t1 = t;
         while (t1 + 1 < T.num_tiles && starts[t1 + 1] < off[s + 1]) ++t1;
@@ -397,6 +420,7 @@ static int build_tile_plan(gxb_graph* g, cudaStream_t st) {
         for (uint64_t u = t + 1; u < t1; ++u) tail[u] = k;
         t = t1;
     }
+    while (kc < K) T.xchunk_span[++kc] = sfirst.size();
     T.num_spans = sfirst.size();
     T.num_partials = pbase;
     int rc = GXB_OK;
@@ -474,6 +498,73 @@ int build_pull_plan(gxb_graph* g, cudaStream_t st) {
     }
     GXB_CUDA(cudaMemsetAsync(P.d_slot_arrive, 0, 4 * (P.chunk_end + 1), st));
     GXB_CUDA(cudaStreamSynchronize(st));
+    return GXB_OK;
+}
+
+// ---- needed-only mirror exchange lists (per-peer need masks) ----
+// send list to peer q: my owned slots that are the source of an edge into q's
+// destinations; recv list from peer p: p's owned slots that are sources of my CSC.
+// Both are sorted by slot, so my send list to q is exactly q's recv list from me.
+__global__ void k_send_keys(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, uint64_t n,
+                            const uint64_t* __restrict__ bounds, int nparts, int part, uint64_t* keys) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = src[i], d = dst[i];
+        const int os = owner_of(bounds, nparts, s), od = owner_of(bounds, nparts, d);
+        keys[i] = (os == part && od != part) ? ((uint64_t)od << 32 | s) : ((uint64_t)nparts << 32);
+    }
+}
+
+__global__ void k_recv_keys(const uint32_t* __restrict__ in_src, uint64_t n, const uint64_t* __restrict__ bounds,
+                            int nparts, int part, uint64_t* keys) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = in_src[i];
+        const int os = owner_of(bounds, nparts, s);
+        keys[i] = (os != part) ? ((uint64_t)os << 32 | s) : ((uint64_t)nparts << 32);
+    }
+}
+
+static int unique_segments(uint64_t* keys, uint64_t* alt, uint64_t n, int nparts, cudaStream_t st,
+                           uint32_t** d_idx, std::vector<uint64_t>& off_host) {
+    uint64_t* kout = nullptr;
+    uint32_t* vdummy = nullptr;
+    GXB_CHECK(sort_pairs(keys, alt, nullptr, nullptr, n, 32 + bits_for((uint64_t)nparts), st, &kout, &vdummy));
+    uint64_t* uniq = (kout == keys) ? alt : keys;
+    uint64_t* d_num = nullptr;
+    GXB_CHECK(dalloc_t(&d_num, 1));
+    size_t temp = 0;
+    GXB_CUDA(cub::DeviceSelect::Unique(nullptr, temp, kout, uniq, d_num, (int64_t)n, st));
+    void* tmp = nullptr;
+    GXB_CHECK(dalloc(&tmp, temp));
+    cudaError_t e = cub::DeviceSelect::Unique(tmp, temp, kout, uniq, d_num, (int64_t)n, st);
+    uint64_t nu = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&nu, d_num, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    dfree(tmp);
+    dfree(d_num);
+    if (e != cudaSuccess) return cuda_fail(e, "unique_segments");
+    uint64_t* d_off = nullptr;
+    GXB_CHECK(dalloc_t(&d_off, nparts + 1));
+    k_offsets<<<grid_e(nu + 1), kBlock, 0, st>>>(uniq, nu, (uint64_t)nparts, d_off);
+    off_host.assign(nparts + 1, 0);
+    e = cudaMemcpyAsync(off_host.data(), d_off, 8 * (nparts + 1), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    dfree(d_off);
+    if (e != cudaSuccess) return cuda_fail(e, "unique_segments offsets");
+    const uint64_t nv = off_host[nparts];  // entries before the sentinel
+    GXB_CHECK(dalloc_t(d_idx, nv + 1));
+    if (nv) k_low32<<<grid_e(nv), kBlock, 0, st>>>(uniq, nv, *d_idx);
+    GXB_CUDA(cudaStreamSynchronize(st));
+    return GXB_OK;
+}
+
+static int build_sparse_exchange(gxb_graph* g, const uint32_t* src, const uint32_t* dst, uint64_t E,
+                                 uint64_t* keyA, uint64_t* keyB, const uint64_t* d_bounds, cudaStream_t st) {
+    k_send_keys<<<grid_e(E), kBlock, 0, st>>>(src, dst, E, d_bounds, g->nparts, g->part, keyA);
+    GXB_CHECK(unique_segments(keyA, keyB, E, g->nparts, st, &g->d_xsend_idx, g->xsend_off));
+    if (g->owned_edges)
+        k_recv_keys<<<grid_e(g->owned_edges), kBlock, 0, st>>>(g->d_in_src, g->owned_edges, d_bounds, g->nparts,
+                                                                g->part, keyA);
+    GXB_CHECK(unique_segments(keyA, keyB, g->owned_edges, g->nparts, st, &g->d_xrecv_idx, g->xrecv_off));
     return GXB_OK;
 }
 
@@ -723,6 +814,7 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
         g->owned_out_edges = owned_edges;
         GXB_CUDA(cudaStreamSynchronize(st));
     }
+    if (g->nparts > 1 && E) GXB_CHECK(build_sparse_exchange(g, src, dst, E, csc_key, key_alt, d_bounds, st));
     GXB_CUDA(cudaGetLastError());
     GXB_CHECK(build_pull_plan(g, st));
     GXB_CHECK(build_tile_plan(g, st));
@@ -782,6 +874,15 @@ int gxb_set_option(const char* name, int64_t value) {
     } else if (n == "l1_hot_kb") {
         if (value < 0) return fail(GXB_EINVAL, "l1_hot_kb must be >= 0");
         o.l1_hot_kb = value;
+    } else if (n == "exchange_chunks") {
+        if (value < 1 || value > 64) return fail(GXB_EINVAL, "exchange_chunks: 1..64");
+        o.exchange_chunks = value;
+    } else if (n == "overlap_reserve_sms") {
+        if (value < 0 || value > 140) return fail(GXB_EINVAL, "overlap_reserve_sms: 0..140");
+        o.overlap_reserve_sms = value;
+    } else if (n == "carveout") {
+        if (value < -1 || value > 100) return fail(GXB_EINVAL, "carveout: -1 or 0..100");
+        o.carveout = value;
     } else if (n == "pr_message_bits") {
         if (value != 32 && value != 64) return fail(GXB_EINVAL, "pr_message_bits: 32 or 64");
         o.pr_message_bits = value;
@@ -803,6 +904,9 @@ int gxb_get_option(const char* name, int64_t* value) {
     else if (n == "push_alpha") *value = o.push_alpha;
     else if (n == "pull_kernel") *value = o.pull_kernel;
     else if (n == "pr_message_bits") *value = o.pr_message_bits;
+    else if (n == "carveout") *value = o.carveout;
+    else if (n == "overlap_reserve_sms") *value = o.overlap_reserve_sms;
+    else if (n == "exchange_chunks") *value = o.exchange_chunks;
     else if (n == "l1_hot_kb") *value = o.l1_hot_kb;
     else return fail(GXB_EINVAL, "unknown option " + n);
     return GXB_OK;
@@ -914,6 +1018,14 @@ int gxb_graph_out_degree(const gxb_graph* g, uint32_t* host_out) {
 int gxb_graph_part_bounds(const gxb_graph* g, uint64_t* host_out) {
     if (!g || !host_out) return fail(GXB_EINVAL, "gxb_graph_part_bounds: null argument");
     std::memcpy(host_out, g->bounds.data(), 8 * g->bounds.size());
+    return GXB_OK;
+}
+
+int gxb_graph_xchunks(const gxb_graph* g, int* K, uint64_t* host_bounds) {
+    if (!g || !K) return fail(GXB_EINVAL, "gxb_graph_xchunks: null argument");
+    *K = g->tiles.num_xchunks;
+    if (host_bounds)
+        for (int k = 0; k <= *K; ++k) host_bounds[k] = g->tiles.xchunk_slot[k];
     return GXB_OK;
 }
 

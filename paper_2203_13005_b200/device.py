@@ -171,6 +171,14 @@ class DeviceGraph:
         L.check(L.lib().gxb_graph_out_degree(self._h, _vp(out)))
         return out
 
+    def xchunks(self) -> np.ndarray:
+        """Relative slot bounds of the exchange chunks of the owned block (K + 1)."""
+        k = ctypes.c_int()
+        L.check(L.lib().gxb_graph_xchunks(self._h, ctypes.byref(k), None))
+        out = np.empty(k.value + 1, dtype=np.uint64)
+        L.check(L.lib().gxb_graph_xchunks(self._h, ctypes.byref(k), _vp(out)))
+        return out
+
     def bounds(self) -> np.ndarray:
         out = np.empty(self.nparts + 1, dtype=np.uint64)
         L.check(L.lib().gxb_graph_part_bounds(self._h, _vp(out)))
@@ -224,6 +232,15 @@ class DeviceState:
     def iterate(self, direction: str = "auto", stream=None):
         L.check(L.lib().gxb_iterate(self._h, DIRECTIONS[direction], _stream_ptr(stream)))
 
+    def iterate_begin(self, stream=None):
+        L.check(L.lib().gxb_iterate_begin(self._h, _stream_ptr(stream)))
+
+    def iterate_chunk(self, k: int, stream=None):
+        L.check(L.lib().gxb_iterate_chunk(self._h, k, _stream_ptr(stream)))
+
+    def iterate_end(self, stream=None):
+        L.check(L.lib().gxb_iterate_end(self._h, _stream_ptr(stream)))
+
     def request(self, op: int, lo: int, hi: int, stream=None):
         L.check(L.lib().gxb_request(self._h, op, lo, hi, _stream_ptr(stream)))
 
@@ -276,6 +293,22 @@ class DeviceState:
 
     def unpack(self, ptr: int, count: int, stream=None):
         L.check(L.lib().gxb_exchange_unpack(self._h, ctypes.c_void_p(ptr), count, _stream_ptr(stream)))
+
+    def sparse_counts(self):
+        """Per-peer element counts of the needed-only PageRank exchange (send, recv), or None."""
+        n = self.graph.nparts
+        if n < 2 or self.algo != "pagerank":
+            return None
+        snd = np.zeros(n, dtype=np.uint64)
+        rcv = np.zeros(n, dtype=np.uint64)
+        L.check(L.lib().gxb_exchange_sparse_counts(self._h, _vp(snd), _vp(rcv)))
+        return [int(x) for x in snd], [int(x) for x in rcv]
+
+    def sparse_pack(self, stream=None):
+        L.check(L.lib().gxb_exchange_sparse_pack(self._h, _stream_ptr(stream)))
+
+    def sparse_unpack(self, stream=None):
+        L.check(L.lib().gxb_exchange_sparse_unpack(self._h, _stream_ptr(stream)))
 
     def free(self):
         if getattr(self, "_h", None):

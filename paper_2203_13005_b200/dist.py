@@ -135,20 +135,62 @@ class PartitionedRun:
     records: list = field(default_factory=list)
     device: object = None
     phase_times: dict | None = None   # per-phase seconds when profiling (adds a sync per phase)
+    needed_only: bool = False         # PR: send each peer only the values its CSC reads (NCCL
+                                      # all-to-all; measured slower than the all-gather at N <= 4)
+    sparse_ratio: float = 0.8         # ... when that is below this fraction of the dense volume
+    overlap: bool = False             # pipeline shuffle: chunked PR rounds with the exchange overlapped
+                                      # (needs exchange_chunks > 1; measured slower than one all-gather
+                                      # at N <= 4, where the tile kernel and NCCL contend for L2)
 
     def __post_init__(self):
         self.algo = self.state.algo
         self.iteration = 0
         self.skipped_rounds = 0
         self._pr_remote = None
+        self._sparse = None
+        self._pending = []
+        self.xchunks = 1
+        if self.overlap and self.algo == "pagerank" and hasattr(self.state, "graph") and \
+                hasattr(self.state.graph, "xchunks"):
+            self.xchunks = len(self.state.graph.xchunks()) - 1
 
     # ---- the sync round ---------------------------------------------------
+    def _exchange_needed(self) -> int | None:
+        """PageRank, needed-only: each peer receives just my values its CSC reads (static,
+        slot-sorted lists), packed by a gather kernel and moved with one NCCL all-to-all."""
+        if self._sparse is None:
+            counts = self.state.sparse_counts() if hasattr(self.state, "sparse_counts") else None
+            if counts is None:
+                self._sparse = False
+            else:
+                snd, rcv = counts
+                own = int(self.bounds[self.comm.rank + 1] - self.bounds[self.comm.rank])
+                dense = int(self.bounds[-1]) - own
+                self._sparse = (snd, rcv) if sum(rcv) < self.sparse_ratio * dense else False
+        if not self._sparse:
+            return None
+        snd, rcv = self._sparse
+        sptr, sbytes = self.state.buffer(L.BUF_SPARSE_SEND)
+        rptr, rbytes = self.state.buffer(L.BUF_SPARSE_RECV)
+        width = sbytes // max(1, sum(snd)) if sum(snd) else (rbytes // max(1, sum(rcv)) if sum(rcv) else 8)
+        dt = "f8" if width == 8 else "f4"
+        self.state.sparse_pack()
+        send = self._view(sptr, sbytes, dt)
+        recv = self._view(rptr, rbytes, dt)
+        self.comm.dist.all_to_all_single(recv, send, output_split_sizes=rcv, input_split_sizes=snd,
+                                         group=self.comm.group)
+        self.state.sparse_unpack()
+        return width * sum(rcv)
+
     def _exchange_dense(self) -> int:
         """PageRank: every vertex changes, so all-gather each owner's contribution slice.
 
         The dealt layout pads every partition block to the same size, so this is one
         in-place NCCL all-gather over the replica (ring / NVLS); other layouts fall back
         to a grouped send/recv all-gather-v."""
+        moved = self._exchange_needed() if self.needed_only else None
+        if moved is not None:
+            return moved
         ptr, nbytes = self.state.buffer(L.BUF_VALUES)
         width = nbytes // max(1, int(self.bounds[-1]))   # 8 (f64 messages) or 4 (pr_message_bits = 32)
         values = self._view(ptr, nbytes, "f8" if width == 8 else "f4")
@@ -196,18 +238,65 @@ class PartitionedRun:
             return t
         return t0
 
+    # ---- pipeline shuffle: chunked PageRank round with the exchange overlapped ----
+    def _chunk_ranges(self, q: int, k: int, K: int) -> tuple[int, int]:
+        lo, hi = int(self.bounds[q]), int(self.bounds[q + 1])
+        owned = hi - lo
+        b0 = owned * k * k // (K * K)   # xchunk_bound (csrc/gxb_store.cu)
+        b1 = owned * (k + 1) * (k + 1) // (K * K)
+        return lo + b0, lo + b1
+
+    def _overlapped_pagerank_round(self):
+        """Chunks run hubs-last (tail chunks hold many slots but few edges); chunk k's new
+        contributions go to every peer while later chunks compute (A/agent.py:282-328's
+        upload/compute overlap, on streams and NCCL instead of threads and queues)."""
+        st = self.state
+        K = self.xchunks
+        ptr, nbytes = st.buffer(L.BUF_VALUES_NEXT)
+        width = nbytes // max(1, int(self.bounds[-1]))
+        values = self._view(ptr, nbytes, "f8" if width == 8 else "f4")
+        st.iterate_begin()
+        works = []
+        for k in reversed(range(K)):
+            st.iterate_chunk(k)
+            ops = []
+            for q in range(self.comm.world):
+                if q == self.comm.rank:
+                    continue
+                a, b = self._chunk_ranges(self.comm.rank, k, K)
+                if b > a:
+                    ops.append(self.comm.dist.P2POp(self.comm.dist.isend, values[a:b], q, self.comm.group))
+                a, b = self._chunk_ranges(q, k, K)
+                if b > a:
+                    ops.append(self.comm.dist.P2POp(self.comm.dist.irecv, values[a:b], q, self.comm.group))
+            if ops:
+                works.extend(self.comm.dist.batch_isend_irecv(ops))
+        st.iterate_end()
+        self._pending = works
+        sizes = np.diff(self.bounds.astype(np.int64))
+        return width * int(self.bounds[-1] - sizes[self.comm.rank])
+
     def step(self, direction: str = "auto") -> StepRecord:
         import time
         t0 = time.perf_counter() if self.phase_times is not None else 0.0
-        self.state.iterate(direction)
+        for w in self._pending:  # the previous round's overlapped exchange
+            w.wait()
+        self._pending = []
+        overlapped = (self.algo == "pagerank" and self.comm.world > 1 and self.overlap and self.xchunks > 1
+                      and self._pr_remote is not None and not (self.enable_skip and self._pr_remote == 0))
+        moved_early = 0
+        if overlapped:
+            moved_early = self._overlapped_pagerank_round()
+        else:
+            self.state.iterate(direction)
         st = self.state.stats()
         t0 = self._tick("compute", t0)
         handle = self.comm.vote_start(
             [st["changed"], st["next_active"], st["next_units"], st["remote_active"]], st["max_stat"],
             self.device)
-        moved = 0
-        early = False
-        if self.algo == "pagerank" and self._pr_remote is not None and self.comm.world > 1:
+        moved = moved_early
+        early = overlapped
+        if not overlapped and self.algo == "pagerank" and self._pr_remote is not None and self.comm.world > 1:
             # every PageRank vertex is active every round, so the skip vote is the same each
             # round: start the dense exchange behind the vote without waiting for its result
             early = not (self.enable_skip and self._pr_remote == 0)
@@ -235,10 +324,17 @@ class PartitionedRun:
         self.records.append(rec)
         return rec
 
+    def finish(self):
+        """Complete any exchange still in flight (the replica is then fully current)."""
+        for w in self._pending:
+            w.wait()
+        self._pending = []
+
     def run(self, max_iterations: int, direction: str = "auto") -> tuple[int, bool]:
         converged = False
         while self.iteration < max_iterations:
             if self.step(direction).converged:
                 converged = True
                 break
+        self.finish()
         return self.iteration, converged
