@@ -381,33 +381,60 @@ def main():
     }
 
     # ---- e2e through the public API with host buffers (agent pull/push per step) ----
+    # Every step installs the attributes from pinned host memory (the agent's
+    # pull_from_upper), runs the round, and reads the result back (push_to_upper).
+    # The copies run on a copy stream, double-buffered, so step t+1's upload and step t's
+    # download overlap the rounds (A/agent.py:282-328's stage tasks beside the compute).
     e2e = None
     if not args.no_e2e:
-        import numpy as np
         st = run.state
         arity = st.arity
-        host_in = torch.empty(V * arity, dtype=torch.float64, pin_memory=True)
-        host_out = torch.empty(V * arity, dtype=torch.float64, pin_memory=True)
-        st.read_attrs_into(host_in.numpy().reshape(V, arity))
+        host_in = [torch.empty(V * arity, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+        host_out = [torch.empty(V * arity, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+        st.read_attrs_into(host_in[0].numpy().reshape(V, arity))
+        host_in[1].copy_(host_in[0])
         e2e_run = PartitionedRun(st, bounds, comm, enable_skip=True, device=dev)
+        copy = torch.cuda.Stream(dev)       # host -> device
+        copy_out = torch.cuda.Stream(dev)   # device -> host (the link is full duplex)
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        ev_in, ev_inst, ev_out, ev_d2h = ([ev(), ev()] for _ in range(4))
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            st.write_attrs(host_in, stream)            # update("pull_from_upper")
-            e2e_run.step()                             # requestGen/Merge/Apply + sync round
-            st.read_attrs_into(host_out.numpy().reshape(V, arity), owned_only=False, stream=stream)
+        st.attrs_h2d(host_in[0], 0, copy)
+        ev_in[0].record(copy)
+        for t in range(args.steps):
+            b, nb = t % 2, (t + 1) % 2
+            stream.wait_event(ev_in[b])
+            st.attrs_install(b, stream)                       # update("pull_from_upper")
+            ev_inst[b].record(stream)
+            if t + 1 < args.steps:
+                if t >= 1:
+                    copy.wait_event(ev_inst[nb])              # staging buffer nb was installed at t-1
+                st.attrs_h2d(host_in[nb], nb, copy)
+                ev_in[nb].record(copy)
+            e2e_run.step()                                    # requestGen/Merge/Apply + sync round
+            if t >= 2:
+                stream.wait_event(ev_d2h[b])                  # output buffer b drained at t-2
+            st.attrs_extract(b, stream)                       # update("push_to_upper")
+            ev_out[b].record(stream)
+            copy_out.wait_event(ev_out[b])
+            st.attrs_d2h(host_out[b], b, copy_out)
+            ev_d2h[b].record(copy_out)
+        copy.synchronize()
+        copy_out.synchronize()
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
+        e2e_run.finish()
         if world > 1:
             t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
         e2e = {"value": round(E * args.steps / e2e_s / 1e9, 3), "unit": "GTEPS",
                "h2d_bytes_per_step": 8 * V * arity, "d2h_bytes_per_step": 8 * V * arity,
-               "path": "DeviceState.write_attrs (pull_from_upper) -> gxb_iterate + sync round -> "
-                       "gxb_read_attrs (push_to_upper), pinned host buffers"}
+               "path": "gxb_attrs_h2d/install (pull_from_upper) -> round -> gxb_attrs_extract/d2h "
+                       "(push_to_upper), pinned host buffers, double-buffered, one copy stream per direction"}
 
     # ---- secondary workload (SSSP on the same scale) and CPU baseline, rank 0 / N = 1 ----
     skipped_rounds = run.skipped_rounds

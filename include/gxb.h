@@ -252,6 +252,16 @@ int gxb_read_attrs(gxb_state* s, double* host_out, int owned_only, void* stream)
  * for distances), else GXB_ERANGE. */
 int gxb_write_attrs(gxb_state* s, const double* host_in, void* stream);
 
+/* asynchronous staging for a pipelined agent loop (no host synchronisation; the
+ * caller orders the copy and compute streams with events): h2d copies pinned host
+ * attributes into staging buffer `buf` (0/1), install scatters them into the state,
+ * extract gathers the state into output buffer `buf`, d2h copies it to pinned host
+ * memory. install does not validate values (use gxb_write_attrs for checked input). */
+int gxb_attrs_h2d(gxb_state* s, const double* host_in, int buf, void* stream);
+int gxb_attrs_install(gxb_state* s, int buf, void* stream);
+int gxb_attrs_extract(gxb_state* s, int buf, void* stream);
+int gxb_attrs_d2h(gxb_state* s, double* host_out, int buf, void* stream);
+
 /* ---- profiling: CUDA events around the main merge kernel of every fused
  * iteration, and a count of every kernel the library launched ---- */
 typedef struct gxb_profile {

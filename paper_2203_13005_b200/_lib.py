@@ -116,6 +116,10 @@ def _sig(L):
         "gxb_exchange_sparse_unpack": (I, [P, P]),
         "gxb_read_attrs": (I, [P, P, I, P]),
         "gxb_write_attrs": (I, [P, P, P]),
+        "gxb_attrs_h2d": (I, [P, P, I, P]),
+        "gxb_attrs_install": (I, [P, I, P]),
+        "gxb_attrs_extract": (I, [P, I, P]),
+        "gxb_attrs_d2h": (I, [P, P, I, P]),
         "gxb_profile_enable": (I, [P, I]),
         "gxb_profile_read": (I, [P, ctypes.POINTER(Profile), I]),
     }

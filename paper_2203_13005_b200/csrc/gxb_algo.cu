@@ -1357,6 +1357,10 @@ int gxb_state_free(gxb_state* s) {
     dfree(s->d_merged);
     dfree(s->d_partials);
     dfree(s->d_stage);
+    for (int i = 0; i < 2; ++i) {
+        dfree(s->d_stage_in[i]);
+        dfree(s->d_stage_out[i]);
+    }
     for (int i = 0; i < 3; ++i)
         if (s->kev[i]) cudaEventDestroy(s->kev[i]);
     dfree(s->d_push_counts);
@@ -1641,6 +1645,60 @@ int gxb_write_attrs(gxb_state* s, const double* host_in, void* stream) {
     GXB_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
     GXB_CUDA(cudaStreamSynchronize(st));
     if (bad) return fail(GXB_ERANGE, "gxb_write_attrs: value not representable on the device");
+    return GXB_OK;
+}
+
+// ---- asynchronous host staging (no host synchronisation; the caller orders streams) ----
+// Two staging buffers per direction let the next step's host->device copy and the
+// previous step's device->host copy run on a copy stream while the round computes.
+static int stage_pair(gxb_state* s) {
+    const uint64_t n = s->g->V * s->arity + 1;
+    for (int i = 0; i < 2; ++i) {
+        if (!s->d_stage_in[i]) GXB_CHECK(dalloc_t(&s->d_stage_in[i], n));
+        if (!s->d_stage_out[i]) GXB_CHECK(dalloc_t(&s->d_stage_out[i], n));
+    }
+    return GXB_OK;
+}
+
+int gxb_attrs_h2d(gxb_state* s, const double* host_in, int buf, void* stream) {
+    if (!s || !host_in || buf < 0 || buf > 1) return fail(GXB_EINVAL, "gxb_attrs_h2d: bad argument");
+    GXB_CHECK(stage_pair(s));
+    GXB_CUDA(cudaMemcpyAsync(s->d_stage_in[buf], host_in, 8 * s->g->V * s->arity, cudaMemcpyHostToDevice,
+                             (cudaStream_t)stream));
+    return GXB_OK;
+}
+
+int gxb_attrs_install(gxb_state* s, int buf, void* stream) {
+    if (!s || buf < 0 || buf > 1) return fail(GXB_EINVAL, "gxb_attrs_install: bad argument");
+    if (s->in_round) return fail(GXB_ESTATE, "gxb_attrs_install: a round is open");
+    GXB_CHECK(stage_pair(s));
+    gxb_graph* g = s->g;
+    if (!g->V) return GXB_OK;
+    uint32_t* d_bad = reinterpret_cast<uint32_t*>(s->d_fcount) + 2;  // sticky flag, checked by gxb_attrs_check
+    k_write_attrs<<<grid_for(g->V), kBlock, 0, (cudaStream_t)stream>>>(
+        s->algo, s->arity, g->d_dense2slot, g->V, g->d_outdeg, s->d_stage_in[buf], s->d_rank, s->d_contrib[s->cur],
+        s->d_dist_cur, s->d_dist_next, s->d_lab_cur, s->d_lab_next, d_bad, s->msg32);
+    GXB_CUDA(cudaGetLastError());
+    return GXB_OK;
+}
+
+int gxb_attrs_extract(gxb_state* s, int buf, void* stream) {
+    if (!s || buf < 0 || buf > 1) return fail(GXB_EINVAL, "gxb_attrs_extract: bad argument");
+    GXB_CHECK(stage_pair(s));
+    gxb_graph* g = s->g;
+    if (!g->V) return GXB_OK;
+    k_read_attrs<<<grid_for(g->V), kBlock, 0, (cudaStream_t)stream>>>(s->algo, s->arity, g->d_dense2slot, g->V, g->lo,
+                                                                       g->hi, 0, s->d_rank, s->d_dist_cur, s->d_lab_cur,
+                                                                       s->d_stage_out[buf]);
+    GXB_CUDA(cudaGetLastError());
+    return GXB_OK;
+}
+
+int gxb_attrs_d2h(gxb_state* s, double* host_out, int buf, void* stream) {
+    if (!s || !host_out || buf < 0 || buf > 1) return fail(GXB_EINVAL, "gxb_attrs_d2h: bad argument");
+    GXB_CHECK(stage_pair(s));
+    GXB_CUDA(cudaMemcpyAsync(host_out, s->d_stage_out[buf], 8 * s->g->V * s->arity, cudaMemcpyDeviceToHost,
+                             (cudaStream_t)stream));
     return GXB_OK;
 }
 

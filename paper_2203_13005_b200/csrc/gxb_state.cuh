@@ -156,6 +156,8 @@ struct gxb_state {
 
     // host<->device attribute staging (ascending-id order)
     double* d_stage = nullptr;
+    double* d_stage_in[2] = {nullptr, nullptr};   // async path: double-buffered
+    double* d_stage_out[2] = {nullptr, nullptr};
 
     // profiling: events around the main merge kernel, launch counter
     bool timing = false;

@@ -273,6 +273,19 @@ class DeviceState:
         else:  # pinned torch tensor
             L.check(L.lib().gxb_write_attrs(self._h, _vp(values), _stream_ptr(stream)))
 
+    # asynchronous staging (pipelined agent loop; pinned host tensors, explicit streams)
+    def attrs_h2d(self, host_in, buf: int, stream):
+        L.check(L.lib().gxb_attrs_h2d(self._h, _vp(host_in), buf, _stream_ptr(stream)))
+
+    def attrs_install(self, buf: int, stream=None):
+        L.check(L.lib().gxb_attrs_install(self._h, buf, _stream_ptr(stream)))
+
+    def attrs_extract(self, buf: int, stream=None):
+        L.check(L.lib().gxb_attrs_extract(self._h, buf, _stream_ptr(stream)))
+
+    def attrs_d2h(self, host_out, buf: int, stream):
+        L.check(L.lib().gxb_attrs_d2h(self._h, _vp(host_out), buf, _stream_ptr(stream)))
+
     def profile(self, enable: bool | None = None, reset: bool = False) -> dict:
         if enable is not None:
             L.check(L.lib().gxb_profile_enable(self._h, int(enable)))
