@@ -131,9 +131,11 @@ int gxb_reinit(gxb_ctx* ctx);                       /* always GXB_EPROTO (A/daem
 int gxb_init_count(const gxb_ctx* ctx, int* out);
 int gxb_shutdown(gxb_ctx* ctx);                     /* idempotent (A/daemon.py:163-168) */
 
-/* ---- tuning knobs (process-wide): "tile_minblocks" (0/4/6/8), "l2_hot_mb",
- * "push_alpha" (push when frontier out-edges * alpha < |E|), "pull_kernel"
- * (0 = edge-balanced warp tiles, 1 = degree-binned groups) ---- */
+/* ---- tuning knobs (process-wide): "tile_minblocks" (0/4/6/8), "l2_hot_mb", "l1_hot_kb",
+ * "push_alpha" (push when frontier out-edges * alpha < |E|), "pull_dense_div" (SSSP/CC
+ * pull gathers every source, no active-bitmap test, when frontier out-edges * div >= |E|;
+ * 0 = always test), "pull_kernel" (0 = edge-balanced warp tiles, 1 = degree-binned groups),
+ * "carveout", "exchange_chunks", "overlap_reserve_sms", "pr_message_bits" (64 / 32) ---- */
 int gxb_set_option(const char* name, int64_t value);
 int gxb_get_option(const char* name, int64_t* value);
 

@@ -48,6 +48,7 @@ struct HotPrefix {
 };
 
 struct PrOps {  // PageRank (A/algorithms.py:125-171)
+    static constexpr bool kPublishes = false;
     struct Acc {
         double s;
     };
@@ -90,7 +91,8 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
     };
     __device__ Pre preload(uint32_t slot) const { return {rank[slot], __ldg(f.outdeg + slot)}; }
     __device__ void apply(uint32_t slot, Acc a, LocalStats& st) const { apply_pre(slot, a, preload(slot), st); }
-    __device__ void apply_pre(uint32_t slot, Acc a, Pre p, LocalStats& st) const {
+    // returns whether the slot joins the next frontier as a changed vertex (never: always active)
+    __device__ bool apply_pre(uint32_t slot, Acc a, Pre p, LocalStats& st) const {
         const double old = p.old;
         const double nw = __dadd_rn(0.15, __dmul_rn(0.85, a.s));
         rank[slot] = nw;
@@ -102,6 +104,7 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
             st.changed++;
             st.max_stat = fmax(st.max_stat, fabs(nw - old));
         }
+        return false;
     }
 };
 
@@ -113,6 +116,7 @@ __device__ __forceinline__ bool eq4(uint4 a, uint4 b) {
 }
 
 struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-122)
+    static constexpr bool kPublishes = true;
     // The accumulator is the lane-wise min; "received a message" <=> some lane is
     // finite: a message comes from an active source, which always holds a finite
     // lane (it changed, or is a source at 0), and the host rejects weights for
@@ -127,6 +131,11 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
     const uint32_t* active_cur;
     FrontierView f;
     bool commit_inline;  // apply runs in its own kernel after every gather: write cur too, no commit pass
+    // Gen from active sources only. A dense pull may skip the bitmap: an inactive source
+    // already sent d + w to every out-neighbour the round after it last changed and
+    // distances only decrease, so its message never lowers a destination (same values,
+    // same changed set) — and the random bitmap read costs as much as the gather.
+    bool check_active;
     HotPrefix hp;
     uint32_t hot, hot1;
     static constexpr bool kWeighted = true;
@@ -146,7 +155,7 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
     __device__ static bool has(const Acc& a) { return (a.m.x & a.m.y & a.m.z & a.m.w) != kInf32; }
     // Gen: d + w per lane from an active source (102-105); inf stays inf
     __device__ bool gen(uint32_t s, uint32_t w, Msg& m) const {
-        if (!bit_test(active_cur, s)) return false;
+        if (check_active && !bit_test(active_cur, s)) return false;
         const uint32_t r = hp.rank(s);
         const uint64_t pol = r < hot ? l2_evict_last() : l2_evict_first();
         const uint4 d = r < hot1 ? ld_l1_v4(dist_cur + s, pol) : ld_nol1_v4(dist_cur + s, pol);
@@ -161,22 +170,23 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
     __device__ Pre preload(uint32_t slot) const { return {dist_cur[slot]}; }
     __device__ void apply(uint32_t slot, Acc a, LocalStats& st) const {
         if (!has(a)) return;
-        apply_pre(slot, a, preload(slot), st);
+        if (apply_pre(slot, a, preload(slot), st)) publish_changed(f, slot, st);
     }
-    __device__ void apply_pre(uint32_t slot, Acc a, Pre p, LocalStats& st) const {
-        if (!has(a)) return;
+    // returns whether the slot changed (the caller publishes it to the next frontier)
+    __device__ bool apply_pre(uint32_t slot, Acc a, Pre p, LocalStats& st) const {
+        if (!has(a)) return false;
         st.targets++;
         const uint4 o = p.o;
         const uint4 n = min4(o, a.m);
-        if (!eq4(n, o)) {
-            dist_next[slot] = n;
-            if (commit_inline) const_cast<uint4*>(dist_cur)[slot] = n;
-            publish_changed(f, slot, st);
-        }
+        if (eq4(n, o)) return false;
+        dist_next[slot] = n;
+        if (commit_inline) const_cast<uint4*>(dist_cur)[slot] = n;
+        return true;
     }
 };
 
 struct CcOps {  // min-label propagation; labels < 0xFFFFFFFF
+    static constexpr bool kPublishes = true;
     struct Acc {
         uint32_t m;
     };
@@ -186,6 +196,7 @@ struct CcOps {  // min-label propagation; labels < 0xFFFF
     const uint32_t* active_cur;
     FrontierView f;
     bool commit_inline;
+    bool check_active;  // see SsspOps::check_active (labels only decrease)
     HotPrefix hp;
     uint32_t hot, hot1;
     static constexpr bool kWeighted = false;
@@ -198,7 +209,7 @@ struct CcOps {  // min-label propagation; labels < 0xFFFF
     __device__ static Acc ld_cg(const Acc* p) { return {__ldcg(&p->m)}; }
     __device__ static bool has(const Acc& a) { return a.m != kInf32; }
     __device__ bool gen(uint32_t s, uint32_t, Msg& m) const {
-        if (!bit_test(active_cur, s)) return false;
+        if (check_active && !bit_test(active_cur, s)) return false;
         const uint32_t r = hp.rank(s);
         const uint64_t pol = r < hot ? l2_evict_last() : l2_evict_first();
         m = r < hot1 ? ld_l1_u32(lab_cur + s, pol) : ld_nol1_u32(lab_cur + s, pol);
@@ -211,18 +222,17 @@ struct CcOps {  // min-label propagation; labels < 0xFFFF
     __device__ Pre preload(uint32_t slot) const { return {lab_cur[slot]}; }
     __device__ void apply(uint32_t slot, Acc a, LocalStats& st) const {
         if (!has(a)) return;
-        apply_pre(slot, a, preload(slot), st);
+        if (apply_pre(slot, a, preload(slot), st)) publish_changed(f, slot, st);
     }
-    __device__ void apply_pre(uint32_t slot, Acc a, Pre p, LocalStats& st) const {
-        if (!has(a)) return;
+    __device__ bool apply_pre(uint32_t slot, Acc a, Pre p, LocalStats& st) const {
+        if (!has(a)) return false;
         st.targets++;
         const uint32_t o = p.o;
         const uint32_t n = min(o, a.m);
-        if (n != o) {
-            lab_next[slot] = n;
-            if (commit_inline) const_cast<uint32_t*>(lab_cur)[slot] = n;
-            publish_changed(f, slot, st);
-        }
+        if (n == o) return false;
+        lab_next[slot] = n;
+        if (commit_inline) const_cast<uint32_t*>(lab_cur)[slot] = n;
+        return true;
     }
 };
 
@@ -566,19 +576,44 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_t(const Pol p, cons
     }
 }
 
-// fold the per-tile partials of every span in tile order (deterministic)
+// fold the per-tile partials of every span (deterministic: a fixed order per span).
+// A warp takes 32 consecutive spans: short spans (< 16 partials) fold sequentially in
+// their own lane; long ones (hubs, hundreds of tiles) are folded by the whole warp —
+// lane-strided partial folds, then a fixed butterfly — so no lane walks a hub alone.
 template <class Ops>
-__global__ void k_span_fold(const uint32_t* __restrict__ span_slot, const uint32_t* __restrict__ span_count,
-                            const uint64_t* __restrict__ span_pbase, uint64_t span_lo, uint64_t span_hi,
-                            const typename Ops::Acc* __restrict__ partials, typename Ops::Acc* sums) {
+__global__ void __launch_bounds__(kBlock) k_span_fold(const uint32_t* __restrict__ span_slot,
+                                                      const uint32_t* __restrict__ span_count,
+                                                      const uint64_t* __restrict__ span_pbase, uint64_t span_lo,
+                                                      uint64_t span_hi, const typename Ops::Acc* __restrict__ partials,
+                                                      typename Ops::Acc* sums) {
     using Acc = typename Ops::Acc;
-    for (uint64_t k = span_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < span_hi;
-         k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t b = span_pbase[k];
-        const uint32_t n = span_count[k];
-        Acc tot = Ops::identity();
-        for (uint32_t i = 0; i < n; ++i) tot = Ops::combine(tot, partials[b + i]);
-        sums[span_slot[k]] = tot;
+    constexpr uint32_t kLong = 16;
+    const int lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
+    for (uint64_t w = span_lo + (blockIdx.x * (uint64_t)kBlock + threadIdx.x) / 32 * 32; w < span_hi;
+         w += nwarps * 32) {
+        const uint64_t k = w + lane;
+        const uint32_t n = k < span_hi ? span_count[k] : 0u;
+        if (n < kLong && k < span_hi) {
+            const uint64_t b = span_pbase[k];
+            Acc tot = Ops::identity();
+            for (uint32_t i = 0; i < n; ++i) tot = Ops::combine(tot, partials[b + i]);
+            sums[span_slot[k]] = tot;
+        }
+        unsigned big = __ballot_sync(kFull, n >= kLong);
+        while (big) {
+            const int src = __ffs(big) - 1;
+            big &= big - 1;
+            const uint64_t kk = w + src;
+            const uint32_t nn = __shfl_sync(kFull, n, src);
+            const uint64_t b = span_pbase[kk];
+            Acc tot = Ops::identity();
+#pragma unroll 8
+            for (uint32_t i = lane; i < nn; i += 32) tot = Ops::combine(tot, partials[b + i]);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) tot = Ops::combine(tot, Ops::shfl(tot, o));
+            if (lane == 0) sums[span_slot[kk]] = tot;
+        }
     }
 }
 
@@ -588,11 +623,14 @@ template <class Ops>
 __global__ void __launch_bounds__(kBlock) k_apply_sums(const Ops ops, const typename Ops::Acc* __restrict__ sums,
                                                         uint64_t lo, uint64_t rlo, uint64_t owned, uint64_t nz,
                                                         StatStripe* stats) {
-    // relative slots [rlo, owned); four independent slots per step: all loads before any store
+    // relative slots [rlo, owned); four independent slots per step: all loads before any store.
+    // The loop is warp-uniform so changed slots publish with one bitmap OR per word and
+    // one frontier reservation per warp.
     constexpr int kU = 4;
     LocalStats st;
     const uint64_t stride = (uint64_t)gridDim.x * kBlock;
-    for (uint64_t r0 = rlo + blockIdx.x * (uint64_t)kBlock + threadIdx.x; r0 < owned; r0 += kU * stride) {
+    const uint64_t lane = threadIdx.x & 31;
+    for (uint64_t r0 = rlo + blockIdx.x * (uint64_t)kBlock + threadIdx.x; r0 - lane < owned; r0 += kU * stride) {
         typename Ops::Acc a[kU];
         typename Ops::Pre pre[kU];
 #pragma unroll
@@ -601,11 +639,15 @@ __global__ void __launch_bounds__(kBlock) k_apply_sums(const Ops ops, const type
             a[u] = (r < nz) ? sums[r] : Ops::identity();
             if (r < owned) pre[u] = ops.preload((uint32_t)(lo + r));
         }
+        bool ch[kU];
+        uint32_t slot[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const uint64_t r = r0 + u * stride;
-            if (r < owned) ops.apply_pre((uint32_t)(lo + r), a[u], pre[u], st);
+            slot[u] = (uint32_t)(lo + r);
+            ch[u] = r < owned && ops.apply_pre(slot[u], a[u], pre[u], st);
         }
+        if constexpr (Ops::kPublishes) publish_changed_warp<kU>(ops.f, slot, ch, st);
     }
     flush_stats(st, stats);
 }
@@ -1040,6 +1082,7 @@ SsspOps sssp_ops(gxb_state* s) {
     o.active_cur = s->d_active[0];
     o.f = frontier_view(s);
     o.commit_inline = false;
+    o.check_active = true;
     o.hp = hot_prefix(s);
     o.hot = hot_slots(s, sizeof(uint4)) / s->g->nparts;
     o.hot1 = hot_l1_slots(s, sizeof(uint4));
@@ -1052,10 +1095,18 @@ CcOps cc_ops(gxb_state* s) {
     o.active_cur = s->d_active[0];
     o.f = frontier_view(s);
     o.commit_inline = false;
+    o.check_active = true;
     o.hp = hot_prefix(s);
     o.hot = hot_slots(s, sizeof(uint32_t)) / s->g->nparts;
     o.hot1 = hot_l1_slots(s, sizeof(uint32_t));
     return o;
+}
+
+// a pull round gathers every source (no active-bitmap test) once the frontier's GEN units
+// reach 1 / pull_dense_div of the edges (0 = always test)
+bool dense_pull(const gxb_state* s) {
+    const uint32_t div = options().pull_dense_div;
+    return div != 0 && s->units_cur * (uint64_t)div >= s->g->E;
 }
 
 int begin_round(gxb_state* s, cudaStream_t st) {
@@ -1407,8 +1458,18 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
     if (dir == GXB_DIR_PULL && s->algo != GXB_ALGO_LP && !use_binned_pull()) {
         switch (s->algo) {
             case GXB_ALGO_PAGERANK: GXB_CHECK(launch_tile_and_apply(s, pr_ops(s), st)); break;
-            case GXB_ALGO_SSSP: GXB_CHECK(launch_tile_and_apply(s, sssp_ops(s), st)); break;
-            case GXB_ALGO_CC: GXB_CHECK(launch_tile_and_apply(s, cc_ops(s), st)); break;
+            case GXB_ALGO_SSSP: {
+                SsspOps o = sssp_ops(s);
+                o.check_active = !dense_pull(s);
+                GXB_CHECK(launch_tile_and_apply(s, o, st));
+                break;
+            }
+            case GXB_ALGO_CC: {
+                CcOps o = cc_ops(s);
+                o.check_active = !dense_pull(s);
+                GXB_CHECK(launch_tile_and_apply(s, o, st));
+                break;
+            }
         }
     } else if (dir == GXB_DIR_PULL) {
         const PullLaunch L = pull_launch(s, 0, owned);

@@ -266,6 +266,7 @@ struct Options {
     int64_t l2_hot_mb = 64;       // L2 budget (MB) of the evict-last prefix of gathered values
     int64_t l1_hot_kb = 160;      // L1 budget (KB) of the L1-allocating prefix (others bypass L1)
     int64_t push_alpha = 20;      // push when frontier out-edges * alpha < |E|
+    int64_t pull_dense_div = 4;   // SSSP/CC pull skips the active bitmap when frontier out-edges * div >= |E|
     int64_t pull_kernel = 0;      // 0 = warp tiles, 1 = degree-binned groups
     int64_t carveout = -1;        // tile kernel shared-memory carveout in % (-1 = driver default)
     int64_t exchange_chunks = 1;  // multi-GPU: chunks of the dense exchange overlapped with compute

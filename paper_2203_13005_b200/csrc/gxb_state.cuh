@@ -55,6 +55,56 @@ __device__ __forceinline__ void publish_changed(const FrontierView& f, uint32_t 
     warp_append(f.frontier_next, f.frontier_count, slot);
 }
 
+// publish_changed for a full warp over kU groups of 32 CONSECUTIVE slots (all lanes call
+// it; `changed[u]` per lane): each group spans at most two bitmap words, so one OR per word
+// replaces 32 same-word atomics, one frontier reservation covers all groups, and the
+// per-slot loads are issued together — three L2 round trips per call instead of 3·kU.
+template <int kU>
+__device__ __forceinline__ void publish_changed_warp(const FrontierView& f, const uint32_t (&slot)[kU],
+                                                     const bool (&changed)[kU], LocalStats& st) {
+    unsigned m[kU];
+    unsigned total = 0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+        m[u] = __ballot_sync(kFull, changed[u]);
+        total += __popc(m[u]);
+    }
+    if (!total) return;
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(f.frontier_count, (unsigned long long)total);
+    uint32_t od[kU];
+    bool rem[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+        od[u] = changed[u] ? __ldg(f.outdeg + slot[u]) : 0u;
+        rem[u] = changed[u] && bit_test(f.remote_src, slot[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+        if (!m[u]) continue;
+        const uint32_t word = slot[u] >> 5;
+        const uint32_t w0 = __shfl_sync(kFull, word, 0);
+        const uint32_t mybit = changed[u] ? (1u << (slot[u] & 31)) : 0u;
+        const uint32_t b0 = __reduce_or_sync(kFull, word == w0 ? mybit : 0u);
+        const uint32_t b1 = __reduce_or_sync(kFull, word != w0 ? mybit : 0u);
+        if (lane == 0 && b0) atomicOr(f.active_next + w0, b0);
+        if (lane == 31 && b1) atomicOr(f.active_next + word, b1);
+    }
+    base = __shfl_sync(kFull, base, 0);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+        if (changed[u]) {
+            f.frontier_next[base + __popc(m[u] & ((1u << lane) - 1u))] = slot[u];
+            st.changed++;
+            st.next_active++;
+            st.next_units += od[u];
+            if (rem[u]) st.remote_active++;
+        }
+        base += __popc(m[u]);
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);

@@ -871,6 +871,9 @@ int gxb_set_option(const char* name, int64_t value) {
     } else if (n == "push_alpha") {
         if (value < 0) return fail(GXB_EINVAL, "push_alpha must be >= 0");
         o.push_alpha = value;
+    } else if (n == "pull_dense_div") {
+        if (value < 0) return fail(GXB_EINVAL, "pull_dense_div must be >= 0 (0 = always test active bits)");
+        o.pull_dense_div = value;
     } else if (n == "l1_hot_kb") {
         if (value < 0) return fail(GXB_EINVAL, "l1_hot_kb must be >= 0");
         o.l1_hot_kb = value;
@@ -903,6 +906,7 @@ int gxb_get_option(const char* name, int64_t* value) {
     else if (n == "l2_hot_mb") *value = o.l2_hot_mb;
     else if (n == "push_alpha") *value = o.push_alpha;
     else if (n == "pull_kernel") *value = o.pull_kernel;
+    else if (n == "pull_dense_div") *value = o.pull_dense_div;
     else if (n == "pr_message_bits") *value = o.pr_message_bits;
     else if (n == "carveout") *value = o.carveout;
     else if (n == "overlap_reserve_sms") *value = o.overlap_reserve_sms;
