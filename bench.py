@@ -363,10 +363,11 @@ def main():
         kbytes = 8 * owned_E + 4 * (hi - lo)
     achieved = kbytes / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else None
     it_bytes = algorithmic_bytes(algo, E, V)
+    kname = "k_tile_a" if L.get_option("tile_async") else "k_tile_t"
     traffic = None
     try:  # dram bytes per launch of the same kernel from the committed ncu --set full capture
         with open(os.path.join(HERE, "profiles", "r01_traffic.json")) as fh:
-            tr = json.load(fh).get(f"{algo}-s{scale}", {}).get("k_tile_t")
+            tr = json.load(fh).get(f"{algo}-s{scale}", {}).get(kname)
         if tr and world == 1:
             traffic = int(tr["dram_read_bytes"] + tr["dram_write_bytes"])
     except Exception:  # noqa: BLE001
@@ -374,7 +375,7 @@ def main():
     roofline = {
         "bound": "hbm", "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
         "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
-        "kernel": "k_tile_t (fused MSGGen+MSGMerge warp tiles)", "kernel_ms": round(kern_ms, 4),
+        "kernel": f"{kname} (fused MSGGen+MSGMerge warp tiles)", "kernel_ms": round(kern_ms, 4),
         "algorithmic_bytes_per_launch": kbytes, "peak_kind": peak_kind,
         "iteration_frac": round(it_bytes * world / (ms_per_step * 1e-3) / 1e9 / (peak * world), 4)
         if algo == "pagerank" else None,

@@ -83,6 +83,19 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
         return true;
     }
     __device__ static void fold(Acc& a, Msg m) { a.s += m; }
+    // async-gather interface (k_tile_a): the raw gathered value lands in shared memory
+    using Raw = double;
+    __device__ static Raw identity_raw() { return 0.0; }
+    __device__ bool gather_async(uint32_t saddr, uint32_t s) const {
+        const uint32_t r = hp.rank(s);
+        const uint64_t pol = r < hot ? l2_evict_last() : l2_evict_first();
+        if (msg32) cp_async_ca<4>(saddr, reinterpret_cast<const float*>(contrib_cur) + s, pol);
+        else cp_async_ca<8>(saddr, contrib_cur + s, pol);
+        return true;
+    }
+    __device__ Acc from_raw(const Raw* p, uint32_t) const {
+        return {msg32 ? (double)*reinterpret_cast<const float*>(p) : *p};
+    }
     // Apply: 0.15 + 0.85 * sum with two roundings (157-159; no FMA contraction),
     // convergence_stat |new - old| (161-162), always active.
     struct Pre {
@@ -163,6 +176,20 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
         return true;
     }
     __device__ static void fold(Acc& a, Msg m) { a.m = min4(a.m, m); }
+    using Raw = uint4;
+    __device__ static Raw identity_raw() { return make_uint4(kInf32, kInf32, kInf32, kInf32); }
+    __device__ bool gather_async(uint32_t saddr, uint32_t s) const {
+        if (check_active && !bit_test(active_cur, s)) return false;
+        const uint32_t r = hp.rank(s);
+        const uint64_t pol = r < hot ? l2_evict_last() : l2_evict_first();
+        if (r < hot1) cp_async_ca<16>(saddr, dist_cur + s, pol);
+        else cp_async_cg16(saddr, dist_cur + s, pol);
+        return true;
+    }
+    __device__ Acc from_raw(const Raw* p, uint32_t w) const {
+        const uint4 d = *p;
+        return {make_uint4(sat_add(d.x, w), sat_add(d.y, w), sat_add(d.z, w), sat_add(d.w, w))};
+    }
     // Apply: elementwise min, active iff changed (113-115)
     struct Pre {
         uint4 o;
@@ -216,6 +243,16 @@ struct CcOps {  // min-label propagation; labels < 0xFFFF
         return true;
     }
     __device__ static void fold(Acc& a, Msg m) { a.m = min(a.m, m); }
+    using Raw = uint32_t;
+    __device__ static Raw identity_raw() { return kInf32; }
+    __device__ bool gather_async(uint32_t saddr, uint32_t s) const {
+        if (check_active && !bit_test(active_cur, s)) return false;
+        const uint32_t r = hp.rank(s);
+        const uint64_t pol = r < hot ? l2_evict_last() : l2_evict_first();
+        cp_async_ca<4>(saddr, lab_cur + s, pol);
+        return true;
+    }
+    __device__ Acc from_raw(const Raw* p, uint32_t) const { return {*p}; }
     struct Pre {
         uint32_t o;
     };
@@ -428,6 +465,8 @@ struct TileLaunch {
     const uint32_t* lane_slot;
     const uint8_t* lane_mask;
     const uint32_t* in_w;
+    const uint32_t* in_sw;  // packed (src << sw_shift) | w, or nullptr
+    uint32_t sw_shift;
     const uint32_t* tile_head;
     const uint32_t* tile_tail;
     const uint32_t* span_first;
@@ -477,6 +516,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_t(const Pol p, cons
     const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
     const uint64_t pol = l2_evict_first();
     const bool weighted = kW && L.in_w != nullptr;
+    const bool packed = kW && L.in_sw != nullptr;
     uint64_t t = L.tile_begin + (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
     uint32_t nidx[kTileK], nw[kTileK];
     uint32_t nsa = 0, nmask = 0;
@@ -490,11 +530,21 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_t(const Pol p, cons
         nbeg = __ldg(L.tile_start + tt);  // tiles restart at every exchange chunk
         nend = __ldg(L.tile_start + tt + 1);
         const uint64_t e = nbeg + (uint64_t)lane;
+        if (packed) {  // one stream: source and weight in one word
+            const uint32_t wmask = (1u << L.sw_shift) - 1u;
 #pragma unroll
-        for (int j = 0; j < kTileK; ++j) nidx[j] = ld_stream_u32(L.in_src + e + 32 * j, pol);
-        if (weighted) {
+            for (int j = 0; j < kTileK; ++j) {
+                const uint32_t x = ld_stream_u32(L.in_sw + e + 32 * j, pol);
+                nidx[j] = x >> L.sw_shift;
+                nw[j] = x & wmask;
+            }
+        } else {
 #pragma unroll
-            for (int j = 0; j < kTileK; ++j) nw[j] = ld_stream_u32(L.in_w + e + 32 * j, pol);
+            for (int j = 0; j < kTileK; ++j) nidx[j] = ld_stream_u32(L.in_src + e + 32 * j, pol);
+            if (weighted) {
+#pragma unroll
+                for (int j = 0; j < kTileK; ++j) nw[j] = ld_stream_u32(L.in_w + e + 32 * j, pol);
+            }
         }
         nsa = ld_stream_u32(L.lane_slot + tt * 32 + lane, pol);
         nmask = ld_stream_u8(L.lane_mask + tt * 32 + lane, pol);
@@ -551,6 +601,122 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_t(const Pol p, cons
                 acc = Ops::identity();
             }
         }
+        const uint32_t lkey = live ? key : kNone;
+        const Acc lval = acc;
+        if (!multi) {
+            fkey = lkey;
+            fval = lval;
+        }
+        Acc c = lval;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const Acc up = Ops::shfl_up(c, d);
+            const uint32_t k = __shfl_up_sync(kFull, lkey, d);
+            if (lane >= d && k == lkey) c = Ops::combine(up, c);
+        }
+        const uint32_t prev_key = __shfl_up_sync(kFull, lkey, 1);
+        const Acc prev_c = Ops::shfl_up(c, 1);
+        const uint32_t next_first = __shfl_down_sync(kFull, fkey, 1);
+        if (multi && live) {
+            const Acc tot = (lane > 0 && prev_key == fkey) ? Ops::combine(prev_c, fval) : fval;
+            tile_emit(p, L, t, __ldg(L.tile_head + t), __ldg(L.tile_tail + t), fkey, tot);
+        }
+        if (lkey != kNone && (lane == 31 || next_first != lkey))
+            tile_emit(p, L, t, __ldg(L.tile_head + t), __ldg(L.tile_tail + t), lkey, c);
+    }
+}
+
+// Async-gather variant: the kTileK gathers of a lane are LDGSTS copies straight into the
+// warp's shared row (no registers held while they are in flight), so the kernel fits
+// more resident warps without spilling; weights (SSSP) ride in a parallel shared row.
+// The fold is the same as k_tile_t's, reading each value when it is combined.
+// shared-row position of edge p of a tile: 16-B values use an XOR swizzle (conflict-free
+// for both the 32-consecutive-edges writes and the 8-edges-per-lane reads, no padding);
+// narrower values use the padded layout of k_tile_t
+template <class Raw>
+__device__ __forceinline__ uint32_t apos(uint32_t p) {
+    if constexpr (sizeof(Raw) == 16) return p ^ ((p >> 3) & 7u);
+    else return tpos(p);
+}
+
+template <class Pol, int kMinBlocks>
+__global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_a(const Pol p, const TileLaunch L) {
+    using Ops = decltype(p.ops);
+    using Acc = typename Ops::Acc;
+    using Raw = typename Ops::Raw;
+    constexpr bool kW = Ops::kWeighted;  // weighted launches always come with the packed stream
+    constexpr uint32_t kRow = sizeof(Raw) == 16 ? kTileEdges : kTileEdges + kTileEdges / kTileK;
+    __shared__ Raw sraw[kBlock / 32][kRow];
+    __shared__ uint8_t swt[kW ? kBlock / 32 : 1][kW ? kTileEdges + kTileEdges / kTileK : 1];
+    const uint32_t lane = threadIdx.x & 31;
+    Raw* buf = sraw[threadIdx.x >> 5];
+    uint8_t* wbuf = swt[kW ? threadIdx.x >> 5 : 0];
+    // 32-bit tile / edge indices (the launcher guarantees padded edges < 2^32)
+    const uint32_t nwarps = gridDim.x * (kBlock / 32);
+    const uint32_t ntiles = (uint32_t)L.num_tiles;
+    const uint64_t pol = l2_evict_first();
+    const uint32_t shift = kW ? L.sw_shift : 0u;
+    const uint32_t* stream = kW ? L.in_sw : L.in_src;
+    uint32_t t = (uint32_t)L.tile_begin + blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+    uint32_t nidx[kTileK];
+    uint32_t nsa = 0, nmask = 0, nbeg = 0, ncnt = 0;
+#pragma unroll
+    for (int j = 0; j < kTileK; ++j) nidx[j] = 0;
+    auto prefetch = [&](uint32_t tt) {
+        nbeg = (uint32_t)__ldg(L.tile_start + tt);
+        ncnt = (uint32_t)__ldg(L.tile_start + tt + 1) - nbeg;
+        const uint32_t* e = stream + nbeg + lane;
+#pragma unroll
+        for (int j = 0; j < kTileK; ++j) nidx[j] = ld_stream_u32(e + 32 * j, pol);
+        nsa = ld_stream_u32(L.lane_slot + (uint64_t)tt * 32 + lane, pol);
+        nmask = ld_stream_u8(L.lane_mask + (uint64_t)tt * 32 + lane, pol);
+    };
+    if (t < ntiles) prefetch(t);
+    for (; t < ntiles; t += nwarps) {
+        const uint32_t cnt = ncnt;
+        // Gen: issue the tile's gathers (32 consecutive edges per instruction) into shared memory
+#pragma unroll
+        for (int j = 0; j < kTileK; ++j) {
+            const uint32_t q = 32 * j + lane;
+            const uint32_t pos = apos<Raw>(q);
+            bool issued = false;
+            if (q < cnt) issued = p.ops.gather_async(smem_addr(buf + pos), nidx[j] >> shift);
+            if (!issued) buf[pos] = Ops::identity_raw();
+            if (kW) wbuf[tpos(q)] = (uint8_t)(nidx[j] & ((1u << shift) - 1u));
+        }
+        const uint32_t sa = nsa;
+        uint32_t endmask = nmask;
+        if (t + nwarps < ntiles) prefetch(t + nwarps);
+        cp_async_wait_all();
+        __syncwarp();
+        const uint32_t q0 = lane * kTileK;
+        const bool live = q0 < cnt;
+        const uint32_t nvalid = live ? min((uint32_t)kTileK, cnt - q0) : 0u;
+        endmask &= (1u << nvalid) - 1u;
+        if (nvalid) endmask &= ~(1u << (nvalid - 1));
+        uint32_t fkey = kNone;
+        Acc fval = Ops::identity();
+        const bool multi = endmask != 0;
+        Acc acc = Ops::identity();
+        uint32_t key = sa;
+        bool first = true;
+#pragma unroll
+        for (int j = 0; j < kTileK; ++j) {
+            const uint32_t q = q0 + j;
+            acc = Ops::combine(acc, p.ops.from_raw(buf + apos<Raw>(q), kW ? (uint32_t)wbuf[tpos(q)] : 0u));
+            if ((endmask >> j) & 1u) {
+                if (first) {
+                    fkey = key;
+                    fval = acc;
+                    first = false;
+                } else {
+                    reinterpret_cast<Acc*>(L.sums)[key] = acc;
+                }
+                ++key;
+                acc = Ops::identity();
+            }
+        }
+        __syncwarp();  // the next tile's copies overwrite the row
         const uint32_t lkey = live ? key : kNone;
         const Acc lval = acc;
         if (!multi) {
@@ -969,6 +1135,8 @@ TileLaunch tile_launch(gxb_state* s) {
     L.lane_slot = T.d_lane_slot;
     L.lane_mask = T.d_lane_mask;
     L.in_w = g->d_in_w;
+    L.in_sw = g->d_in_sw;
+    L.sw_shift = g->sw_shift;
     L.tile_head = T.d_tile_head;
     L.tile_tail = T.d_tile_tail;
     L.span_first = T.d_span_first;
@@ -1000,6 +1168,14 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st, int chu
     using Pol = FusedPolicy<Ops>;
     void (*kern)(const Pol, const TileLaunch) = (variant == 8) ? k_tile_t<Pol, 8> : (variant == 6) ? k_tile_t<Pol, 6>
              : (variant == 4) ? k_tile_t<Pol, 4> : k_tile_t<Pol, 1>;
+    // LDGSTS gathers; weighted launches need the packed index+weight stream with <= 8 weight bits
+    const bool async_ok = (!Ops::kWeighted || (g->d_in_sw && g->sw_shift <= 8)) &&
+                          L.num_tiles * (uint64_t)kTileEdges + kTileEdges < (1ull << 32);
+    if (options().tile_async && async_ok) {  // min-blocks from the option, or the measured best
+        int av = options().tile_async_minblocks;
+        if (av == 0) av = sizeof(typename Ops::Raw) >= 16 ? 4 : sizeof(typename Ops::Raw) == 8 ? 6 : 8;
+        kern = (av == 8) ? k_tile_a<Pol, 8> : (av == 6) ? k_tile_a<Pol, 6> : (av == 4) ? k_tile_a<Pol, 4> : k_tile_a<Pol, 1>;
+    }
     if (options().carveout >= 0)  // shared-memory carveout (% of max): the rest of the 256 KB is L1
         GXB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)options().carveout));
     int per_sm = 0;

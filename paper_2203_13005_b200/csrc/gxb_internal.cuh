@@ -129,6 +129,10 @@ struct gxb_graph {
     uint64_t* d_in_off = nullptr;       // owned+1 offsets into d_in_src (0-based)
     uint32_t* d_in_src = nullptr;       // source slot per owned in-edge (sorted by (dst, src))
     uint32_t* d_in_w = nullptr;         // weight per owned in-edge (nullptr = unweighted)
+    // (src << sw_shift) | w per owned in-edge, when slot and weight bits fit 32 (weighted graphs):
+    // the tile kernel's single index+weight stream (4 B/edge instead of 8)
+    uint32_t* d_in_sw = nullptr;
+    uint32_t sw_shift = 0;
     uint64_t* d_out_off = nullptr;      // V+1: push CSR restricted to owned destinations
     uint32_t* d_out_dst = nullptr;
     uint32_t* d_out_w = nullptr;
@@ -245,6 +249,21 @@ __device__ __forceinline__ float ld_nol1_f32(const float* ptr, uint64_t pol) {
     return r;
 }
 
+// asynchronous gathers straight into shared memory (LDGSTS): no registers held while the
+// load is in flight. .ca allocates in L1 (4/8/16 B), .cg bypasses it (16 B only).
+template <int kBytes>
+__device__ __forceinline__ void cp_async_ca(uint32_t saddr, const void* g, uint64_t pol) {
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], %2, %3;" ::"r"(saddr), "l"(g), "n"(kBytes),
+                 "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_cg16(uint32_t saddr, const void* g, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
 __device__ __forceinline__ uint32_t sat_add(uint32_t d, uint32_t w) {
     const uint32_t s = d + w;
     return (s < d || d == kInf32) ? kInf32 : s;
@@ -267,7 +286,9 @@ struct Options {
     int64_t l1_hot_kb = 160;      // L1 budget (KB) of the L1-allocating prefix (others bypass L1)
     int64_t push_alpha = 20;      // push when frontier out-edges * alpha < |E|
     int64_t pull_dense_div = 4;   // SSSP/CC pull skips the active bitmap when frontier out-edges * div >= |E|
-    int64_t pull_kernel = 0;      // 0 = warp tiles, 1 = degree-binned groups
+    int64_t pull_kernel = 0;
+    int64_t tile_async = 1;       // 1 = LDGSTS-gather tile kernel (k_tile_a), 0 = register gathers (k_tile_t)
+    int64_t tile_async_minblocks = 0;  // its min-blocks variant (0 = auto: 8 / 6 / 4 for 4 / 8 / 16-B values)      // 0 = warp tiles, 1 = degree-binned groups
     int64_t carveout = -1;        // tile kernel shared-memory carveout in % (-1 = driver default)
     int64_t exchange_chunks = 1;  // multi-GPU: chunks of the dense exchange overlapped with compute
     int64_t overlap_reserve_sms = 8;  // SMs left to NCCL while a chunked round computes

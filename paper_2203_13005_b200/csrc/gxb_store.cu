@@ -33,6 +33,7 @@ Options& options() {
         if (const char* e = getenv("GXB_PUSH_ALPHA")) o.push_alpha = atol(e);
         if (const char* e = getenv("GXB_PULL_KERNEL")) o.pull_kernel = std::string(e) == "binned" ? 1 : 0;
         if (const char* e = getenv("GXB_PR_MESSAGE_BITS")) o.pr_message_bits = atol(e) == 32 ? 32 : 64;
+        if (const char* e = getenv("GXB_TILE_ASYNC")) o.tile_async = atol(e) ? 1 : 0;
     }
     return o;
 }
@@ -259,6 +260,13 @@ __global__ void k_deal(const uint32_t* __restrict__ s2d, const uint32_t* __restr
 
 static uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
 
+__global__ void k_pack_sw(const uint32_t* __restrict__ src, const uint32_t* __restrict__ w, uint64_t n,
+                          uint32_t shift, uint32_t* out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = (src[i] << shift) | w[i];
+}
+
 __global__ void k_low32(const uint64_t* __restrict__ keys, uint64_t n, uint32_t* out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
@@ -335,6 +343,7 @@ static void graph_release(gxb_graph* g) {
     dfree(g->d_in_off);
     dfree(g->d_in_src);
     dfree(g->d_in_w);
+    dfree(g->d_in_sw);
     dfree(g->d_out_off);
     dfree(g->d_out_dst);
     dfree(g->d_out_w);
@@ -794,7 +803,16 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
             if (owned_edges)
                 GXB_CUDA(cudaMemcpyAsync(g->d_in_w, vout, 4 * owned_edges, cudaMemcpyDeviceToDevice, st));
         }
-        GXB_CUDA(cudaStreamSynchronize(st));
+        GXB_CUDA(cudaStreamSynchronize(st));  // also publishes g->max_w to the host
+        if (w) {
+            const int wb = std::max(1, bits_for(g->max_w));
+            if (wb < 32 && bits_for(g->S ? g->S - 1 : 0) + wb <= 32) {
+                g->sw_shift = (uint32_t)wb;
+                GXB_CHECK(dalloc_t(&g->d_in_sw, padded));
+                k_pack_sw<<<grid_e(padded), kBlock, 0, st>>>(g->d_in_src, g->d_in_w, padded, g->sw_shift, g->d_in_sw);
+                GXB_CUDA(cudaStreamSynchronize(st));
+            }
+        }
     }
     // push CSR (sources -> owned destinations)
     if (want_csr) {
@@ -874,6 +892,13 @@ int gxb_set_option(const char* name, int64_t value) {
     } else if (n == "pull_dense_div") {
         if (value < 0) return fail(GXB_EINVAL, "pull_dense_div must be >= 0 (0 = always test active bits)");
         o.pull_dense_div = value;
+    } else if (n == "tile_async") {
+        if (value != 0 && value != 1) return fail(GXB_EINVAL, "tile_async: 0 or 1");
+        o.tile_async = value;
+    } else if (n == "tile_async_minblocks") {
+        if (value != 0 && value != 1 && value != 4 && value != 6 && value != 8)
+            return fail(GXB_EINVAL, "tile_async_minblocks: 0 (auto) / 1 / 4 / 6 / 8");
+        o.tile_async_minblocks = value;
     } else if (n == "l1_hot_kb") {
         if (value < 0) return fail(GXB_EINVAL, "l1_hot_kb must be >= 0");
         o.l1_hot_kb = value;
@@ -907,6 +932,8 @@ int gxb_get_option(const char* name, int64_t* value) {
     else if (n == "push_alpha") *value = o.push_alpha;
     else if (n == "pull_kernel") *value = o.pull_kernel;
     else if (n == "pull_dense_div") *value = o.pull_dense_div;
+    else if (n == "tile_async") *value = o.tile_async;
+    else if (n == "tile_async_minblocks") *value = o.tile_async_minblocks;
     else if (n == "pr_message_bits") *value = o.pr_message_bits;
     else if (n == "carveout") *value = o.carveout;
     else if (n == "overlap_reserve_sms") *value = o.overlap_reserve_sms;
