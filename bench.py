@@ -191,7 +191,7 @@ def run_reference_arm(args):
                                    "the reference itself is pure Python and GIL-bound"},
         "e2e": {"value": round(v, 4), "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -249,6 +249,16 @@ def time_frontier_run(ctx, comm, dev, stream, name, algo, params, cap):
     return out
 
 
+_STDOUT_FD = None
+
+
+def emit(line: dict):
+    sys.stdout.flush()
+    if _STDOUT_FD is not None:
+        os.dup2(_STDOUT_FD, 1)
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -262,6 +272,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
+    # stdout carries exactly one JSON line: library banners (NCCL prints its version when a
+    # communicator is created) go to stderr until the line is printed
+    global _STDOUT_FD
+    sys.stdout.flush()
+    _STDOUT_FD = os.dup(1)
+    os.dup2(2, 1)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
@@ -281,6 +297,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"  # the version banner would precede the JSON line on stdout
         dist.init_process_group("nccl", device_id=dev)
     comm = Collective()
     algo, scale, over, cap, text = WORKLOADS[args.workload]
@@ -390,9 +408,14 @@ def main():
     if not args.no_e2e:
         st = run.state
         arity = st.arity
-        host_in = [torch.empty(V * arity, dtype=torch.float64, pin_memory=True) for _ in range(2)]
-        host_out = [torch.empty(V * arity, dtype=torch.float64, pin_memory=True) for _ in range(2)]
-        st.read_attrs_into(host_in[0].numpy().reshape(V, arity))
+        # one agent per partition moves its own vertices (N = 1: all of them)
+        st.attrs_scope(world > 1)
+        nv = len(graph.owned_ids()) if world > 1 else V
+        host_in = [torch.empty(nv * arity, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+        host_out = [torch.empty(nv * arity, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+        st.attrs_extract(0, stream)
+        st.attrs_d2h(host_in[0], 0, stream)
+        torch.cuda.synchronize()
         host_in[1].copy_(host_in[0])
         e2e_run = PartitionedRun(st, bounds, comm, enable_skip=True, device=dev)
         copy = torch.cuda.Stream(dev)       # host -> device
@@ -432,6 +455,7 @@ def main():
             t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
+        # whole-job bytes: the owned sets partition the vertices
         e2e = {"value": round(E * args.steps / e2e_s / 1e9, 3), "unit": "GTEPS",
                "h2d_bytes_per_step": 8 * V * arity, "d2h_bytes_per_step": 8 * V * arity,
                "path": "gxb_attrs_h2d/install (pull_from_upper) -> round -> gxb_attrs_extract/d2h "
@@ -480,7 +504,7 @@ def main():
         }
         if secondary:
             line["secondary"] = secondary
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

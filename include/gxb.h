@@ -171,6 +171,9 @@ int gxb_graph_ids(const gxb_graph* g, uint32_t* host_out);
 int gxb_graph_out_degree(const gxb_graph* g, uint32_t* host_out);
 /* partition boundaries in device slot order (host, nparts+1) */
 int gxb_graph_part_bounds(const gxb_graph* g, uint64_t* host_out);
+/* owned present ids of this partition in ascending order (host, *count entries; host_out
+ * may be NULL to query the count) */
+int gxb_graph_owned_ids(gxb_graph* g, uint32_t* host_out, uint64_t* count);
 int gxb_graph_free(gxb_graph* g);
 
 /* ---- algorithm state ---- */
@@ -209,6 +212,19 @@ int gxb_stats(gxb_state* s, void* stream, gxb_iter_stats* out);
  *     changed owned vertices; gxb_exchange_unpack installs received records
  *     into the replica and marks them active for the next iteration. */
 int gxb_exchange_buffer(gxb_state* s, int which, void** dev_ptr, uint64_t* bytes);
+
+/* fused PageRank exchange over peer memory: every rank exports the IPC handles of its
+ * two contribution buffers (which = 0 / 1), opens its peers' handles, and from then on
+ * the Apply kernel stores each new contribution of an owned vertex into every peer's
+ * replica over NVLink / NVSwitch — no separate all-gather (the reference's gqq/gdq
+ * mirror shuffle, A/engine.py:248-285, fused into MSGApply). All ranks must iterate in
+ * lockstep (the round's vote collective orders the stores before the next gather).
+ * set_peer_ptrs takes device pointers directly (same-process peers). */
+#define GXB_IPC_HANDLE_BYTES 64
+int gxb_exchange_ipc_handle(gxb_state* s, int which, void* handle_out);
+int gxb_exchange_open_peers(gxb_state* s, int npeers, const void* handles);   /* npeers x 2 handles */
+int gxb_exchange_set_peer_ptrs(gxb_state* s, int npeers, void* const* ptrs);  /* npeers x 2 pointers */
+int gxb_exchange_close_peers(gxb_state* s);
 int gxb_exchange_pack(gxb_state* s, void* stream, uint64_t* count_out);
 int gxb_exchange_unpack(gxb_state* s, const void* d_records, uint64_t count, void* stream);
 int gxb_exchange_finish(gxb_state* s, void* stream);
@@ -219,6 +235,8 @@ int gxb_exchange_finish(gxb_state* s, void* stream);
 #define GXB_BUF_VALUES_NEXT 4   /* PageRank: the contribution array the open round writes */
 #define GXB_BUF_SPARSE_SEND 5   /* PageRank needed-only exchange: my values, grouped by peer */
 #define GXB_BUF_SPARSE_RECV 6   /* PageRank needed-only exchange: peers' values, grouped by peer */
+#define GXB_BUF_CONTRIB0    7   /* PageRank: contribution buffer 0 (absolute, not rotating) */
+#define GXB_BUF_CONTRIB1    8   /* PageRank: contribution buffer 1 */
 
 /* Needed-only dense exchange (PageRank, nparts > 1): peer q receives exactly my owned
  * slots that are sources of edges into q's destinations (static lists built with the
@@ -260,6 +278,10 @@ int gxb_write_attrs(gxb_state* s, const double* host_in, void* stream);
  * extract gathers the state into output buffer `buf`, d2h copies it to pinned host
  * memory. install does not validate values (use gxb_write_attrs for checked input). */
 int gxb_attrs_h2d(gxb_state* s, const double* host_in, int buf, void* stream);
+/* staging scope: 0 = every present vertex (default), 1 = this partition's owned vertices
+ * only, ascending id order (gxb_graph_owned_ids) — the agent of one partition moves only
+ * its own vertices (A/agent.py:224-232, 433-443) */
+int gxb_attrs_scope(gxb_state* s, int owned_only);
 int gxb_attrs_install(gxb_state* s, int buf, void* stream);
 int gxb_attrs_extract(gxb_state* s, int buf, void* stream);
 int gxb_attrs_d2h(gxb_state* s, double* host_out, int buf, void* stream);

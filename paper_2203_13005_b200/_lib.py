@@ -26,6 +26,7 @@ BUILD_HOST_INPUT, BUILD_NO_CSR, BUILD_ID_RANGES, BUILD_RANGES = 0x1, 0x2, 0x4, 0
 DIR_AUTO, DIR_PULL, DIR_PUSH = 0, 1, 2
 BUF_VALUES, BUF_SEND, BUF_RECV, BUF_RECORD_SIZE, BUF_VALUES_NEXT = 0, 1, 2, 3, 4
 BUF_SPARSE_SEND, BUF_SPARSE_RECV = 5, 6
+BUF_CONTRIB0, BUF_CONTRIB1 = 7, 8
 
 
 class GraphInfo(ctypes.Structure):
@@ -95,6 +96,7 @@ def _sig(L):
         "gxb_graph_ids": (I, [P, P]),
         "gxb_graph_out_degree": (I, [P, P]),
         "gxb_graph_part_bounds": (I, [P, P]),
+        "gxb_graph_owned_ids": (I, [P, P, P]),
         "gxb_graph_free": (I, [P]),
         "gxb_graph_xchunks": (I, [P, ctypes.POINTER(I), P]),
         "gxb_iterate_begin": (I, [P, P]),
@@ -117,6 +119,11 @@ def _sig(L):
         "gxb_read_attrs": (I, [P, P, I, P]),
         "gxb_write_attrs": (I, [P, P, P]),
         "gxb_attrs_h2d": (I, [P, P, I, P]),
+        "gxb_attrs_scope": (I, [P, I]),
+        "gxb_exchange_ipc_handle": (I, [P, I, P]),
+        "gxb_exchange_open_peers": (I, [P, I, P]),
+        "gxb_exchange_set_peer_ptrs": (I, [P, I, P]),
+        "gxb_exchange_close_peers": (I, [P]),
         "gxb_attrs_install": (I, [P, I, P]),
         "gxb_attrs_extract": (I, [P, I, P]),
         "gxb_attrs_d2h": (I, [P, P, I, P]),

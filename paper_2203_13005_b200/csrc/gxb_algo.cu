@@ -58,6 +58,8 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
     double* contrib_next;
     FrontierView f;
     bool msg32;    // messages (rank / out_deg) stored and gathered as float32 (option pr_message_bits = 32)
+    int npeers;    // peer replicas written by Apply (fused exchange), next-buffer pointers below
+    double* peer_next[kMaxPeers];
     HotPrefix hp;  // degree rank of a slot inside its partition block
     uint32_t hot;  // ranks [0, hot) keep L2 priority (degree-sorted: the most-gathered sources)
     uint32_t hot1; // ranks [0, hot1) also allocate in L1; the rest bypass L1
@@ -111,8 +113,14 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
         rank[slot] = nw;
         const uint32_t od = p.od;
         const double c = od ? __ddiv_rn(nw, (double)od) : 0.0;
-        if (msg32) reinterpret_cast<float*>(contrib_next)[slot] = __double2float_rn(c);
-        else contrib_next[slot] = c;
+        if (msg32) {
+            const float c32 = __double2float_rn(c);
+            reinterpret_cast<float*>(contrib_next)[slot] = c32;
+            for (int q = 0; q < npeers; ++q) reinterpret_cast<float*>(peer_next[q])[slot] = c32;
+        } else {
+            contrib_next[slot] = c;
+            for (int q = 0; q < npeers; ++q) peer_next[q][slot] = c;
+        }
         if (nw != old) {
             st.changed++;
             st.max_stat = fmax(st.max_stat, fabs(nw - old));
@@ -815,6 +823,9 @@ __global__ void __launch_bounds__(kBlock) k_apply_sums(const Ops ops, const type
         }
         if constexpr (Ops::kPublishes) publish_changed_warp<kU>(ops.f, slot, ch, st);
     }
+    if constexpr (std::is_same<Ops, PrOps>::value) {
+        if (ops.npeers) __threadfence_system();  // peer stores visible before the round's vote
+    }
     flush_stats(st, stats);
 }
 
@@ -1150,8 +1161,11 @@ TileLaunch tile_launch(gxb_state* s) {
 }
 
 // one exchange chunk (or all of them for k < 0): Gen∘Merge tiles, span folds, Apply
+// With `ast`, the chunk's span fold and Apply run on that stream after the tile kernel
+// (an event orders them), so Apply(k) — and its peer stores — overlap the tiles of k+1.
 template <class Ops>
-int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st, int chunk = -1) {
+int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st, int chunk = -1,
+                          cudaStream_t ast = nullptr) {
     const gxb_graph* g = s->g;
     const TilePlan& T = g->tiles;
     const int K = T.num_xchunks;
@@ -1187,13 +1201,22 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st, int chu
     if (ntiles) {
         const uint64_t want = (ntiles + (kBlock / 32) - 1) / (kBlock / 32);
         const unsigned grid = (unsigned)std::min<uint64_t>(want, (uint64_t)max_blocks);
-        if (s->timing && chunk <= 0) GXB_CUDA(cudaEventRecord(s->kev[0], st));
+        const bool first = chunk < 0 || s->round_chunks == 0, last = chunk < 0 || s->round_chunks == K - 1;
+        if (s->timing && first) GXB_CUDA(cudaEventRecord(s->kev[0], st));
         kern<<<grid, kBlock, 0, st>>>(p, L);
-        if (s->timing && (chunk < 0 || chunk == K - 1)) {
+        if (s->timing && last) {
             GXB_CUDA(cudaEventRecord(s->kev[1], st));
             s->timing_pending = true;
         }
         s->launches++;
+    }
+    if (chunk >= 0) s->round_chunks++;
+    if (ast) {
+        GXB_CUDA(cudaEventRecord(s->ev_tile, st));
+        GXB_CUDA(cudaStreamWaitEvent(ast, s->ev_tile, 0));
+        st = ast;
+    }
+    if (ntiles) {
         if (span_hi > span_lo) {
             k_span_fold<Ops><<<grid_for(span_hi - span_lo), kBlock, 0, st>>>(
                 T.d_span_slot, T.d_span_count, T.d_span_pbase, span_lo, span_hi,
@@ -1216,6 +1239,7 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st, int chu
 }
 
 bool use_binned_pull() { return options().pull_kernel == 1; }
+
 
 // L2 budget for the gathered value prefix (GXB_L2_HOT_MB, default 64 of the 126 MB)
 HotPrefix hot_prefix(const gxb_state* s) {
@@ -1245,6 +1269,9 @@ PrOps pr_ops(gxb_state* s) {
     o.rank = s->d_rank;
     o.contrib_next = s->d_contrib[s->cur ^ 1];
     o.msg32 = s->msg32;
+    o.npeers = s->npeers;
+    for (int q = 0; q < kMaxPeers; ++q)
+        o.peer_next[q] = q < s->npeers ? static_cast<double*>(s->peer_contrib[q][s->cur ^ 1]) : nullptr;
     o.f = frontier_view(s);
     o.hp = hot_prefix(s);
     o.hot = hot_slots(s, sizeof(double)) / s->g->nparts;
@@ -1278,6 +1305,24 @@ CcOps cc_ops(gxb_state* s) {
     return o;
 }
 
+// PageRank round with the fused peer exchange pipelined: chunks run hubs-last (the last
+// chunk has the fewest slots, so the Apply left after the final tile kernel is the
+// shortest) and each chunk's Apply, with its NVLink stores, overlaps the next chunk's tiles
+int pipelined_pagerank(gxb_state* s, cudaStream_t st) {
+    if (!s->aux_stream) {
+        GXB_CUDA(cudaStreamCreateWithFlags(&s->aux_stream, cudaStreamNonBlocking));
+        GXB_CUDA(cudaEventCreateWithFlags(&s->ev_tile, cudaEventDisableTiming));
+        GXB_CUDA(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+    }
+    GXB_CUDA(cudaEventRecord(s->ev_join, st));  // after begin_round's resets
+    GXB_CUDA(cudaStreamWaitEvent(s->aux_stream, s->ev_join, 0));
+    const PrOps ops = pr_ops(s);
+    for (int k = s->g->tiles.num_xchunks - 1; k >= 0; --k) GXB_CHECK(launch_tile_and_apply(s, ops, st, k, s->aux_stream));
+    GXB_CUDA(cudaEventRecord(s->ev_join, s->aux_stream));
+    GXB_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
+    return GXB_OK;
+}
+
 // a pull round gathers every source (no active-bitmap test) once the frontier's GEN units
 // reach 1 / pull_dense_div of the edges (0 = always test)
 bool dense_pull(const gxb_state* s) {
@@ -1295,6 +1340,7 @@ int begin_round(gxb_state* s, cudaStream_t st) {
     GXB_CUDA(cudaMemsetAsync(s->d_active[1], 0, 4 * s->words, st));
     s->in_round = true;
     s->committed_inline = false;
+    s->round_chunks = 0;
     return GXB_OK;
 }
 
@@ -1560,8 +1606,14 @@ int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, 
     return GXB_OK;
 }
 
+int gxb_exchange_close_peers(gxb_state* s);  // gxb_exchange.cu
+
 int gxb_state_free(gxb_state* s) {
     if (!s) return GXB_OK;
+    gxb_exchange_close_peers(s);
+    if (s->aux_stream) cudaStreamDestroy(s->aux_stream);
+    if (s->ev_tile) cudaEventDestroy(s->ev_tile);
+    if (s->ev_join) cudaEventDestroy(s->ev_join);
     dfree(s->d_rank);
     dfree(s->d_contrib[0]);
     dfree(s->d_contrib[1]);
@@ -1633,7 +1685,10 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
     const uint64_t owned = g->hi - g->lo;
     if (dir == GXB_DIR_PULL && s->algo != GXB_ALGO_LP && !use_binned_pull()) {
         switch (s->algo) {
-            case GXB_ALGO_PAGERANK: GXB_CHECK(launch_tile_and_apply(s, pr_ops(s), st)); break;
+            case GXB_ALGO_PAGERANK:
+                if (s->npeers > 0 && g->tiles.num_xchunks > 1) GXB_CHECK(pipelined_pagerank(s, st));
+                else GXB_CHECK(launch_tile_and_apply(s, pr_ops(s), st));
+                break;
             case GXB_ALGO_SSSP: {
                 SsspOps o = sssp_ops(s);
                 o.check_active = !dense_pull(s);
@@ -1889,18 +1944,48 @@ int gxb_write_attrs(gxb_state* s, const double* host_in, void* stream) {
 // Two staging buffers per direction let the next step's host->device copy and the
 // previous step's device->host copy run on a copy stream while the round computes.
 static int stage_pair(gxb_state* s) {
-    const uint64_t n = s->g->V * s->arity + 1;
+    const gxb_graph* g = s->g;
+    const uint64_t nv = s->attrs_scope ? g->owned_present : g->V;
+    if (s->stage_n != nv) {
+        for (int i = 0; i < 2; ++i) {
+            dfree(s->d_stage_in[i]);
+            dfree(s->d_stage_out[i]);
+            s->d_stage_in[i] = s->d_stage_out[i] = nullptr;
+        }
+    }
+    const uint64_t n = nv * s->arity + 1;
     for (int i = 0; i < 2; ++i) {
         if (!s->d_stage_in[i]) GXB_CHECK(dalloc_t(&s->d_stage_in[i], n));
         if (!s->d_stage_out[i]) GXB_CHECK(dalloc_t(&s->d_stage_out[i], n));
     }
+    s->stage_n = nv;
     return GXB_OK;
+}
+
+// vertex order of the staging buffers: every present id, or the owned ones (both ascending)
+static void stage_order(const gxb_state* s, const uint32_t** d2s, uint64_t* n) {
+    const gxb_graph* g = s->g;
+    if (s->attrs_scope) {
+        *d2s = g->d_owned_d2s;
+        *n = g->owned_present;
+    } else {
+        *d2s = g->d_dense2slot;
+        *n = g->V;
+    }
+}
+
+int gxb_attrs_scope(gxb_state* s, int owned_only) {
+    if (!s || (owned_only != 0 && owned_only != 1)) return fail(GXB_EINVAL, "gxb_attrs_scope: bad argument");
+    GXB_CUDA(cudaSetDevice(s->g->ctx->device));
+    if (owned_only) GXB_CHECK(build_owned_order(s->g));
+    s->attrs_scope = owned_only;
+    return stage_pair(s);
 }
 
 int gxb_attrs_h2d(gxb_state* s, const double* host_in, int buf, void* stream) {
     if (!s || !host_in || buf < 0 || buf > 1) return fail(GXB_EINVAL, "gxb_attrs_h2d: bad argument");
     GXB_CHECK(stage_pair(s));
-    GXB_CUDA(cudaMemcpyAsync(s->d_stage_in[buf], host_in, 8 * s->g->V * s->arity, cudaMemcpyHostToDevice,
+    GXB_CUDA(cudaMemcpyAsync(s->d_stage_in[buf], host_in, 8 * s->stage_n * s->arity, cudaMemcpyHostToDevice,
                              (cudaStream_t)stream));
     return GXB_OK;
 }
@@ -1910,10 +1995,13 @@ int gxb_attrs_install(gxb_state* s, int buf, void* stream) {
     if (s->in_round) return fail(GXB_ESTATE, "gxb_attrs_install: a round is open");
     GXB_CHECK(stage_pair(s));
     gxb_graph* g = s->g;
-    if (!g->V) return GXB_OK;
+    const uint32_t* d2s;
+    uint64_t n;
+    stage_order(s, &d2s, &n);
+    if (!n) return GXB_OK;
     uint32_t* d_bad = reinterpret_cast<uint32_t*>(s->d_fcount) + 2;  // sticky flag, checked by gxb_attrs_check
-    k_write_attrs<<<grid_for(g->V), kBlock, 0, (cudaStream_t)stream>>>(
-        s->algo, s->arity, g->d_dense2slot, g->V, g->d_outdeg, s->d_stage_in[buf], s->d_rank, s->d_contrib[s->cur],
+    k_write_attrs<<<grid_for(n), kBlock, 0, (cudaStream_t)stream>>>(
+        s->algo, s->arity, d2s, n, g->d_outdeg, s->d_stage_in[buf], s->d_rank, s->d_contrib[s->cur],
         s->d_dist_cur, s->d_dist_next, s->d_lab_cur, s->d_lab_next, d_bad, s->msg32);
     GXB_CUDA(cudaGetLastError());
     return GXB_OK;
@@ -1923,10 +2011,13 @@ int gxb_attrs_extract(gxb_state* s, int buf, void* stream) {
     if (!s || buf < 0 || buf > 1) return fail(GXB_EINVAL, "gxb_attrs_extract: bad argument");
     GXB_CHECK(stage_pair(s));
     gxb_graph* g = s->g;
-    if (!g->V) return GXB_OK;
-    k_read_attrs<<<grid_for(g->V), kBlock, 0, (cudaStream_t)stream>>>(s->algo, s->arity, g->d_dense2slot, g->V, g->lo,
-                                                                       g->hi, 0, s->d_rank, s->d_dist_cur, s->d_lab_cur,
-                                                                       s->d_stage_out[buf]);
+    const uint32_t* d2s;
+    uint64_t n;
+    stage_order(s, &d2s, &n);
+    if (!n) return GXB_OK;
+    k_read_attrs<<<grid_for(n), kBlock, 0, (cudaStream_t)stream>>>(s->algo, s->arity, d2s, n, g->lo, g->hi, 0,
+                                                                   s->d_rank, s->d_dist_cur, s->d_lab_cur,
+                                                                   s->d_stage_out[buf]);
     GXB_CUDA(cudaGetLastError());
     return GXB_OK;
 }
@@ -1934,7 +2025,7 @@ int gxb_attrs_extract(gxb_state* s, int buf, void* stream) {
 int gxb_attrs_d2h(gxb_state* s, double* host_out, int buf, void* stream) {
     if (!s || !host_out || buf < 0 || buf > 1) return fail(GXB_EINVAL, "gxb_attrs_d2h: bad argument");
     GXB_CHECK(stage_pair(s));
-    GXB_CUDA(cudaMemcpyAsync(host_out, s->d_stage_out[buf], 8 * s->g->V * s->arity, cudaMemcpyDeviceToHost,
+    GXB_CUDA(cudaMemcpyAsync(host_out, s->d_stage_out[buf], 8 * s->stage_n * s->arity, cudaMemcpyDeviceToHost,
                              (cudaStream_t)stream));
     return GXB_OK;
 }

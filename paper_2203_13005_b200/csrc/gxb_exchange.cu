@@ -94,6 +94,72 @@ using namespace gxb;
 
 extern "C" {
 
+// ---- fused PageRank exchange over peer memory (NVLink / NVSwitch) ----
+int gxb_exchange_ipc_handle(gxb_state* s, int which, void* handle_out) {
+    if (!s || !handle_out || which < 0 || which > 1) return fail(GXB_EINVAL, "gxb_exchange_ipc_handle: bad argument");
+    if (s->algo != GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "peer replicas are PageRank-only");
+    cudaIpcMemHandle_t h;
+    GXB_CUDA(cudaIpcGetMemHandle(&h, s->d_contrib[which]));
+    static_assert(sizeof(h) == GXB_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle_out, &h, sizeof(h));
+    return GXB_OK;
+}
+
+int gxb_exchange_close_peers(gxb_state* s) {
+    if (!s) return fail(GXB_EINVAL, "gxb_exchange_close_peers: null state");
+    if (s->peer_ipc) {
+        cudaSetDevice(s->g->ctx->device);
+        for (int q = 0; q < s->npeers; ++q)
+            for (int b = 0; b < 2; ++b)
+                if (s->peer_contrib[q][b]) cudaIpcCloseMemHandle(s->peer_contrib[q][b]);
+    }
+    for (int q = 0; q < kMaxPeers; ++q) s->peer_contrib[q][0] = s->peer_contrib[q][1] = nullptr;
+    s->npeers = 0;
+    s->peer_ipc = false;
+    return GXB_OK;
+}
+
+int gxb_exchange_open_peers(gxb_state* s, int npeers, const void* handles) {
+    if (!s || npeers < 0 || npeers > kMaxPeers || (npeers && !handles))
+        return fail(GXB_EINVAL, "gxb_exchange_open_peers: bad argument");
+    if (s->algo != GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "peer replicas are PageRank-only");
+    GXB_CHECK(gxb_exchange_close_peers(s));
+    GXB_CUDA(cudaSetDevice(s->g->ctx->device));
+    const auto* hb = static_cast<const unsigned char*>(handles);
+    for (int q = 0; q < npeers; ++q) {
+        for (int b = 0; b < 2; ++b) {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, hb + (2 * q + b) * GXB_IPC_HANDLE_BYTES, sizeof(h));
+            void* p = nullptr;
+            const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                s->npeers = q + (b ? 1 : 0);
+                s->peer_ipc = true;
+                gxb_exchange_close_peers(s);
+                return cuda_fail(e, "gxb_exchange_open_peers: cudaIpcOpenMemHandle");
+            }
+            s->peer_contrib[q][b] = p;
+        }
+        s->npeers = q + 1;
+    }
+    s->peer_ipc = npeers > 0;
+    return GXB_OK;
+}
+
+int gxb_exchange_set_peer_ptrs(gxb_state* s, int npeers, void* const* ptrs) {
+    if (!s || npeers < 0 || npeers > kMaxPeers || (npeers && !ptrs))
+        return fail(GXB_EINVAL, "gxb_exchange_set_peer_ptrs: bad argument");
+    if (s->algo != GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "peer replicas are PageRank-only");
+    GXB_CHECK(gxb_exchange_close_peers(s));
+    for (int q = 0; q < npeers; ++q) {
+        s->peer_contrib[q][0] = ptrs[2 * q];
+        s->peer_contrib[q][1] = ptrs[2 * q + 1];
+    }
+    s->npeers = npeers;
+    return GXB_OK;
+}
+
 int gxb_exchange_buffer(gxb_state* s, int which, void** dev_ptr, uint64_t* bytes) {
     if (!s || !dev_ptr || !bytes) return fail(GXB_EINVAL, "gxb_exchange_buffer: null argument");
     gxb_graph* g = s->g;
@@ -111,6 +177,12 @@ int gxb_exchange_buffer(gxb_state* s, int which, void** dev_ptr, uint64_t* bytes
                 *dev_ptr = s->d_lab_cur;
                 *bytes = 4 * V;
             }
+            return GXB_OK;
+        case GXB_BUF_CONTRIB0:
+        case GXB_BUF_CONTRIB1:
+            if (s->algo != GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "GXB_BUF_CONTRIB* are PageRank-only");
+            *dev_ptr = s->d_contrib[which == GXB_BUF_CONTRIB1 ? 1 : 0];
+            *bytes = (s->msg32 ? 4 : 8) * V;
             return GXB_OK;
         case GXB_BUF_VALUES_NEXT:  // PR: the contributions being written by the open round
             if (s->algo != GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "GXB_BUF_VALUES_NEXT is PageRank-only");

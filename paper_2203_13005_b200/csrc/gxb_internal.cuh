@@ -50,6 +50,7 @@ constexpr int kTileK = 8;
 constexpr uint64_t kTileEdges = 32 * kTileK;
 constexpr uint64_t kOffPad = 16;           // extra offset entries (= owned_edges) after the CSC offsets
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr int kMaxPeers = 7;  // peer replicas a PageRank Apply writes directly (8 GPUs per NVSwitch node)
 
 struct TilePlan {
     uint64_t nz_slots = 0;       // owned slots with in-degree > 0 (a prefix: slots are degree-sorted)
@@ -132,6 +133,9 @@ struct gxb_graph {
     // (src << sw_shift) | w per owned in-edge, when slot and weight bits fit 32 (weighted graphs):
     // the tile kernel's single index+weight stream (4 B/edge instead of 8)
     uint32_t* d_in_sw = nullptr;
+    // owned present slots in ascending-id order (lazily built by gxb_attrs_scope / gxb_graph_owned_ids)
+    uint32_t* d_owned_d2s = nullptr;
+    uint64_t owned_present = 0;
     uint32_t sw_shift = 0;
     uint64_t* d_out_off = nullptr;      // V+1: push CSR restricted to owned destinations
     uint32_t* d_out_dst = nullptr;
@@ -277,6 +281,7 @@ inline unsigned grid_for(uint64_t n, int block = kBlock, uint64_t cap = 148ull *
 }
 
 int build_pull_plan(gxb_graph* g, cudaStream_t st);
+int build_owned_order(gxb_graph* g);  // d_owned_d2s / owned_present
 uint64_t xchunk_bound(uint64_t owned, int k, int K);  // relative slot bound k of K exchange chunks
 
 // runtime tuning knobs (gxb_set_option); defaults are the measured best on B200
@@ -290,8 +295,8 @@ struct Options {
     int64_t tile_async = 1;       // 1 = LDGSTS-gather tile kernel (k_tile_a), 0 = register gathers (k_tile_t)
     int64_t tile_async_minblocks = 0;  // its min-blocks variant (0 = auto: 8 / 6 / 4 for 4 / 8 / 16-B values)      // 0 = warp tiles, 1 = degree-binned groups
     int64_t carveout = -1;        // tile kernel shared-memory carveout in % (-1 = driver default)
-    int64_t exchange_chunks = 1;  // multi-GPU: chunks of the dense exchange overlapped with compute
-    int64_t overlap_reserve_sms = 8;  // SMs left to NCCL while a chunked round computes
+    int64_t exchange_chunks = 2;  // multi-GPU: exchange chunks (pipelined peer-write rounds; 2 measured best at N = 4)
+    int64_t overlap_reserve_sms = 0;  // SMs left free while a chunked round computes (0 measured best)
     int64_t pr_message_bits = 64; // PageRank message (rank / out_deg) precision: 64 or 32 (f64 accumulation)
 };
 Options& options();

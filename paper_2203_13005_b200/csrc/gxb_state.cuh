@@ -206,6 +206,16 @@ struct gxb_state {
 
     // host<->device attribute staging (ascending-id order)
     double* d_stage = nullptr;
+    // peer replicas of d_contrib[0/1] (PageRank): Apply stores each new contribution into
+    // every peer's next buffer over NVLink, fusing the mirror exchange into the kernel
+    int npeers = 0;
+    void* peer_contrib[gxb::kMaxPeers][2] = {};
+    bool peer_ipc = false;  // opened with cudaIpcOpenMemHandle (closed on free)
+    int round_chunks = 0;   // exchange chunks launched in the open round
+    cudaStream_t aux_stream = nullptr;  // pipelined rounds: span folds + Apply beside the tiles
+    cudaEvent_t ev_tile = nullptr, ev_join = nullptr;
+    int attrs_scope = 0;                          // async staging: 0 = every vertex, 1 = owned vertices
+    uint64_t stage_n = 0;                         // vertices per staging buffer (allocated)
     double* d_stage_in[2] = {nullptr, nullptr};   // async path: double-buffered
     double* d_stage_out[2] = {nullptr, nullptr};
 

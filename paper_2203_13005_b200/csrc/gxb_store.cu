@@ -34,6 +34,8 @@ Options& options() {
         if (const char* e = getenv("GXB_PULL_KERNEL")) o.pull_kernel = std::string(e) == "binned" ? 1 : 0;
         if (const char* e = getenv("GXB_PR_MESSAGE_BITS")) o.pr_message_bits = atol(e) == 32 ? 32 : 64;
         if (const char* e = getenv("GXB_TILE_ASYNC")) o.tile_async = atol(e) ? 1 : 0;
+        if (const char* e = getenv("GXB_EXCHANGE_CHUNKS")) o.exchange_chunks = std::min(64L, std::max(1L, atol(e)));
+        if (const char* e = getenv("GXB_OVERLAP_RESERVE_SMS")) o.overlap_reserve_sms = std::min(140L, std::max(0L, atol(e)));
     }
     return o;
 }
@@ -344,6 +346,7 @@ static void graph_release(gxb_graph* g) {
     dfree(g->d_in_src);
     dfree(g->d_in_w);
     dfree(g->d_in_sw);
+    dfree(g->d_owned_d2s);
     dfree(g->d_out_off);
     dfree(g->d_out_dst);
     dfree(g->d_out_w);
@@ -845,6 +848,30 @@ using namespace gxb;
 
 // ------------------------------------------------------------------ C ABI
 
+namespace gxb {
+struct InRange {
+    uint32_t lo, hi;
+    __host__ __device__ bool operator()(uint32_t s) const { return s >= lo && s < hi; }
+};
+int build_owned_order(gxb_graph* g) {
+    if (g->d_owned_d2s || !g->V) return GXB_OK;
+    cudaStream_t st = 0;
+    uint64_t* d_num = nullptr;
+    GXB_CHECK(dalloc_t(&g->d_owned_d2s, g->V));
+    GXB_CHECK(dalloc_t(&d_num, 1));
+    const InRange f{(uint32_t)g->lo, (uint32_t)g->hi};
+    size_t tb = 0;
+    GXB_CUDA(cub::DeviceSelect::If(nullptr, tb, g->d_dense2slot, g->d_owned_d2s, d_num, (int64_t)g->V, f, st));
+    void* tmp = nullptr;
+    GXB_CHECK(dalloc(&tmp, tb));
+    GXB_CUDA(cub::DeviceSelect::If(tmp, tb, g->d_dense2slot, g->d_owned_d2s, d_num, (int64_t)g->V, f, st));
+    GXB_CUDA(cudaMemcpy(&g->owned_present, d_num, 8, cudaMemcpyDeviceToHost));
+    dfree(tmp);
+    dfree(d_num);
+    return GXB_OK;
+}
+}  // namespace gxb
+
 extern "C" {
 
 const char* gxb_last_error(void) { return gxb::g_last_error.c_str(); }
@@ -1044,6 +1071,28 @@ int gxb_graph_ids(const gxb_graph* g, uint32_t* host_out) {
 int gxb_graph_out_degree(const gxb_graph* g, uint32_t* host_out) {
     if (!g || (!host_out && g->V)) return fail(GXB_EINVAL, "gxb_graph_out_degree: null argument");
     return read_dense_u32(g, g->d_outdeg, host_out);
+}
+
+
+__global__ void k_gather_ids(const uint32_t* __restrict__ d2s, uint64_t n, const uint32_t* __restrict__ slot2id,
+                             uint32_t* out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = slot2id[d2s[i]];
+}
+
+int gxb_graph_owned_ids(gxb_graph* g, uint32_t* host_out, uint64_t* count) {
+    if (!g || !count) return fail(GXB_EINVAL, "gxb_graph_owned_ids: null argument");
+    GXB_CUDA(cudaSetDevice(g->ctx->device));
+    GXB_CHECK(build_owned_order(g));
+    *count = g->owned_present;
+    if (!host_out || !g->owned_present) return GXB_OK;
+    uint32_t* d = nullptr;
+    GXB_CHECK(dalloc_t(&d, g->owned_present));
+    k_gather_ids<<<grid_for(g->owned_present), kBlock>>>(g->d_owned_d2s, g->owned_present, g->d_slot2id, d);
+    const cudaError_t e = cudaMemcpy(host_out, d, 4 * g->owned_present, cudaMemcpyDeviceToHost);
+    dfree(d);
+    if (e != cudaSuccess) return cuda_fail(e, "gxb_graph_owned_ids");
+    return GXB_OK;
 }
 
 int gxb_graph_part_bounds(const gxb_graph* g, uint64_t* host_out) {

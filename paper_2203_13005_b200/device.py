@@ -179,6 +179,14 @@ class DeviceGraph:
         L.check(L.lib().gxb_graph_xchunks(self._h, ctypes.byref(k), _vp(out)))
         return out
 
+    def owned_ids(self) -> np.ndarray:
+        """This partition's present ids, ascending (the order of owned-scope staging)."""
+        n = ctypes.c_uint64()
+        L.check(L.lib().gxb_graph_owned_ids(self._h, None, ctypes.byref(n)))
+        out = np.empty(n.value, dtype=np.uint32)
+        L.check(L.lib().gxb_graph_owned_ids(self._h, _vp(out), ctypes.byref(n)))
+        return out
+
     def bounds(self) -> np.ndarray:
         out = np.empty(self.nparts + 1, dtype=np.uint64)
         L.check(L.lib().gxb_graph_part_bounds(self._h, _vp(out)))
@@ -273,7 +281,41 @@ class DeviceState:
         else:  # pinned torch tensor
             L.check(L.lib().gxb_write_attrs(self._h, _vp(values), _stream_ptr(stream)))
 
+    # fused PageRank exchange: Apply stores into the peers' replicas (NVLink / NVSwitch)
+    IPC_HANDLE_BYTES = 64
+
+    def ipc_handle(self, which: int) -> bytes:
+        buf = (ctypes.c_ubyte * self.IPC_HANDLE_BYTES)()
+        L.check(L.lib().gxb_exchange_ipc_handle(self._h, which, buf))
+        return bytes(buf)
+
+    def open_peers(self, handles: bytes, npeers: int):
+        """handles: npeers x (buffer 0, buffer 1) IPC handles of the other ranks' states."""
+        if len(handles) != 2 * npeers * self.IPC_HANDLE_BYTES:
+            raise ValueError("open_peers: expected 2 handles per peer")
+        buf = (ctypes.c_ubyte * max(1, len(handles))).from_buffer_copy(handles or b"\0")
+        L.check(L.lib().gxb_exchange_open_peers(self._h, npeers, buf))
+
+    def set_peer_states(self, peers):
+        """Same-process peers (other DeviceStates): Apply writes their replicas directly."""
+        ptrs = (ctypes.c_void_p * max(1, 2 * len(peers)))()
+        for q, st in enumerate(peers):
+            for b in range(2):
+                ptrs[2 * q + b] = st._contrib_ptr(b)
+        L.check(L.lib().gxb_exchange_set_peer_ptrs(self._h, len(peers), ptrs))
+
+    def close_peers(self):
+        L.check(L.lib().gxb_exchange_close_peers(self._h))
+
+    def _contrib_ptr(self, b: int) -> int:
+        return self.buffer(L.BUF_CONTRIB1 if b else L.BUF_CONTRIB0)[0]
+
     # asynchronous staging (pipelined agent loop; pinned host tensors, explicit streams)
+    def attrs_scope(self, owned_only: bool):
+        """Stage every vertex (False) or only this partition's owned vertices (True, in
+        `DeviceGraph.owned_ids()` order)."""
+        L.check(L.lib().gxb_attrs_scope(self._h, int(bool(owned_only))))
+
     def attrs_h2d(self, host_in, buf: int, stream):
         L.check(L.lib().gxb_attrs_h2d(self._h, _vp(host_in), buf, _stream_ptr(stream)))
 

@@ -138,6 +138,8 @@ class PartitionedRun:
     needed_only: bool = False         # PR: send each peer only the values its CSC reads (NCCL
                                       # all-to-all; measured slower than the all-gather at N <= 4)
     sparse_ratio: float = 0.8         # ... when that is below this fraction of the dense volume
+    peer_writes: bool = True          # PR: Apply stores new contributions into the peers' replicas over
+                                      # NVLink (IPC-mapped), fusing the exchange into the kernel
     overlap: bool = False             # pipeline shuffle: chunked PR rounds with the exchange overlapped
                                       # (needs exchange_chunks > 1; measured slower than one all-gather
                                       # at N <= 4, where the tile kernel and NCCL contend for L2)
@@ -149,6 +151,7 @@ class PartitionedRun:
         self._pr_remote = None
         self._sparse = None
         self._pending = []
+        self._peers = None
         self.xchunks = 1
         if self.overlap and self.algo == "pagerank" and hasattr(self.state, "graph") and \
                 hasattr(self.state.graph, "xchunks"):
@@ -226,6 +229,41 @@ class PartitionedRun:
             return self.state.view(ptr, nbytes, dtype)
         return device_view(ptr, nbytes, dtype)
 
+    def _setup_peers(self) -> bool:
+        """Map every peer's contribution buffers (CUDA IPC handles, all-gathered once) so
+        PageRank's Apply writes the mirrors itself; all ranks must agree or none uses it."""
+        if self._peers is not None:
+            return self._peers
+        self._peers = False
+        if not (self.peer_writes and self.algo == "pagerank" and self.comm.world > 1
+                and hasattr(self.state, "ipc_handle") and hasattr(self.comm.dist, "all_gather_object")):
+            return False
+        import torch
+        ok = 1
+        try:
+            mine = self.state.ipc_handle(0) + self.state.ipc_handle(1)
+        except Exception:  # noqa: BLE001 - no IPC on this platform: fall back to NCCL
+            mine, ok = b"", 0
+        handles = [None] * self.comm.world
+        self.comm.dist.all_gather_object(handles, mine, group=self.comm.group)
+        if ok and all(handles):
+            try:
+                peers = b"".join(h for q, h in enumerate(handles) if q != self.comm.rank)
+                self.state.open_peers(peers, self.comm.world - 1)
+            except Exception:  # noqa: BLE001
+                ok = 0
+        else:
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=self.device)
+        self.comm.dist.all_reduce(flag, op=self.comm.dist.ReduceOp.MIN, group=self.comm.group)
+        if int(flag.item()) != 1:
+            if ok:
+                self.state.close_peers()
+            return False
+        # peer order on this rank = ranks ascending without me; the library writes them all
+        self._peers = True
+        return True
+
     # ---- one iteration ----------------------------------------------------
     def _tick(self, name, t0):
         if self.phase_times is not None:
@@ -282,8 +320,10 @@ class PartitionedRun:
         for w in self._pending:  # the previous round's overlapped exchange
             w.wait()
         self._pending = []
-        overlapped = (self.algo == "pagerank" and self.comm.world > 1 and self.overlap and self.xchunks > 1
-                      and self._pr_remote is not None and not (self.enable_skip and self._pr_remote == 0))
+        peers = self._setup_peers()
+        overlapped = (not peers and self.algo == "pagerank" and self.comm.world > 1 and self.overlap
+                      and self.xchunks > 1 and self._pr_remote is not None
+                      and not (self.enable_skip and self._pr_remote == 0))
         moved_early = 0
         if overlapped:
             moved_early = self._overlapped_pagerank_round()
@@ -296,7 +336,12 @@ class PartitionedRun:
             self.device)
         moved = moved_early
         early = overlapped
-        if not overlapped and self.algo == "pagerank" and self._pr_remote is not None and self.comm.world > 1:
+        if peers:  # the round's Apply already stored every owned contribution in every replica
+            sizes = np.diff(self.bounds.astype(np.int64))
+            ptr, nbytes = self.state.buffer(L.BUF_VALUES)
+            moved = nbytes // max(1, int(self.bounds[-1])) * int(self.bounds[-1] - sizes[self.comm.rank])
+            early = True
+        elif not overlapped and self.algo == "pagerank" and self._pr_remote is not None and self.comm.world > 1:
             # every PageRank vertex is active every round, so the skip vote is the same each
             # round: start the dense exchange behind the vote without waiting for its result
             early = not (self.enable_skip and self._pr_remote == 0)

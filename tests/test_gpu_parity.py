@@ -167,6 +167,7 @@ def test_chunked_round_equals_fused_round(ctx):
     from paper_2203_13005_b200.device import DeviceGraph, DeviceState
     from paper_2203_13005_b200.rmat import RmatParams, rmat_host
     src, dst, _ = rmat_host(RmatParams(scale=13, seed=71))
+    prev = L.get_option("exchange_chunks")
     L.set_option("exchange_chunks", 4)
     try:
         g = DeviceGraph(ctx, src, dst, None, part=1, nparts=2, csr=False)
@@ -183,7 +184,7 @@ def test_chunked_round_equals_fused_round(ctx):
             assert sa["changed"] == sb["changed"] and sa["max_stat"] == sb["max_stat"]
             np.testing.assert_array_equal(a.read_attrs(owned_only=True), b.read_attrs(owned_only=True))
     finally:
-        L.set_option("exchange_chunks", 1)
+        L.set_option("exchange_chunks", prev)
 
 
 def test_needed_only_exchange_matches_dense(ctx):
@@ -246,3 +247,45 @@ def test_async_staging_round_trip(ctx):
         s2.attrs_d2h(hout, 0, st)
         st.synchronize()
         np.testing.assert_array_equal(hout.numpy().reshape(V, a), ref)
+
+
+@pytest.mark.parametrize("chunks", [1, 4])
+@pytest.mark.parametrize("msg_bits", [64, 32])
+def test_peer_write_exchange_matches_dense(ctx, msg_bits, chunks):
+    """Fused exchange: each partition's Apply stores its new contributions into the other
+    partitions' replicas; values equal the dense all-gather exchange bit for bit."""
+    import torch
+    from paper_2203_13005_b200 import _lib as L
+    from paper_2203_13005_b200.device import DeviceGraph, DeviceState
+    from paper_2203_13005_b200.dist import device_view
+    from paper_2203_13005_b200.engine import exchange_local
+    from paper_2203_13005_b200.rmat import RmatParams, rmat_host
+    src, dst, _ = rmat_host(RmatParams(scale=12, seed=75))
+    L.set_option("pr_message_bits", msg_bits)
+    prev = L.get_option("exchange_chunks")
+    L.set_option("exchange_chunks", chunks)  # > 1: pipelined rounds (Apply of chunk k beside tiles of k+1)
+    try:
+        for nparts in (2, 3):
+            gs = [DeviceGraph(ctx, src, dst, None, part=p, nparts=nparts, csr=False) for p in range(nparts)]
+            dense = [DeviceState(g, "pagerank") for g in gs]
+            fused = [DeviceState(g, "pagerank") for g in gs]
+            for p, s in enumerate(fused):
+                s.set_peer_states([fused[q] for q in range(nparts) if q != p])
+            bounds = gs[0].bounds()
+            dt = "f8" if msg_bits == 64 else "f4"
+            for _ in range(4):
+                for s in dense + fused:
+                    s.iterate("pull")
+                    s.stats()
+                exchange_local(dense, bounds)
+                torch.cuda.synchronize()
+                for d, f in zip(dense, fused):
+                    np.testing.assert_array_equal(d.read_attrs(owned_only=True), f.read_attrs(owned_only=True))
+                    a = device_view(*d.buffer(L.BUF_VALUES), dt)
+                    b = device_view(*f.buffer(L.BUF_VALUES), dt)
+                    assert torch.equal(a, b)
+            for s in fused:
+                s.close_peers()
+    finally:
+        L.set_option("pr_message_bits", 64)
+        L.set_option("exchange_chunks", prev)

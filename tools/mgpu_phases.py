@@ -18,9 +18,11 @@ def main():
     g = DeviceGraph(ctx, src, dst, None, part=rank, nparts=world, csr=False)
     del src, dst; torch.cuda.empty_cache()
     st = DeviceState(g, "pagerank"); st.profile(enable=True, reset=True)
-    run = PartitionedRun(st, g.bounds(), Collective(), device=dev)
+    run = PartitionedRun(st, g.bounds(), Collective(), device=dev,
+                         peer_writes=os.environ.get("GXB_PEER_WRITES", "1") == "1")
     for _ in range(3): run.step()
-    run.phase_times = {}
+    if os.environ.get("GXB_PHASES", "1") == "1":
+        run.phase_times = {}
     st.profile(reset=True)
     n = 10
     t = time.perf_counter()
@@ -30,7 +32,8 @@ def main():
     lo, hi = g.owned
     out = {"rank": rank, "owned_slots": hi - lo, "owned_edges": int(g.info.owned_edges),
            "ms_per_step": round(1e3 * el / n, 3), "kernel_ms": round(prof["main_kernel_ms"] / max(1, prof["main_kernel_launches"]), 3),
-           **{k: round(1e3 * v / n, 3) for k, v in run.phase_times.items()}}
+           "rest_ms": round(prof["rest_ms"] / max(1, prof["main_kernel_launches"]), 3),
+           **{k: round(1e3 * v / n, 3) for k, v in (run.phase_times or {}).items()}}
     allv = [None] * world
     dist.all_gather_object(allv, out)
     if rank == 0:
