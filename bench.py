@@ -206,7 +206,7 @@ def algorithmic_bytes(algo, E, V, units=None, nz=None):
     return 8 * (units if units is not None else E) + 12 * V
 
 
-def time_frontier_run(ctx, comm, dev, stream, name, algo, params, cap):
+def time_frontier_run(ctx, comm, dev, stream, name, algo, params, cap, peak=None):
     """One full run (to convergence or cap) of a frontier algorithm; the first run warms
     allocations, the second is timed per iteration with CUDA events."""
     import torch
@@ -245,6 +245,15 @@ def time_frontier_run(ctx, comm, dev, stream, name, algo, params, cap):
            "iteration_ms": [round(a.elapsed_time(b), 3) for a, b, _ in per_iter],
            "directions": ["push" if x.direction == 2 else "pull" for _, _, x in per_iter],
            "note": "GTEPS_ref counts the reference's GEN units (out-edges of active vertices)"}
+    # a pull round scans every in-edge: its algorithmic bytes (E_scanned = E)
+    # over the round's device time, against the measured HBM peak
+    pull_ms = sorted(a.elapsed_time(b) for a, b, x in per_iter if x.direction != 2)
+    if pull_ms and peak:
+        med = pull_ms[len(pull_ms) // 2]
+        gbs = algorithmic_bytes(algo, g.num_edges, g.num_vertices) / (med * 1e-3) / 1e9
+        out["pull_round_roofline"] = {"bytes": algorithmic_bytes(algo, g.num_edges, g.num_vertices),
+                                      "median_ms": round(med, 3), "achieved": round(gbs, 1), "peak": peak,
+                                      "unit": "GB/s", "frac": round(gbs / peak, 4)}
     g.free()
     return out
 
@@ -473,7 +482,7 @@ def main():
                 ("sssp-s26", "sssp", RmatParams(scale=scale, seed=1, wmax=63), None),
                 ("cc-s24", "cc", RmatParams(scale=min(scale, 24), seed=1, symmetric=True), None),
                 ("lp-s24-a65", "lp", RmatParams(scale=min(scale, 24), seed=1, a=0.65, b=0.15, c=0.15), 15)):
-            secondary.append(time_frontier_run(ctx, comm, dev, stream, wname, walgo, wparams, wcap))
+            secondary.append(time_frontier_run(ctx, comm, dev, stream, wname, walgo, wparams, wcap, peak))
             torch.cuda.empty_cache()
 
     cpu = None
