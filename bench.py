@@ -213,7 +213,7 @@ def time_frontier_run(ctx, comm, dev, stream, name, algo, params, cap, peak=None
     from paper_2203_13005_b200.device import DeviceGraph, DeviceState
     from paper_2203_13005_b200.dist import PartitionedRun
     s, d, w = ctx.rmat(params, stream)
-    g = DeviceGraph(ctx, s, d, w, csr=algo in ("sssp", "cc"), stream=stream)
+    g = DeviceGraph(ctx, s, d, w, csr=algo in ("sssp", "cc", "lp"), stream=stream)
     del s, d, w
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
@@ -319,7 +319,7 @@ def main():
 
     # graph: same device-generated edge stream on every rank, own destination range kept
     src, dst, w = ctx.rmat(params, stream)
-    graph = DeviceGraph(ctx, src, dst, w, part=rank, nparts=world, csr=algo in ("sssp", "cc"), stream=stream)
+    graph = DeviceGraph(ctx, src, dst, w, part=rank, nparts=world, csr=algo in ("sssp", "cc", "lp"), stream=stream)
     del src, dst, w
     torch.cuda.synchronize()
     torch.cuda.empty_cache()

@@ -222,7 +222,7 @@ def run_device(algorithm: Algorithm, vertices, edges, max_iterations: int | None
     try:
         algo = algorithm.device_name
         w = ea.weight if algo == "sssp" else None
-        g = DeviceGraph(ctx, ea.src, ea.dst, w, csr=algo in ("sssp", "cc"))
+        g = DeviceGraph(ctx, ea.src, ea.dst, w, csr=algo in ("sssp", "cc", "lp"))
         sources = getattr(algorithm, "sources", None) if algo == "sssp" else None
         maxw = int(np.max(w)) if (w is not None and w.size) else 1
         s = DeviceState(g, algo, sources=sources, max_weight=maxw if algo == "sssp" else None)

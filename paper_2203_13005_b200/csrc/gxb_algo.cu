@@ -853,11 +853,11 @@ struct PushLaunch {
 constexpr uint32_t kPushChunk = 256;
 
 __global__ void k_push_counts(const uint32_t* __restrict__ frontier, uint64_t n, const uint64_t* __restrict__ out_off,
-                              uint32_t* counts) {
+                              uint32_t* counts, uint32_t chunk = kPushChunk) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t s = frontier[i];
         const uint64_t d = out_off[s + 1] - out_off[s];
-        counts[i] = (uint32_t)((d + kPushChunk - 1) / kPushChunk);
+        counts[i] = (uint32_t)((d + chunk - 1) / chunk);
     }
 }
 
@@ -894,14 +894,21 @@ __global__ void __launch_bounds__(kBlock) k_push(const Op op, const PushLaunch L
     const int lane = threadIdx.x & 31;
     if (L.nfront == 0) return;
     const uint64_t total = cpre[L.nfront - 1];
+    // each warp takes a contiguous run of chunks: one binary search, then walk forward
     const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
-    for (uint64_t c = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); c < total; c += nwarps) {
-        // first f with cpre[f] > c
-        uint64_t lo = 0, hi = L.nfront - 1;
+    const uint64_t w = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+    const uint64_t per = (total + nwarps - 1) / nwarps;
+    const uint64_t c0 = w * per, c1 = min(total, c0 + per);
+    uint64_t lo = 0;
+    if (c0 < c1) {  // first f with cpre[f] > c0
+        uint64_t hi = L.nfront - 1;
         while (lo < hi) {
             const uint64_t mid = (lo + hi) >> 1;
-            if (__ldg(cpre + mid) > c) hi = mid; else lo = mid + 1;
+            if (__ldg(cpre + mid) > c0) hi = mid; else lo = mid + 1;
         }
+    }
+    for (uint64_t c = c0; c < c1; ++c) {
+        while (__ldg(cpre + lo) <= c) ++lo;
         const uint64_t k = c - (lo ? __ldg(cpre + lo - 1) : 0);
         const uint32_t s = __ldg(L.frontier + lo);
         const uint64_t beg = __ldg(L.out_off + s) + k * kPushChunk;
@@ -1597,7 +1604,7 @@ int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, 
         }
         s->last.remote_active = c;
     }
-    if ((algo == GXB_ALGO_SSSP || algo == GXB_ALGO_CC) && g->has_csr && (rc = alloc_push(s)) != GXB_OK)
+    if (algo != GXB_ALGO_PAGERANK && g->has_csr && (rc = alloc_push(s)) != GXB_OK)
         return bail(rc);
     if (algo == GXB_ALGO_LP && (rc = gxb_lp_prepare(s, st)) != GXB_OK) return bail(rc);
     cudaError_t e = cudaStreamSynchronize(st);
@@ -1662,7 +1669,8 @@ int gxb_state_arity(const gxb_state* s, int* out) {
     return GXB_OK;
 }
 
-int gxb_lp_pull(gxb_state* s, cudaStream_t st);     // gxb_lp.cu
+int gxb_lp_pull(gxb_state* s, cudaStream_t st);  // gxb_lp.cu
+int gxb_lp_push(gxb_state* s, cudaStream_t st, const uint32_t* rowpre);
 
 
 int gxb_iterate(gxb_state* s, int direction, void* stream) {
@@ -1682,7 +1690,33 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
             dir = GXB_DIR_PULL;
         }
     }
+    // LP "push": mark the frontier's out-neighbours over the CSR, then take the mode of the
+    // marked destinations only (the others receive no message and keep their label)
+    bool lp_sparse = false;
+    if (s->algo == GXB_ALGO_LP && g->has_csr) {
+        if (direction == GXB_DIR_PUSH) lp_sparse = true;
+        else if (direction == GXB_DIR_AUTO) lp_sparse = s->units_cur * (uint64_t)options().push_alpha < g->E;
+        if (lp_sparse) dir = GXB_DIR_PUSH;
+    } else if (s->algo == GXB_ALGO_LP && direction == GXB_DIR_PUSH) {
+        return fail(GXB_EINVAL, "push requested but the graph has no CSR");
+    }
     const uint64_t owned = g->hi - g->lo;
+    if (lp_sparse) {
+        if (!s->d_push_counts) GXB_CHECK(alloc_push(s));
+        const uint64_t nf = s->frontier_len;
+        if (nf) {
+            // row lengths (chunk 1): the push is edge-balanced over the concatenated rows
+            k_push_counts<<<grid_for(nf), kBlock, 0, st>>>(s->d_frontier[0], nf, g->d_out_off, s->d_push_counts, 1u);
+            size_t tb = s->push_tmp_bytes;
+            GXB_CUDA(cub::DeviceScan::InclusiveSum(s->d_push_tmp, tb, s->d_push_counts, s->d_push_cpre, (int64_t)nf, st));
+            s->launches += 2;
+        }
+        GXB_CHECK(gxb_lp_push(s, st, s->d_push_cpre));
+        s->launches += 1;
+        GXB_CHECK(end_round(s, GXB_DIR_PULL, st));  // commits lab_next like a pull round
+        s->last_direction = GXB_DIR_PUSH;
+        return GXB_OK;
+    }
     if (dir == GXB_DIR_PULL && s->algo != GXB_ALGO_LP && !use_binned_pull()) {
         switch (s->algo) {
             case GXB_ALGO_PAGERANK:
@@ -1722,7 +1756,7 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
             }
             case GXB_ALGO_LP:
                 GXB_CHECK(gxb_lp_pull(s, st));
-                s->launches += 3;
+                s->launches += 2;
                 break;
         }
         if (s->algo != GXB_ALGO_LP) s->launches++;

@@ -34,9 +34,18 @@ struct LpHub {
     uint64_t entries;
 };
 
+struct LpPush;
 struct LpScratch {
     LpHub hub;
     uint64_t chunk_end = 0;
+    uint32_t hot_end = 0;  // slots with in-degree >= kLpHotDegree: pushed through shared memory
+    // sparse rounds (allocated on the first one)
+    unsigned long long* pkeys = nullptr;
+    uint32_t* pcounts = nullptr;
+    unsigned long long* pbest = nullptr;
+    uint32_t* ptargets = nullptr;
+    unsigned long long* pntargets = nullptr;
+    uint64_t pcapacity = 0;
 };
 
 __device__ __forceinline__ uint32_t mix32(uint32_t x) {
@@ -199,10 +208,190 @@ __global__ void __launch_bounds__(kBlock) k_lp_hub_apply(const LpLaunch L, uint6
     flush_stats(st, L.stats);
 }
 
+// ---- sparse rounds: push the frontier's labels along the CSR ----
+// Only active sources send, so a sparse round's multisets are small: every (destination,
+// label) pair of the round is counted in one open-addressing table keyed by
+// dst << 32 | label (warp-aggregated: a chunk's edges share their source and label, so
+// equal keys are parallel edges), each update raises the destination's packed running
+// argmax, and the first update of a destination appends it to the round's target list.
+struct LpPush {
+    unsigned long long* keys;  // capacity (power of two), ~0 = empty
+    uint32_t* counts;
+    unsigned long long* best;  // per owned slot, 0 = no message
+    uint32_t* targets;         // relative slots that received a message this round
+    unsigned long long* ntargets;
+    uint64_t capacity;
+};
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ull;
+    x ^= x >> 33;
+    return x;
+}
+
+__device__ __forceinline__ uint32_t pair_add(const LpPush& P, uint64_t mask, unsigned long long key, uint32_t c) {
+    uint64_t i = mix64(key) & mask;
+    while (true) {
+        unsigned long long k = __ldcg(P.keys + i);
+        if (k == ~0ull) {
+            k = atomicCAS(P.keys + i, ~0ull, key);
+            if (k == ~0ull) k = key;
+        }
+        if (k == key) return atomicAdd(P.counts + i, c) + c;
+        i = (i + 1) & mask;
+    }
+}
+
+// Pairs aimed at the largest hubs (relative slot < hub_end: slots are in-degree sorted, and
+// hub_end covers in-degree >= kLpHotDegree) are first counted
+// in a block-local shared table and flushed once per block: many frontier sources with the
+// same label hit the same hub, and folding them in shared memory keeps the global table
+// from serialising on a few hot (hub, label) counters.
+constexpr int kLpSmemPairs = 2048;
+
+__device__ __forceinline__ bool smem_pair_add(unsigned long long* keys, uint32_t* counts, unsigned long long key,
+                                              uint32_t c) {
+    uint32_t i = (uint32_t)mix64(key) & (kLpSmemPairs - 1);
+#pragma unroll 1
+    for (int probe = 0; probe < 16; ++probe) {
+        unsigned long long k = keys[i];
+        if (k == ~0ull) {
+            k = atomicCAS(keys + i, ~0ull, key);
+            if (k == ~0ull) k = key;
+        }
+        if (k == key) {
+            atomicAdd(counts + i, c);
+            return true;
+        }
+        i = (i + 1) & (kLpSmemPairs - 1);
+    }
+    return false;  // crowded: the caller goes to the global table
+}
+
+// returns whether this update was the destination's first message of the round (the
+// caller appends it to the target list, warp-aggregated)
+__device__ __forceinline__ bool global_pair(const LpPush& P, uint64_t mask, unsigned long long key, uint32_t c) {
+    const uint32_t rel = (uint32_t)(key >> 32), lab = (uint32_t)key;
+    const uint32_t nc = pair_add(P, mask, key, c);
+    const unsigned long long pk = ((unsigned long long)nc << 32) | (unsigned long long)(~lab);
+    if (pk > __ldcg(P.best + rel)) return atomicMax(P.best + rel, pk) == 0ull;
+    return false;
+}
+
+// all lanes of the warp call it: one reservation per warp for the new targets
+__device__ __forceinline__ void append_targets(const LpPush& P, bool first, uint32_t rel) {
+    const unsigned m = __ballot_sync(kFull, first);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(P.ntargets, (unsigned long long)__popc(m));
+    base = __shfl_sync(kFull, base, __ffs(m) - 1);
+    if (first) P.targets[base + __popc(m & ((1u << lane) - 1u))] = rel;
+}
+
+// Edge-balanced over the concatenated CSR rows of the frontier (rowpre = inclusive prefix
+// of row lengths): a warp takes 256 consecutive edges, finds the first one's row with one
+// binary search, and each lane walks forward to its own rows — many short rows cost no
+// more than one long one.
+constexpr uint32_t kLpItemEdges = 256;
+
+__global__ void __launch_bounds__(kBlock) k_lp_push(const uint32_t* __restrict__ frontier, uint64_t nfront,
+                                                    const uint32_t* __restrict__ rowpre,
+                                                    const uint64_t* __restrict__ out_off,
+                                                    const uint32_t* __restrict__ out_dst,
+                                                    const uint32_t* __restrict__ lab_cur, uint64_t lo, LpPush P,
+                                                    uint64_t mask, uint32_t hub_end) {
+    __shared__ unsigned long long skeys[kLpSmemPairs];
+    __shared__ uint32_t scounts[kLpSmemPairs];
+    for (int i = threadIdx.x; i < kLpSmemPairs; i += kBlock) {
+        skeys[i] = ~0ull;
+        scounts[i] = 0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint64_t total = nfront ? rowpre[nfront - 1] : 0;
+    const uint64_t items = (total + kLpItemEdges - 1) / kLpItemEdges;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
+    for (uint64_t it = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); it < items; it += nwarps) {
+        const uint64_t g0 = it * kLpItemEdges, g1 = min(total, g0 + kLpItemEdges);
+        uint64_t a = 0, b = nfront - 1;  // row of edge g0: first f with rowpre[f] > g0
+        while (a < b) {
+            const uint64_t mid = (a + b) >> 1;
+            if (__ldg(rowpre + mid) > g0) b = mid; else a = mid + 1;
+        }
+        uint64_t f = a;  // this lane's row cursor (monotone over its edges)
+#pragma unroll 1
+        for (uint32_t j = 0; j < kLpItemEdges / 32; ++j) {
+            const uint64_t gl = g0 + j * 32 + lane;
+            const bool ok = gl < g1;
+            uint32_t rel = 0, lab = 0;
+            if (ok) {
+                while (__ldg(rowpre + f) <= gl) ++f;
+                const uint32_t s = __ldg(frontier + f);
+                const uint64_t e = __ldg(out_off + s) + (gl - (f ? __ldg(rowpre + f - 1) : 0));
+                rel = (uint32_t)(__ldg(out_dst + e) - lo);
+                lab = __ldg(lab_cur + s);
+            }
+            const unsigned long long key = ok ? ((unsigned long long)rel << 32 | lab) : (~0ull - 1 - lane);
+            const unsigned m = __match_any_sync(kFull, key);
+            bool first = false;
+            if (ok && lane == __ffs(m) - 1) {
+                if (!(rel < hub_end && smem_pair_add(skeys, scounts, key, __popc(m))))
+                    first = global_pair(P, mask, key, __popc(m));
+            }
+            append_targets(P, first, rel);
+        }
+    }
+    __syncthreads();
+    for (int i0 = 0; i0 < kLpSmemPairs; i0 += kBlock) {  // block-uniform trip count
+        const int i = i0 + threadIdx.x;
+        const unsigned long long key = skeys[i];
+        const bool first = key != ~0ull && global_pair(P, mask, key, scounts[i]);
+        append_targets(P, first, (uint32_t)(key >> 32));
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_lp_push_apply(const LpLaunch L, LpPush P) {
+    LocalStats st;
+    const uint64_t n = *P.ntargets;
+    for (uint64_t i = blockIdx.x * (uint64_t)kBlock + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kBlock) {
+        const uint32_t rel = P.targets[i];
+        const unsigned long long best = P.best[rel];
+        P.best[rel] = 0ull;
+        lp_finish(L, (uint32_t)(L.lo + rel), best, st);
+    }
+    flush_stats(st, L.stats);
+}
+
 static uint64_t next_pow2(uint64_t x) {
     uint64_t p = 1;
     while (p < x) p <<= 1;
     return p;
+}
+
+// sparse-round scratch: a pair table of `cap` entries, per-slot argmax and target list
+static int lp_push_reserve(gxb_state* s, LpScratch* S, uint64_t cap, cudaStream_t st) {
+    const uint64_t owned = s->g->hi - s->g->lo;
+    if (!S->pntargets) GXB_CHECK(dalloc_t(&S->pntargets, 2));
+    if (!S->pbest) {
+        GXB_CHECK(dalloc_t(&S->pbest, owned + 1));
+        GXB_CHECK(dalloc_t(&S->ptargets, owned + 1));
+        GXB_CUDA(cudaMemsetAsync(S->pbest, 0, 8 * (owned + 1), st));
+    }
+    if (cap > S->pcapacity) {
+        dfree(S->pkeys);
+        dfree(S->pcounts);
+        S->pkeys = nullptr;
+        S->pcounts = nullptr;
+        S->pcapacity = 0;
+        GXB_CHECK(dalloc_t(&S->pkeys, cap));
+        GXB_CHECK(dalloc_t(&S->pcounts, cap));
+        S->pcapacity = cap;
+    }
+    return GXB_OK;
 }
 
 static void lp_free(LpScratch* S) {
@@ -213,14 +402,22 @@ static void lp_free(LpScratch* S) {
     dfree(H.keys);
     dfree(H.counts);
     dfree(H.best);
+    dfree(S->pkeys);
+    dfree(S->pcounts);
+    dfree(S->pbest);
+    dfree(S->ptargets);
+    dfree(S->pntargets);
     delete S;
 }
+
+constexpr uint32_t kLpHotDegree = 16384;
 
 static int lp_setup(gxb_state* s, cudaStream_t st) {
     const gxb_graph* g = s->g;
     const PullPlan& P = g->plan;
     LpScratch* S = new LpScratch();
     S->chunk_end = P.chunk_end;
+    while (S->hot_end < g->h_indeg_sorted.size() && g->h_indeg_sorted[S->hot_end] >= kLpHotDegree) ++S->hot_end;
     LpHub& H = S->hub;
     std::vector<uint64_t> off(P.chunk_end + 1);
     std::vector<uint32_t> mask(P.chunk_end + 1);
@@ -263,24 +460,9 @@ static int lp_setup(gxb_state* s, cudaStream_t st) {
 
 using namespace gxb;
 
-extern "C" void gxb_lp_free(gxb_state* s) {
-    if (s && s->d_lp_scratch) {
-        lp_free(reinterpret_cast<LpScratch*>(s->d_lp_scratch));
-        s->d_lp_scratch = nullptr;
-    }
-}
-
-extern "C" int gxb_lp_prepare(gxb_state* s, cudaStream_t st) {
-    if (!s->d_lp_scratch) GXB_CHECK(lp_setup(s, st));
-    return GXB_OK;
-}
-
-extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
-    if (!s->d_lp_scratch) GXB_CHECK(lp_setup(s, st));
-    LpScratch* S = reinterpret_cast<LpScratch*>(s->d_lp_scratch);
+static LpLaunch lp_launch(gxb_state* s) {
     const gxb_graph* g = s->g;
-    const PullPlan& P = g->plan;
-    LpLaunch L;
+    LpLaunch L{};
     L.lo = g->lo;
     L.in_off = g->d_in_off;
     L.in_src = g->d_in_src;
@@ -294,6 +476,32 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
     L.f.frontier_next = s->d_frontier[1];
     L.f.frontier_count = s->d_fcount + 1;
     L.stats = s->d_stats;
+    return L;
+}
+
+extern "C" void gxb_lp_free(gxb_state* s) {
+    if (s && s->d_lp_scratch) {
+        lp_free(reinterpret_cast<LpScratch*>(s->d_lp_scratch));
+        s->d_lp_scratch = nullptr;
+    }
+}
+
+extern "C" int gxb_lp_prepare(gxb_state* s, cudaStream_t st) {
+    if (!s->d_lp_scratch) GXB_CHECK(lp_setup(s, st));
+    if (s->g->has_csr) {  // sparse rounds push at most E / push_alpha edges: no cudaMalloc mid-run
+        const uint64_t alpha = std::max<int64_t>(1, options().push_alpha);
+        const uint64_t cap = std::max<uint64_t>(1024, next_pow2(2 * (s->g->E / alpha) + 2));
+        GXB_CHECK(lp_push_reserve(s, reinterpret_cast<LpScratch*>(s->d_lp_scratch), cap, st));
+    }
+    return GXB_OK;
+}
+
+extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
+    if (!s->d_lp_scratch) GXB_CHECK(lp_setup(s, st));
+    LpScratch* S = reinterpret_cast<LpScratch*>(s->d_lp_scratch);
+    const gxb_graph* g = s->g;
+    const PullPlan& P = g->plan;
+    LpLaunch L = lp_launch(s);
     L.num_items = P.num_items;
     L.item_slot = P.d_item_slot;
     L.item_begin = P.d_item_begin;
@@ -316,6 +524,36 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
         GXB_CUDA(cudaMemsetAsync(S->hub.keys, 0xFF, 4 * S->hub.entries, st));
         GXB_CUDA(cudaMemsetAsync(S->hub.counts, 0, 4 * S->hub.entries, st));
     }
+    GXB_CUDA(cudaGetLastError());
+    return GXB_OK;
+}
+
+// sparse round: cpre = inclusive scan of the frontier's chunk counts (chunk_edges-edge
+// chunks of each frontier vertex's CSR row), `units` = the frontier's out-edges
+extern "C" int gxb_lp_push(gxb_state* s, cudaStream_t st, const uint32_t* rowpre) {
+    if (!s->d_lp_scratch) GXB_CHECK(lp_setup(s, st));
+    LpScratch* S = reinterpret_cast<LpScratch*>(s->d_lp_scratch);
+    const gxb_graph* g = s->g;
+    GXB_CHECK(lp_push_reserve(s, S, 0, st));
+    // the pair table holds at most one entry per pushed edge
+    uint32_t total = 0;
+    if (s->frontier_len) {
+        GXB_CUDA(cudaMemcpyAsync(&total, rowpre + s->frontier_len - 1, 4, cudaMemcpyDeviceToHost, st));
+        GXB_CUDA(cudaStreamSynchronize(st));
+    }
+    const uint64_t cap = std::max<uint64_t>(1024, next_pow2(2ull * total + 2));
+    GXB_CHECK(lp_push_reserve(s, S, cap, st));
+    LpPush P{S->pkeys, S->pcounts, S->pbest, S->ptargets, S->pntargets, cap};
+    GXB_CUDA(cudaMemsetAsync(S->pkeys, 0xFF, 8 * cap, st));
+    GXB_CUDA(cudaMemsetAsync(S->pcounts, 0, 4 * cap, st));
+    GXB_CUDA(cudaMemsetAsync(S->pntargets, 0, 8, st));
+    if (total) {
+        const uint64_t items = (total + kLpItemEdges - 1) / kLpItemEdges;
+        const unsigned grid = grid_for(items * 32, kBlock, 148ull * 16);
+        k_lp_push<<<grid, kBlock, 0, st>>>(s->d_frontier[0], s->frontier_len, rowpre, g->d_out_off, g->d_out_dst,
+                                           s->d_lab_cur, g->lo, P, cap - 1, S->hot_end);
+    }
+    k_lp_push_apply<<<grid_for(g->hi - g->lo), kBlock, 0, st>>>(lp_launch(s), P);
     GXB_CUDA(cudaGetLastError());
     return GXB_OK;
 }

@@ -212,7 +212,7 @@ class Engine:
         w = ea.weight if algo == "sssp" else None
         maxw = int(np.max(w)) if (w is not None and w.size) else 1
         for j in range(m):
-            g = DeviceGraph(self.ctx, ea.src, ea.dst, w, part=j, nparts=m, csr=algo in ("sssp", "cc"),
+            g = DeviceGraph(self.ctx, ea.src, ea.dst, w, part=j, nparts=m, csr=algo in ("sssp", "cc", "lp"),
                             partitioning=cfg.partitioning, sizes=cfg.sizes)
             s = DeviceState(g, algo, sources=getattr(self.algorithm, "sources", None) if algo == "sssp" else None,
                             max_weight=maxw if algo == "sssp" else None)

@@ -22,7 +22,7 @@ def ctx():
 
 def device_run(ctx, src, dst, w, algo, cap=None, direction="auto", sources=None):
     from paper_2203_13005_b200.device import DeviceGraph, DeviceState, run_state
-    g = DeviceGraph(ctx, src, dst, w if algo == "sssp" else None, csr=algo in ("sssp", "cc"))
+    g = DeviceGraph(ctx, src, dst, w if algo == "sssp" else None, csr=algo in ("sssp", "cc", "lp"))
     maxw = None if w is None else int(np.max(w)) if len(w) else 0
     s = DeviceState(g, algo, sources=sources, max_weight=maxw if algo == "sssp" else None)
     it, conv, hist = run_state(s, cap, direction, keep_history=True)
@@ -54,8 +54,8 @@ CASES = [
 @pytest.mark.parametrize("direction", ["auto", "pull", "push"])
 def test_oracle_parity(ctx, oracle_lib, case, algo, direction):
     from paper_2203_13005_b200.rmat import RmatParams, rmat_host
-    if direction == "push" and algo in ("pagerank", "lp"):
-        pytest.skip("push mode exists for SSSP/CC only")
+    if direction == "push" and algo == "pagerank":
+        pytest.skip("push mode exists for SSSP/CC/LP only")
     p = RmatParams(**case, symmetric=(algo == "cc"))
     src, dst, w = rmat_host(p)
     cap = {"pagerank": 10, "lp": None, "sssp": None, "cc": None}[algo]

@@ -40,7 +40,7 @@ def main():
         over = {"sssp": dict(wmax=63), "cc": dict(symmetric=True), "lp": dict(a=0.65, b=0.15, c=0.15)}.get(algo, {})
         p = RmatParams(scale=args.scale, seed=77, **over)
         src, dst, w = ctx.rmat(p)
-        g = DeviceGraph(ctx, src, dst, w, part=rank, nparts=world, csr=algo in ("sssp", "cc"),
+        g = DeviceGraph(ctx, src, dst, w, part=rank, nparts=world, csr=algo in ("sssp", "cc", "lp"),
                         partitioning=args.partitioning)
         st = DeviceState(g, algo)
         run = PartitionedRun(st, g.bounds(), comm, enable_skip=True, device=dev)

@@ -31,7 +31,7 @@ def main():
     src, dst, w = ctx.rmat(p)
     torch.cuda.synchronize()
     t1 = time.time()
-    g = DeviceGraph(ctx, src, dst, w, csr=args.algo in ("sssp", "cc"))
+    g = DeviceGraph(ctx, src, dst, w, csr=args.algo in ("sssp", "cc", "lp"))
     torch.cuda.synchronize()
     t2 = time.time()
     del src, dst, w

@@ -40,7 +40,7 @@ def main():
     ctx = DeviceContext(0)
     p = RmatParams(scale=args.scale, seed=1, wmax=63 if args.algo == "sssp" else 0, symmetric=args.algo == "cc")
     src, dst, w = ctx.rmat(p)
-    g = DeviceGraph(ctx, src, dst, w, csr=args.algo in ("sssp", "cc"))
+    g = DeviceGraph(ctx, src, dst, w, csr=args.algo in ("sssp", "cc", "lp"))
     del src, dst, w
     torch.cuda.empty_cache()
     keys = list(grid)
