@@ -889,35 +889,33 @@ struct CcPush {
     }
 };
 
+// Edge-balanced over the concatenated CSR rows of the frontier (rowpre = inclusive prefix
+// of the row lengths): a warp takes kPushChunk consecutive edges, finds the first one's row
+// with one binary search, and each lane walks forward to its own rows, so a frontier of
+// millions of short rows costs the same per edge as one hub row.
 template <class Op>
-__global__ void __launch_bounds__(kBlock) k_push(const Op op, const PushLaunch L, const uint32_t* __restrict__ cpre) {
+__global__ void __launch_bounds__(kBlock) k_push(const Op op, const PushLaunch L, const uint32_t* __restrict__ rowpre) {
     const int lane = threadIdx.x & 31;
     if (L.nfront == 0) return;
-    const uint64_t total = cpre[L.nfront - 1];
-    // each warp takes a contiguous run of chunks: one binary search, then walk forward
+    const uint64_t total = rowpre[L.nfront - 1];
+    const uint64_t items = (total + kPushChunk - 1) / kPushChunk;
     const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
-    const uint64_t w = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
-    const uint64_t per = (total + nwarps - 1) / nwarps;
-    const uint64_t c0 = w * per, c1 = min(total, c0 + per);
-    uint64_t lo = 0;
-    if (c0 < c1) {  // first f with cpre[f] > c0
-        uint64_t hi = L.nfront - 1;
-        while (lo < hi) {
-            const uint64_t mid = (lo + hi) >> 1;
-            if (__ldg(cpre + mid) > c0) hi = mid; else lo = mid + 1;
+    for (uint64_t it = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); it < items; it += nwarps) {
+        const uint64_t g0 = it * kPushChunk, g1 = min(total, g0 + kPushChunk);
+        uint64_t a = 0, b = L.nfront - 1;  // row of edge g0: first f with rowpre[f] > g0
+        while (a < b) {
+            const uint64_t mid = (a + b) >> 1;
+            if (__ldg(rowpre + mid) > g0) b = mid; else a = mid + 1;
         }
-    }
-    for (uint64_t c = c0; c < c1; ++c) {
-        while (__ldg(cpre + lo) <= c) ++lo;
-        const uint64_t k = c - (lo ? __ldg(cpre + lo - 1) : 0);
-        const uint32_t s = __ldg(L.frontier + lo);
-        const uint64_t beg = __ldg(L.out_off + s) + k * kPushChunk;
-        const uint64_t end = min(beg + kPushChunk, __ldg(L.out_off + s + 1));
-        const typename Op::Val v = op.load(s);
-        for (uint64_t e = beg + lane; e < end; e += 32) {
+        uint64_t f = a;
+#pragma unroll 1
+        for (uint64_t gl = g0 + lane; gl < g1; gl += 32) {
+            while (__ldg(rowpre + f) <= gl) ++f;
+            const uint32_t s = __ldg(L.frontier + f);
+            const uint64_t e = __ldg(L.out_off + s) + (gl - (f ? __ldg(rowpre + f - 1) : 0));
             const uint32_t t = __ldg(L.out_dst + e);
             const uint32_t w = L.out_w ? __ldg(L.out_w + e) : 1u;
-            if (op.relax(v, t, w) && bit_set_atomic(L.touched, (uint32_t)(t - L.lo)))
+            if (op.relax(op.load(s), t, w) && bit_set_atomic(L.touched, (uint32_t)(t - L.lo)))
                 warp_append(L.list_next, L.count_next, t);
         }
     }
@@ -1776,11 +1774,11 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
         if (!s->d_push_counts) GXB_CHECK(alloc_push(s));
         if (P.nfront) {
             s->launches += 3;  // counts, scan, push
-            k_push_counts<<<grid_for(P.nfront), kBlock, 0, st>>>(P.frontier, P.nfront, P.out_off, s->d_push_counts);
+            k_push_counts<<<grid_for(P.nfront), kBlock, 0, st>>>(P.frontier, P.nfront, P.out_off, s->d_push_counts, 1u);
             size_t tb = s->push_tmp_bytes;
             GXB_CUDA(cub::DeviceScan::InclusiveSum(s->d_push_tmp, tb, s->d_push_counts, s->d_push_cpre,
                                                    (int64_t)P.nfront, st));
-            const unsigned grid = grid_for((s->units_cur / kPushChunk + P.nfront) * 32, kBlock, 148ull * 16);
+            const unsigned grid = grid_for((s->units_cur / kPushChunk + 1) * 32, kBlock, 148ull * 16);
             if (s->algo == GXB_ALGO_SSSP)
                 k_push<SsspPush><<<grid, kBlock, 0, st>>>(SsspPush{s->d_dist_cur, s->d_dist_next}, P, s->d_push_cpre);
             else
