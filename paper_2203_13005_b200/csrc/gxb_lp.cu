@@ -141,44 +141,80 @@ __device__ __forceinline__ void lp_group(const LpLaunch& L, int k, unsigned b, u
     if (valid && gl == 0) lp_finish(L, (uint32_t)(L.lo + rel), best, st);
 }
 
-// large destinations: warp-aggregated inserts into the per-slot global table
-__device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item) {
+// large destinations: a warp streams a kChunkEdges-edge chunk of one hub. Equal labels are
+// merged per 32 edges (__match_any_sync), then counted in a per-warp shared table for the
+// whole chunk; the chunk's distinct (label, count) pairs go to the hub's global table once
+// (overflow goes straight to it). Each global update also raises the hub's running packed
+// argmax (a label's (count, ~label) only grows, so the max over all updates is the max over
+// the final counts).
+constexpr int kWarpPairs = 128;
+
+__device__ __forceinline__ void hub_add(const LpLaunch& L, uint64_t rel, uint64_t base, uint32_t mask, uint32_t lab,
+                                        uint32_t c) {
+    const uint32_t nc = table_add(L.hub.keys, L.hub.counts, base, mask, lab, c);
+    const unsigned long long pk = ((unsigned long long)nc << 32) | (unsigned long long)(~lab);
+    if (pk > __ldcg(L.hub.best + rel)) atomicMax(L.hub.best + rel, pk);
+}
+
+__device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint32_t* wkeys, uint32_t* wcnts) {
     const int lane = threadIdx.x & 31;
     const uint32_t rel = __ldg(L.item_slot + item);
     const uint64_t beg = __ldg(L.item_begin + item);
     const uint64_t end = min(beg + (uint64_t)kChunkEdges, __ldg(L.in_off + rel + 1));
     const uint64_t base = __ldg(L.hub.tab_off + rel);
     const uint32_t mask = __ldg(L.hub.tab_mask + rel);
-    for (uint64_t e0 = beg; e0 < end; e0 += 32) {
-        const uint64_t e = e0 + lane;
-        bool ok = false;
-        uint32_t lab = 0;
-        if (e < end) {
-            const uint32_t s = __ldg(L.in_src + e);
-            if (bit_test(L.active_cur, s)) {
-                ok = true;
-                lab = __ldg(L.lab_cur + s);
+    for (int i = lane; i < kWarpPairs; i += 32) {
+        wkeys[i] = kEmpty;
+        wcnts[i] = 0;
+    }
+    __syncwarp();
+    constexpr int kB = 8;  // the loads of 8 steps are issued together
+    for (uint64_t e0 = beg; e0 < end; e0 += 32 * kB) {
+        uint32_t src[kB], lab[kB];
+        bool ok[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            const uint64_t e = e0 + 32 * j + lane;
+            src[j] = e < end ? __ldg(L.in_src + e) : kEmpty;
+        }
+#pragma unroll
+        for (int j = 0; j < kB; ++j) ok[j] = src[j] != kEmpty && bit_test(L.active_cur, src[j]);
+#pragma unroll
+        for (int j = 0; j < kB; ++j) lab[j] = ok[j] ? __ldg(L.lab_cur + src[j]) : 0u;
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            const unsigned long long key = ok[j] ? (unsigned long long)lab[j] : (0x100000000ull | (unsigned)lane);
+            const unsigned m = __match_any_sync(kFull, key);
+            if (ok[j] && lane == __ffs(m) - 1) {
+                uint32_t h = mix32(lab[j]) & (kWarpPairs - 1);
+                bool done = false;
+#pragma unroll 1
+                for (int probe = 0; probe < 8 && !done; ++probe) {
+                    const uint32_t k = atomicCAS(wkeys + h, kEmpty, lab[j]);
+                    if (k == kEmpty || k == lab[j]) {
+                        atomicAdd(wcnts + h, (uint32_t)__popc(m));
+                        done = true;
+                    }
+                    h = (h + 1) & (kWarpPairs - 1);
+                }
+                if (!done) hub_add(L, rel, base, mask, lab[j], __popc(m));
             }
         }
-        const unsigned long long key = ok ? (unsigned long long)lab : (0x100000000ull | (unsigned)lane);
-        const unsigned m = __match_any_sync(kFull, key);
-        if (ok && lane == __ffs(m) - 1) {
-            // the running argmax: a label's packed (count, ~label) only grows, so the max over
-            // every update equals the max over final counts
-            const uint32_t nc = table_add(L.hub.keys, L.hub.counts, base, mask, lab, __popc(m));
-            const unsigned long long pk = ((unsigned long long)nc << 32) | (unsigned long long)(~lab);
-            if (pk > __ldcg(L.hub.best + rel)) atomicMax(L.hub.best + rel, pk);
-        }
     }
+    __syncwarp();
+    for (int i = lane; i < kWarpPairs; i += 32)
+        if (wkeys[i] != kEmpty) hub_add(L, rel, base, mask, wkeys[i], wcnts[i]);
 }
 
 __global__ void __launch_bounds__(kBlock) k_lp_pull(const LpLaunch L) {
-    __shared__ uint32_t buf[4 * kBlock];
+    // group path: 4 labels per thread; chunk path: a (label, count) table per warp
+    __shared__ uint32_t buf[4 * kBlock > 2 * kWarpPairs * (kBlock / 32) ? 4 * kBlock : 2 * kWarpPairs * (kBlock / 32)];
     LocalStats st;
     unsigned b = blockIdx.x;
     if (b < L.chunk_blocks) {
         const uint64_t item = (uint64_t)b * (kBlock / 32) + (threadIdx.x >> 5);
-        if (item < L.num_items) lp_chunk(L, item);
+        uint32_t* wk = buf + (threadIdx.x >> 5) * 2 * kWarpPairs;  // the group path's buffer, reused
+        if (item < L.num_items) lp_chunk(L, item, wk, wk + kWarpPairs);
         return;  // chunked slots are applied by k_lp_hub_apply
     }
     b -= L.chunk_blocks;
