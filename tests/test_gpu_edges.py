@@ -1,0 +1,132 @@
+"""GPU edge cases against the oracle: degenerate graphs, extreme ids, zero weights, heavy
+multi-edges, partitions that own nothing, and the device limits' error behaviour."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import assert_attrs_match
+
+pytestmark = pytest.mark.gpu
+
+ALGOS = ["sssp", "pagerank", "cc", "lp"]
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2203_13005_b200.device import DeviceContext
+    c = DeviceContext(0)
+    yield c
+    c.shutdown()
+
+
+def run_both(ctx, oracle_lib, src, dst, w, algo, direction="auto", cap=None):
+    from paper_2203_13005_b200.device import DeviceGraph, DeviceState, run_state
+    src = np.asarray(src, np.uint32)
+    dst = np.asarray(dst, np.uint32)
+    wd = None if w is None else np.asarray(w, np.float64)
+    g = DeviceGraph(ctx, src, dst, wd if algo == "sssp" else None, csr=algo != "pagerank")
+    s = DeviceState(g, algo)
+    it, conv, hist = run_state(s, cap if algo != "pagerank" else (cap or 10), direction, keep_history=True)
+    ref = oracle_lib.OracleGraph(src, dst, wd).run(algo, max_iterations=cap if algo != "pagerank" else (cap or 10))
+    assert it == ref.iterations and conv == ref.converged
+    np.testing.assert_array_equal(g.ids().astype(np.uint64), np.unique(np.concatenate([src, dst])).astype(np.uint64))
+    assert_attrs_match(algo, s.read_attrs(), ref.attrs)
+    if algo != "pagerank":
+        assert [h["changed"] for h in hist] == ref.changed.tolist()
+    return g, s
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("direction", ["auto", "pull", "push"])
+def test_single_self_loop(ctx, oracle_lib, algo, direction):
+    if direction == "push" and algo == "pagerank":
+        pytest.skip("no push mode for PageRank")
+    run_both(ctx, oracle_lib, [7], [7], [3], algo, direction)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_extreme_ids(ctx, oracle_lib, algo):
+    """Ids at both ends of the u32 range (0xFFFFFFFF is the device's reserved sentinel)."""
+    big = 0xFFFFFFFE
+    src = [0, big, big - 1, 5, big, 0]
+    dst = [big, big - 1, 0, big, 5, 5]
+    run_both(ctx, oracle_lib, src, dst, [1, 2, 3, 4, 5, 6], algo)
+
+
+@pytest.mark.parametrize("algo", ["sssp", "cc", "lp"])
+def test_heavy_multi_edges(ctx, oracle_lib, algo):
+    """Parallel edges count once per edge in LP's multiset (ties to the smallest label)."""
+    rng = np.random.default_rng(5)
+    src = rng.integers(0, 40, 3000)
+    dst = rng.integers(0, 12, 3000)
+    w = rng.integers(0, 4, 3000)
+    run_both(ctx, oracle_lib, src, dst, w, algo)
+
+
+def test_zero_weights(ctx, oracle_lib):
+    src = np.arange(0, 50)
+    dst = np.arange(1, 51)
+    run_both(ctx, oracle_lib, src, dst, np.zeros(50), "sssp")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_hub_in_and_out(ctx, oracle_lib, algo):
+    """One destination with ~300 K in-edges (spans hundreds of tiles, LP hub tables and the
+    push hot-pair path) and one source with as many out-edges."""
+    rng = np.random.default_rng(6)
+    n = 300_000
+    src = np.concatenate([rng.integers(1, 5000, n), np.zeros(n, np.int64), rng.integers(0, 5000, 20_000)])
+    dst = np.concatenate([np.zeros(n, np.int64), rng.integers(1, 5000, n), rng.integers(0, 5000, 20_000)])
+    w = rng.integers(1, 63, src.size)
+    run_both(ctx, oracle_lib, src, dst, w, algo)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_more_partitions_than_vertices(oracle_lib, algo):
+    """Dealt partitioning of 3 vertices over 4 partitions: one partition owns only padding."""
+    from paper_2203_13005_b200.algorithms import make_algorithm
+    from paper_2203_13005_b200.engine import RunConfig, run
+    from paper_2203_13005_b200.graph import EdgeArrays
+    src = np.array([0, 1, 2, 2], np.uint32)
+    dst = np.array([1, 2, 0, 1], np.uint32)
+    w = np.array([1.0, 2.0, 3.0, 4.0])
+    ea = EdgeArrays(src, dst, w)
+    ids = ea.vertex_ids()
+    alg = make_algorithm(algo, [int(v) for v in ids], ea.out_degree())
+    cap = 10 if algo == "pagerank" else None
+    attrs, metrics = run(ea, alg, "bsp", RunConfig(partitions=4, block_size=2, max_iterations=cap,
+                                                   partitioning="edges", enable_skip=True))
+    ref = oracle_lib.OracleGraph(src, dst, w).run(algo, max_iterations=cap)
+    got = np.array([alg.row_from_attr(attrs[int(v)]) for v in ids], dtype=np.float64)
+    assert_attrs_match(algo, got, ref.attrs)
+    assert metrics.iterations == ref.iterations
+
+
+def test_device_limits_raise(ctx):
+    """Inputs the exact u32 device arithmetic cannot represent fail loudly (ValueError)."""
+    from paper_2203_13005_b200.device import DeviceGraph, DeviceState
+    with pytest.raises(ValueError):  # id 0xFFFFFFFF is the reserved sentinel
+        DeviceGraph(ctx, np.array([0xFFFFFFFF], np.uint32), np.array([1], np.uint32))
+    g = DeviceGraph(ctx, np.array([0, 1], np.uint32), np.array([1, 2], np.uint32),
+                    np.array([3.0e9, 1.0]))
+    with pytest.raises(ValueError):  # max_w * |V| >= 2^32 - 1: sums could saturate
+        DeviceState(g, "sssp")
+
+
+@pytest.mark.parametrize("algo", ["pagerank", "cc", "lp"])
+def test_empty_graph(ctx, oracle_lib, algo):
+    """No edges, no vertices: one round that converges (the oracle's / reference's loop)."""
+    run_both(ctx, oracle_lib, [], [], None, algo)
+
+
+def test_empty_graph_sssp(ctx):
+    from paper_2203_13005_b200.device import DeviceGraph, DeviceState, run_state
+    g = DeviceGraph(ctx, np.array([], np.uint32), np.array([], np.uint32), None)
+    try:
+        s = DeviceState(g, "sssp")
+    except ValueError:
+        return  # no source vertex to start from: refused loudly
+    it, conv, _ = run_state(s)
+    assert conv and s.read_attrs().shape[0] == 0
