@@ -763,10 +763,12 @@ __global__ void __launch_bounds__(kBlock) k_span_fold(const uint32_t* __restrict
     using Acc = typename Ops::Acc;
     constexpr uint32_t kLong = 16;
     const int lane = threadIdx.x & 31;
+    // lane l of warp w takes span w + l * nwarps: spans are in slot (= in-degree) order, so
+    // the long hub spans at the front land in different warps instead of queueing in one
     const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
-    for (uint64_t w = span_lo + (blockIdx.x * (uint64_t)kBlock + threadIdx.x) / 32 * 32; w < span_hi;
-         w += nwarps * 32) {
-        const uint64_t k = w + lane;
+    const uint64_t w = (blockIdx.x * (uint64_t)kBlock + threadIdx.x) / 32;
+    for (uint64_t base = span_lo; base < span_hi; base += 32 * nwarps) {
+        const uint64_t k = base + w + (uint64_t)lane * nwarps;
         const uint32_t n = k < span_hi ? span_count[k] : 0u;
         if (n < kLong && k < span_hi) {
             const uint64_t b = span_pbase[k];
@@ -778,7 +780,7 @@ __global__ void __launch_bounds__(kBlock) k_span_fold(const uint32_t* __restrict
         while (big) {
             const int src = __ffs(big) - 1;
             big &= big - 1;
-            const uint64_t kk = w + src;
+            const uint64_t kk = base + w + (uint64_t)src * nwarps;
             const uint32_t nn = __shfl_sync(kFull, n, src);
             const uint64_t b = span_pbase[kk];
             Acc tot = Ops::identity();
