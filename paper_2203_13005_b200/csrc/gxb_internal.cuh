@@ -268,10 +268,9 @@ __device__ __forceinline__ void cp_async_cg16(uint32_t saddr, const void* g, uin
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__device__ __forceinline__ uint32_t sat_add(uint32_t d, uint32_t w) {
-    const uint32_t s = d + w;
-    return (s < d || d == kInf32) ? kInf32 : s;
-}
+// d + w saturating at the inf sentinel, in two instructions: min(d, ~w) + w is d + w when
+// d + w <= 0xFFFFFFFF - 0 (never wraps) and exactly 0xFFFFFFFF otherwise (d = inf included)
+__device__ __forceinline__ uint32_t sat_add(uint32_t d, uint32_t w) { return min(d, ~w) + w; }
 
 inline unsigned grid_for(uint64_t n, int block = kBlock, uint64_t cap = 148ull * 64) {
     uint64_t g = (n + block - 1) / block;
