@@ -1194,8 +1194,9 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st, int chu
                           L.num_tiles * (uint64_t)kTileEdges + kTileEdges < (1ull << 32);
     if (options().tile_async && async_ok) {  // min-blocks from the option, or the measured best
         int av = options().tile_async_minblocks;
-        if (av == 0) av = sizeof(typename Ops::Raw) >= 16 ? 4 : sizeof(typename Ops::Raw) == 8 ? 6 : 8;
-        kern = (av == 8) ? k_tile_a<Pol, 8> : (av == 6) ? k_tile_a<Pol, 6> : (av == 4) ? k_tile_a<Pol, 4> : k_tile_a<Pol, 1>;
+        if (av == 0) av = sizeof(typename Ops::Raw) >= 16 ? 4 : sizeof(typename Ops::Raw) == 8 ? 6 : 5;
+        kern = (av == 8) ? k_tile_a<Pol, 8> : (av == 6) ? k_tile_a<Pol, 6> : (av == 5) ? k_tile_a<Pol, 5>
+             : (av == 4) ? k_tile_a<Pol, 4> : k_tile_a<Pol, 1>;
     }
     if (options().carveout >= 0)  // shared-memory carveout (% of max): the rest of the 256 KB is L1
         GXB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)options().carveout));

@@ -292,7 +292,7 @@ struct Options {
     int64_t pull_dense_div = 4;   // SSSP/CC pull skips the active bitmap when frontier out-edges * div >= |E|
     int64_t pull_kernel = 0;
     int64_t tile_async = 1;       // 1 = LDGSTS-gather tile kernel (k_tile_a), 0 = register gathers (k_tile_t)
-    int64_t tile_async_minblocks = 0;  // its min-blocks variant (0 = auto: 8 / 6 / 4 for 4 / 8 / 16-B values)      // 0 = warp tiles, 1 = degree-binned groups
+    int64_t tile_async_minblocks = 0;  // its min-blocks variant (0 = auto: 5 / 6 / 4 for 4 / 8 / 16-B values)      // 0 = warp tiles, 1 = degree-binned groups
     int64_t carveout = -1;        // tile kernel shared-memory carveout in % (-1 = driver default)
     int64_t exchange_chunks = 2;  // multi-GPU: exchange chunks (pipelined peer-write rounds; 2 measured best at N = 4)
     int64_t overlap_reserve_sms = 0;  // SMs left free while a chunked round computes (0 measured best)

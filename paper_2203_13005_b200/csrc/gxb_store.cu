@@ -923,8 +923,8 @@ int gxb_set_option(const char* name, int64_t value) {
         if (value != 0 && value != 1) return fail(GXB_EINVAL, "tile_async: 0 or 1");
         o.tile_async = value;
     } else if (n == "tile_async_minblocks") {
-        if (value != 0 && value != 1 && value != 4 && value != 6 && value != 8)
-            return fail(GXB_EINVAL, "tile_async_minblocks: 0 (auto) / 1 / 4 / 6 / 8");
+        if (value != 0 && value != 1 && value != 4 && value != 5 && value != 6 && value != 8)
+            return fail(GXB_EINVAL, "tile_async_minblocks: 0 (auto) / 1 / 4 / 5 / 6 / 8");
         o.tile_async_minblocks = value;
     } else if (n == "l1_hot_kb") {
         if (value < 0) return fail(GXB_EINVAL, "l1_hot_kb must be >= 0");
