@@ -144,6 +144,15 @@ def cpu_graph(algo, scale, over, seed=1):
     return _CPU_GRAPHS[key]
 
 
+def host_threads() -> int:
+    """Every host core this process may run on (torchrun sets OMP_NUM_THREADS=1 for its
+    ranks; the CPU baseline still uses the whole host)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def cpu_sample(algo, scale, over, iters, threads=0, seed=1):
     """Time the CPU restatement of run_reference (oracle/, OpenMP, all host threads)."""
     from oracle import oracle
@@ -162,16 +171,15 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     algo, scale, over, _, text = WORKLOADS[args.workload]
-    from oracle import oracle
-    threads = oracle.max_threads()
+    threads = host_threads()
     sample_scale = min(scale, args.cpu_scale)
     vals = []
     for _ in range(args.warmup):
-        cpu_sample(algo, sample_scale, over, 1)
+        cpu_sample(algo, sample_scale, over, 1, threads)
     t_total = 0.0
     edges = 0
     for _ in range(args.steps):
-        r = cpu_sample(algo, sample_scale, over, 1)
+        r = cpu_sample(algo, sample_scale, over, 1, threads)
         vals.append(r["gteps"])
         t_total += r["seconds"]
         edges += r["edges"]
@@ -277,6 +285,7 @@ def main():
     ap.add_argument("--workload", default="pr-s26", choices=sorted(WORKLOADS))
     ap.add_argument("--scale", type=int, default=None, help="override the R-MAT scale")
     ap.add_argument("--cpu-scale", type=int, default=22)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
@@ -488,10 +497,15 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            r = cpu_sample(algo, min(scale, args.cpu_scale), over, 1)
+            # a bounded sample of about args.cpu_seconds of CPU work: one timed iteration sizes it
+            cs = min(scale, args.cpu_scale)
+            r1 = cpu_sample(algo, cs, over, 1, host_threads())
+            iters = max(1, min(2000, int(args.cpu_seconds / max(r1["seconds"], 1e-6))))
+            r = cpu_sample(algo, cs, over, iters, host_threads())
             cpu = {"value": round(r["gteps"], 4), "unit": "GTEPS", "cores": r["threads"], "kind": "port",
-                   "sample": f"one {algo} iteration on R-MAT scale-{min(scale, args.cpu_scale)} "
-                             f"({r['edges']} edges, {r['seconds']:.2f} s), oracle/gx_oracle.c OpenMP restatement"}
+                   "sample": f"{r['iterations']} {algo} BSP iterations on R-MAT scale-{cs} "
+                             f"({r['edges']} edges, {r['seconds']:.1f} s), oracle/gx_oracle.c OpenMP "
+                             "restatement of run_reference on every host core"}
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": "GTEPS", "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
 
