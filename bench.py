@@ -357,6 +357,7 @@ def main():
     launches = 0
     step_ms = []
     units = 0
+    xbytes = 0
     clocks.wait_first()
     clocks.mark(True)
     t_wall = time.perf_counter()
@@ -367,6 +368,7 @@ def main():
         ev1.synchronize()
         step_ms.append(ev0.elapsed_time(ev1))
         units += rec.units
+        xbytes += rec.exchanged_bytes
         if rec.converged and algo != "pagerank":
             launches += run.state.profile()["kernels_launched"]
             run = new_run()
@@ -525,6 +527,13 @@ def main():
             "clocks": clocks.summary(), "wall_s": round(t_wall, 3),
             "skipped_rounds": skipped_rounds,
         }
+        if world > 1:  # mirror-exchange bytes each GPU receives per round, against NVLink 5
+            per = xbytes / max(1, args.steps)
+            line["exchange"] = {
+                "bytes_per_gpu_per_step": int(per), "gbs_per_gpu": round(per / (ms_per_step * 1e-3) / 1e9, 1),
+                "link_peak_gbs": 900, "peer_writes": bool(getattr(run, "_peers", False)),
+                "mechanism": "Apply stores into IPC-mapped peer replicas over NVLink (pipelined chunks)"
+                if getattr(run, "_peers", False) else "NCCL in-place all-gather"}
         if secondary:
             line["secondary"] = secondary
         emit(line)
