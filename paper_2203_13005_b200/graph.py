@@ -119,3 +119,59 @@ class EdgeArrays:
         cnt = np.zeros(ids.size, dtype=np.int64)
         np.add.at(cnt, np.searchsorted(ids, self.src), 1)
         return {int(v): int(c) for v, c in zip(ids, cnt)}
+
+
+# ---- binary edge format (ingest at scale without the text path) ----
+#
+# Layout (little endian): 32-byte header  b"GXEDGE01" | u64 num_edges | u32 flags | u32 0,
+# then src u32[E], dst u32[E] and, when flags & 1, weights f64[E]. The arrays are read as
+# memory maps, so a 1 G-edge file feeds DeviceGraph (which copies host arrays once to HBM)
+# without a per-edge Python object (the text loader costs ~190 B and ~5 µs per edge).
+EDGE_MAGIC = b"GXEDGE01"
+_HEADER = np.dtype([("magic", "S8"), ("num_edges", "<u8"), ("flags", "<u4"), ("pad", "<u4"),
+                    ("reserved", "<u8")])
+
+
+def write_edge_binary(path, edges: "EdgeArrays") -> None:
+    """Write an EdgeArrays in the binary edge format."""
+    h = np.zeros(1, dtype=_HEADER)
+    h["magic"] = EDGE_MAGIC
+    h["num_edges"] = len(edges)
+    h["flags"] = 1 if edges.weight is not None else 0
+    with open(path, "wb") as fh:
+        fh.write(h.tobytes())
+        fh.write(np.ascontiguousarray(edges.src, dtype="<u4").tobytes())
+        fh.write(np.ascontiguousarray(edges.dst, dtype="<u4").tobytes())
+        if edges.weight is not None:
+            fh.write(np.ascontiguousarray(edges.weight, dtype="<f8").tobytes())
+
+
+def read_edge_binary(path) -> "EdgeArrays":
+    """Read the binary edge format (memory-mapped columns); raises GraphParseError (line 0)
+    for a malformed file."""
+    import os
+    size = os.path.getsize(path)
+    if size < _HEADER.itemsize:
+        raise GraphParseError(0, "binary edge file shorter than its header")
+    h = np.fromfile(path, dtype=_HEADER, count=1)[0]
+    if bytes(h["magic"]) != EDGE_MAGIC:
+        raise GraphParseError(0, "not a GXEDGE01 binary edge file")
+    n, weighted = int(h["num_edges"]), bool(int(h["flags"]) & 1)
+    need = _HEADER.itemsize + 8 * n + (8 * n if weighted else 0)
+    if size != need:
+        raise GraphParseError(0, f"binary edge file has {size} bytes, expected {need} for {n} edges")
+    off = _HEADER.itemsize
+    src = np.memmap(path, dtype="<u4", mode="r", offset=off, shape=(n,)) if n else np.empty(0, np.uint32)
+    dst = np.memmap(path, dtype="<u4", mode="r", offset=off + 4 * n, shape=(n,)) if n else np.empty(0, np.uint32)
+    w = None
+    if weighted:
+        w = np.memmap(path, dtype="<f8", mode="r", offset=off + 8 * n, shape=(n,)) if n else np.empty(0)
+    return EdgeArrays(src, dst, w)
+
+
+def edge_list_to_binary(text_path, bin_path) -> int:
+    """Convert a reference text edge list (load_edge_list rules) to the binary format."""
+    _, edges = load_edge_list(text_path)
+    ea = EdgeArrays.from_edges(edges)
+    write_edge_binary(bin_path, ea)
+    return len(ea)

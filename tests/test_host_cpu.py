@@ -64,6 +64,38 @@ def test_load_edge_list_matches_reference(tmp_path):
             assert str(exc.value) == case["message"], name
 
 
+def test_binary_edge_format_round_trip(tmp_path):
+    """Binary ingest (GXEDGE01) == the reference text loader on every golden edge list."""
+    from paper_2203_13005_b200.graph import edge_list_to_binary, read_edge_binary, write_edge_binary
+    with open(os.path.join(GOLDEN, "edge_lists.json")) as fh:
+        cases = json.load(fh)
+    for name, case in cases.items():
+        if not case["ok"]:
+            continue
+        t = tmp_path / f"{name}.txt"
+        t.write_bytes(case["text"].encode("ascii"))
+        b = tmp_path / f"{name}.gxe"
+        n = edge_list_to_binary(t, b)
+        ea = read_edge_binary(b)
+        assert n == len(ea) == len(case["edges"])
+        assert [[int(s), int(d)] for s, d in zip(ea.src, ea.dst)] == [[e[0], e[1]] for e in case["edges"]]
+        ws = [e[2] for e in case["edges"]]
+        if ea.weight is None:
+            assert all(w == 1.0 for w in ws)
+        else:
+            assert ea.weight.tolist() == ws
+    rng = np.random.default_rng(1)
+    big = EdgeArrays(rng.integers(0, 1 << 31, 100_000), rng.integers(0, 1 << 31, 100_000),
+                     rng.integers(1, 64, 100_000).astype(np.float64))
+    write_edge_binary(tmp_path / "big.gxe", big)
+    back = read_edge_binary(tmp_path / "big.gxe")
+    assert np.array_equal(back.src, big.src) and np.array_equal(back.dst, big.dst)
+    assert np.array_equal(back.weight, big.weight)
+    (tmp_path / "bad.gxe").write_bytes(b"GXEDGE01" + b"\0" * 30)
+    with pytest.raises(GraphParseError):
+        read_edge_binary(tmp_path / "bad.gxe")
+
+
 def test_edge_arrays():
     ea = EdgeArrays.from_edges([(5, 7), (7, 5, 2.0), (5, 5)])
     assert ea.vertex_ids().tolist() == [5, 7]
