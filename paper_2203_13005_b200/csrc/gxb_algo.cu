@@ -3,24 +3,26 @@
 //
 // Fused path (gxb_iterate): one pull pass over the owned CSC computes, for each
 // destination slot, Gen (the per-edge message, A/algorithms.py:102-105,
-// 147-149) folded with Merge (A/algorithms.py:107-108, 151-152) and finishes
-// with Apply (A/algorithms.py:113-115, 157-159) plus change detection, the
+// 147-149) folded with Merge (A/algorithms.py:107-108, 151-152); Apply
+// (A/algorithms.py:113-115, 157-159) follows with change detection, the
 // next-frontier bitmap/list and the vote statistics (A/agent.py:404-417,
-// A/algorithms.py:327-341). Destinations are degree-binned (slots are sorted
-// by in-degree, so every bin is a contiguous range): groups of 1..32 lanes per
-// destination, and above kChunkMinDeg one warp per kChunkEdges-edge chunk with
-// the chunks of a hub combined by the last-arriving warp (deterministic order).
+// A/algorithms.py:327-341). The merge is edge-balanced: every warp owns a fixed
+// 256-edge tile of the CSC (k_tile_a: gathers as LDGSTS copies into shared memory;
+// k_tile_t: register gathers), runs crossing tiles leave per-tile partials that
+// k_span_fold combines in tile order (deterministic PageRank rounding).
 //
-// SSSP and CC also have a push pass over the CSR for sparse frontiers
-// (SURVEY.md §8(f) row 3): atomicMin into the next-value array plus a touched
-// bitmap; synchronous BSP semantics are kept because every message is built
-// from the frozen current values (A/algorithms.py:319-325).
+// SSSP, CC and LP also have a push pass over the CSR for sparse frontiers
+// (SURVEY.md §8(f) row 3), edge-balanced over the concatenated frontier rows:
+// atomicMin into the next-value array plus a touched bitmap (LP: a (destination,
+// label) pair table, gxb_lp.cu); synchronous BSP semantics are kept because every
+// message is built from the frozen current values (A/algorithms.py:319-325).
 //
 // Request path (gxb_request): GEN materialises one message per CSC edge
-// (coalesced, edge-parallel), MERGE folds them per destination with the same
-// binned segmented reduction, APPLY runs the vertex update — the reference's
-// execute_request over a WorkItem (A/daemon.py:86-130) with range descriptors
-// instead of Python triplet blocks.
+// (coalesced, edge-parallel), MERGE folds them per destination with a
+// degree-binned segmented reduction (groups of 1..32 lanes per destination, warp
+// chunks for hubs combined by the last-arriving warp), APPLY runs the vertex
+// update — the reference's execute_request over a WorkItem (A/daemon.py:86-130)
+// with range descriptors instead of Python triplet blocks.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -453,14 +455,14 @@ __global__ void __launch_bounds__(kBlock) k_pull(const Pol p, const PullLaunch L
 // ======================================================================
 // the edge-balanced pull merge ("warp tiles", merge-path style)
 //
-// Warp w owns CSC edges [kTileEdges * t, kTileEdges * (t + 1)); lane l owns
-// kTileK consecutive edges of it. A lane loads its source indices with two
-// 16-byte vector loads, issues kTileK independent gathers (Gen), and folds runs
-// of equal destination (Merge) using the offsets of at most kTileK + 1 slots.
-// Runs crossing lanes are combined by a segmented warp scan keyed by slot (the
-// keys are monotone); runs crossing tiles ("spans") publish a per-tile partial
-// and the last-arriving tile folds the partials in tile order, so the fold
-// order — and therefore the PageRank rounding — is deterministic.
+// Warp w owns tile t = 256 consecutive CSC edges (tiles restart at exchange-chunk
+// boundaries); lane l gathers edges 32 j + l (one instruction covers 32 consecutive
+// edges), the values are transposed through shared memory so lane l then folds the
+// kTileK consecutive edges 8 l .. 8 l + 7 (Merge), cutting runs at the precomputed
+// segment-end mask. Runs crossing lanes are combined by a segmented warp scan keyed
+// by slot (the keys are monotone); runs crossing tiles ("spans") write a per-tile
+// partial that k_span_fold folds in tile order, so the fold order — and therefore
+// the PageRank rounding — is deterministic.
 // ======================================================================
 
 struct TileLaunch {
@@ -481,7 +483,6 @@ struct TileLaunch {
     const uint32_t* span_count;
     const uint64_t* span_pbase;
     const uint32_t* span_slot;
-    uint32_t* span_arrive;
     void* partials;
     void* sums;   // per relative slot: folded accumulator
 };
@@ -1161,7 +1162,6 @@ TileLaunch tile_launch(gxb_state* s) {
     L.span_count = T.d_span_count;
     L.span_pbase = T.d_span_pbase;
     L.span_slot = T.d_span_slot;
-    L.span_arrive = T.d_span_arrive;
     L.partials = s->d_tile_partials;
     L.sums = s->d_sums;
     return L;

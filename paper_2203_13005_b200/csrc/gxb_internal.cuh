@@ -70,7 +70,6 @@ struct TilePlan {
     uint32_t* d_span_count = nullptr;  // per span: tiles touched
     uint64_t* d_span_pbase = nullptr;  // per span: first partial index
     uint32_t* d_span_slot = nullptr;   // per span: relative slot
-    uint32_t* d_span_arrive = nullptr; // per span: arrival counter (reset by the last arriver)
 };
 
 struct DeviceBuffer {

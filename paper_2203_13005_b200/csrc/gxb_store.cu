@@ -366,7 +366,6 @@ static void graph_release(gxb_graph* g) {
     dfree(g->tiles.d_span_count);
     dfree(g->tiles.d_span_pbase);
     dfree(g->tiles.d_span_slot);
-    dfree(g->tiles.d_span_arrive);
 }
 
 // warp-tile plan of the edge-balanced pull merge: kTileEdges edges per warp;
@@ -457,8 +456,6 @@ static int build_tile_plan(gxb_graph* g, cudaStream_t st) {
     if (nchunks)
         k_lane_slot<<<grid_e(nchunks), kBlock, 0, st>>>(g->d_in_off, nz, T.d_tile_start, nchunks, T.d_lane_slot,
                                                          T.d_lane_mask);
-    GXB_CHECK(dalloc_t(&T.d_span_arrive, T.num_spans + 1));
-    GXB_CUDA(cudaMemsetAsync(T.d_span_arrive, 0, 4 * (T.num_spans + 1), st));
     GXB_CUDA(cudaStreamSynchronize(st));
     return GXB_OK;
 }
