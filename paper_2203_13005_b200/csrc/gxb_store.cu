@@ -34,6 +34,7 @@ Options& options() {
         if (const char* e = getenv("GXB_PULL_KERNEL")) o.pull_kernel = std::string(e) == "binned" ? 1 : 0;
         if (const char* e = getenv("GXB_PR_MESSAGE_BITS")) o.pr_message_bits = atol(e) == 32 ? 32 : 64;
         if (const char* e = getenv("GXB_TILE_ASYNC")) o.tile_async = atol(e) ? 1 : 0;
+        if (const char* e = getenv("GXB_XCHUNK_POWER")) o.xchunk_power = std::min(4L, std::max(1L, atol(e)));
         if (const char* e = getenv("GXB_EXCHANGE_CHUNKS")) o.exchange_chunks = std::min(64L, std::max(1L, atol(e)));
         if (const char* e = getenv("GXB_OVERLAP_RESERVE_SMS")) o.overlap_reserve_sms = std::min(140L, std::max(0L, atol(e)));
     }
@@ -370,8 +371,16 @@ static void graph_release(gxb_graph* g) {
 
 // warp-tile plan of the edge-balanced pull merge: kTileEdges edges per warp;
 // slots crossing a tile boundary ("spans") combine per-tile partials
+// slot bound of exchange chunk k of K: owned * (k / K)^p (p = option xchunk_power, 1..4).
+// Slots are in-degree sorted, so the first chunk is the short hub-heavy one; a pipelined
+// round runs chunks hubs-last and only the last chunk's Apply is left exposed.
 uint64_t xchunk_bound(uint64_t owned, int k, int K) {
-    return owned * (uint64_t)k * (uint64_t)k / ((uint64_t)K * (uint64_t)K);  // exact: peers recompute it
+    uint64_t num = 1, den = 1;
+    for (int i = 0; i < options().xchunk_power; ++i) {
+        num *= (uint64_t)k;
+        den *= (uint64_t)K;
+    }
+    return (uint64_t)((unsigned __int128)owned * num / den);  // exact: peers recompute it
 }
 
 static int build_tile_plan(gxb_graph* g, cudaStream_t st) {
@@ -916,6 +925,9 @@ int gxb_set_option(const char* name, int64_t value) {
     } else if (n == "pull_dense_div") {
         if (value < 0) return fail(GXB_EINVAL, "pull_dense_div must be >= 0 (0 = always test active bits)");
         o.pull_dense_div = value;
+    } else if (n == "xchunk_power") {
+        if (value < 1 || value > 4) return fail(GXB_EINVAL, "xchunk_power: 1..4");
+        o.xchunk_power = value;
     } else if (n == "tile_async") {
         if (value != 0 && value != 1) return fail(GXB_EINVAL, "tile_async: 0 or 1");
         o.tile_async = value;
@@ -957,6 +969,7 @@ int gxb_get_option(const char* name, int64_t* value) {
     else if (n == "pull_kernel") *value = o.pull_kernel;
     else if (n == "pull_dense_div") *value = o.pull_dense_div;
     else if (n == "tile_async") *value = o.tile_async;
+    else if (n == "xchunk_power") *value = o.xchunk_power;
     else if (n == "tile_async_minblocks") *value = o.tile_async_minblocks;
     else if (n == "pr_message_bits") *value = o.pr_message_bits;
     else if (n == "carveout") *value = o.carveout;

@@ -280,8 +280,9 @@ class PartitionedRun:
     def _chunk_ranges(self, q: int, k: int, K: int) -> tuple[int, int]:
         lo, hi = int(self.bounds[q]), int(self.bounds[q + 1])
         owned = hi - lo
-        b0 = owned * k * k // (K * K)   # xchunk_bound (csrc/gxb_store.cu)
-        b1 = owned * (k + 1) * (k + 1) // (K * K)
+        pw = L.get_option("xchunk_power") if hasattr(L, "get_option") else 2   # xchunk_bound (csrc/gxb_store.cu)
+        b0 = owned * k ** pw // K ** pw
+        b1 = owned * (k + 1) ** pw // K ** pw
         return lo + b0, lo + b1
 
     def _overlapped_pagerank_round(self):
