@@ -202,6 +202,10 @@ int gxb_request(gxb_state* s, int op, uint64_t lo, uint64_t hi, void* stream);
 int gxb_commit(gxb_state* s, void* stream);
 
 int gxb_stats(gxb_state* s, void* stream, gxb_iter_stats* out);
+/* the last closed round's vote block written on the device, no host synchronisation:
+ * d_out[0..4] = changed, next_active, next_units, remote_active, max_stat (doubles) —
+ * what the sync round all-gathers (A/engine.py:267-285) */
+int gxb_stats_device(gxb_state* s, double* d_out, void* stream);
 
 /* ---- mirror exchange (A/engine.py:242-266) ----
  * Multi-partition runs keep a full-length replica of every source value. After

@@ -120,6 +120,7 @@ def _sig(L):
         "gxb_write_attrs": (I, [P, P, P]),
         "gxb_attrs_h2d": (I, [P, P, I, P]),
         "gxb_attrs_scope": (I, [P, I]),
+        "gxb_stats_device": (I, [P, P, P]),
         "gxb_exchange_ipc_handle": (I, [P, I, P]),
         "gxb_exchange_open_peers": (I, [P, I, P]),
         "gxb_exchange_set_peer_ptrs": (I, [P, I, P]),

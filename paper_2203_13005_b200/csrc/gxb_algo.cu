@@ -1924,6 +1924,46 @@ int gxb_commit(gxb_state* s, void* stream) {
     return end_round(s, GXB_DIR_PULL, (cudaStream_t)stream);
 }
 
+}  // extern "C"
+
+// the closed round's vote block from the device stripes: changed, next_active, next_units,
+// remote_active, max_stat as doubles (counts are exact below 2^53); PageRank's constant
+// counters come from the host (every vertex stays active)
+__global__ void k_vote_block(const StatStripe* __restrict__ st, double* out, int pagerank,
+                             unsigned long long pr_active, unsigned long long pr_units,
+                             unsigned long long pr_remote) {
+    const int lane = threadIdx.x;
+    const StatStripe t = st[lane];
+    unsigned long long c[4] = {t.changed, t.next_active, t.next_units, t.remote_active};
+    unsigned long long m = t.max_stat_bits;
+    for (int o = 16; o > 0; o >>= 1) {
+        for (int i = 0; i < 4; ++i) c[i] += __shfl_xor_sync(kFull, c[i], o);
+        const unsigned long long q = __shfl_xor_sync(kFull, m, o);
+        m = q > m ? q : m;
+    }
+    if (lane == 0) {
+        if (pagerank) {
+            c[1] = pr_active;
+            c[2] = pr_units;
+            c[3] = pr_remote;
+        }
+        for (int i = 0; i < 4; ++i) out[i] = (double)c[i];
+        out[4] = __longlong_as_double((long long)m);
+    }
+}
+
+extern "C" {
+
+int gxb_stats_device(gxb_state* s, double* d_out, void* stream) {
+    if (!s || !d_out) return fail(GXB_EINVAL, "gxb_stats_device: null argument");
+    if (s->in_round) return fail(GXB_ESTATE, "gxb_stats_device: a round is open");
+    const bool pr = s->algo == GXB_ALGO_PAGERANK;
+    k_vote_block<<<1, 32, 0, (cudaStream_t)stream>>>(s->d_stats, d_out, pr ? 1 : 0, s->g->hi - s->g->lo,
+                                                     s->owned_outdeg_sum, s->last.remote_active);
+    GXB_CUDA(cudaGetLastError());
+    return GXB_OK;
+}
+
 int gxb_stats(gxb_state* s, void* stream, gxb_iter_stats* out) {
     if (!s || !out) return fail(GXB_EINVAL, "gxb_stats: null argument");
     (void)stream;

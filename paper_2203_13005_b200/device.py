@@ -260,6 +260,11 @@ class DeviceState:
         L.check(L.lib().gxb_stats(self._h, _stream_ptr(stream), ctypes.byref(st)))
         return st.as_dict()
 
+    def stats_device(self, out, stream=None):
+        """Write the closed round's vote block (changed, next_active, next_units, remote_active,
+        max_stat; float64) into a device tensor without a host synchronisation."""
+        L.check(L.lib().gxb_stats_device(self._h, _vp(out), _stream_ptr(stream)))
+
     def read_attrs(self, owned_only: bool = False, stream=None) -> np.ndarray:
         V = self.graph.num_vertices
         out = np.empty((V, self.arity), dtype=np.float64)

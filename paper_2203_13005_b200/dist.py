@@ -81,6 +81,13 @@ class Collective:
         self.dist.all_gather_into_tensor(out, mine, group=self.group)
         return out
 
+    def vote_start_device(self, mine):
+        """The vote from a device-resident block (gxb_stats_device): no host round trip."""
+        import torch
+        out = torch.empty(self.world * mine.numel(), dtype=torch.float64, device=mine.device)
+        self.dist.all_gather_into_tensor(out, mine, group=self.group)
+        return out
+
     def vote_finish(self, handle) -> tuple[list[int], float]:
         """SUM of the counters (exact below 2^53) and MAX of the statistic over ranks."""
         if isinstance(handle, tuple):
@@ -330,11 +337,21 @@ class PartitionedRun:
             moved_early = self._overlapped_pagerank_round()
         else:
             self.state.iterate(direction)
-        st = self.state.stats()
+        if self.comm.world > 1 and hasattr(self.state, "stats_device") and hasattr(self.comm, "vote_start_device"):
+            # the vote block goes from device stripes straight into the all-gather; the host
+            # reads the round's statistics after the collective (one synchronisation per round)
+            import torch
+            if getattr(self, "_vote_buf", None) is None:
+                self._vote_buf = torch.empty(5, dtype=torch.float64, device=self.device)
+            self.state.stats_device(self._vote_buf)
+            handle = self.comm.vote_start_device(self._vote_buf)
+            st = None
+        else:
+            st = self.state.stats()
+            handle = self.comm.vote_start(
+                [st["changed"], st["next_active"], st["next_units"], st["remote_active"]], st["max_stat"],
+                self.device)
         t0 = self._tick("compute", t0)
-        handle = self.comm.vote_start(
-            [st["changed"], st["next_active"], st["next_units"], st["remote_active"]], st["max_stat"],
-            self.device)
         moved = moved_early
         early = overlapped
         if peers:  # the round's Apply already stored every owned contribution in every replica
@@ -349,6 +366,8 @@ class PartitionedRun:
             if early:
                 moved = self._exchange_dense()
         counts, max_stat = self.comm.vote_finish(handle)
+        if st is None:
+            st = self.state.stats()  # the round is complete: no wait
         t0 = self._tick("vote", t0)
         changed, next_active, next_units, remote_active = counts
         if self.algo == "pagerank":
