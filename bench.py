@@ -337,7 +337,7 @@ def main():
 
     def new_run():
         st = DeviceState(graph, algo)
-        return PartitionedRun(st, bounds, comm, enable_skip=True, device=dev)
+        return PartitionedRun(st, bounds, comm, enable_skip=True, device=dev).prepare()
 
     # ---- device-timed steps ----
     clocks = ClockSampler(local).__enter__()
@@ -437,7 +437,7 @@ def main():
         st.attrs_d2h(host_in[0], 0, stream)
         torch.cuda.synchronize()
         host_in[1].copy_(host_in[0])
-        e2e_run = PartitionedRun(st, bounds, comm, enable_skip=True, device=dev)
+        e2e_run = PartitionedRun(st, bounds, comm, enable_skip=True, device=dev).prepare()
         copy = torch.cuda.Stream(dev)       # host -> device
         copy_out = torch.cuda.Stream(dev)   # device -> host (the link is full duplex)
         ev = lambda: torch.cuda.Event()  # noqa: E731

@@ -236,6 +236,11 @@ class PartitionedRun:
             return self.state.view(ptr, nbytes, dtype)
         return device_view(ptr, nbytes, dtype)
 
+    def prepare(self):
+        """One-time setup outside any timed region (maps the peers' replicas)."""
+        self._setup_peers()
+        return self
+
     def _setup_peers(self) -> bool:
         """Map every peer's contribution buffers (CUDA IPC handles, all-gathered once) so
         PageRank's Apply writes the mirrors itself; all ranks must agree or none uses it."""
