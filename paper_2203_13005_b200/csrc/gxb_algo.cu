@@ -1378,6 +1378,7 @@ int end_round(gxb_state* s, int direction, cudaStream_t st) {
     s->stats_pending = true;
     s->in_round = false;
     s->iteration++;
+    s->lab_injective = false;
     s->last_direction = direction;
     return GXB_OK;
 }
@@ -1570,6 +1571,7 @@ int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, 
     } else {
         // LP / CC: label = vertex id, every vertex active (A/algorithms.py:179-183)
         s->arity = 1;
+        s->lab_injective = true;
         if ((rc = dalloc_t(&s->d_lab_cur, V)) != GXB_OK) return bail(rc);
         if ((rc = dalloc_t(&s->d_lab_next, V)) != GXB_OK) return bail(rc);
         if (V) {
@@ -2000,6 +2002,7 @@ int gxb_write_attrs(gxb_state* s, const double* host_in, void* stream) {
     if (!V) return GXB_OK;
     if (!host_in) return fail(GXB_EINVAL, "gxb_write_attrs: null input");
     cudaStream_t st = (cudaStream_t)stream;
+    s->lab_injective = false;  // installed labels need not be distinct
     GXB_CHECK(collect_stats(s));
     GXB_CHECK(stage(s));
     GXB_CUDA(cudaMemcpyAsync(s->d_stage, host_in, 8 * V * s->arity, cudaMemcpyHostToDevice, st));
@@ -2068,6 +2071,7 @@ int gxb_attrs_h2d(gxb_state* s, const double* host_in, int buf, void* stream) {
 int gxb_attrs_install(gxb_state* s, int buf, void* stream) {
     if (!s || buf < 0 || buf > 1) return fail(GXB_EINVAL, "gxb_attrs_install: bad argument");
     if (s->in_round) return fail(GXB_ESTATE, "gxb_attrs_install: a round is open");
+    s->lab_injective = false;
     GXB_CHECK(stage_pair(s));
     gxb_graph* g = s->g;
     const uint32_t* d2s;

@@ -90,6 +90,7 @@ struct LpLaunch {
     uint64_t bin_lo[kNumGroupBins], bin_hi[kNumGroupBins];
     unsigned bin_blocks[kNumGroupBins];
     LpHub hub;
+    bool injective;  // labels are distinct (round 1): hub counts are edge multiplicities
 };
 
 __device__ __forceinline__ void lp_finish(const LpLaunch& L, uint32_t slot, unsigned long long best, LocalStats& st) {
@@ -206,6 +207,47 @@ __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint3
         if (wkeys[i] != kEmpty) hub_add(L, rel, base, mask, wkeys[i], wcnts[i]);
 }
 
+// Round 1 (labels = distinct vertex ids): a label's count at a hub is the multiplicity of
+// one source, and the CSC keeps a hub's sources sorted, so counting is run-length over the
+// chunk — no hash table, no atomics per edge. A run belongs to the chunk / lane where it
+// starts: a lane skips a leading run that continues from the previous edge and extends its
+// last run past its range (and past the chunk end) until the source changes.
+__device__ __forceinline__ void lp_chunk_injective(const LpLaunch& L, uint64_t item) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t rel = __ldg(L.item_slot + item);
+    const uint64_t seg_beg = __ldg(L.in_off + rel), seg_end = __ldg(L.in_off + rel + 1);
+    const uint64_t beg = __ldg(L.item_begin + item);
+    const uint64_t end = min(beg + (uint64_t)kChunkEdges, seg_end);
+    constexpr uint32_t kPer = kChunkEdges / 32;
+    uint64_t e = beg + (uint64_t)lane * kPer;
+    const uint64_t stop = min(e + kPer, end);
+    unsigned long long best = 0ull;
+    if (e < stop) {
+        if (e > seg_beg) {  // a run continuing from the previous edge is counted where it starts
+            const uint32_t prev = __ldg(L.in_src + e - 1);
+            while (e < stop && __ldg(L.in_src + e) == prev) ++e;
+        }
+        while (e < stop) {
+            const uint32_t s = __ldg(L.in_src + e);
+            uint32_t c = 0;
+            while (e < seg_end && __ldg(L.in_src + e) == s) {
+                ++c;
+                ++e;
+            }
+            if (bit_test(L.active_cur, s)) {
+                const uint32_t lab = __ldg(L.lab_cur + s);
+                const unsigned long long pk = ((unsigned long long)c << 32) | (unsigned long long)(~lab);
+                best = pk > best ? pk : best;
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long q = __shfl_xor_sync(kFull, best, o);
+        best = q > best ? q : best;
+    }
+    if (lane == 0 && best && best > __ldcg(L.hub.best + rel)) atomicMax(L.hub.best + rel, best);
+}
+
 __global__ void __launch_bounds__(kBlock) k_lp_pull(const LpLaunch L) {
     // group path: 4 labels per thread; chunk path: a (label, count) table per warp
     __shared__ uint32_t buf[4 * kBlock > 2 * kWarpPairs * (kBlock / 32) ? 4 * kBlock : 2 * kWarpPairs * (kBlock / 32)];
@@ -214,7 +256,10 @@ __global__ void __launch_bounds__(kBlock) k_lp_pull(const LpLaunch L) {
     if (b < L.chunk_blocks) {
         const uint64_t item = (uint64_t)b * (kBlock / 32) + (threadIdx.x >> 5);
         uint32_t* wk = buf + (threadIdx.x >> 5) * 2 * kWarpPairs;  // the group path's buffer, reused
-        if (item < L.num_items) lp_chunk(L, item, wk, wk + kWarpPairs);
+        if (item < L.num_items) {
+            if (L.injective) lp_chunk_injective(L, item);
+            else lp_chunk(L, item, wk, wk + kWarpPairs);
+        }
         return;  // chunked slots are applied by k_lp_hub_apply
     }
     b -= L.chunk_blocks;
@@ -553,12 +598,16 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
         prev = L.bin_hi[k];
     }
     L.hub = S->hub;
+    L.injective = s->lab_injective;
     if (grid) k_lp_pull<<<grid, kBlock, 0, st>>>(L);
     if (S->chunk_end) {
         k_lp_hub_apply<<<grid_for(S->chunk_end), kBlock, 0, st>>>(L, S->chunk_end);
-        // empty the tables for the next round (plain memsets: no read-back of the tables)
-        GXB_CUDA(cudaMemsetAsync(S->hub.keys, 0xFF, 4 * S->hub.entries, st));
-        GXB_CUDA(cudaMemsetAsync(S->hub.counts, 0, 4 * S->hub.entries, st));
+        // empty the tables for the next round (plain memsets: no read-back of the tables);
+        // a run-length round leaves them untouched
+        if (!L.injective) {
+            GXB_CUDA(cudaMemsetAsync(S->hub.keys, 0xFF, 4 * S->hub.entries, st));
+            GXB_CUDA(cudaMemsetAsync(S->hub.counts, 0, 4 * S->hub.entries, st));
+        }
     }
     GXB_CUDA(cudaGetLastError());
     return GXB_OK;

@@ -214,6 +214,7 @@ struct gxb_state {
     int round_chunks = 0;   // exchange chunks launched in the open round
     cudaStream_t aux_stream = nullptr;  // pipelined rounds: span folds + Apply beside the tiles
     cudaEvent_t ev_tile = nullptr, ev_join = nullptr;
+    bool lab_injective = false;  // LP: labels are still the distinct vertex ids (before round 1)
     int attrs_scope = 0;                          // async staging: 0 = every vertex, 1 = owned vertices
     uint64_t stage_n = 0;                         // vertices per staging buffer (allocated)
     double* d_stage_in[2] = {nullptr, nullptr};   // async path: double-buffered
