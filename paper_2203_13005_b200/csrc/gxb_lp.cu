@@ -148,7 +148,7 @@ __device__ __forceinline__ void lp_group(const LpLaunch& L, int k, unsigned b, u
 // (overflow goes straight to it). Each global update also raises the hub's running packed
 // argmax (a label's (count, ~label) only grows, so the max over all updates is the max over
 // the final counts).
-constexpr int kWarpPairs = 128;
+constexpr int kWarpPairs = 256;
 
 __device__ __forceinline__ void hub_add(const LpLaunch& L, uint64_t rel, uint64_t base, uint32_t mask, uint32_t lab,
                                         uint32_t c) {
@@ -157,7 +157,8 @@ __device__ __forceinline__ void hub_add(const LpLaunch& L, uint64_t rel, uint64_
     if (pk > __ldcg(L.hub.best + rel)) atomicMax(L.hub.best + rel, pk);
 }
 
-__device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint32_t* wkeys, uint32_t* wcnts) {
+__device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint32_t* wkeys, uint32_t* wcnts,
+                                         uint32_t* wfull) {
     const int lane = threadIdx.x & 31;
     const uint32_t rel = __ldg(L.item_slot + item);
     const uint64_t beg = __ldg(L.item_begin + item);
@@ -168,6 +169,7 @@ __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint3
         wkeys[i] = kEmpty;
         wcnts[i] = 0;
     }
+    if (lane == 0) *wfull = 0u;
     __syncwarp();
     constexpr int kB = 8;  // the loads of 8 steps are issued together
     for (uint64_t e0 = beg; e0 < end; e0 += 32 * kB) {
@@ -189,8 +191,10 @@ __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint3
             if (ok[j] && lane == __ffs(m) - 1) {
                 uint32_t h = mix32(lab[j]) & (kWarpPairs - 1);
                 bool done = false;
+                // once a probe sequence has failed the table is crowded: look at the home slot only
+                const int probes = *reinterpret_cast<volatile uint32_t*>(wfull) ? 1 : 8;
 #pragma unroll 1
-                for (int probe = 0; probe < 8 && !done; ++probe) {
+                for (int probe = 0; probe < probes && !done; ++probe) {
                     const uint32_t k = atomicCAS(wkeys + h, kEmpty, lab[j]);
                     if (k == kEmpty || k == lab[j]) {
                         atomicAdd(wcnts + h, (uint32_t)__popc(m));
@@ -198,7 +202,10 @@ __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint3
                     }
                     h = (h + 1) & (kWarpPairs - 1);
                 }
-                if (!done) hub_add(L, rel, base, mask, lab[j], __popc(m));
+                if (!done) {
+                    *reinterpret_cast<volatile uint32_t*>(wfull) = 1u;
+                    hub_add(L, rel, base, mask, lab[j], __popc(m));
+                }
             }
         }
     }
@@ -251,6 +258,7 @@ __device__ __forceinline__ void lp_chunk_injective(const LpLaunch& L, uint64_t i
 __global__ void __launch_bounds__(kBlock) k_lp_pull(const LpLaunch L) {
     // group path: 4 labels per thread; chunk path: a (label, count) table per warp
     __shared__ uint32_t buf[4 * kBlock > 2 * kWarpPairs * (kBlock / 32) ? 4 * kBlock : 2 * kWarpPairs * (kBlock / 32)];
+    __shared__ uint32_t wfull[kBlock / 32];
     LocalStats st;
     unsigned b = blockIdx.x;
     if (b < L.chunk_blocks) {
@@ -258,7 +266,7 @@ __global__ void __launch_bounds__(kBlock) k_lp_pull(const LpLaunch L) {
         uint32_t* wk = buf + (threadIdx.x >> 5) * 2 * kWarpPairs;  // the group path's buffer, reused
         if (item < L.num_items) {
             if (L.injective) lp_chunk_injective(L, item);
-            else lp_chunk(L, item, wk, wk + kWarpPairs);
+            else lp_chunk(L, item, wk, wk + kWarpPairs, wfull + (threadIdx.x >> 5));
         }
         return;  // chunked slots are applied by k_lp_hub_apply
     }
