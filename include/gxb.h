@@ -203,7 +203,8 @@ int gxb_commit(gxb_state* s, void* stream);
 
 int gxb_stats(gxb_state* s, void* stream, gxb_iter_stats* out);
 /* the last closed round's vote block written on the device, no host synchronisation:
- * d_out[0..4] = changed, next_active, next_units, remote_active, max_stat (doubles) —
+ * d_out[0..5] = changed, next_active, next_units, remote_active, records packed by
+ * gxb_exchange_pack_async (else 0), max_stat (doubles) —
  * what the sync round all-gathers (A/engine.py:267-285) */
 int gxb_stats_device(gxb_state* s, double* d_out, void* stream);
 
@@ -231,6 +232,13 @@ int gxb_exchange_set_peer_ptrs(gxb_state* s, int npeers, void* const* ptrs);  /*
 int gxb_exchange_close_peers(gxb_state* s);
 int gxb_exchange_pack(gxb_state* s, void* stream, uint64_t* count_out);
 int gxb_exchange_unpack(gxb_state* s, const void* d_records, uint64_t count, void* stream);
+/* asynchronous delta exchange (no host synchronisation): pack_async writes the records into
+ * GXB_BUF_SEND and leaves their count for the vote block (gxb_stats_device, entry 4); after
+ * a padded all-gather of nblocks blocks of block_records records, unpack_regions installs
+ * counts[q] records of block q (the caller passes 0 for its own block) */
+int gxb_exchange_pack_async(gxb_state* s, void* stream);
+int gxb_exchange_unpack_regions(gxb_state* s, const void* d_records, const uint64_t* counts, int nblocks,
+                                uint64_t block_records, void* stream);
 int gxb_exchange_finish(gxb_state* s, void* stream);
 #define GXB_BUF_VALUES      0   /* the value replica (contributions / distances / labels) */
 #define GXB_BUF_SEND        1   /* packed (slot, value) records of this rank */

@@ -1383,6 +1383,22 @@ int end_round(gxb_state* s, int direction, cudaStream_t st) {
     return GXB_OK;
 }
 
+int collect_stats(gxb_state* s);
+
+// an asynchronous unpack (gxb_exchange_unpack_regions) appended received vertices to the
+// frontier on the device: refresh the host copies of its length and GEN units
+int settle_unpack(gxb_state* s) {
+    if (!s->unpack_pending) return GXB_OK;
+    GXB_CHECK(collect_stats(s));
+    unsigned long long v[2] = {0, 0};
+    GXB_CUDA(cudaMemcpy(&v[0], s->d_fcount, 8, cudaMemcpyDeviceToHost));
+    GXB_CUDA(cudaMemcpy(&v[1], s->d_xscratch + 1, 8, cudaMemcpyDeviceToHost));
+    s->frontier_len = v[0];
+    s->units_cur += v[1];
+    s->unpack_pending = false;
+    return GXB_OK;
+}
+
 // host reduction of the stat stripes
 int collect_stats(gxb_state* s) {
     if (s->stats_pending) {
@@ -1610,6 +1626,7 @@ int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, 
     if (algo != GXB_ALGO_PAGERANK && g->has_csr && (rc = alloc_push(s)) != GXB_OK)
         return bail(rc);
     if (algo == GXB_ALGO_LP && (rc = gxb_lp_prepare(s, st)) != GXB_OK) return bail(rc);
+    if (algo != GXB_ALGO_PAGERANK && (rc = dalloc_t(&s->d_xscratch, 4)) != GXB_OK) return bail(rc);
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return bail(cuda_fail(e, "gxb_state_create"));
     *out = s;
@@ -1662,6 +1679,7 @@ int gxb_state_free(gxb_state* s) {
     dfree(s->d_xsend);
     dfree(s->d_xrecv);
     dfree(s->d_recv);
+    dfree(s->d_xscratch);
     delete s;
     return GXB_OK;
 }
@@ -1683,6 +1701,7 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     gxb_graph* g = s->g;
     GXB_CHECK(collect_stats(s));
+    GXB_CHECK(settle_unpack(s));
     GXB_CHECK(begin_round(s, st));
     int dir = GXB_DIR_PULL;
     if (s->algo == GXB_ALGO_SSSP || s->algo == GXB_ALGO_CC) {
@@ -1842,6 +1861,7 @@ int gxb_request(gxb_state* s, int op, uint64_t lo, uint64_t hi, void* stream) {
     }
     if (!s->in_round) {  // the first request of an iteration opens the round
         GXB_CHECK(collect_stats(s));
+        GXB_CHECK(settle_unpack(s));
         GXB_CHECK(begin_round(s, st));
     }
     if (op == GXB_OP_GEN) {
@@ -1933,7 +1953,7 @@ int gxb_commit(gxb_state* s, void* stream) {
 // counters come from the host (every vertex stays active)
 __global__ void k_vote_block(const StatStripe* __restrict__ st, double* out, int pagerank,
                              unsigned long long pr_active, unsigned long long pr_units,
-                             unsigned long long pr_remote) {
+                             unsigned long long pr_remote, const unsigned long long* packed) {
     const int lane = threadIdx.x;
     const StatStripe t = st[lane];
     unsigned long long c[4] = {t.changed, t.next_active, t.next_units, t.remote_active};
@@ -1950,7 +1970,8 @@ __global__ void k_vote_block(const StatStripe* __restrict__ st, double* out, int
             c[3] = pr_remote;
         }
         for (int i = 0; i < 4; ++i) out[i] = (double)c[i];
-        out[4] = __longlong_as_double((long long)m);
+        out[4] = packed ? (double)*packed : 0.0;
+        out[5] = __longlong_as_double((long long)m);
     }
 }
 
@@ -1961,7 +1982,9 @@ int gxb_stats_device(gxb_state* s, double* d_out, void* stream) {
     if (s->in_round) return fail(GXB_ESTATE, "gxb_stats_device: a round is open");
     const bool pr = s->algo == GXB_ALGO_PAGERANK;
     k_vote_block<<<1, 32, 0, (cudaStream_t)stream>>>(s->d_stats, d_out, pr ? 1 : 0, s->g->hi - s->g->lo,
-                                                     s->owned_outdeg_sum, s->last.remote_active);
+                                                     s->owned_outdeg_sum, s->last.remote_active,
+                                                     s->packed_async ? s->d_xscratch : nullptr);
+    s->packed_async = false;
     GXB_CUDA(cudaGetLastError());
     return GXB_OK;
 }

@@ -29,11 +29,21 @@ __global__ void k_pack(int algo, const uint32_t* __restrict__ list, const unsign
                        uint32_t* out, unsigned long long* packed) {
     const uint64_t n = *count;
     const int W = record_words(algo);
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = list[i];
+    const int lane = threadIdx.x & 31;
+    // warp-uniform trip count: the record slots are reserved once per warp
+    for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < n;
+         i0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = i0 + lane;
+        const uint32_t s = i < n ? list[i] : 0u;
         // own changes only (received slots are appended after them)
-        if (s < lo || s >= hi) continue;
-        const unsigned long long k = atomicAdd(packed, 1ull);
+        const bool mine = i < n && s >= lo && s < hi;
+        const unsigned m = __ballot_sync(0xffffffffu, mine);
+        if (!m) continue;
+        unsigned long long base = 0;
+        if (lane == __ffs(m) - 1) base = atomicAdd(packed, (unsigned long long)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+        if (!mine) continue;
+        const unsigned long long k = base + __popc(m & ((1u << lane) - 1u));
         uint32_t* r = out + k * W;
         r[0] = s;
         if (algo == GXB_ALGO_SSSP) {
@@ -53,26 +63,35 @@ __global__ void k_unpack(int algo, const uint32_t* __restrict__ rec, uint64_t n,
                          uint32_t* list, unsigned long long* count, const uint32_t* __restrict__ outdeg,
                          unsigned long long* units) {
     const int W = record_words(algo);
+    const int lane = threadIdx.x & 31;
     unsigned long long u = 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < n;
+         i0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = i0 + lane;
         const uint32_t* r = rec + i * W;
-        const uint32_t s = r[0];
-        if (s >= lo && s < hi) continue;  // own record echoed back by the all-gather
-        if (algo == GXB_ALGO_SSSP) {
-            const uint4 d = make_uint4(r[1], r[2], r[3], r[4]);
-            dist_cur[s] = d;
-            dist_next[s] = d;
-        } else {
-            lab_cur[s] = r[1];
-            lab_next[s] = r[1];
+        const uint32_t s = i < n ? r[0] : lo;
+        const bool take = i < n && (s < lo || s >= hi);  // skip own records echoed back by the all-gather
+        if (take) {
+            if (algo == GXB_ALGO_SSSP) {
+                const uint4 d = make_uint4(r[1], r[2], r[3], r[4]);
+                dist_cur[s] = d;
+                dist_next[s] = d;
+            } else {
+                lab_cur[s] = r[1];
+                lab_next[s] = r[1];
+            }
+            atomicOr(active + (s >> 5), 1u << (s & 31));
+            u += outdeg[s];
         }
-        atomicOr(active + (s >> 5), 1u << (s & 31));
-        const unsigned long long k = atomicAdd(count, 1ull);
-        list[k] = s;
-        u += outdeg[s];
+        const unsigned m = __ballot_sync(0xffffffffu, take);
+        if (!m) continue;
+        unsigned long long base = 0;
+        if (lane == __ffs(m) - 1) base = atomicAdd(count, (unsigned long long)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+        if (take) list[base + __popc(m & ((1u << lane) - 1u))] = s;
     }
     for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
-    if ((threadIdx.x & 31) == 0 && u) atomicAdd(units, u);
+    if (lane == 0 && u) atomicAdd(units, u);
 }
 
 // needed-only dense exchange (PageRank): gather my values for every peer / scatter theirs
@@ -202,15 +221,24 @@ int gxb_exchange_buffer(gxb_state* s, int which, void** dev_ptr, uint64_t* bytes
             *bytes = w * n;
             return GXB_OK;
         }
-        case GXB_BUF_SEND:
-            if (!s->d_send) GXB_CHECK(dalloc(&s->d_send, rec * (owned + 1) + 16));
+        case GXB_BUF_SEND: {
+            // sized for the largest partition: a padded all-gather sends max-count blocks
+            uint64_t mx = owned;
+            for (int q = 0; q < g->nparts; ++q) mx = std::max<uint64_t>(mx, g->bounds[q + 1] - g->bounds[q]);
+            if (!s->d_send) GXB_CHECK(dalloc(&s->d_send, rec * (mx + 1) + 16));
             *dev_ptr = s->d_send;
-            *bytes = rec * (owned + 1);
+            *bytes = rec * (mx + 1);
             return GXB_OK;
+        }
         case GXB_BUF_RECV:
             if (!s->d_recv) {
-                GXB_CHECK(dalloc(&s->d_recv, rec * (V + 1) + 16));
-                s->recv_cap = V + 1;
+                // room for every record of every rank, and for the padded all-gather of
+                // nparts blocks of the largest owned range
+                uint64_t mx = 0;
+                for (int q = 0; q < g->nparts; ++q) mx = std::max<uint64_t>(mx, g->bounds[q + 1] - g->bounds[q]);
+                const uint64_t cap = std::max<uint64_t>(V + 1, (uint64_t)g->nparts * (mx + 1));
+                GXB_CHECK(dalloc(&s->d_recv, rec * cap + 16));
+                s->recv_cap = cap;
             }
             *dev_ptr = s->d_recv;
             *bytes = rec * s->recv_cap;
@@ -244,6 +272,54 @@ int gxb_exchange_pack(gxb_state* s, void* stream, uint64_t* count_out) {
     GXB_CUDA(cudaMemcpyAsync(&n, d_cnt + 1, 8, cudaMemcpyDeviceToHost, st));
     GXB_CUDA(cudaStreamSynchronize(st));
     *count_out = n;
+    return GXB_OK;
+}
+
+// asynchronous delta exchange: no host synchronisation; the record count travels in the
+// vote block (gxb_stats_device) and the host-side frontier length is refreshed when the
+// next round starts
+int gxb_exchange_pack_async(gxb_state* s, void* stream) {
+    if (!s) return fail(GXB_EINVAL, "gxb_exchange_pack_async: null state");
+    if (s->algo == GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "gxb_exchange_pack_async: PageRank uses the dense exchange");
+    if (s->in_round) return fail(GXB_ESTATE, "gxb_exchange_pack_async: round still open");
+    void* p;
+    uint64_t b;
+    GXB_CHECK(gxb_exchange_buffer(s, GXB_BUF_SEND, &p, &b));
+    if (!s->d_xscratch) GXB_CHECK(dalloc_t(&s->d_xscratch, 4));
+    cudaStream_t st = (cudaStream_t)stream;
+    gxb_graph* g = s->g;
+    GXB_CUDA(cudaMemsetAsync(s->d_xscratch, 0, 8, st));
+    // the closed round's frontier (its length is on the device) holds exactly the changed owned slots
+    k_pack<<<grid_for(std::max<uint64_t>(1, g->hi - g->lo)), kBlock, 0, st>>>(
+        s->algo, s->d_frontier[0], s->d_fcount, g->lo, g->hi, s->d_dist_cur, s->d_lab_cur, (uint32_t*)s->d_send,
+        s->d_xscratch);
+    GXB_CUDA(cudaGetLastError());
+    s->packed_async = true;
+    s->launches++;
+    return GXB_OK;
+}
+
+int gxb_exchange_unpack_regions(gxb_state* s, const void* d_records, const uint64_t* counts, int nblocks,
+                                uint64_t block_records, void* stream) {
+    if (!s || !counts || nblocks < 0) return fail(GXB_EINVAL, "gxb_exchange_unpack_regions: bad argument");
+    if (s->algo == GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "gxb_exchange_unpack_regions: PageRank uses the dense exchange");
+    if (!s->d_xscratch) GXB_CHECK(dalloc_t(&s->d_xscratch, 4));
+    gxb_graph* g = s->g;
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint64_t W = (s->algo == GXB_ALGO_SSSP) ? 5 : 2;
+    GXB_CUDA(cudaMemsetAsync(s->d_xscratch + 1, 0, 8, st));
+    for (int q = 0; q < nblocks; ++q) {
+        if (!counts[q]) continue;
+        if (counts[q] > block_records) return fail(GXB_EINVAL, "gxb_exchange_unpack_regions: count exceeds the block");
+        if (!d_records) return fail(GXB_EINVAL, "gxb_exchange_unpack_regions: null records");
+        const uint32_t* rec = (const uint32_t*)d_records + (uint64_t)q * block_records * W;
+        k_unpack<<<grid_for(counts[q]), kBlock, 0, st>>>(s->algo, rec, counts[q], g->lo, g->hi, s->d_dist_cur,
+                                                         s->d_dist_next, s->d_lab_cur, s->d_lab_next, s->d_active[0],
+                                                         s->d_frontier[0], s->d_fcount, g->d_outdeg, s->d_xscratch + 1);
+        s->launches++;
+    }
+    GXB_CUDA(cudaGetLastError());
+    s->unpack_pending = true;
     return GXB_OK;
 }
 

@@ -235,4 +235,7 @@ struct gxb_state {
     void* d_send = nullptr;
     void* d_recv = nullptr;
     uint64_t recv_cap = 0;
+    unsigned long long* d_xscratch = nullptr;  // [0] async pack count, [1] async unpack GEN units
+    bool packed_async = false;    // the closed round's records are packed; the vote carries their count
+    bool unpack_pending = false;  // frontier_len / units_cur still to be refreshed from the device
 };

@@ -351,6 +351,16 @@ class DeviceState:
         L.check(L.lib().gxb_exchange_pack(self._h, _stream_ptr(stream), ctypes.byref(n)))
         return int(n.value)
 
+    def pack_async(self, stream=None):
+        """Pack the closed round's changed owned values; the count rides in the vote block."""
+        L.check(L.lib().gxb_exchange_pack_async(self._h, _stream_ptr(stream)))
+
+    def unpack_regions(self, ptr: int, counts, block_records: int, stream=None):
+        """Install counts[q] records from block q of a padded all-gather (0 for the own block)."""
+        arr = (ctypes.c_uint64 * max(1, len(counts)))(*[int(c) for c in counts])
+        L.check(L.lib().gxb_exchange_unpack_regions(self._h, ctypes.c_void_p(ptr), arr, len(counts),
+                                                     int(block_records), _stream_ptr(stream)))
+
     def unpack(self, ptr: int, count: int, stream=None):
         L.check(L.lib().gxb_exchange_unpack(self._h, ctypes.c_void_p(ptr), count, _stream_ptr(stream)))
 

@@ -93,6 +93,7 @@ class Collective:
         if isinstance(handle, tuple):
             return handle
         rows = handle.view(self.world, -1).cpu().tolist()
+        self.last_rows = rows  # per-rank blocks (e.g. the packed record counts)
         counts = [int(sum(r[i] for r in rows)) for i in range(len(rows[0]) - 1)]
         return counts, max(r[-1] for r in rows)
 
@@ -231,14 +232,35 @@ class PartitionedRun:
         self.state.unpack(rptr, total)
         return (total - n) * rec
 
+    def _exchange_delta_async(self, packed: list[int]) -> int:
+        """SSSP / CC / LP without host round trips: the record counts came with the vote, the
+        records move in one padded all-gather, unpack installs each peer's block."""
+        rec = self.state.buffer(L.BUF_RECORD_SIZE)[1]
+        maxc = max(packed)
+        if maxc == 0:
+            return 0
+        sptr, sbytes = self.state.buffer(L.BUF_SEND)
+        rptr, rbytes = self.state.buffer(L.BUF_RECV)
+        send = self._view(sptr, sbytes, "u1")[: maxc * rec]
+        recv = self._view(rptr, rbytes, "u1")[: self.comm.world * maxc * rec]
+        self.comm.dist.all_gather_into_tensor(recv, send, group=self.comm.group)
+        counts = list(packed)
+        counts[self.comm.rank] = 0
+        self.state.unpack_regions(rptr, counts, maxc)
+        return sum(counts) * rec
+
     def _view(self, ptr, nbytes, dtype):
         if hasattr(self.state, "view"):
             return self.state.view(ptr, nbytes, dtype)
         return device_view(ptr, nbytes, dtype)
 
     def prepare(self):
-        """One-time setup outside any timed region (maps the peers' replicas)."""
+        """One-time setup outside any timed region: maps the peers' replicas (PageRank) or
+        allocates the delta-record buffers (frontier algorithms)."""
         self._setup_peers()
+        if self.comm.world > 1 and self.algo != "pagerank" and hasattr(self.state, "buffer"):
+            for which in (L.BUF_SEND, L.BUF_RECV):
+                self.state.buffer(which)
         return self
 
     def _setup_peers(self) -> bool:
@@ -342,19 +364,25 @@ class PartitionedRun:
             moved_early = self._overlapped_pagerank_round()
         else:
             self.state.iterate(direction)
-        if self.comm.world > 1 and hasattr(self.state, "stats_device") and hasattr(self.comm, "vote_start_device"):
+        device_vote = (self.comm.world > 1 and hasattr(self.state, "stats_device")
+                       and hasattr(self.comm, "vote_start_device"))
+        async_delta = device_vote and self.algo != "pagerank" and hasattr(self.state, "pack_async")
+        if device_vote:
             # the vote block goes from device stripes straight into the all-gather; the host
-            # reads the round's statistics after the collective (one synchronisation per round)
+            # reads the round's statistics after the collective (one synchronisation per round).
+            # Frontier algorithms pack their changed values first: the record count rides along.
             import torch
             if getattr(self, "_vote_buf", None) is None:
-                self._vote_buf = torch.empty(5, dtype=torch.float64, device=self.device)
+                self._vote_buf = torch.empty(6, dtype=torch.float64, device=self.device)
+            if async_delta:
+                self.state.pack_async()
             self.state.stats_device(self._vote_buf)
             handle = self.comm.vote_start_device(self._vote_buf)
             st = None
         else:
             st = self.state.stats()
             handle = self.comm.vote_start(
-                [st["changed"], st["next_active"], st["next_units"], st["remote_active"]], st["max_stat"],
+                [st["changed"], st["next_active"], st["next_units"], st["remote_active"], 0], st["max_stat"],
                 self.device)
         t0 = self._tick("compute", t0)
         moved = moved_early
@@ -374,14 +402,19 @@ class PartitionedRun:
         if st is None:
             st = self.state.stats()  # the round is complete: no wait
         t0 = self._tick("vote", t0)
-        changed, next_active, next_units, remote_active = counts
+        changed, next_active, next_units, remote_active, _packed = counts
         if self.algo == "pagerank":
             self._pr_remote = remote_active
         self.iteration += 1
         # skip iff no next-active vertex anywhere has a consumer on another partition
         skip = self.comm.world == 1 or (self.enable_skip and remote_active == 0)
         if not skip and not early:
-            moved = self._exchange_dense() if self.algo == "pagerank" else self._exchange_delta()
+            if self.algo == "pagerank":
+                moved = self._exchange_dense()
+            elif async_delta:
+                moved = self._exchange_delta_async([int(r[4]) for r in self.comm.last_rows])
+            else:
+                moved = self._exchange_delta()
         t0 = self._tick("exchange", t0)
         if self.algo == "pagerank":
             converged = max_stat < 1e-9           # PageRank.vote (A/algorithms.py:164-165)
