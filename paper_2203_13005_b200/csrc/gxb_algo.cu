@@ -1742,7 +1742,8 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
     if (dir == GXB_DIR_PULL && s->algo != GXB_ALGO_LP && !use_binned_pull()) {
         switch (s->algo) {
             case GXB_ALGO_PAGERANK:
-                if (s->npeers > 0 && g->tiles.num_xchunks > 1) GXB_CHECK(pipelined_pagerank(s, st));
+                if ((s->npeers > 0 || options().pipeline_apply) && g->tiles.num_xchunks > 1)
+                    GXB_CHECK(pipelined_pagerank(s, st));
                 else GXB_CHECK(launch_tile_and_apply(s, pr_ops(s), st));
                 break;
             case GXB_ALGO_SSSP: {

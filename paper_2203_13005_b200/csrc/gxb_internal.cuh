@@ -290,6 +290,7 @@ struct Options {
     int64_t push_alpha = 20;      // push when frontier out-edges * alpha < |E|
     int64_t pull_dense_div = 4;   // SSSP/CC pull skips the active bitmap when frontier out-edges * div >= |E|
     int64_t pull_kernel = 0;
+    int64_t pipeline_apply = 0;   // PageRank: pipelined chunk rounds even without peer replicas (N = 1)
     int64_t xchunk_power = 4;     // exchange chunk bounds owned * (k / K)^p (4 measured best at N = 2, 4)
     int64_t tile_async = 1;       // 1 = LDGSTS-gather tile kernel (k_tile_a), 0 = register gathers (k_tile_t)
     int64_t tile_async_minblocks = 0;  // its min-blocks variant (0 = auto: 5 / 6 / 4 for 4 / 8 / 16-B values)      // 0 = warp tiles, 1 = degree-binned groups

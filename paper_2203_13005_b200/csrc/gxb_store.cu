@@ -34,6 +34,7 @@ Options& options() {
         if (const char* e = getenv("GXB_PULL_KERNEL")) o.pull_kernel = std::string(e) == "binned" ? 1 : 0;
         if (const char* e = getenv("GXB_PR_MESSAGE_BITS")) o.pr_message_bits = atol(e) == 32 ? 32 : 64;
         if (const char* e = getenv("GXB_TILE_ASYNC")) o.tile_async = atol(e) ? 1 : 0;
+        if (const char* e = getenv("GXB_PIPELINE_APPLY")) o.pipeline_apply = atol(e) ? 1 : 0;
         if (const char* e = getenv("GXB_XCHUNK_POWER")) o.xchunk_power = std::min(4L, std::max(1L, atol(e)));
         if (const char* e = getenv("GXB_EXCHANGE_CHUNKS")) o.exchange_chunks = std::min(64L, std::max(1L, atol(e)));
         if (const char* e = getenv("GXB_OVERLAP_RESERVE_SMS")) o.overlap_reserve_sms = std::min(140L, std::max(0L, atol(e)));
@@ -391,10 +392,11 @@ static int build_tile_plan(gxb_graph* g, cudaStream_t st) {
     while (nz < owned && deg[nz] > 0) ++nz;
     T.nz_slots = nz;
     // Exchange chunks (multi-GPU pipeline shuffle): the owned slots are cut into K chunks
-    // at quadratic fractions (k/K)^2 of the owned count, so chunk 0 holds the few hub slots
-    // (most of the edges) and the last chunk the many tail slots. Every rank cuts its own
-    // block with the same formula, so peers know each other's chunk ranges.
-    const int K = std::max(1, g->nparts > 1 ? (int)options().exchange_chunks : 1);
+    // at fractions (k/K)^p of the owned count (xchunk_bound), so chunk 0 holds the few hub
+    // slots (most of the edges) and the last chunk the many tail slots. Every rank cuts its
+    // own block with the same formula, so peers know each other's chunk ranges.
+    const bool chunked = g->nparts > 1 || options().pipeline_apply;
+    const int K = std::max(1, chunked ? (int)options().exchange_chunks : 1);
     T.num_xchunks = K;
     T.xchunk_slot.assign(K + 1, 0);
     for (int k = 0; k <= K; ++k) T.xchunk_slot[k] = xchunk_bound(owned, k, K);
@@ -925,6 +927,9 @@ int gxb_set_option(const char* name, int64_t value) {
     } else if (n == "pull_dense_div") {
         if (value < 0) return fail(GXB_EINVAL, "pull_dense_div must be >= 0 (0 = always test active bits)");
         o.pull_dense_div = value;
+    } else if (n == "pipeline_apply") {
+        if (value != 0 && value != 1) return fail(GXB_EINVAL, "pipeline_apply: 0 or 1");
+        o.pipeline_apply = value;
     } else if (n == "xchunk_power") {
         if (value < 1 || value > 4) return fail(GXB_EINVAL, "xchunk_power: 1..4");
         o.xchunk_power = value;
@@ -970,6 +975,7 @@ int gxb_get_option(const char* name, int64_t* value) {
     else if (n == "pull_dense_div") *value = o.pull_dense_div;
     else if (n == "tile_async") *value = o.tile_async;
     else if (n == "xchunk_power") *value = o.xchunk_power;
+    else if (n == "pipeline_apply") *value = o.pipeline_apply;
     else if (n == "tile_async_minblocks") *value = o.tile_async_minblocks;
     else if (n == "pr_message_bits") *value = o.pr_message_bits;
     else if (n == "carveout") *value = o.carveout;
