@@ -292,6 +292,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-run-ahead", action="store_true", help="PageRank: wait for every vote before the next round")
     args = ap.parse_args()
     # stdout carries exactly one JSON line: library banners (NCCL prints its version when a
     # communicator is created) go to stderr until the line is printed
@@ -346,7 +347,11 @@ def main():
     clocks = ClockSampler(local).__enter__()
     run = new_run()
     run.state.profile(enable=True, reset=True)
-    for _ in range(args.warmup):
+    ahead = algo == "pagerank" and not args.no_run_ahead and run.can_run_ahead() and \
+        (world == 1 or bool(run._peers))
+    if ahead:
+        run.run_rounds(args.warmup)
+    for _ in range(0 if ahead else args.warmup):
         run.step()
     if algo != "pagerank":
         # frontier algorithms: time whole runs (a step = one iteration of a fresh run)
@@ -364,7 +369,17 @@ def main():
     clocks.wait_first()
     clocks.mark(True)
     t_wall = time.perf_counter()
-    for _ in range(args.steps):
+    if ahead:
+        # PageRank: the K rounds run back to back (round k+1 launched before the host reads
+        # vote k), timed as one block on the launching stream
+        ev0.record(stream)
+        recs = run.run_rounds(args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+        units += sum(r.units for r in recs)
+        xbytes += sum(r.exchanged_bytes for r in recs)
+    for _ in range(0 if ahead else args.steps):
         ev0.record(stream)
         rec = run.step()
         ev1.record(stream)

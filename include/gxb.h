@@ -207,6 +207,13 @@ int gxb_stats(gxb_state* s, void* stream, gxb_iter_stats* out);
  * gxb_exchange_pack_async (else 0), max_stat (doubles) —
  * what the sync round all-gathers (A/engine.py:267-285) */
 int gxb_stats_device(gxb_state* s, double* d_out, void* stream);
+/* PageRank back-to-back rounds: in async mode a round leaves its statistics on the device
+ * (read them with gxb_stats_device), so the host can launch round k+1 before it has read
+ * round k's vote; rank and contributions are double-buffered, so a round launched after
+ * the converged one is undone exactly by gxb_round_rollback (A/algorithms.py:318-341:
+ * the reference stops at the first converged round) */
+int gxb_stats_async(gxb_state* s, int on);
+int gxb_round_rollback(gxb_state* s);
 
 /* ---- mirror exchange (A/engine.py:242-266) ----
  * Multi-partition runs keep a full-length replica of every source value. After

@@ -123,6 +123,8 @@ def _sig(L):
         "gxb_attrs_h2d": (I, [P, P, I, P]),
         "gxb_attrs_scope": (I, [P, I]),
         "gxb_stats_device": (I, [P, P, P]),
+        "gxb_stats_async": (I, [P, I]),
+        "gxb_round_rollback": (I, [P]),
         "gxb_exchange_ipc_handle": (I, [P, I, P]),
         "gxb_exchange_open_peers": (I, [P, I, P]),
         "gxb_exchange_set_peer_ptrs": (I, [P, I, P]),

@@ -56,7 +56,8 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
     };
     using Msg = double;
     const double* contrib_cur;
-    double* rank;
+    const double* rank_old;  // rank of the previous round (double-buffered: a speculative round
+    double* rank_new;        // leaves the previous state intact until the host commits it)
     double* contrib_next;
     FrontierView f;
     bool msg32;    // messages (rank / out_deg) stored and gathered as float32 (option pr_message_bits = 32)
@@ -106,13 +107,13 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
         double old;
         uint32_t od;
     };
-    __device__ Pre preload(uint32_t slot) const { return {rank[slot], __ldg(f.outdeg + slot)}; }
+    __device__ Pre preload(uint32_t slot) const { return {rank_old[slot], __ldg(f.outdeg + slot)}; }
     __device__ void apply(uint32_t slot, Acc a, LocalStats& st) const { apply_pre(slot, a, preload(slot), st); }
     // returns whether the slot joins the next frontier as a changed vertex (never: always active)
     __device__ bool apply_pre(uint32_t slot, Acc a, Pre p, LocalStats& st) const {
         const double old = p.old;
         const double nw = __dadd_rn(0.15, __dmul_rn(0.85, a.s));
-        rank[slot] = nw;
+        rank_new[slot] = nw;
         const uint32_t od = p.od;
         const double c = od ? __ddiv_rn(nw, (double)od) : 0.0;
         if (msg32) {
@@ -1167,6 +1168,27 @@ TileLaunch tile_launch(gxb_state* s) {
     return L;
 }
 
+// the timing event i of the open round: the fixed triple, or the ring slot in async mode
+cudaEvent_t kev_at(gxb_state* s, int i) {
+    if (!s->async_stats || !s->kring) return s->kev[i];
+    return s->kring[(s->kring_n % gxb_state::kRing) * 3 + i];
+}
+
+// accumulate the first n recorded ring rounds into the profile counters
+int drain_kring(gxb_state* s, int n) {
+    for (int r = 0; r < n; ++r) {
+        cudaEvent_t* e = s->kring + (r % gxb_state::kRing) * 3;
+        float ms = 0.f;
+        GXB_CUDA(cudaEventSynchronize(e[2]));
+        GXB_CUDA(cudaEventElapsedTime(&ms, e[0], e[1]));
+        s->kernel_ms += ms;
+        GXB_CUDA(cudaEventElapsedTime(&ms, e[1], e[2]));
+        s->rest_ms += ms;
+        s->kernel_launches++;
+    }
+    return GXB_OK;
+}
+
 // one exchange chunk (or all of them for k < 0): Gen∘Merge tiles, span folds, Apply
 // With `ast`, the chunk's span fold and Apply run on that stream after the tile kernel
 // (an event orders them), so Apply(k) — and its peer stores — overlap the tiles of k+1.
@@ -1210,10 +1232,10 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st, int chu
         const uint64_t want = (ntiles + (kBlock / 32) - 1) / (kBlock / 32);
         const unsigned grid = (unsigned)std::min<uint64_t>(want, (uint64_t)max_blocks);
         const bool first = chunk < 0 || s->round_chunks == 0, last = chunk < 0 || s->round_chunks == K - 1;
-        if (s->timing && first) GXB_CUDA(cudaEventRecord(s->kev[0], st));
+        if (s->timing && first) GXB_CUDA(cudaEventRecord(kev_at(s, 0), st));
         kern<<<grid, kBlock, 0, st>>>(p, L);
         if (s->timing && last) {
-            GXB_CUDA(cudaEventRecord(s->kev[1], st));
+            GXB_CUDA(cudaEventRecord(kev_at(s, 1), st));
             s->timing_pending = true;
         }
         s->launches++;
@@ -1274,7 +1296,8 @@ uint32_t hot_l1_slots(const gxb_state* s, size_t bytes_per_slot) {
 PrOps pr_ops(gxb_state* s) {
     PrOps o;
     o.contrib_cur = s->d_contrib[s->cur];
-    o.rank = s->d_rank;
+    o.rank_old = s->d_rank[s->cur];
+    o.rank_new = s->d_rank[s->cur ^ 1];
     o.contrib_next = s->d_contrib[s->cur ^ 1];
     o.msg32 = s->msg32;
     o.npeers = s->npeers;
@@ -1371,11 +1394,18 @@ int end_round(gxb_state* s, int direction, cudaStream_t st) {
         std::swap(s->d_frontier[0], s->d_frontier[1]);
         GXB_CUDA(cudaMemcpyAsync(s->d_fcount, s->d_fcount + 1, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
     }
-    if (s->timing_pending) GXB_CUDA(cudaEventRecord(s->kev[2], st));  // end of the round's kernels
-    GXB_CUDA(cudaMemcpyAsync(s->h_stats, s->d_stats, sizeof(StatStripe) * kStripes, cudaMemcpyDeviceToHost, st));
-    GXB_CUDA(cudaMemcpyAsync(s->h_fcount, s->d_fcount, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    GXB_CUDA(cudaEventRecord(s->stats_ready, st));
-    s->stats_pending = true;
+    if (s->timing_pending) GXB_CUDA(cudaEventRecord(kev_at(s, 2), st));  // end of the round's kernels
+    if (s->timing_pending && s->async_stats) {
+        s->kring_n++;
+        s->timing_pending = false;
+        if (s->kring_n % gxb_state::kRing == 0) GXB_CHECK(drain_kring(s, gxb_state::kRing));
+    }
+    if (!s->async_stats) {  // async mode: the caller reads the round through gxb_stats_device
+        GXB_CUDA(cudaMemcpyAsync(s->h_stats, s->d_stats, sizeof(StatStripe) * kStripes, cudaMemcpyDeviceToHost, st));
+        GXB_CUDA(cudaMemcpyAsync(s->h_fcount, s->d_fcount, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        GXB_CUDA(cudaEventRecord(s->stats_ready, st));
+        s->stats_pending = true;
+    }
     s->in_round = false;
     s->iteration++;
     s->lab_injective = false;
@@ -1438,7 +1468,7 @@ int collect_stats(gxb_state* s) {
         s->units_cur = o.next_units;
         s->last = o;
     }
-    if (s->timing_pending) {
+    if (s->timing_pending && !s->async_stats) {
         float ms = 0.f;
         GXB_CUDA(cudaEventSynchronize(s->kev[2]));
         GXB_CUDA(cudaEventElapsedTime(&ms, s->kev[0], s->kev[1]));
@@ -1519,11 +1549,15 @@ int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, 
     uint64_t nfront = 0, units0 = 0;
     if (algo == GXB_ALGO_PAGERANK) {
         s->arity = 1;
-        if ((rc = dalloc_t(&s->d_rank, V)) != GXB_OK) return bail(rc);
+        for (int i = 0; i < 2; ++i)
+            if ((rc = dalloc_t(&s->d_rank[i], V)) != GXB_OK) return bail(rc);
         for (int i = 0; i < 2; ++i)
             if ((rc = dalloc_t(&s->d_contrib[i], V)) != GXB_OK) return bail(rc);
         s->msg32 = options().pr_message_bits == 32;
-        if (V) k_pr_init<<<grid, kBlock, 0, st>>>(s->d_rank, s->d_contrib[0], g->d_outdeg, g->d_slot2id, V, s->msg32);
+        if (V) {
+            k_pr_init<<<grid, kBlock, 0, st>>>(s->d_rank[0], s->d_contrib[0], g->d_outdeg, g->d_slot2id, V, s->msg32);
+            cudaMemcpyAsync(s->d_rank[1], s->d_rank[0], 8 * V, cudaMemcpyDeviceToDevice, st);
+        }
         units0 = s->owned_outdeg_sum;
     } else if (algo == GXB_ALGO_SSSP) {
         if (nsrc < 0 || nsrc > 4) return bail(fail(GXB_EINVAL, "sssp supports 1..4 sources"));
@@ -1641,7 +1675,8 @@ int gxb_state_free(gxb_state* s) {
     if (s->aux_stream) cudaStreamDestroy(s->aux_stream);
     if (s->ev_tile) cudaEventDestroy(s->ev_tile);
     if (s->ev_join) cudaEventDestroy(s->ev_join);
-    dfree(s->d_rank);
+    dfree(s->d_rank[0]);
+    dfree(s->d_rank[1]);
     dfree(s->d_contrib[0]);
     dfree(s->d_contrib[1]);
     dfree(s->d_dist_cur);
@@ -1669,6 +1704,11 @@ int gxb_state_free(gxb_state* s) {
     }
     for (int i = 0; i < 3; ++i)
         if (s->kev[i]) cudaEventDestroy(s->kev[i]);
+    if (s->kring) {
+        for (int i = 0; i < 3 * gxb_state::kRing; ++i)
+            if (s->kring[i]) cudaEventDestroy(s->kring[i]);
+        delete[] s->kring;
+    }
     dfree(s->d_push_counts);
     dfree(s->d_push_cpre);
     dfree(s->d_push_tmp);
@@ -1990,6 +2030,34 @@ int gxb_stats_device(gxb_state* s, double* d_out, void* stream) {
     return GXB_OK;
 }
 
+int gxb_stats_async(gxb_state* s, int on) {
+    if (!s) return fail(GXB_EINVAL, "gxb_stats_async: null state");
+    if (on && s->algo != GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "gxb_stats_async: PageRank only");
+    if (s->in_round) return fail(GXB_ESTATE, "gxb_stats_async: a round is open");
+    GXB_CHECK(collect_stats(s));
+    if (on && s->timing && !s->kring) {
+        s->kring = new cudaEvent_t[3 * gxb_state::kRing]();
+        for (int i = 0; i < 3 * gxb_state::kRing; ++i) GXB_CUDA(cudaEventCreate(&s->kring[i]));
+    }
+    if (!on && s->async_stats && s->kring) GXB_CHECK(drain_kring(s, s->kring_n % gxb_state::kRing));
+    s->kring_n = 0;
+    s->async_stats = on != 0;
+    return GXB_OK;
+}
+
+int gxb_round_rollback(gxb_state* s) {
+    if (!s) return fail(GXB_EINVAL, "gxb_round_rollback: null state");
+    if (s->algo != GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "gxb_round_rollback: PageRank only");
+    if (s->in_round || s->iteration == 0) return fail(GXB_ESTATE, "gxb_round_rollback: no closed round");
+    // the round wrote only the next rank / contribution buffers: make the previous ones current
+    s->cur ^= 1;
+    s->iteration--;
+    s->stats_pending = false;
+    s->timing_pending = false;
+    if (s->async_stats && s->kring_n % gxb_state::kRing) s->kring_n--;  // its timing is not a round
+    return GXB_OK;
+}
+
 int gxb_stats(gxb_state* s, void* stream, gxb_iter_stats* out) {
     if (!s || !out) return fail(GXB_EINVAL, "gxb_stats: null argument");
     (void)stream;
@@ -2012,7 +2080,7 @@ int gxb_read_attrs(gxb_state* s, double* host_out, int owned_only, void* stream)
     cudaStream_t st = (cudaStream_t)stream;
     GXB_CHECK(stage(s));
     k_read_attrs<<<grid_for(V), kBlock, 0, st>>>(s->algo, s->arity, g->d_dense2slot, V, g->lo, g->hi,
-                                                 owned_only, s->d_rank, s->d_dist_cur, s->d_lab_cur, s->d_stage);
+                                                 owned_only, s->d_rank[s->cur], s->d_dist_cur, s->d_lab_cur, s->d_stage);
     GXB_CUDA(cudaMemcpyAsync(host_out, s->d_stage, 8 * V * s->arity, cudaMemcpyDeviceToHost, st));
     GXB_CUDA(cudaStreamSynchronize(st));
     return GXB_OK;
@@ -2033,7 +2101,7 @@ int gxb_write_attrs(gxb_state* s, const double* host_in, void* stream) {
     uint32_t* d_bad = reinterpret_cast<uint32_t*>(s->d_fcount) + 2;  // scratch word of counter [1]
     GXB_CUDA(cudaMemsetAsync(d_bad, 0, 4, st));
     k_write_attrs<<<grid_for(V), kBlock, 0, st>>>(s->algo, s->arity, g->d_dense2slot, V, g->d_outdeg, s->d_stage,
-                                                  s->d_rank, s->d_contrib[s->cur], s->d_dist_cur, s->d_dist_next,
+                                                  s->d_rank[s->cur], s->d_contrib[s->cur], s->d_dist_cur, s->d_dist_next,
                                                   s->d_lab_cur, s->d_lab_next, d_bad, s->msg32);
     uint32_t bad = 0;
     GXB_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
@@ -2104,7 +2172,7 @@ int gxb_attrs_install(gxb_state* s, int buf, void* stream) {
     if (!n) return GXB_OK;
     uint32_t* d_bad = reinterpret_cast<uint32_t*>(s->d_fcount) + 2;  // sticky flag, checked by gxb_attrs_check
     k_write_attrs<<<grid_for(n), kBlock, 0, (cudaStream_t)stream>>>(
-        s->algo, s->arity, d2s, n, g->d_outdeg, s->d_stage_in[buf], s->d_rank, s->d_contrib[s->cur],
+        s->algo, s->arity, d2s, n, g->d_outdeg, s->d_stage_in[buf], s->d_rank[s->cur], s->d_contrib[s->cur],
         s->d_dist_cur, s->d_dist_next, s->d_lab_cur, s->d_lab_next, d_bad, s->msg32);
     GXB_CUDA(cudaGetLastError());
     return GXB_OK;
@@ -2119,7 +2187,7 @@ int gxb_attrs_extract(gxb_state* s, int buf, void* stream) {
     stage_order(s, &d2s, &n);
     if (!n) return GXB_OK;
     k_read_attrs<<<grid_for(n), kBlock, 0, (cudaStream_t)stream>>>(s->algo, s->arity, d2s, n, g->lo, g->hi, 0,
-                                                                   s->d_rank, s->d_dist_cur, s->d_lab_cur,
+                                                                   s->d_rank[s->cur], s->d_dist_cur, s->d_lab_cur,
                                                                    s->d_stage_out[buf]);
     GXB_CUDA(cudaGetLastError());
     return GXB_OK;

@@ -155,7 +155,8 @@ struct gxb_state {
     uint64_t owned_targets = 0;      // owned slots with in-degree > 0 (PR targets)
 
     // values (full-length replica over slots)
-    double* d_rank = nullptr;               // PR: rank per slot
+    double* d_rank[2] = {nullptr, nullptr}; // PR: rank per slot, double-buffered like the contributions
+    bool async_stats = false;               // PR: rounds leave their statistics on the device only
     double* d_contrib[2] = {nullptr, nullptr};  // PR: rank/outdeg, double-buffered
     int cur = 0;
     bool msg32 = false;                     // PR messages in float32 (gathered / exchanged at 4 B)
@@ -224,6 +225,10 @@ struct gxb_state {
     bool timing = false;
     bool timing_pending = false;
     cudaEvent_t kev[3] = {nullptr, nullptr, nullptr};
+    // async-stats rounds: per-round timing events kept in a ring, read when async mode ends
+    static constexpr int kRing = 512;
+    cudaEvent_t* kring = nullptr;  // kRing x 3
+    int kring_n = 0;               // rounds recorded since async mode began (pending)
     double kernel_ms = 0.0;
     double rest_ms = 0.0;  // device time after the main kernel until the round closes
     uint64_t kernel_launches = 0;

@@ -265,6 +265,14 @@ class DeviceState:
         max_stat; float64) into a device tensor without a host synchronisation."""
         L.check(L.lib().gxb_stats_device(self._h, _vp(out), _stream_ptr(stream)))
 
+    def stats_async(self, on: bool):
+        """PageRank: rounds leave their statistics on the device (read with stats_device)."""
+        L.check(L.lib().gxb_stats_async(self._h, int(bool(on))))
+
+    def rollback(self):
+        """Undo the last PageRank round (its outputs went to the next buffers only)."""
+        L.check(L.lib().gxb_round_rollback(self._h))
+
     def read_attrs(self, owned_only: bool = False, stream=None) -> np.ndarray:
         V = self.graph.num_vertices
         out = np.empty((V, self.arity), dtype=np.float64)

@@ -433,6 +433,73 @@ class PartitionedRun:
             w.wait()
         self._pending = []
 
+    def can_run_ahead(self) -> bool:
+        return (self.algo == "pagerank" and hasattr(self.state, "stats_async")
+                and hasattr(self.state, "stats_device") and hasattr(self.state, "rollback"))
+
+    def run_rounds(self, n: int) -> list:
+        """Up to n PageRank rounds back to back: round k+1 is launched before the host reads
+        round k's vote, so the GPU never waits for the host between rounds. The vote blocks go
+        from the device (all-gathered at N > 1) into a pinned ring read one round behind; when
+        round k converged, the already-launched round k+1 is rolled back (its rank and
+        contributions went to the next buffers only), so results and iteration counts equal
+        the round-by-round loop (A/algorithms.py:318-341)."""
+        import torch
+        if not self.can_run_ahead() or n <= 0:
+            return [self.step() for _ in range(n)]
+        world = self.comm.world
+        dev = self.device
+        peers = self._setup_peers() if world > 1 else False
+        if world > 1 and not peers:
+            return [self.step() for _ in range(n)]  # the NCCL dense exchange is issued per round
+        out = []
+        bufs = [torch.empty(6, dtype=torch.float64, device=dev) for _ in range(2)]
+        host = [torch.empty(world * 6, dtype=torch.float64).pin_memory() for _ in range(2)]
+        evs = [torch.cuda.Event() for _ in range(2)]
+        sizes = np.diff(self.bounds.astype(np.int64))
+        ptr, nbytes = self.state.buffer(L.BUF_VALUES)
+        moved = 0 if world == 1 else nbytes // max(1, int(self.bounds[-1])) * int(self.bounds[-1] - sizes[self.comm.rank])
+        self.state.stats()  # settle the last synchronous round
+        self.state.stats_async(True)
+        try:
+            launched = 0
+
+            def launch(k):
+                self.state.iterate("pull")
+                self.state.stats_device(bufs[k % 2])
+                rows = self.comm.vote_start_device(bufs[k % 2]) if world > 1 else bufs[k % 2]
+                host[k % 2].copy_(rows, non_blocking=True)
+                evs[k % 2].record()
+
+            launch(0)
+            launched = 1
+            for k in range(n):
+                if launched < n:
+                    launch(launched)
+                    launched += 1
+                evs[k % 2].synchronize()
+                rows = host[k % 2].view(world, 6).tolist()
+                changed, next_active, next_units, remote_active = (int(sum(r[i] for r in rows)) for i in range(4))
+                max_stat = max(r[5] for r in rows)
+                self.iteration += 1
+                self._pr_remote = remote_active
+                converged = max_stat < 1e-9  # PageRank.vote (A/algorithms.py:164-165)
+                skip = world == 1 or (self.enable_skip and remote_active == 0)
+                units = int(rows[self.comm.rank][2])  # this rank's GEN units (every owned vertex)
+                rec = StepRecord(self.iteration, changed, next_active, units, remote_active, max_stat,
+                                 skip and world > 1, converged, moved, 1)
+                self.records.append(rec)
+                out.append(rec)
+                if converged:
+                    if launched > k + 1:  # round k+2 (1-based) already ran: undo it
+                        torch.cuda.synchronize(dev)
+                        self.state.rollback()
+                    break
+        finally:
+            torch.cuda.synchronize(dev)
+            self.state.stats_async(False)
+        return out
+
     def run(self, max_iterations: int, direction: str = "auto") -> tuple[int, bool]:
         converged = False
         while self.iteration < max_iterations:
