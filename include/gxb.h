@@ -212,7 +212,7 @@ int gxb_stats_device(gxb_state* s, double* d_out, void* stream);
  * round k's vote; rank and contributions are double-buffered, so a round launched after
  * the converged one is undone exactly by gxb_round_rollback (A/algorithms.py:318-341:
  * the reference stops at the first converged round) */
-int gxb_stats_async(gxb_state* s, int on);
+int gxb_stats_async(gxb_state* s, int on);  /* gxb_stats keeps reporting the last synchronous round */
 int gxb_round_rollback(gxb_state* s);
 
 /* ---- mirror exchange (A/engine.py:242-266) ----
