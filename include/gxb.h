@@ -242,10 +242,13 @@ int gxb_exchange_unpack(gxb_state* s, const void* d_records, uint64_t count, voi
 /* asynchronous delta exchange (no host synchronisation): pack_async writes the records into
  * GXB_BUF_SEND and leaves their count for the vote block (gxb_stats_device, entry 4); after
  * a padded all-gather of nblocks blocks of block_records records, unpack_regions installs
- * counts[q] records of block q (the caller passes 0 for its own block) */
+ * counts[q] records of block q (the caller passes 0 for its own block); frontier_after /
+ * units_after are the next frontier's length and GEN units when the caller knows them from
+ * the vote (own changed + received records; the sum of every rank's next_units) */
 int gxb_exchange_pack_async(gxb_state* s, void* stream);
 int gxb_exchange_unpack_regions(gxb_state* s, const void* d_records, const uint64_t* counts, int nblocks,
-                                uint64_t block_records, void* stream);
+                                uint64_t block_records, uint64_t frontier_after, uint64_t units_after,
+                                void* stream);  /* *_after = ~0: read back from the device */
 int gxb_exchange_finish(gxb_state* s, void* stream);
 #define GXB_BUF_VALUES      0   /* the value replica (contributions / distances / labels) */
 #define GXB_BUF_SEND        1   /* packed (slot, value) records of this rank */

@@ -113,7 +113,7 @@ def _sig(L):
         "gxb_exchange_pack": (I, [P, P, ctypes.POINTER(U64)]),
         "gxb_exchange_unpack": (I, [P, P, U64, P]),
         "gxb_exchange_pack_async": (I, [P, P]),
-        "gxb_exchange_unpack_regions": (I, [P, P, P, I, U64, P]),
+        "gxb_exchange_unpack_regions": (I, [P, P, P, I, U64, U64, U64, P]),
         "gxb_exchange_finish": (I, [P, P]),
         "gxb_exchange_sparse_counts": (I, [P, P, P]),
         "gxb_exchange_sparse_pack": (I, [P, P]),

@@ -300,7 +300,8 @@ int gxb_exchange_pack_async(gxb_state* s, void* stream) {
 }
 
 int gxb_exchange_unpack_regions(gxb_state* s, const void* d_records, const uint64_t* counts, int nblocks,
-                                uint64_t block_records, void* stream) {
+                                uint64_t block_records, uint64_t frontier_after, uint64_t units_after,
+                                void* stream) {
     if (!s || !counts || nblocks < 0) return fail(GXB_EINVAL, "gxb_exchange_unpack_regions: bad argument");
     if (s->algo == GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "gxb_exchange_unpack_regions: PageRank uses the dense exchange");
     if (!s->d_xscratch) GXB_CHECK(dalloc_t(&s->d_xscratch, 4));
@@ -319,7 +320,17 @@ int gxb_exchange_unpack_regions(gxb_state* s, const void* d_records, const uint6
         s->launches++;
     }
     GXB_CUDA(cudaGetLastError());
-    s->unpack_pending = true;
+    if (frontier_after != ~0ull && units_after != ~0ull) {
+        // the caller knows both from the vote: own changed + received records, and every
+        // sender's next_units (a record is a changed vertex of its sender) — no read-back
+        gxb_iter_stats tmp;
+        GXB_CHECK(gxb_stats(s, stream, &tmp));  // the round's own statistics are collected first
+        s->frontier_len = frontier_after;
+        s->units_cur = units_after;
+        s->unpack_pending = false;
+    } else {
+        s->unpack_pending = true;
+    }
     return GXB_OK;
 }
 

@@ -363,11 +363,16 @@ class DeviceState:
         """Pack the closed round's changed owned values; the count rides in the vote block."""
         L.check(L.lib().gxb_exchange_pack_async(self._h, _stream_ptr(stream)))
 
-    def unpack_regions(self, ptr: int, counts, block_records: int, stream=None):
-        """Install counts[q] records from block q of a padded all-gather (0 for the own block)."""
+    def unpack_regions(self, ptr: int, counts, block_records: int, frontier_after=None, units_after=None,
+                       stream=None):
+        """Install counts[q] records from block q of a padded all-gather (0 for the own block);
+        frontier_after / units_after: the next frontier's size and GEN units when known."""
         arr = (ctypes.c_uint64 * max(1, len(counts)))(*[int(c) for c in counts])
+        unknown = (1 << 64) - 1
+        fa = unknown if frontier_after is None else int(frontier_after)
+        ua = unknown if units_after is None else int(units_after)
         L.check(L.lib().gxb_exchange_unpack_regions(self._h, ctypes.c_void_p(ptr), arr, len(counts),
-                                                     int(block_records), _stream_ptr(stream)))
+                                                     int(block_records), fa, ua, _stream_ptr(stream)))
 
     def unpack(self, ptr: int, count: int, stream=None):
         L.check(L.lib().gxb_exchange_unpack(self._h, ctypes.c_void_p(ptr), count, _stream_ptr(stream)))

@@ -246,7 +246,12 @@ class PartitionedRun:
         self.comm.dist.all_gather_into_tensor(recv, send, group=self.comm.group)
         counts = list(packed)
         counts[self.comm.rank] = 0
-        self.state.unpack_regions(rptr, counts, maxc)
+        rows = self.comm.last_rows
+        # next frontier = my changed vertices + every received record; its GEN units = every
+        # rank's next_units (a record is a changed vertex of its sender)
+        frontier = int(rows[self.comm.rank][1]) + sum(counts)
+        units = int(sum(r[2] for r in rows))
+        self.state.unpack_regions(rptr, counts, maxc, frontier, units)
         return sum(counts) * rec
 
     def _view(self, ptr, nbytes, dtype):

@@ -147,7 +147,7 @@ class AsyncNumpyPartition(NumpyPartition):
                                 self._packed, st["max_stat"]], dtype=torch.float64))
         self._packed = 0
 
-    def unpack_regions(self, ptr, counts, block):
+    def unpack_regions(self, ptr, counts, block, frontier_after=None, units_after=None):
         for q, n in enumerate(counts):
             if not n:
                 continue
