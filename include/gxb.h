@@ -164,6 +164,14 @@ int gxb_graph_build(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst, cons
 int gxb_graph_build_sized(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint32_t* w,
                           uint64_t num_edges, int part, int nparts, const uint64_t* sizes, uint32_t flags,
                           void* stream, gxb_graph** out);
+/* heterogeneous devices: contiguous degree-sorted ranges (GXB_BUILD_RANGES) whose in-edge
+ * cost is split in proportion to per-partition capacity factors (units per unit time =
+ * 1 / unit_cost): the data-resizing planner balance_data (A/balancer.py:79-98) applied to
+ * the graph's cost line; every factor must be > 0 and finite, else GXB_EINVAL; combining
+ * with GXB_BUILD_ID_RANGES is GXB_EINVAL */
+int gxb_graph_build_balanced(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint32_t* w,
+                             uint64_t num_edges, int part, int nparts, const double* capacity, uint32_t flags,
+                             void* stream, gxb_graph** out);
 int gxb_graph_get_info(const gxb_graph* g, gxb_graph_info* out);
 /* ascending present ids (host buffer of num_vertices) */
 int gxb_graph_ids(const gxb_graph* g, uint32_t* host_out);

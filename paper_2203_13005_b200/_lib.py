@@ -92,6 +92,7 @@ def _sig(L):
         "gxb_rmat_generate": (I, [P, ctypes.POINTER(RmatArgs), P, P, P, P]),
         "gxb_graph_build": (I, [P, P, P, P, U64, I, I, U32, P, PP]),
         "gxb_graph_build_sized": (I, [P, P, P, P, U64, I, I, P, U32, P, PP]),
+        "gxb_graph_build_balanced": (I, [P, P, P, P, U64, I, I, P, U32, P, PP]),
         "gxb_graph_get_info": (I, [P, ctypes.POINTER(GraphInfo)]),
         "gxb_graph_ids": (I, [P, P]),
         "gxb_graph_out_degree": (I, [P, P]),

@@ -121,6 +121,7 @@ struct gxb_graph {
     bool weighted = false, has_csr = false;
     std::vector<uint64_t> bounds;       // nparts + 1 slot boundaries
     std::vector<uint64_t> part_sizes;   // explicit per-partition vertex counts (id-range mode)
+    std::vector<double> part_capacity;  // per-partition capacity factors (degree-sorted ranges)
 
     uint32_t* d_slot2id = nullptr;      // V: original id per slot
     uint32_t* d_dense2slot = nullptr;   // V: slot of the i-th smallest id

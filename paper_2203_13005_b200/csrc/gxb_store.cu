@@ -13,6 +13,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -753,9 +754,15 @@ static int graph_build_impl(gxb_graph* g, const uint32_t* src_in, const uint32_t
         auto cost = [&](uint64_t s) { return 12ull * h_indeg[s] + 64ull; };
         uint64_t total = 0;
         for (uint64_t s = 0; s < V; ++s) total += cost(s);
+        // heterogeneous devices: partition p's share of the cost is its capacity factor
+        // over the sum (balance_data, A/balancer.py:79-98, applied to the continuous cost
+        // line instead of integer units); no factors = equal shares
+        std::vector<long double> cum(g->nparts + 1, 0.0L);
+        for (int p = 0; p < g->nparts; ++p)
+            cum[p + 1] = cum[p] + (g->part_capacity.empty() ? 1.0L : (long double)g->part_capacity[p]);
         uint64_t acc = 0, s = 0;
         for (int p = 1; p < g->nparts; ++p) {
-            const uint64_t target = (uint64_t)((long double)total * p / g->nparts);
+            const uint64_t target = (uint64_t)((long double)total * cum[p] / cum[g->nparts]);
             while (s < V && acc < target) acc += cost(s++);
             g->bounds[p] = s;
         }
@@ -1033,6 +1040,37 @@ int gxb_graph_build_sized(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst
         flags |= GXB_BUILD_ID_RANGES;
     }
     int rc = graph_build_impl(g, src, dst, w, num_edges, flags, (cudaStream_t)stream);
+    if (rc != GXB_OK) {
+        graph_release(g);
+        delete g;
+        return rc;
+    }
+    *out = g;
+    return GXB_OK;
+}
+
+int gxb_graph_build_balanced(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint32_t* w,
+                             uint64_t num_edges, int part, int nparts, const double* capacity, uint32_t flags,
+                             void* stream, gxb_graph** out) {
+    if (!ctx || !ctx->alive) return fail(GXB_ESTATE, "gxb_graph_build: daemon not initialised");
+    if (!out) return fail(GXB_EINVAL, "gxb_graph_build: null out");
+    if (!capacity) return fail(GXB_EINVAL, "gxb_graph_build_balanced: null capacity factors");
+    if (nparts < 1 || nparts > 64 || part < 0 || part >= nparts)
+        return fail(GXB_EINVAL, "gxb_graph_build: bad partition index");
+    for (int p = 0; p < nparts; ++p)  // NodeCost's precondition (A/balancer.py:26-28)
+        if (!(capacity[p] > 0.0) || !std::isfinite(capacity[p]))
+            return fail(GXB_EINVAL, "gxb_graph_build_balanced: capacity factors must be positive and finite");
+    if (flags & GXB_BUILD_ID_RANGES)
+        return fail(GXB_EINVAL, "gxb_graph_build_balanced: capacity factors apply to degree-sorted ranges only");
+    if (num_edges && (!src || !dst)) return fail(GXB_EINVAL, "gxb_graph_build: null edge arrays");
+    if (num_edges >= (1ull << 32)) return fail(GXB_ERANGE, "gxb_graph_build: more than 2^32-1 edges");
+    GXB_CUDA(cudaSetDevice(ctx->device));
+    gxb_graph* g = new gxb_graph();
+    g->ctx = ctx;
+    g->part = part;
+    g->nparts = nparts;
+    g->part_capacity.assign(capacity, capacity + nparts);
+    int rc = graph_build_impl(g, src, dst, w, num_edges, flags | GXB_BUILD_RANGES, (cudaStream_t)stream);
     if (rc != GXB_OK) {
         graph_release(g);
         delete g;

@@ -106,11 +106,14 @@ class DeviceGraph:
     """Device-resident CSC (+ push CSR) of one destination partition (A/graph.py:175-212)."""
 
     def __init__(self, ctx: DeviceContext, src, dst, w=None, part: int = 0, nparts: int = 1,
-                 csr: bool = True, stream=None, partitioning: str = "edges", sizes=None):
+                 csr: bool = True, stream=None, partitioning: str = "edges", sizes=None,
+                 capacity=None):
         """partitioning: "edges" = the degree-sorted order dealt round-robin to the
         partitions (balanced edges, vertices and exchange; default); "ranges" = contiguous
         degree-sorted ranges balanced by in-edge cost; "ids" = the reference's contiguous
-        ascending-id ranges (even_sizes, or explicit `sizes`)."""
+        ascending-id ranges (even_sizes, or explicit `sizes`).
+        capacity: per-partition capacity factors (balancer.capacity_factors); implies
+        "ranges" with partition p taking capacity[p] / sum(capacity) of the cost."""
         self.ctx = ctx
         flags = 0 if csr else L.BUILD_NO_CSR
         if partitioning not in ("edges", "ranges", "ids"):
@@ -122,6 +125,13 @@ class DeviceGraph:
         sizes_arr = None if sizes is None else np.ascontiguousarray(sizes, dtype=np.uint64)
         if sizes_arr is not None and sizes_arr.size != nparts:
             raise ValueError("one size per partition required")
+        cap_arr = None
+        if capacity is not None:
+            if sizes is not None or partitioning == "ids":
+                raise ValueError("capacity factors apply to degree-sorted ranges, not id ranges")
+            cap_arr = np.ascontiguousarray(capacity, dtype=np.float64)
+            if cap_arr.size != nparts:
+                raise ValueError("one capacity factor per partition required")
         if hasattr(src, "is_cuda") and src.is_cuda:
             n = int(src.numel())
             keep = (src, dst, w)
@@ -140,8 +150,12 @@ class DeviceGraph:
             keep = (src, dst, w)
         self._keep = keep  # inputs must outlive the async copies
         h = ctypes.c_void_p()
-        L.check(L.lib().gxb_graph_build_sized(ctx.handle, _vp(src), _vp(dst), _vp(w), n, part, nparts,
-                                              _vp(sizes_arr), flags, _stream_ptr(stream), ctypes.byref(h)))
+        if cap_arr is not None:
+            L.check(L.lib().gxb_graph_build_balanced(ctx.handle, _vp(src), _vp(dst), _vp(w), n, part, nparts,
+                                                     _vp(cap_arr), flags, _stream_ptr(stream), ctypes.byref(h)))
+        else:
+            L.check(L.lib().gxb_graph_build_sized(ctx.handle, _vp(src), _vp(dst), _vp(w), n, part, nparts,
+                                                  _vp(sizes_arr), flags, _stream_ptr(stream), ctypes.byref(h)))
         self._h = h
         self._keep = None
         info = L.GraphInfo()

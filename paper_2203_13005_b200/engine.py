@@ -64,6 +64,8 @@ class RunConfig:
     partitioning: str = "ids"    # "ids": contiguous ascending-id ranges like partition_graph (A/graph.py:175-212);
                                  # "edges": destination ranges balanced by in-edges (the multi-GPU default)
     sizes: list[int] | None = None  # explicit partition sizes (partition_graph's `sizes`)
+    capacity: list[float] | None = None  # per-partition capacity factors (balancer.capacity_factors):
+                                         # degree-sorted ranges cut in proportion (A/balancer.py:79-98)
 
 
 @dataclass
@@ -213,7 +215,7 @@ class Engine:
         maxw = int(np.max(w)) if (w is not None and w.size) else 1
         for j in range(m):
             g = DeviceGraph(self.ctx, ea.src, ea.dst, w, part=j, nparts=m, csr=algo in ("sssp", "cc", "lp"),
-                            partitioning=cfg.partitioning, sizes=cfg.sizes)
+                            partitioning=cfg.partitioning, sizes=cfg.sizes, capacity=cfg.capacity)
             s = DeviceState(g, algo, sources=getattr(self.algorithm, "sources", None) if algo == "sssp" else None,
                             max_weight=maxw if algo == "sssp" else None)
             self.graphs.append(g)
