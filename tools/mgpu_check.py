@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--scale", type=int, default=18)
     ap.add_argument("--algos", default="pagerank,sssp,cc,lp")
     ap.add_argument("--partitioning", default="edges")
+    ap.add_argument("--capacity", default=None, help="comma-separated capacity factors (one per rank)")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -41,7 +42,8 @@ def main():
         p = RmatParams(scale=args.scale, seed=77, **over)
         src, dst, w = ctx.rmat(p)
         g = DeviceGraph(ctx, src, dst, w, part=rank, nparts=world, csr=algo in ("sssp", "cc", "lp"),
-                        partitioning=args.partitioning)
+                        partitioning=args.partitioning,
+                        capacity=None if args.capacity is None else [float(x) for x in args.capacity.split(",")])
         st = DeviceState(g, algo)
         run = PartitionedRun(st, g.bounds(), comm, enable_skip=True, device=dev)
         cap = {"pagerank": 10, "lp": 15}.get(algo, g.num_vertices + 1)
