@@ -66,6 +66,7 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
     HotPrefix hp;  // degree rank of a slot inside its partition block
     uint32_t hot;  // ranks [0, hot) keep L2 priority (degree-sorted: the most-gathered sources)
     uint32_t hot1; // ranks [0, hot1) also allocate in L1; the rest bypass L1
+    const double* hub_sum;  // hub split: per-slot sum of the hub in-edges, added before Apply (or null)
 
     __device__ static Acc identity() { return {0.0}; }
     __device__ static Acc combine(Acc a, Acc b) { return {a.s + b.s}; }
@@ -112,7 +113,9 @@ struct PrOps {  // PageRank (A/algorithms.py:125-171)
     // returns whether the slot joins the next frontier as a changed vertex (never: always active)
     __device__ bool apply_pre(uint32_t slot, Acc a, Pre p, LocalStats& st) const {
         const double old = p.old;
-        const double nw = __dadd_rn(0.15, __dmul_rn(0.85, a.s));
+        // hub split: the hub sources' edges come first in source order (A/algorithms.py:243-251)
+        const double sum = hub_sum ? __dadd_rn(hub_sum[slot], a.s) : a.s;
+        const double nw = __dadd_rn(0.15, __dmul_rn(0.85, sum));
         rank_new[slot] = nw;
         const uint32_t od = p.od;
         const double c = od ? __ddiv_rn(nw, (double)od) : 0.0;
@@ -486,6 +489,7 @@ struct TileLaunch {
     const uint32_t* span_slot;
     void* partials;
     void* sums;   // per relative slot: folded accumulator
+    const uint32_t* key_slot;  // compacted plan (PageRank hub split): plan key -> owned slot, else null
 };
 
 __device__ __forceinline__ uint4 ldg_v4(const uint32_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
@@ -496,6 +500,7 @@ __device__ __forceinline__ void tile_emit(const Pol& p, const TileLaunch& L, uin
     using Ops = decltype(p.ops);
     using Acc = typename Ops::Acc;
     uint32_t span = kNone;
+    if (L.key_slot) key = __ldg(L.key_slot + key);  // span_slot holds owned slots in that case
     if (head != kNone && key == __ldg(L.span_slot + head)) span = head;
     else if (tail != kNone && key == __ldg(L.span_slot + tail)) span = tail;
     if (span == kNone) {
@@ -605,7 +610,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_t(const Pol p, cons
                     fval = acc;
                     first = false;
                 } else {
-                    reinterpret_cast<Acc*>(L.sums)[key] = acc;
+                    reinterpret_cast<Acc*>(L.sums)[L.key_slot ? __ldg(L.key_slot + key) : key] = acc;
                 }
                 ++key;
                 acc = Ops::identity();
@@ -720,7 +725,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_a(const Pol p, cons
                     fval = acc;
                     first = false;
                 } else {
-                    reinterpret_cast<Acc*>(L.sums)[key] = acc;
+                    reinterpret_cast<Acc*>(L.sums)[L.key_slot ? __ldg(L.key_slot + key) : key] = acc;
                 }
                 ++key;
                 acc = Ops::identity();
@@ -1165,6 +1170,7 @@ TileLaunch tile_launch(gxb_state* s) {
     L.span_slot = T.d_span_slot;
     L.partials = s->d_tile_partials;
     L.sums = s->d_sums;
+    L.key_slot = nullptr;
     return L;
 }
 
@@ -1268,6 +1274,314 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st, int chu
     return GXB_OK;
 }
 
+// ======================================================================
+// PageRank hub split (option pr_hub_slots, one partition)
+// ======================================================================
+// CSC segments are source-sorted, so the in-edges of a destination that come from the
+// H highest-out-degree sources (slots < H in the degree-sorted order) are a prefix of its
+// segment. Those "hub" edges are summed from a shared-memory copy of contrib[0, H)
+// (one table per SM, LDS instead of an L1 data-pipe wavefront per gathered element); the
+// remaining "cold" edges run the LDGSTS tile kernel. Both CSCs are compacted to their
+// non-empty destinations and planned with the same warp tiles; plan keys map back to
+// owned slots through d_split_slot.
+constexpr int kHubBlock = 1024;
+PrOps pr_ops(gxb_state* s);
+
+// per destination slot: number of in-edges from sources < H (lower bound in its segment)
+__global__ void k_hub_count(const uint64_t* __restrict__ off, const uint32_t* __restrict__ src, uint64_t nz,
+                            uint32_t H, uint32_t* hcnt) {
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < nz; r += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t lo = off[r], hi = off[r + 1];
+        const uint64_t b = lo;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (src[mid] < H) lo = mid + 1; else hi = mid;
+        }
+        hcnt[r] = (uint32_t)(lo - b);
+    }
+}
+
+// copy the selected part of each listed destination's segment into the compacted CSC
+// (warp per destination); hub = the prefix [0, hcnt), cold = the rest
+__global__ void k_split_copy(const uint64_t* __restrict__ off, const uint32_t* __restrict__ src,
+                             const uint32_t* __restrict__ hcnt, const uint32_t* __restrict__ list, uint64_t n,
+                             const uint64_t* __restrict__ coff, int hub, uint32_t* out) {
+    const uint64_t lane = threadIdx.x & 31;
+    const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = w0; i < n; i += nw) {
+        const uint32_t r = list[i];
+        const uint64_t b = off[r] + (hub ? 0 : hcnt[r]);
+        const uint64_t c = coff[i + 1] - coff[i];
+        for (uint64_t k = lane; k < c; k += 32) out[coff[i] + k] = src[b + k];
+    }
+}
+
+__global__ void k_remap_u32(uint32_t* a, uint64_t n, const uint32_t* __restrict__ map) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        a[i] = map[a[i]];
+}
+
+// hub pass: the tile kernel's segmented fold over the compacted hub CSC, values from the
+// shared-memory table (each lane reads its own kTileK consecutive indices: two 16-B loads)
+__global__ void __launch_bounds__(kHubBlock, 1) k_tile_hub(const double* __restrict__ contrib, uint32_t H,
+                                                            const TileLaunch L) {
+    extern __shared__ double tab[];
+    for (uint32_t i = threadIdx.x; i < H; i += kHubBlock) tab[i] = __ldcg(contrib + i);
+    __syncthreads();
+    using Ops = PrOps;
+    using Acc = PrOps::Acc;
+    const FusedPolicy<PrOps> p{};
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nwarps = gridDim.x * (kHubBlock / 32);
+    const uint32_t ntiles = (uint32_t)L.num_tiles;
+    const uint32_t q0 = lane * kTileK;
+    // one tile ahead: its indices and lane descriptors load while this tile folds
+    uint4 na = make_uint4(0, 0, 0, 0), nb = na;
+    uint32_t ncnt = 0, nsa = 0, nmask = 0;
+    auto prefetch = [&](uint32_t tt) {
+        const uint32_t b0 = (uint32_t)__ldg(L.tile_start + tt);
+        ncnt = (uint32_t)__ldg(L.tile_start + tt + 1) - b0;
+        nsa = __ldg(L.lane_slot + (uint64_t)tt * 32 + lane);
+        nmask = __ldg(L.lane_mask + (uint64_t)tt * 32 + lane);
+        if (q0 < ncnt) {
+            na = ldg_v4(L.in_src + b0 + q0);
+            nb = ldg_v4(L.in_src + b0 + q0 + 4);
+        }
+    };
+    uint32_t t = blockIdx.x * (kHubBlock / 32) + (threadIdx.x >> 5);
+    if (t < ntiles) prefetch(t);
+    for (; t < ntiles; t += nwarps) {
+        const uint32_t cnt = ncnt;
+        const uint32_t sa = nsa;
+        uint32_t endmask = nmask;
+        const uint4 a = na, b = nb;
+        if (t + nwarps < ntiles) prefetch(t + nwarps);
+        const bool live = q0 < cnt;
+        const uint32_t nvalid = live ? min((uint32_t)kTileK, cnt - q0) : 0u;
+        double v[kTileK];
+        if (live) {
+            const uint32_t idx[kTileK] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int j = 0; j < kTileK; ++j) v[j] = ((uint32_t)j < nvalid) ? tab[idx[j]] : 0.0;
+        } else {
+#pragma unroll
+            for (int j = 0; j < kTileK; ++j) v[j] = 0.0;
+        }
+        endmask &= (1u << nvalid) - 1u;
+        if (nvalid) endmask &= ~(1u << (nvalid - 1));
+        uint32_t fkey = kNone;
+        Acc fval = Ops::identity();
+        const bool multi = endmask != 0;
+        Acc acc = Ops::identity();
+        uint32_t key = sa;
+        bool first = true;
+#pragma unroll
+        for (int j = 0; j < kTileK; ++j) {
+            acc = Ops::combine(acc, Acc{v[j]});
+            if ((endmask >> j) & 1u) {
+                if (first) {
+                    fkey = key;
+                    fval = acc;
+                    first = false;
+                } else {
+                    reinterpret_cast<Acc*>(L.sums)[__ldg(L.key_slot + key)] = acc;
+                }
+                ++key;
+                acc = Ops::identity();
+            }
+        }
+        const uint32_t lkey = live ? key : kNone;
+        const Acc lval = acc;
+        if (!multi) {
+            fkey = lkey;
+            fval = lval;
+        }
+        Acc c = lval;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const Acc up = Ops::shfl_up(c, d);
+            const uint32_t k = __shfl_up_sync(kFull, lkey, d);
+            if (lane >= d && k == lkey) c = Ops::combine(up, c);
+        }
+        const uint32_t prev_key = __shfl_up_sync(kFull, lkey, 1);
+        const Acc prev_c = Ops::shfl_up(c, 1);
+        const uint32_t next_first = __shfl_down_sync(kFull, fkey, 1);
+        if (multi && live) {
+            const Acc tot = (lane > 0 && prev_key == fkey) ? Ops::combine(prev_c, fval) : fval;
+            tile_emit(p, L, t, __ldg(L.tile_head + t), __ldg(L.tile_tail + t), fkey, tot);
+        }
+        if (lkey != kNone && (lane == 31 || next_first != lkey))
+            tile_emit(p, L, t, __ldg(L.tile_head + t), __ldg(L.tile_tail + t), lkey, c);
+    }
+}
+
+void pr_split_free(gxb_state* s) {
+    for (int k = 0; k < 2; ++k) {
+        shadow_graph_free(s->split_g[k]);
+        s->split_g[k] = nullptr;
+        dfree(s->d_split_slot[k]);
+        dfree(s->d_split_partials[k]);
+        dfree(s->d_split_sum[k]);
+        s->d_split_slot[k] = nullptr;
+        s->d_split_partials[k] = nullptr;
+        s->d_split_sum[k] = nullptr;
+    }
+    s->hub_n = 0;
+}
+
+bool pr_split_wanted(const gxb_state* s) {
+    const gxb_graph* g = s->g;
+    return s->algo == GXB_ALGO_PAGERANK && options().pr_hub_slots > 0 && g->nparts == 1 && !s->msg32 &&
+           s->npeers == 0 && !options().pipeline_apply && g->tiles.num_xchunks == 1 && g->S > 0;
+}
+
+// build the hub / cold compacted CSCs and their tile plans (once per state and H)
+int pr_split_prepare(gxb_state* s, cudaStream_t st) {
+    gxb_graph* g = s->g;
+    const uint32_t H = (uint32_t)std::min<uint64_t>((uint64_t)options().pr_hub_slots, g->S);
+    if (s->hub_n == H && s->split_g[0]) return GXB_OK;
+    pr_split_free(s);
+    const uint64_t nz = g->tiles.nz_slots;
+    const uint64_t owned = g->hi - g->lo;
+    uint32_t* d_hcnt = nullptr;
+    GXB_CHECK(dalloc_t(&d_hcnt, nz + 1));
+    if (nz) k_hub_count<<<grid_for(nz), kBlock, 0, st>>>(g->d_in_off, g->d_in_src, nz, H, d_hcnt);
+    std::vector<uint32_t> hcnt(nz);
+    if (nz) GXB_CUDA(cudaMemcpyAsync(hcnt.data(), d_hcnt, 4 * nz, cudaMemcpyDeviceToHost, st));
+    GXB_CUDA(cudaStreamSynchronize(st));
+    const std::vector<uint32_t>& deg = g->h_indeg_sorted;
+    int rc = GXB_OK;
+    for (int k = 0; k < 2 && rc == GXB_OK; ++k) {
+        const bool hub = k == 1;
+        std::vector<uint32_t> list, cdeg;
+        for (uint64_t r = 0; r < nz; ++r) {
+            const uint32_t c = hub ? hcnt[r] : deg[r] - hcnt[r];
+            if (c) {
+                list.push_back((uint32_t)r);
+                cdeg.push_back(c);
+            }
+        }
+        const uint64_t n = list.size();
+        std::vector<uint64_t> coff(n + 1 + kOffPad, 0);
+        for (uint64_t i = 0; i < n; ++i) coff[i + 1] = coff[i] + cdeg[i];
+        const uint64_t total = coff[n];
+        for (uint64_t i = n + 1; i < coff.size(); ++i) coff[i] = total;
+        gxb_graph* sg = new gxb_graph();
+        s->split_g[k] = sg;
+        sg->ctx = g->ctx;
+        sg->part = 0;
+        sg->nparts = 1;
+        sg->lo = 0;
+        sg->hi = n;
+        sg->S = n;
+        sg->E = total;
+        sg->owned_edges = total;
+        sg->h_indeg_sorted = cdeg;
+        GXB_CHECK(dalloc_t(&sg->d_in_off, coff.size()));
+        GXB_CHECK(dalloc_t(&sg->d_in_src, total + kTileEdges));
+        GXB_CUDA(cudaMemsetAsync(sg->d_in_src, 0, 4 * (total + kTileEdges), st));
+        GXB_CHECK(dalloc_t(&s->d_split_slot[k], n + 1));
+        GXB_CUDA(cudaMemcpyAsync(sg->d_in_off, coff.data(), 8 * coff.size(), cudaMemcpyHostToDevice, st));
+        if (n) GXB_CUDA(cudaMemcpyAsync(s->d_split_slot[k], list.data(), 4 * n, cudaMemcpyHostToDevice, st));
+        if (n) k_split_copy<<<grid_for(32 * n), kBlock, 0, st>>>(g->d_in_off, g->d_in_src, d_hcnt, s->d_split_slot[k],
+                                                                  n, sg->d_in_off, hub ? 1 : 0, sg->d_in_src);
+        GXB_CUDA(cudaStreamSynchronize(st));  // list / coff host buffers die with this scope
+        rc = build_tile_plan(sg, st);
+        if (rc != GXB_OK) break;
+        if (sg->tiles.num_spans)
+            k_remap_u32<<<grid_for(sg->tiles.num_spans), kBlock, 0, st>>>(sg->tiles.d_span_slot, sg->tiles.num_spans,
+                                                                          s->d_split_slot[k]);
+        GXB_CHECK(dalloc(&s->d_split_partials[k], sizeof(PrOps::Acc) * (sg->tiles.num_partials + 1)));
+        GXB_CHECK(dalloc_t(&s->d_split_sum[k], owned + 1));
+        GXB_CUDA(cudaMemsetAsync(s->d_split_sum[k], 0, 8 * (owned + 1), st));
+    }
+    dfree(d_hcnt);
+    GXB_CUDA(cudaStreamSynchronize(st));
+    if (rc != GXB_OK) {
+        pr_split_free(s);
+        return rc;
+    }
+    s->hub_n = H;
+    return GXB_OK;
+}
+
+TileLaunch split_launch(gxb_state* s, int k) {
+    const gxb_graph* sg = s->split_g[k];
+    const TilePlan& T = sg->tiles;
+    TileLaunch L = tile_launch(s);
+    L.num_tiles = T.num_tiles;
+    L.tile_begin = 0;
+    L.owned_edges = sg->owned_edges;
+    L.in_off = sg->d_in_off;
+    L.in_src = sg->d_in_src;
+    L.tile_start = T.d_tile_start;
+    L.lane_slot = T.d_lane_slot;
+    L.lane_mask = T.d_lane_mask;
+    L.in_w = nullptr;
+    L.in_sw = nullptr;
+    L.sw_shift = 0;
+    L.tile_head = T.d_tile_head;
+    L.tile_tail = T.d_tile_tail;
+    L.span_first = T.d_span_first;
+    L.span_count = T.d_span_count;
+    L.span_pbase = T.d_span_pbase;
+    L.span_slot = T.d_span_slot;
+    L.partials = s->d_split_partials[k];
+    L.sums = s->d_split_sum[k];
+    L.key_slot = s->d_split_slot[k];
+    return L;
+}
+
+// one PageRank round over the split CSCs: hub pass, cold tiles, span folds, Apply
+int launch_pr_split(gxb_state* s, cudaStream_t st) {
+    GXB_CHECK(pr_split_prepare(s, st));
+    gxb_graph* g = s->g;
+    PrOps o = pr_ops(s);
+    const TileLaunch Lh = split_launch(s, 1), Lc = split_launch(s, 0);
+    using Pol = FusedPolicy<PrOps>;
+    Pol p{o, nullptr};
+    const size_t tab_bytes = 8ull * s->hub_n;
+    GXB_CUDA(cudaFuncSetAttribute(k_tile_hub, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 28672));
+    auto kern = k_tile_a<Pol, 6>;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, 0);
+    if (s->timing) GXB_CUDA(cudaEventRecord(kev_at(s, 0), st));
+    if (Lh.num_tiles) {
+        k_tile_hub<<<kNumSMs, kHubBlock, tab_bytes, st>>>(o.contrib_cur, s->hub_n, Lh);
+        s->launches++;
+    }
+    if (Lc.num_tiles) {
+        const uint64_t want = (Lc.num_tiles + (kBlock / 32) - 1) / (kBlock / 32);
+        const unsigned grid = (unsigned)std::min<uint64_t>(want, (uint64_t)std::max(1, per_sm) * kNumSMs);
+        kern<<<grid, kBlock, 0, st>>>(p, Lc);
+        s->launches++;
+    }
+    if (s->timing) {
+        GXB_CUDA(cudaEventRecord(kev_at(s, 1), st));
+        s->timing_pending = true;
+    }
+    for (int k = 0; k < 2; ++k) {
+        const TilePlan& T = s->split_g[k]->tiles;
+        if (T.num_spans) {
+            k_span_fold<PrOps><<<grid_for(T.num_spans), kBlock, 0, st>>>(
+                T.d_span_slot, T.d_span_count, T.d_span_pbase, 0, T.num_spans,
+                (const PrOps::Acc*)s->d_split_partials[k], (PrOps::Acc*)s->d_split_sum[k]);
+            s->launches++;
+        }
+    }
+    PrOps a = o;
+    a.hub_sum = s->d_split_sum[1];
+    const uint64_t owned = g->hi - g->lo;
+    if (owned) {
+        k_apply_sums<PrOps><<<grid_for(owned), kBlock, 0, st>>>(a, (const PrOps::Acc*)s->d_split_sum[0], g->lo, 0,
+                                                                 owned, g->tiles.nz_slots, s->d_stats);
+        s->launches++;
+    }
+    GXB_CUDA(cudaGetLastError());
+    return GXB_OK;
+}
+
 bool use_binned_pull() { return options().pull_kernel == 1; }
 
 
@@ -1307,6 +1621,7 @@ PrOps pr_ops(gxb_state* s) {
     o.hp = hot_prefix(s);
     o.hot = hot_slots(s, sizeof(double)) / s->g->nparts;
     o.hot1 = hot_l1_slots(s, sizeof(double));
+    o.hub_sum = nullptr;
     return o;
 }
 SsspOps sssp_ops(gxb_state* s) {
@@ -1714,6 +2029,7 @@ int gxb_state_free(gxb_state* s) {
     dfree(s->d_push_tmp);
     dfree(s->d_tile_partials);
     dfree(s->d_sums);
+    pr_split_free(s);
     gxb_lp_free(s);
     dfree(s->d_send);
     dfree(s->d_xsend);
@@ -1784,6 +2100,7 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
             case GXB_ALGO_PAGERANK:
                 if ((s->npeers > 0 || options().pipeline_apply) && g->tiles.num_xchunks > 1)
                     GXB_CHECK(pipelined_pagerank(s, st));
+                else if (pr_split_wanted(s)) GXB_CHECK(launch_pr_split(s, st));
                 else GXB_CHECK(launch_tile_and_apply(s, pr_ops(s), st));
                 break;
             case GXB_ALGO_SSSP: {

@@ -280,6 +280,8 @@ inline unsigned grid_for(uint64_t n, int block = kBlock, uint64_t cap = 148ull *
 }
 
 int build_pull_plan(gxb_graph* g, cudaStream_t st);
+int build_tile_plan(gxb_graph* g, cudaStream_t st);  // warp-tile plan over g->h_indeg_sorted / d_in_off
+void shadow_graph_free(gxb_graph* g);                // release a plan-only graph (device arrays + delete)
 int build_owned_order(gxb_graph* g);  // d_owned_d2s / owned_present
 uint64_t xchunk_bound(uint64_t owned, int k, int K);  // relative slot bound k of K exchange chunks
 
@@ -299,6 +301,8 @@ struct Options {
     int64_t exchange_chunks = 2;  // multi-GPU: exchange chunks (pipelined peer-write rounds; 2 measured best at N = 4)
     int64_t overlap_reserve_sms = 0;  // SMs left free while a chunked round computes (0 measured best)
     int64_t pr_message_bits = 64; // PageRank message (rank / out_deg) precision: 64 or 32 (f64 accumulation)
+    int64_t pr_hub_slots = 0;     // PageRank, one partition: in-edges from the first H source slots (the
+                                  // highest out-degrees) are summed from a shared-memory table (<= 28672)
 };
 Options& options();
 

@@ -195,6 +195,15 @@ struct gxb_state {
     void* d_tile_partials = nullptr;
     void* d_sums = nullptr;  // per owned slot: folded accumulator of the tile kernel
 
+    // PageRank hub split (option pr_hub_slots, one partition): in-edges from source slots
+    // < hub_n form the "hub" CSC (summed from a shared-memory table), the rest the "cold"
+    // CSC (LDGSTS tile kernel); both are compacted to their non-empty destinations
+    uint32_t hub_n = 0;
+    gxb_graph* split_g[2] = {nullptr, nullptr};   // 0 = cold, 1 = hub: CSC + tile plan only
+    uint32_t* d_split_slot[2] = {nullptr, nullptr};  // compacted destination -> owned slot
+    void* d_split_partials[2] = {nullptr, nullptr};
+    double* d_split_sum[2] = {nullptr, nullptr};  // per owned slot (zero where no such edge)
+
     // push scheduling (chunk counts, their inclusive scan, CUB scratch)
     uint32_t* d_push_counts = nullptr;
     uint32_t* d_push_cpre = nullptr;

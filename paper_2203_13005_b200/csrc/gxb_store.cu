@@ -34,6 +34,7 @@ Options& options() {
         if (const char* e = getenv("GXB_PUSH_ALPHA")) o.push_alpha = atol(e);
         if (const char* e = getenv("GXB_PULL_KERNEL")) o.pull_kernel = std::string(e) == "binned" ? 1 : 0;
         if (const char* e = getenv("GXB_PR_MESSAGE_BITS")) o.pr_message_bits = atol(e) == 32 ? 32 : 64;
+        if (const char* e = getenv("GXB_PR_HUB_SLOTS")) o.pr_hub_slots = std::min(28672L, std::max(0L, atol(e)));
         if (const char* e = getenv("GXB_TILE_ASYNC")) o.tile_async = atol(e) ? 1 : 0;
         if (const char* e = getenv("GXB_PIPELINE_APPLY")) o.pipeline_apply = atol(e) ? 1 : 0;
         if (const char* e = getenv("GXB_XCHUNK_POWER")) o.xchunk_power = std::min(4L, std::max(1L, atol(e)));
@@ -371,6 +372,12 @@ static void graph_release(gxb_graph* g) {
     dfree(g->tiles.d_span_slot);
 }
 
+void shadow_graph_free(gxb_graph* g) {
+    if (!g) return;
+    graph_release(g);
+    delete g;
+}
+
 // warp-tile plan of the edge-balanced pull merge: kTileEdges edges per warp;
 // slots crossing a tile boundary ("spans") combine per-tile partials
 // slot bound of exchange chunk k of K: owned * (k / K)^p (p = option xchunk_power, 1..4).
@@ -385,7 +392,7 @@ uint64_t xchunk_bound(uint64_t owned, int k, int K) {
     return (uint64_t)((unsigned __int128)owned * num / den);  // exact: peers recompute it
 }
 
-static int build_tile_plan(gxb_graph* g, cudaStream_t st) {
+int build_tile_plan(gxb_graph* g, cudaStream_t st) {
     TilePlan& T = g->tiles;
     const std::vector<uint32_t>& deg = g->h_indeg_sorted;
     const uint64_t owned = deg.size();
@@ -959,6 +966,9 @@ int gxb_set_option(const char* name, int64_t value) {
     } else if (n == "carveout") {
         if (value < -1 || value > 100) return fail(GXB_EINVAL, "carveout: -1 or 0..100");
         o.carveout = value;
+    } else if (n == "pr_hub_slots") {
+        if (value < 0 || value > 28672) return fail(GXB_EINVAL, "pr_hub_slots: 0..28672");
+        o.pr_hub_slots = value;
     } else if (n == "pr_message_bits") {
         if (value != 32 && value != 64) return fail(GXB_EINVAL, "pr_message_bits: 32 or 64");
         o.pr_message_bits = value;
@@ -985,6 +995,7 @@ int gxb_get_option(const char* name, int64_t* value) {
     else if (n == "pipeline_apply") *value = o.pipeline_apply;
     else if (n == "tile_async_minblocks") *value = o.tile_async_minblocks;
     else if (n == "pr_message_bits") *value = o.pr_message_bits;
+    else if (n == "pr_hub_slots") *value = o.pr_hub_slots;
     else if (n == "carveout") *value = o.carveout;
     else if (n == "overlap_reserve_sms") *value = o.overlap_reserve_sms;
     else if (n == "exchange_chunks") *value = o.exchange_chunks;
