@@ -31,7 +31,7 @@ class NumpyPartition:
         s = np.searchsorted(ids, src)
         d = np.searchsorted(ids, dst)
         self.V = V
-        b = [V * p // nparts for p in range(nparts + 1)]
+        b = self._cut(V, nparts, d)
         self.bounds = np.array(b, dtype=np.uint64)
         self.lo, self.hi = b[part], b[part + 1]
         owner = np.searchsorted(np.array(b[1:]), np.arange(V), side="right")
@@ -54,6 +54,9 @@ class NumpyPartition:
         self._arrays = {}
         self._last = None
         self.changed_slots = np.zeros(0, dtype=np.int64)
+
+    def _cut(self, V, nparts, d):
+        return [V * p // nparts for p in range(nparts + 1)]
 
     def _ptr(self, a):
         self._arrays[a.ctypes.data] = a
@@ -248,3 +251,37 @@ def test_cc_async_delta_exchange_matches_oracle(oracle_lib):
     ref = oracle_lib.OracleGraph(src, dst).run("cc")
     assert all(r[1] == ref.iterations and r[2] == ref.converged for r in res)
     np.testing.assert_array_equal(got, ref.attrs[:, 0])
+
+
+class CapacityNumpyPartition(NumpyPartition):
+    """Uneven partitions as gxb_graph_build_balanced cuts them: contiguous ranges whose
+    cost (12 B per in-edge + 64 B per vertex) is split 3 : 1 (balancer capacity factors)."""
+
+    CAPACITY = (3.0, 1.0)
+
+    def _cut(self, V, nparts, d):
+        cost = 12 * np.bincount(d, minlength=V).astype(np.float64) + 64
+        cum = np.concatenate([[0.0], np.cumsum(cost)])
+        share = np.cumsum([0.0] + list(self.CAPACITY[:nparts]))
+        share /= share[-1]
+        return [int(np.searchsorted(cum, cum[-1] * f, side="left")) if 0 < f < 1 else (0 if f == 0 else V)
+                for f in share]
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("algo", ["pagerank", "cc"])
+def test_capacity_weighted_partitions_match_oracle(oracle_lib, algo):
+    """Uneven owned slices (heterogeneous balancing): the dense all-gather with unequal
+    sizes (PageRank) and the delta exchange (CC) still give the oracle's results."""
+    from paper_2203_13005_b200.rmat import RmatParams, rmat_host
+    src, dst, _ = rmat_host(RmatParams(scale=9, seed=24, symmetric=algo == "cc"))
+    cap = 10 if algo == "pagerank" else 1000
+    res, got = _run(algo, src, dst, cap, cls=CapacityNumpyPartition)
+    sizes = [r[5] - r[4] for r in res]
+    assert sizes[0] > 2 * sizes[1]  # really uneven
+    ref = oracle_lib.OracleGraph(src, dst).run(algo, max_iterations=cap if algo == "pagerank" else None)
+    assert all(r[1] == ref.iterations for r in res)
+    if algo == "pagerank":
+        assert np.allclose(got, ref.attrs[:, 0], rtol=1e-12, atol=0)
+    else:
+        np.testing.assert_array_equal(got, ref.attrs[:, 0])
