@@ -1445,6 +1445,10 @@ int pr_split_prepare(gxb_state* s, cudaStream_t st) {
     const uint64_t nz = g->tiles.nz_slots;
     const uint64_t owned = g->hi - g->lo;
     uint32_t* d_hcnt = nullptr;
+    struct Scratch {  // freed on every exit path (GXB_CHECK returns early)
+        uint32_t*& p;
+        ~Scratch() { dfree(p); }
+    } scratch{d_hcnt};
     GXB_CHECK(dalloc_t(&d_hcnt, nz + 1));
     if (nz) k_hub_count<<<grid_for(nz), kBlock, 0, st>>>(g->d_in_off, g->d_in_src, nz, H, d_hcnt);
     std::vector<uint32_t> hcnt(nz);
@@ -1496,7 +1500,6 @@ int pr_split_prepare(gxb_state* s, cudaStream_t st) {
         GXB_CHECK(dalloc_t(&s->d_split_sum[k], owned + 1));
         GXB_CUDA(cudaMemsetAsync(s->d_split_sum[k], 0, 8 * (owned + 1), st));
     }
-    dfree(d_hcnt);
     GXB_CUDA(cudaStreamSynchronize(st));
     if (rc != GXB_OK) {
         pr_split_free(s);
