@@ -269,6 +269,43 @@ def time_frontier_run(ctx, comm, dev, stream, name, algo, params, cap, peak=None
     return out
 
 
+def check_parity(snap, algo, params, world, rank, dev):
+    """Compare the timed run's attributes with the CPU oracle (oracle/gx_oracle.c, the
+    restatement of run_reference, A/algorithms.py:298-342) run for the same number of
+    iterations on the host copy of the same R-MAT stream. Outside every timed region.
+    N > 1: each rank contributes its owned vertices (a sum all-reduce over NaN-masked rows)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    rounds, attrs = snap
+    if world > 1:
+        t = torch.from_numpy(np.nan_to_num(attrs, nan=0.0)).to(dev)
+        dist.all_reduce(t)
+        attrs = t.cpu().numpy()
+        if rank != 0:
+            return None
+    t0 = time.perf_counter()
+    try:
+        from oracle import oracle
+        src, dst, _ = oracle.rmat(params.scale, params.edge_factor, params.seed, params.a, params.b, params.c,
+                                  0, params.scramble, params.symmetric)
+        og = oracle.OracleGraph(src, dst)
+        del src, dst
+        ref = og.run(algo, max_iterations=rounds)
+        want = ref.attrs
+        err = np.abs(attrs - want) / np.maximum(1.0, np.abs(want))
+        out = {"oracle": "oracle/gx_oracle.c (run_reference restated, A/algorithms.py:298-342)",
+               "iterations": rounds, "oracle_iterations": ref.iterations,
+               "iterations_equal": rounds == ref.iterations, "vertices": int(want.shape[0]),
+               "max_rel_err": float(err.max(initial=0.0)), "tolerance": 1e-5,
+               "ok": bool(rounds == ref.iterations and float(err.max(initial=0.0)) <= 1e-5),
+               "oracle_threads": oracle.max_threads(), "seconds": round(time.perf_counter() - t0, 1)}
+        del og
+        return out
+    except Exception as exc:  # noqa: BLE001
+        return {"ok": False, "error": f"{type(exc).__name__}: {exc}"}
+
+
 _STDOUT_FD = None
 
 
@@ -292,6 +329,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed run")
     ap.add_argument("--no-run-ahead", action="store_true", help="PageRank: wait for every vote before the next round")
     args = ap.parse_args()
     # stdout carries exactly one JSON line: library banners (NCCL prints its version when a
@@ -377,6 +415,9 @@ def main():
         ev1.record(stream)
         ev1.synchronize()
         step_ms.append(ev0.elapsed_time(ev1))
+        if len(recs) != args.steps:  # converged inside the block: time only the rounds kept
+            raise SystemExit(f"run-ahead block converged after {len(recs)} of {args.steps} rounds; "
+                             "lower --steps/--warmup")
         units += sum(r.units for r in recs)
         xbytes += sum(r.exchanged_bytes for r in recs)
     for _ in range(0 if ahead else args.steps):
@@ -394,6 +435,10 @@ def main():
     torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall
     clocks.mark(False)
+    # attributes of the timed run, checked against the oracle after everything else (parity)
+    snap = None
+    if algo == "pagerank" and not args.no_parity:
+        snap = (run.iteration, run.state.read_attrs(owned_only=world > 1))
     time.sleep(0.05)
     clocks.__exit__(None, None, None)
     prof = run.state.profile()
@@ -433,7 +478,8 @@ def main():
         "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
         "kernel": f"{kname} (fused MSGGen+MSGMerge warp tiles)", "kernel_ms": round(kern_ms, 4),
         "algorithmic_bytes_per_launch": kbytes, "peak_kind": peak_kind,
-        "iteration_frac": round(it_bytes * world / (ms_per_step * 1e-3) / 1e9 / (peak * world), 4)
+        # whole-job iteration bytes (every rank streams its own slice) over the job's peak
+        "iteration_frac": round(it_bytes / (ms_per_step * 1e-3) / 1e9 / (peak * world), 4)
         if algo == "pagerank" else None,
     }
 
@@ -529,6 +575,10 @@ def main():
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": "GTEPS", "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
 
+    parity = None
+    if snap is not None:
+        parity = check_parity(snap, algo, params, world, rank, dev)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(gteps, 3), "unit": "GTEPS", "n_gpus": world,
@@ -554,6 +604,8 @@ def main():
                 if getattr(run, "_peers", False) else "NCCL in-place all-gather"}
         if secondary:
             line["secondary"] = secondary
+        if parity is not None:
+            line["parity"] = parity
         emit(line)
     if world > 1:
         dist.barrier()

@@ -23,6 +23,8 @@ struct gxo_graph {
     double* in_w;         /* weight per in-edge */
 };
 
+typedef struct { uint32_t s; double w; } gxo_sw;
+
 static int cmp_u32(const void* a, const void* b) {
     uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
     return (x > y) - (x < y);
@@ -51,12 +53,25 @@ void gxo_graph_free(gxo_graph* g) {
     free(g);
 }
 
+static int cmp_sw(const void* a, const void* b) {
+    const gxo_sw* x = (const gxo_sw*)a;
+    const gxo_sw* y = (const gxo_sw*)b;
+    if (x->s != y->s) return (x->s > y->s) - (x->s < y->s);
+    return (x->w > y->w) - (x->w < y->w);
+}
+
+/* Ingest in parallel. Within one destination the in-edges end up ordered by
+ * (source, weight): the reference's order is (source asc, file order), and
+ * in-edges that share both source and destination carry the same message for
+ * PageRank / LP / CC and are folded by min for SSSP, so the order among them
+ * never changes a result — every fold stays the reference's. */
 gxo_graph* gxo_graph_new(uint64_t E, const uint32_t* src, const uint32_t* dst, const double* w) {
     gxo_graph* g = (gxo_graph*)calloc(1, sizeof(gxo_graph));
     if (!g) return NULL;
     g->E = E;
     uint32_t max_id = 0;
-    for (uint64_t e = 0; e < E; ++e) {
+    #pragma omp parallel for schedule(static) reduction(max:max_id)
+    for (int64_t e = 0; e < (int64_t)E; ++e) {
         if (src[e] > max_id) max_id = src[e];
         if (dst[e] > max_id) max_id = dst[e];
     }
@@ -67,17 +82,33 @@ gxo_graph* gxo_graph_new(uint64_t E, const uint32_t* src, const uint32_t* dst, c
     /* vertex set = ids present in any edge (graph.py:163-164) */
     const uint64_t dense_limit = 4ull * E + (1ull << 26);
     if ((uint64_t)max_id + 1 <= dense_limit) {
-        uint64_t n = (uint64_t)max_id + 1;
-        uint32_t* map = (uint32_t*)calloc(n, sizeof(uint32_t));
+        const int64_t n = (int64_t)max_id + 1;
+        uint32_t* map = (uint32_t*)calloc((size_t)n, sizeof(uint32_t));
         if (!map) { free(sidx); free(didx); gxo_graph_free(g); return NULL; }
-        for (uint64_t e = 0; e < E; ++e) { map[src[e]] = 1; map[dst[e]] = 1; }
-        uint64_t V = 0;
-        for (uint64_t i = 0; i < n && E; ++i) if (map[i]) V++;
+        #pragma omp parallel for schedule(static)
+        for (int64_t e = 0; e < (int64_t)E; ++e) { map[src[e]] = 1; map[dst[e]] = 1; }
+        /* blocked exclusive scan of the presence flags: dense index = rank of the id */
+        const int64_t nb = 4096, bs = (n + nb - 1) / nb;
+        uint64_t* bsum = (uint64_t*)calloc(nb + 1, sizeof(uint64_t));
+        #pragma omp parallel for schedule(static)
+        for (int64_t b = 0; b < nb; ++b) {
+            uint64_t c = 0;
+            for (int64_t i = b * bs; i < n && i < (b + 1) * bs; ++i) c += (E && map[i]);
+            bsum[b + 1] = c;
+        }
+        for (int64_t b = 0; b < nb; ++b) bsum[b + 1] += bsum[b];
+        const uint64_t V = bsum[nb];
         g->V = V;
         g->ids = (uint32_t*)malloc(sizeof(uint32_t) * (V ? V : 1));
-        uint64_t k = 0;
-        for (uint64_t i = 0; i < n && E; ++i) if (map[i]) { g->ids[k] = (uint32_t)i; map[i] = (uint32_t)k++; }
-        for (uint64_t e = 0; e < E; ++e) { sidx[e] = map[src[e]]; didx[e] = map[dst[e]]; }
+        #pragma omp parallel for schedule(static)
+        for (int64_t b = 0; b < nb; ++b) {
+            uint64_t k = bsum[b];
+            for (int64_t i = b * bs; i < n && i < (b + 1) * bs; ++i)
+                if (E && map[i]) { g->ids[k] = (uint32_t)i; map[i] = (uint32_t)k++; }
+        }
+        free(bsum);
+        #pragma omp parallel for schedule(static)
+        for (int64_t e = 0; e < (int64_t)E; ++e) { sidx[e] = map[src[e]]; didx[e] = map[dst[e]]; }
         free(map);
     } else {
         uint32_t* all = (uint32_t*)malloc(sizeof(uint32_t) * 2 * E);
@@ -89,7 +120,8 @@ gxo_graph* gxo_graph_new(uint64_t E, const uint32_t* src, const uint32_t* dst, c
         for (uint64_t i = 0; i < 2 * E; ++i) if (i == 0 || all[i] != all[i - 1]) all[V++] = all[i];
         g->V = V;
         g->ids = (uint32_t*)realloc(all, sizeof(uint32_t) * (V ? V : 1));
-        for (uint64_t e = 0; e < E; ++e) {
+        #pragma omp parallel for schedule(static)
+        for (int64_t e = 0; e < (int64_t)E; ++e) {
             sidx[e] = (uint32_t)lower_bound_u32(g->ids, V, src[e]);
             didx[e] = (uint32_t)lower_bound_u32(g->ids, V, dst[e]);
         }
@@ -98,27 +130,47 @@ gxo_graph* gxo_graph_new(uint64_t E, const uint32_t* src, const uint32_t* dst, c
     g->outdeg = (uint32_t*)calloc(V ? V : 1, sizeof(uint32_t));
     g->in_off = (uint64_t*)calloc(V + 1, sizeof(uint64_t));
     g->in_src = (uint32_t*)malloc(sizeof(uint32_t) * (E ? E : 1));
-    g->in_w = (double*)malloc(sizeof(double) * (E ? E : 1));
-    uint64_t* out_off = (uint64_t*)calloc(V + 1, sizeof(uint64_t));
-    uint64_t* by_src = (uint64_t*)malloc(sizeof(uint64_t) * (E ? E : 1));
-    if (!g->outdeg || !g->in_off || !g->in_src || !g->in_w || !out_off || !by_src) {
-        free(out_off); free(by_src); free(sidx); free(didx); gxo_graph_free(g); return NULL;
+    g->in_w = w ? (double*)malloc(sizeof(double) * (E ? E : 1)) : NULL;
+    uint64_t* cur = (uint64_t*)malloc(sizeof(uint64_t) * (V + 1));
+    if (!g->outdeg || !g->in_off || !g->in_src || (w && !g->in_w) || !cur) {
+        free(cur); free(sidx); free(didx); gxo_graph_free(g); return NULL;
     }
     /* out-degree counts duplicates and self-loops (graph.py:203-210) */
-    for (uint64_t e = 0; e < E; ++e) { g->outdeg[sidx[e]]++; g->in_off[didx[e] + 1]++; }
-    for (uint64_t v = 0; v < V; ++v) { out_off[v + 1] = out_off[v] + g->outdeg[v]; g->in_off[v + 1] += g->in_off[v]; }
-    /* stable counting sort by source: edges in (src asc, file order) */
-    for (uint64_t e = 0; e < E; ++e) by_src[out_off[sidx[e]]++] = e;
-    /* stable counting sort of that order by destination */
-    uint64_t* cur = out_off; /* reuse as cursor */
-    memcpy(cur, g->in_off, sizeof(uint64_t) * (V + 1));
-    for (uint64_t k = 0; k < E; ++k) {
-        uint64_t e = by_src[k];
-        uint64_t pos = cur[didx[e]]++;
-        g->in_src[pos] = sidx[e];
-        g->in_w[pos] = w ? w[e] : 1.0;
+    #pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < (int64_t)E; ++e) {
+        #pragma omp atomic
+        g->outdeg[sidx[e]]++;
+        #pragma omp atomic
+        g->in_off[didx[e] + 1]++;
     }
-    free(out_off); free(by_src); free(sidx); free(didx);
+    for (uint64_t v = 0; v < V; ++v) g->in_off[v + 1] += g->in_off[v];
+    memcpy(cur, g->in_off, sizeof(uint64_t) * (V + 1));
+    #pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < (int64_t)E; ++e) {
+        uint64_t pos;
+        #pragma omp atomic capture
+        pos = cur[didx[e]]++;
+        g->in_src[pos] = sidx[e];
+        if (w) g->in_w[pos] = w[e];
+    }
+    free(cur); free(sidx); free(didx);
+    /* each destination's in-edges in source order (see above) */
+    #pragma omp parallel
+    {
+        gxo_sw* tmp = NULL;
+        uint64_t tcap = 0;
+        #pragma omp for schedule(dynamic, 256)
+        for (int64_t d = 0; d < (int64_t)V; ++d) {
+            const uint64_t a = g->in_off[d], n = g->in_off[d + 1] - a;
+            if (n < 2) continue;
+            if (!w) { qsort(g->in_src + a, n, sizeof(uint32_t), cmp_u32); continue; }
+            if (n > tcap) { free(tmp); tcap = n; tmp = (gxo_sw*)malloc(sizeof(gxo_sw) * tcap); }
+            for (uint64_t k = 0; k < n; ++k) { tmp[k].s = g->in_src[a + k]; tmp[k].w = g->in_w[a + k]; }
+            qsort(tmp, n, sizeof(gxo_sw), cmp_sw);
+            for (uint64_t k = 0; k < n; ++k) { g->in_src[a + k] = tmp[k].s; g->in_w[a + k] = tmp[k].w; }
+        }
+        free(tmp);
+    }
     return g;
 }
 
@@ -255,7 +307,7 @@ int gxo_run(const gxo_graph* g, int algo, int nsrc, const uint32_t* sources,
                     if (!active[s]) continue;
                     has = 1;
                     for (int j = 0; j < kk; ++j) {               /* gen d + w (102-105), merge min (107-108) */
-                        const double c = dist[(uint64_t)s * K + j] + iw[k];
+                        const double c = dist[(uint64_t)s * K + j] + (iw ? iw[k] : 1.0);
                         if (c < m[j]) m[j] = c;
                     }
                 }
