@@ -217,7 +217,7 @@ def algorithmic_bytes(algo, E, V, units=None, nz=None):
     return 8 * (units if units is not None else E) + 12 * V
 
 
-def time_frontier_run(ctx, comm, dev, stream, name, algo, params, cap, peak=None):
+def time_frontier_run(ctx, comm, dev, stream, name, algo, params, cap, peak=None, parity=False):
     """One full run (to convergence or cap) of a frontier algorithm; the first run warms
     allocations, the second is timed per iteration with CUDA events."""
     import torch
@@ -247,6 +247,7 @@ def time_frontier_run(ctx, comm, dev, stream, name, algo, params, cap, peak=None
         t1.record(stream)
         t1.synchronize()
         ms = t0.elapsed_time(t1)
+        attrs = st.read_attrs() if parity and _rep == 1 else None
         st.free()
     scanned = sum(x.units for x in r.records)
     out = {"workload": name, "num_edges": g.num_edges, "num_vertices": g.num_vertices,
@@ -266,13 +267,48 @@ def time_frontier_run(ctx, comm, dev, stream, name, algo, params, cap, peak=None
                                       "median_ms": round(med, 3), "achieved": round(gbs, 1), "peak": peak,
                                       "unit": "GB/s", "frac": round(gbs / peak, 4)}
     g.free()
+    if attrs is not None:  # outside the timed runs: the oracle on the host copy of the stream
+        out["parity"] = oracle_parity(algo, params, r.iteration, attrs,
+                                      [x.changed for x in r.records], [x.units for x in r.records], cap)
     return out
 
 
+def oracle_parity(algo, params, iterations, attrs, changed=None, units=None, cap=None):
+    """Compare a device run with the CPU oracle (oracle/gx_oracle.c, run_reference restated,
+    A/algorithms.py:298-342) on the same R-MAT stream: SSSP / CC / LP bit-exact with equal
+    per-iteration changed / GEN-unit traces, PageRank within 1e-5 relative per vertex."""
+    import numpy as np
+    t0 = time.perf_counter()
+    try:
+        from oracle import oracle
+        src, dst, w = oracle.rmat(params.scale, params.edge_factor, params.seed, params.a, params.b, params.c,
+                                  params.wmax if algo == "sssp" else 0, params.scramble, params.symmetric)
+        og = oracle.OracleGraph(src, dst, None if w is None else w.astype(np.float64))
+        del src, dst, w
+        ref = og.run(algo, max_iterations=cap if cap is not None else (iterations if algo == "pagerank" else None))
+        want = ref.attrs
+        out = {"oracle": "oracle/gx_oracle.c (run_reference restated, A/algorithms.py:298-342)",
+               "iterations": iterations, "oracle_iterations": ref.iterations,
+               "iterations_equal": iterations == ref.iterations, "vertices": int(want.shape[0])}
+        if algo == "pagerank":
+            err = np.abs(attrs - want) / np.maximum(1.0, np.abs(want))
+            out.update(max_rel_err=float(err.max(initial=0.0)), tolerance=1e-5,
+                       ok=bool(out["iterations_equal"] and float(err.max(initial=0.0)) <= 1e-5))
+        else:
+            mism = int((attrs != want).sum())
+            traces = (changed is None or list(changed) == ref.changed.tolist()) and \
+                (units is None or list(units) == ref.units.tolist())
+            out.update(mismatches=mism, bit_exact=mism == 0, traces_equal=bool(traces),
+                       ok=bool(out["iterations_equal"] and mism == 0 and traces))
+        out.update(oracle_threads=oracle.max_threads(), seconds=round(time.perf_counter() - t0, 1))
+        del og
+        return out
+    except Exception as exc:  # noqa: BLE001
+        return {"ok": False, "error": f"{type(exc).__name__}: {exc}"}
+
+
 def check_parity(snap, algo, params, world, rank, dev):
-    """Compare the timed run's attributes with the CPU oracle (oracle/gx_oracle.c, the
-    restatement of run_reference, A/algorithms.py:298-342) run for the same number of
-    iterations on the host copy of the same R-MAT stream. Outside every timed region.
+    """The timed run's attributes against the oracle for the same number of iterations.
     N > 1: each rank contributes its owned vertices (a sum all-reduce over NaN-masked rows)."""
     import numpy as np
     import torch
@@ -284,26 +320,7 @@ def check_parity(snap, algo, params, world, rank, dev):
         attrs = t.cpu().numpy()
         if rank != 0:
             return None
-    t0 = time.perf_counter()
-    try:
-        from oracle import oracle
-        src, dst, _ = oracle.rmat(params.scale, params.edge_factor, params.seed, params.a, params.b, params.c,
-                                  0, params.scramble, params.symmetric)
-        og = oracle.OracleGraph(src, dst)
-        del src, dst
-        ref = og.run(algo, max_iterations=rounds)
-        want = ref.attrs
-        err = np.abs(attrs - want) / np.maximum(1.0, np.abs(want))
-        out = {"oracle": "oracle/gx_oracle.c (run_reference restated, A/algorithms.py:298-342)",
-               "iterations": rounds, "oracle_iterations": ref.iterations,
-               "iterations_equal": rounds == ref.iterations, "vertices": int(want.shape[0]),
-               "max_rel_err": float(err.max(initial=0.0)), "tolerance": 1e-5,
-               "ok": bool(rounds == ref.iterations and float(err.max(initial=0.0)) <= 1e-5),
-               "oracle_threads": oracle.max_threads(), "seconds": round(time.perf_counter() - t0, 1)}
-        del og
-        return out
-    except Exception as exc:  # noqa: BLE001
-        return {"ok": False, "error": f"{type(exc).__name__}: {exc}"}
+    return oracle_parity(algo, params, rounds, attrs)
 
 
 _STDOUT_FD = None
@@ -515,7 +532,7 @@ def main():
         for t in range(args.steps):
             b, nb = t % 2, (t + 1) % 2
             stream.wait_event(ev_in[b])
-            st.attrs_install(b, stream)                       # update("pull_from_upper")
+            e2e_run.install(b, stream)                        # update("pull_from_upper") + peer mirrors
             ev_inst[b].record(stream)
             if t + 1 < args.steps:
                 if t >= 1:
@@ -557,7 +574,8 @@ def main():
                 ("sssp-s26", "sssp", RmatParams(scale=scale, seed=1, wmax=63), None),
                 ("cc-s24", "cc", RmatParams(scale=min(scale, 24), seed=1, symmetric=True), None),
                 ("lp-s24-a65", "lp", RmatParams(scale=min(scale, 24), seed=1, a=0.65, b=0.15, c=0.15), 15)):
-            secondary.append(time_frontier_run(ctx, comm, dev, stream, wname, walgo, wparams, wcap, peak))
+            secondary.append(time_frontier_run(ctx, comm, dev, stream, wname, walgo, wparams, wcap, peak,
+                                               parity=not args.no_parity))
             torch.cuda.empty_cache()
 
     cpu = None

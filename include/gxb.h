@@ -302,6 +302,16 @@ int gxb_read_attrs(gxb_state* s, double* host_out, int owned_only, void* stream)
  * for distances), else GXB_ERANGE. */
 int gxb_write_attrs(gxb_state* s, const double* host_in, void* stream);
 
+/* the sync round's deliver from host values (Agent.deliver, A/agent.py:584-592; the
+ * values come from the upper system's gdq, A/engine.py:255-266): install n mirror values
+ * (vertices owned by OTHER partitions, given as dense indices = rank of the id among the
+ * present ids, same value encoding as gxb_read_attrs) into this partition's source
+ * replica. SSSP / CC / LP: the delivered vertices become active sources of the next
+ * round (changed set = next frontier), exactly like received exchange records.
+ * An owned or absent target is GXB_EINVAL; a non-representable value GXB_ERANGE. */
+int gxb_attrs_deliver(gxb_state* s, const uint64_t* host_dense, const double* host_vals, uint64_t n,
+                      void* stream);
+
 /* asynchronous staging for a pipelined agent loop (no host synchronisation; the
  * caller orders the copy and compute streams with events): h2d copies pinned host
  * attributes into staging buffer `buf` (0/1), install scatters them into the state,

@@ -5,8 +5,28 @@ from __future__ import annotations
 
 import ctypes
 import os
+import sys
 
-from .channel import ProtocolError
+
+class ProtocolError(RuntimeError):
+    """A lifecycle / protocol violation (the reference's accelgraph.channel.ProtocolError)."""
+
+
+_joint_protocol_error = None
+
+
+def _protocol_error_type():
+    """When the reference package is loaded (the drop-in, dropin.py), raise a type that is
+    both this ProtocolError and accelgraph.channel.ProtocolError, so the reference's own
+    handlers and tests catch it (A/channel.py ProtocolError)."""
+    global _joint_protocol_error
+    ref = sys.modules.get("accelgraph.channel")
+    ref_cls = getattr(ref, "ProtocolError", None)
+    if ref_cls is None or issubclass(ProtocolError, ref_cls):
+        return ProtocolError
+    if _joint_protocol_error is None or not issubclass(_joint_protocol_error, ref_cls):
+        _joint_protocol_error = type("ProtocolError", (ProtocolError, ref_cls), {})
+    return _joint_protocol_error
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libgxb200.so")
@@ -122,6 +142,7 @@ def _sig(L):
         "gxb_read_attrs": (I, [P, P, I, P]),
         "gxb_write_attrs": (I, [P, P, P]),
         "gxb_attrs_h2d": (I, [P, P, I, P]),
+        "gxb_attrs_deliver": (I, [P, P, P, U64, P]),
         "gxb_attrs_scope": (I, [P, I]),
         "gxb_stats_device": (I, [P, P, P]),
         "gxb_stats_async": (I, [P, I]),
@@ -178,7 +199,7 @@ def check(rc: int) -> int:
     if rc in (GXB_EINVAL, GXB_ERANGE, GXB_ENOTOWNED):
         raise ValueError(msg)
     if rc in (GXB_EPROTO, GXB_ESTATE):
-        raise ProtocolError(msg)
+        raise _protocol_error_type()(msg)
     if rc == GXB_ENOMEM:
         raise MemoryError(msg)
     raise GxbError(f"{msg} (status {rc})")

@@ -861,13 +861,81 @@ struct PushLaunch {
 // touched bitmap deduplicates the next frontier.
 constexpr uint32_t kPushChunk = 256;
 
-__global__ void k_push_counts(const uint32_t* __restrict__ frontier, uint64_t n, const uint64_t* __restrict__ out_off,
-                              uint32_t* counts, uint32_t chunk = kPushChunk) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = frontier[i];
-        const uint64_t d = out_off[s + 1] - out_off[s];
-        counts[i] = (uint32_t)((d + chunk - 1) / chunk);
+// Inclusive prefix of the frontier's CSR row lengths (rowpre of the edge-balanced push), in
+// one pass: decoupled look-back over kScanTile-element tiles. status[0] is the tile ticket
+// (tiles run in ticket order, so every predecessor is resident or done), status[1 + t] =
+// (flag << 32) | value of tile t, flag 1 = tile aggregate, 2 = inclusive prefix. The caller
+// zeroes status[0 .. tiles] first. Row lengths are < 2^32 in total (E < 2^32 per build).
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kBlock * kScanItems;
+
+__global__ void __launch_bounds__(kBlock) k_push_rowpre(const uint32_t* __restrict__ frontier, uint64_t n,
+                                                        const uint64_t* __restrict__ out_off, uint32_t* rowpre,
+                                                        unsigned long long* status) {
+    __shared__ uint32_t s_tile, s_prefix;
+    __shared__ uint32_t s_warp[kBlock / 32];
+    if (threadIdx.x == 0) s_tile = (uint32_t)atomicAdd(status, 1ull);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t i0 = (uint64_t)tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+    uint32_t run = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        uint32_t d = 0;
+        if (i0 + j < n) {
+            const uint32_t s = __ldg(frontier + i0 + j);
+            d = (uint32_t)(__ldg(out_off + s + 1) - __ldg(out_off + s));
+        }
+        run += d;
+        v[j] = run;
     }
+    // block scan of the per-thread totals
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < kBlock / 32 ? s_warp[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < kBlock / 32) s_warp[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const uint32_t excl_thread = x - run + (warp ? s_warp[warp - 1] : 0u);
+    if (threadIdx.x == 0) {
+        const uint32_t agg = s_warp[kBlock / 32 - 1];
+        unsigned long long* st = status + 1;
+        uint32_t prefix = 0;
+        if (tile == 0) {
+            atomicExch(st, (2ull << 32) | agg);
+        } else {
+            atomicExch(st + tile, (1ull << 32) | agg);
+            for (int64_t p = (int64_t)tile - 1; p >= 0;) {
+                const unsigned long long w = atomicAdd(st + p, 0ull);
+                const uint32_t flag = (uint32_t)(w >> 32);
+                if (flag == 0) continue;  // predecessor still summing its tile
+                prefix += (uint32_t)w;
+                if (flag == 2) break;
+                --p;
+            }
+            atomicExch(st + tile, (2ull << 32) | (uint32_t)(prefix + agg));
+        }
+        s_prefix = prefix;
+    }
+    __syncthreads();
+    const uint32_t base = s_prefix + excl_thread;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j)
+        if (i0 + j < n) rowpre[i0 + j] = base + v[j];
 }
 
 struct SsspPush {
@@ -1044,10 +1112,31 @@ __global__ void k_read_attrs(int algo, int arity, const uint32_t* __restrict__ d
 }
 
 // attributes in ascending-id order -> slots (the agent's pull_from_upper)
+// Frontier algorithms: an installed value that differs from the current one is a change the
+// next round must propagate — the vertex joins the frontier (active bit, list, GEN units),
+// like a received exchange record; raising a distance / label is flagged (raised).
+struct InstallMarks {
+    uint32_t* active = nullptr;          // nullptr: PageRank (every vertex is active anyway)
+    uint32_t* list = nullptr;
+    unsigned long long* count = nullptr;
+    unsigned long long* units = nullptr;
+    unsigned long long* raised = nullptr;
+};
+
+__device__ __forceinline__ void mark_installed(const InstallMarks& m, uint32_t s, const uint32_t* outdeg,
+                                               bool raised) {
+    if (!m.active) return;
+    if (bit_set_atomic(m.active, s)) {
+        m.list[atomicAdd(m.count, 1ull)] = s;
+        atomicAdd(m.units, (unsigned long long)outdeg[s]);
+    }
+    if (raised) atomicOr(m.raised, 1ull);
+}
+
 __global__ void k_write_attrs(int algo, int arity, const uint32_t* __restrict__ d2s, uint64_t V,
                               const uint32_t* __restrict__ outdeg, const double* __restrict__ in, double* rank,
                               double* contrib, uint4* dist_cur, uint4* dist_next, uint32_t* lab_cur,
-                              uint32_t* lab_next, uint32_t* bad, bool msg32) {
+                              uint32_t* lab_next, uint32_t* bad, bool msg32, InstallMarks marks) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < V; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t s = d2s[i];
         if (algo == GXB_ALGO_PAGERANK) {
@@ -1066,15 +1155,20 @@ __global__ void k_write_attrs(int algo, int arity, const uint32_t* __restrict__ 
                 else l[j] = (uint32_t)x;
             }
             const uint4 v = make_uint4(l[0], l[1], l[2], l[3]);
+            const uint4 o = dist_cur[s];
             dist_cur[s] = v;
             dist_next[s] = v;
+            if (v.x != o.x || v.y != o.y || v.z != o.z || v.w != o.w)
+                mark_installed(marks, s, outdeg, v.x > o.x || v.y > o.y || v.z > o.z || v.w > o.w);
         } else {
             const double x = in[i];
             if (!(x >= 0.0 && x < 4294967295.0 && x == floor(x))) {
                 atomicOr(bad, 1u);
             } else {
-                lab_cur[s] = (uint32_t)x;
-                lab_next[s] = (uint32_t)x;
+                const uint32_t o = lab_cur[s], v = (uint32_t)x;
+                lab_cur[s] = v;
+                lab_next[s] = v;
+                if (v != o) mark_installed(marks, s, outdeg, v > o);
             }
         }
     }
@@ -1676,7 +1770,7 @@ int pipelined_pagerank(gxb_state* s, cudaStream_t st) {
 // reach 1 / pull_dense_div of the edges (0 = always test)
 bool dense_pull(const gxb_state* s) {
     const uint32_t div = options().pull_dense_div;
-    return div != 0 && s->units_cur * (uint64_t)div >= s->g->E;
+    return !s->nonmonotone && div != 0 && s->units_cur * (uint64_t)div >= s->g->E;
 }
 
 int begin_round(gxb_state* s, cudaStream_t st) {
@@ -1733,17 +1827,22 @@ int end_round(gxb_state* s, int direction, cudaStream_t st) {
 
 int collect_stats(gxb_state* s);
 
-// an asynchronous unpack (gxb_exchange_unpack_regions) appended received vertices to the
-// frontier on the device: refresh the host copies of its length and GEN units
+// an asynchronous unpack (gxb_exchange_unpack_regions) or an install of changed values
+// (gxb_attrs_install / gxb_write_attrs) appended vertices to the frontier on the device:
+// refresh the host copies of its length and GEN units
 int settle_unpack(gxb_state* s) {
-    if (!s->unpack_pending) return GXB_OK;
+    if (!s->unpack_pending && !s->install_pending) return GXB_OK;
     GXB_CHECK(collect_stats(s));
-    unsigned long long v[2] = {0, 0};
+    unsigned long long v[4] = {0, 0, 0, 0};
     GXB_CUDA(cudaMemcpy(&v[0], s->d_fcount, 8, cudaMemcpyDeviceToHost));
-    GXB_CUDA(cudaMemcpy(&v[1], s->d_xscratch + 1, 8, cudaMemcpyDeviceToHost));
+    GXB_CUDA(cudaMemcpy(&v[1], s->d_xscratch + 1, 24, cudaMemcpyDeviceToHost));
     s->frontier_len = v[0];
-    s->units_cur += v[1];
-    s->unpack_pending = false;
+    if (s->unpack_pending) s->units_cur += v[1];
+    if (s->install_pending) {
+        s->units_cur += v[2];
+        if (v[3]) s->nonmonotone = true;
+    }
+    s->unpack_pending = s->install_pending = false;
     return GXB_OK;
 }
 
@@ -1801,15 +1900,28 @@ int collect_stats(gxb_state* s) {
 
 }  // namespace
 
+namespace gxb {
+int state_settle(gxb_state* s) {
+    GXB_CHECK(collect_stats(s));
+    return settle_unpack(s);
+}
+}  // namespace gxb
+
 // push scheduling buffers, allocated with the state so no iteration pays for cudaMalloc
 static int alloc_push(gxb_state* s) {
     const gxb_graph* g = s->g;
-    GXB_CHECK(dalloc_t(&s->d_push_counts, g->S + 1));
     GXB_CHECK(dalloc_t(&s->d_push_cpre, g->S + 1));
-    size_t tb = 0;
-    GXB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, s->d_push_counts, s->d_push_cpre, (int64_t)(g->S + 1)));
-    s->push_tmp_bytes = tb;
-    GXB_CHECK(dalloc(&s->d_push_tmp, tb));
+    GXB_CHECK(dalloc_t(&s->d_scan_status, g->S / kScanTile + 2));
+    return GXB_OK;
+}
+
+// rowpre of the frontier (k_push_rowpre), one kernel
+static int launch_rowpre(gxb_state* s, uint64_t nf, cudaStream_t st) {
+    const uint64_t tiles = (nf + kScanTile - 1) / kScanTile;
+    GXB_CUDA(cudaMemsetAsync(s->d_scan_status, 0, 8 * (tiles + 1), st));
+    k_push_rowpre<<<(unsigned)tiles, kBlock, 0, st>>>(s->d_frontier[0], nf, s->g->d_out_off, s->d_push_cpre,
+                                                      s->d_scan_status);
+    s->launches++;
     return GXB_OK;
 }
 
@@ -1875,6 +1987,9 @@ int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, 
         if (V) {
             k_pr_init<<<grid, kBlock, 0, st>>>(s->d_rank[0], s->d_contrib[0], g->d_outdeg, g->d_slot2id, V, s->msg32);
             cudaMemcpyAsync(s->d_rank[1], s->d_rank[0], 8 * V, cudaMemcpyDeviceToDevice, st);
+            // both contribution buffers start valid: a mirror that never changes is never
+            // re-sent by a changed-values-only sync (gxb_attrs_deliver)
+            cudaMemcpyAsync(s->d_contrib[1], s->d_contrib[0], (s->msg32 ? 4 : 8) * V, cudaMemcpyDeviceToDevice, st);
         }
         units0 = s->owned_outdeg_sum;
     } else if (algo == GXB_ALGO_SSSP) {
@@ -2027,9 +2142,8 @@ int gxb_state_free(gxb_state* s) {
             if (s->kring[i]) cudaEventDestroy(s->kring[i]);
         delete[] s->kring;
     }
-    dfree(s->d_push_counts);
     dfree(s->d_push_cpre);
-    dfree(s->d_push_tmp);
+    dfree(s->d_scan_status);
     dfree(s->d_tile_partials);
     dfree(s->d_sums);
     pr_split_free(s);
@@ -2083,15 +2197,9 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
     }
     const uint64_t owned = g->hi - g->lo;
     if (lp_sparse) {
-        if (!s->d_push_counts) GXB_CHECK(alloc_push(s));
+        if (!s->d_scan_status) GXB_CHECK(alloc_push(s));
         const uint64_t nf = s->frontier_len;
-        if (nf) {
-            // row lengths (chunk 1): the push is edge-balanced over the concatenated rows
-            k_push_counts<<<grid_for(nf), kBlock, 0, st>>>(s->d_frontier[0], nf, g->d_out_off, s->d_push_counts, 1u);
-            size_t tb = s->push_tmp_bytes;
-            GXB_CUDA(cub::DeviceScan::InclusiveSum(s->d_push_tmp, tb, s->d_push_counts, s->d_push_cpre, (int64_t)nf, st));
-            s->launches += 2;
-        }
+        if (nf) GXB_CHECK(launch_rowpre(s, nf, st));  // the push is edge-balanced over the concatenated rows
         GXB_CHECK(gxb_lp_push(s, st, s->d_push_cpre));
         s->launches += 1;
         GXB_CHECK(end_round(s, GXB_DIR_PULL, st));  // commits lab_next like a pull round
@@ -2156,13 +2264,10 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
         P.list_next = s->d_frontier[1];
         P.count_next = s->d_fcount + 1;
         FrontierView f = frontier_view(s);
-        if (!s->d_push_counts) GXB_CHECK(alloc_push(s));
+        if (!s->d_scan_status) GXB_CHECK(alloc_push(s));
         if (P.nfront) {
-            s->launches += 3;  // counts, scan, push
-            k_push_counts<<<grid_for(P.nfront), kBlock, 0, st>>>(P.frontier, P.nfront, P.out_off, s->d_push_counts, 1u);
-            size_t tb = s->push_tmp_bytes;
-            GXB_CUDA(cub::DeviceScan::InclusiveSum(s->d_push_tmp, tb, s->d_push_counts, s->d_push_cpre,
-                                                   (int64_t)P.nfront, st));
+            GXB_CHECK(launch_rowpre(s, P.nfront, st));
+            s->launches++;  // the push
             const unsigned grid = grid_for((s->units_cur / kPushChunk + 1) * 32, kBlock, 148ull * 16);
             if (s->algo == GXB_ALGO_SSSP)
                 k_push<SsspPush><<<grid, kBlock, 0, st>>>(SsspPush{s->d_dist_cur, s->d_dist_next}, P, s->d_push_cpre);
@@ -2406,6 +2511,21 @@ int gxb_read_attrs(gxb_state* s, double* host_out, int owned_only, void* stream)
     return GXB_OK;
 }
 
+// install marks of one install: counters zeroed by the first install since the last round
+static int install_marks(gxb_state* s, cudaStream_t st, InstallMarks* m) {
+    *m = InstallMarks{};
+    if (s->algo == GXB_ALGO_PAGERANK) return GXB_OK;
+    if (!s->d_xscratch) GXB_CHECK(dalloc_t(&s->d_xscratch, 4));
+    if (!s->install_pending) GXB_CUDA(cudaMemsetAsync(s->d_xscratch + 2, 0, 16, st));
+    s->install_pending = true;
+    m->active = s->d_active[0];
+    m->list = s->d_frontier[0];
+    m->count = s->d_fcount;
+    m->units = s->d_xscratch + 2;
+    m->raised = s->d_xscratch + 3;
+    return GXB_OK;
+}
+
 int gxb_write_attrs(gxb_state* s, const double* host_in, void* stream) {
     if (!s) return fail(GXB_EINVAL, "gxb_write_attrs: null state");
     if (s->in_round) return fail(GXB_ESTATE, "gxb_write_attrs: a round is open");
@@ -2420,9 +2540,11 @@ int gxb_write_attrs(gxb_state* s, const double* host_in, void* stream) {
     GXB_CUDA(cudaMemcpyAsync(s->d_stage, host_in, 8 * V * s->arity, cudaMemcpyHostToDevice, st));
     uint32_t* d_bad = reinterpret_cast<uint32_t*>(s->d_fcount) + 2;  // scratch word of counter [1]
     GXB_CUDA(cudaMemsetAsync(d_bad, 0, 4, st));
+    InstallMarks marks;
+    GXB_CHECK(install_marks(s, st, &marks));
     k_write_attrs<<<grid_for(V), kBlock, 0, st>>>(s->algo, s->arity, g->d_dense2slot, V, g->d_outdeg, s->d_stage,
                                                   s->d_rank[s->cur], s->d_contrib[s->cur], s->d_dist_cur, s->d_dist_next,
-                                                  s->d_lab_cur, s->d_lab_next, d_bad, s->msg32);
+                                                  s->d_lab_cur, s->d_lab_next, d_bad, s->msg32, marks);
     uint32_t bad = 0;
     GXB_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
     GXB_CUDA(cudaStreamSynchronize(st));
@@ -2491,9 +2613,11 @@ int gxb_attrs_install(gxb_state* s, int buf, void* stream) {
     stage_order(s, &d2s, &n);
     if (!n) return GXB_OK;
     uint32_t* d_bad = reinterpret_cast<uint32_t*>(s->d_fcount) + 2;  // sticky flag, checked by gxb_attrs_check
+    InstallMarks marks;
+    GXB_CHECK(install_marks(s, (cudaStream_t)stream, &marks));
     k_write_attrs<<<grid_for(n), kBlock, 0, (cudaStream_t)stream>>>(
         s->algo, s->arity, d2s, n, g->d_outdeg, s->d_stage_in[buf], s->d_rank[s->cur], s->d_contrib[s->cur],
-        s->d_dist_cur, s->d_dist_next, s->d_lab_cur, s->d_lab_next, d_bad, s->msg32);
+        s->d_dist_cur, s->d_dist_next, s->d_lab_cur, s->d_lab_next, d_bad, s->msg32, marks);
     GXB_CUDA(cudaGetLastError());
     return GXB_OK;
 }

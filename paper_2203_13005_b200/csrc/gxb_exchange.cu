@@ -70,7 +70,7 @@ __global__ void k_unpack(int algo, const uint32_t* __restrict__ rec, uint64_t n,
         const uint64_t i = i0 + lane;
         const uint32_t* r = rec + i * W;
         const uint32_t s = i < n ? r[0] : lo;
-        const bool take = i < n && (s < lo || s >= hi);  // skip own records echoed back by the all-gather
+        bool take = i < n && (s < lo || s >= hi);  // skip own records echoed back by the all-gather
         if (take) {
             if (algo == GXB_ALGO_SSSP) {
                 const uint4 d = make_uint4(r[1], r[2], r[3], r[4]);
@@ -80,8 +80,9 @@ __global__ void k_unpack(int algo, const uint32_t* __restrict__ rec, uint64_t n,
                 lab_cur[s] = r[1];
                 lab_next[s] = r[1];
             }
-            atomicOr(active + (s >> 5), 1u << (s & 31));
-            u += outdeg[s];
+            // a vertex already in the frontier (e.g. re-sent after an install) is listed once
+            take = bit_set_atomic(active, s);
+            if (take) u += outdeg[s];
         }
         const unsigned m = __ballot_sync(0xffffffffu, take);
         if (!m) continue;
@@ -92,6 +93,54 @@ __global__ void k_unpack(int algo, const uint32_t* __restrict__ rec, uint64_t n,
     }
     for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
     if (lane == 0 && u) atomicAdd(units, u);
+}
+
+// the sync round's deliver (A/agent.py:584-592) from host values: (dense index, value) pairs
+// of mirror vertices -> exchange records (SSSP / CC / LP), or straight into the PageRank
+// contribution replica. bad: 1 = value not representable, 2 = target owned or out of range.
+__global__ void k_deliver(int algo, int arity, const uint64_t* __restrict__ dense, const double* __restrict__ vals,
+                          uint64_t n, uint64_t V, const uint32_t* __restrict__ d2s, uint64_t lo, uint64_t hi,
+                          const uint32_t* __restrict__ outdeg, double* rank0, double* rank1, double* contrib0,
+                          double* contrib1, bool msg32, uint32_t* rec, uint32_t* bad) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t d = dense[i];
+        if (d >= V) { atomicOr(bad, 2u); continue; }
+        const uint32_t s = d2s[d];
+        if (s >= lo && s < hi) { atomicOr(bad, 2u); continue; }
+        if (algo == GXB_ALGO_PAGERANK) {
+            // both buffers: rounds alternate between them and Apply rewrites only owned slots
+            const double r = vals[i];
+            rank0[s] = rank1[s] = r;
+            const uint32_t od = outdeg[s];
+            const double c = od ? __ddiv_rn(r, (double)od) : 0.0;
+            if (msg32) {
+                reinterpret_cast<float*>(contrib0)[s] = reinterpret_cast<float*>(contrib1)[s] = __double2float_rn(c);
+            } else {
+                contrib0[s] = contrib1[s] = c;
+            }
+            continue;
+        }
+        const int W = record_words(algo);
+        uint32_t* r = rec + i * W;
+        r[0] = s;
+        if (algo == GXB_ALGO_SSSP) {
+            for (int j = 0; j < 4; ++j) {
+                uint32_t x = kInf32;
+                if (j < arity) {
+                    const double v = vals[i * arity + j];
+                    if (!(isinf(v) && v > 0)) {
+                        if (!(v >= 0.0 && v < 4294967295.0 && v == floor(v))) atomicOr(bad, 1u);
+                        else x = (uint32_t)v;
+                    }
+                }
+                r[1 + j] = x;
+            }
+        } else {
+            const double v = vals[i];
+            if (!(v >= 0.0 && v < 4294967295.0 && v == floor(v))) atomicOr(bad, 1u);
+            r[1] = v >= 0.0 && v < 4294967295.0 ? (uint32_t)v : 0u;
+        }
+    }
 }
 
 // needed-only dense exchange (PageRank): gather my values for every peer / scatter theirs
@@ -341,6 +390,7 @@ int gxb_exchange_unpack(gxb_state* s, const void* d_records, uint64_t count, voi
     if (!d_records) return fail(GXB_EINVAL, "gxb_exchange_unpack: null records");
     gxb_graph* g = s->g;
     cudaStream_t st = (cudaStream_t)stream;
+    GXB_CHECK(state_settle(s));  // the closed round's frontier first, then the records on top
     unsigned long long* d_units = reinterpret_cast<unsigned long long*>(s->d_fcount) + 1;
     GXB_CUDA(cudaMemsetAsync(d_units, 0, 8, st));
     k_unpack<<<grid_for(count), kBlock, 0, st>>>(s->algo, (const uint32_t*)d_records, count, g->lo, g->hi,
@@ -354,6 +404,51 @@ int gxb_exchange_unpack(gxb_state* s, const void* d_records, uint64_t count, voi
     s->units_cur += u;
     s->frontier_len = n;
     return GXB_OK;
+}
+
+int gxb_attrs_deliver(gxb_state* s, const uint64_t* host_dense, const double* host_vals, uint64_t n,
+                      void* stream) {
+    if (!s) return fail(GXB_EINVAL, "gxb_attrs_deliver: null state");
+    if (s->in_round) return fail(GXB_ESTATE, "gxb_attrs_deliver: a round is open");
+    if (n == 0) return GXB_OK;
+    if (!host_dense || !host_vals) return fail(GXB_EINVAL, "gxb_attrs_deliver: null input");
+    gxb_graph* g = s->g;
+    GXB_CUDA(cudaSetDevice(g->ctx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int W = s->algo == GXB_ALGO_SSSP ? 5 : 2;
+    uint64_t* d_dense = nullptr;
+    double* d_vals = nullptr;
+    uint32_t* d_rec = nullptr;
+    uint32_t* d_bad = nullptr;
+    int rc = GXB_OK;
+    if (dalloc_t(&d_dense, n) || dalloc_t(&d_vals, n * s->arity) || dalloc_t(&d_rec, n * W + 1) ||
+        dalloc_t(&d_bad, 1)) {
+        rc = fail(GXB_ENOMEM, "gxb_attrs_deliver: out of device memory");
+    }
+    uint32_t bad = 0;
+    if (rc == GXB_OK) {
+        cudaMemcpyAsync(d_dense, host_dense, 8 * n, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(d_vals, host_vals, 8 * n * s->arity, cudaMemcpyHostToDevice, st);
+        cudaMemsetAsync(d_bad, 0, 4, st);
+        k_deliver<<<grid_for(n), kBlock, 0, st>>>(s->algo, s->arity, d_dense, d_vals, n, g->V, g->d_dense2slot,
+                                                  g->lo, g->hi, g->d_outdeg, s->d_rank[0], s->d_rank[1],
+                                                  s->d_contrib[0], s->d_contrib[1], s->msg32, d_rec, d_bad);
+        cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) rc = fail(GXB_ECUDA, "gxb_attrs_deliver: kernel failed");
+    }
+    if (rc == GXB_OK && (bad & 2u)) rc = fail(GXB_EINVAL, "gxb_attrs_deliver: target is owned by this partition or absent");
+    else if (rc == GXB_OK && bad) rc = fail(GXB_ERANGE, "gxb_attrs_deliver: value not representable on the device");
+    // installed mirror values are active sources of the next round (records = the delta path)
+    if (rc == GXB_OK && s->algo != GXB_ALGO_PAGERANK) {
+        s->lab_injective = false;
+        rc = gxb_exchange_unpack(s, d_rec, n, stream);
+    }
+    cudaStreamSynchronize(st);
+    dfree(d_dense);
+    dfree(d_vals);
+    dfree(d_rec);
+    dfree(d_bad);
+    return rc;
 }
 
 int gxb_exchange_sparse_counts(const gxb_state* s, uint64_t* send_counts, uint64_t* recv_counts) {

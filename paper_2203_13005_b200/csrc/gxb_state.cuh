@@ -205,10 +205,8 @@ struct gxb_state {
     double* d_split_sum[2] = {nullptr, nullptr};  // per owned slot (zero where no such edge)
 
     // push scheduling (chunk counts, their inclusive scan, CUB scratch)
-    uint32_t* d_push_counts = nullptr;
     uint32_t* d_push_cpre = nullptr;
-    void* d_push_tmp = nullptr;
-    size_t push_tmp_bytes = 0;
+    unsigned long long* d_scan_status = nullptr;  // k_push_rowpre: tile ticket + look-back words
 
     // LP scratch
     void* d_lp_scratch = nullptr;
@@ -249,7 +247,17 @@ struct gxb_state {
     void* d_send = nullptr;
     void* d_recv = nullptr;
     uint64_t recv_cap = 0;
-    unsigned long long* d_xscratch = nullptr;  // [0] async pack count, [1] async unpack GEN units
+    // [0] async pack count, [1] async unpack GEN units, [2] GEN units of installed changes,
+    // [3] an install raised a distance / label (breaks the monotonicity the dense pull relies on)
+    unsigned long long* d_xscratch = nullptr;
     bool packed_async = false;    // the closed round's records are packed; the vote carries their count
     bool unpack_pending = false;  // frontier_len / units_cur still to be refreshed from the device
+    bool install_pending = false; // installed changes joined the frontier; refresh its length / units
+    bool nonmonotone = false;     // sticky: pull rounds keep the active-bitmap test
 };
+
+// host reduction of the closed round's statistics, then refresh of the frontier after
+// asynchronous unpacks and installs (gxb_algo.cu)
+namespace gxb {
+int state_settle(gxb_state* s);
+}  // namespace gxb

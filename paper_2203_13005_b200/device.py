@@ -308,6 +308,16 @@ class DeviceState:
         else:  # pinned torch tensor
             L.check(L.lib().gxb_write_attrs(self._h, _vp(values), _stream_ptr(stream)))
 
+    def deliver(self, dense, values, stream=None):
+        """Install mirror values (sources owned by other partitions, by dense index = rank of
+        the id among the present ids) delivered by the sync round (A/agent.py:584-592); on
+        SSSP / CC / LP they become active sources of the next round."""
+        d = np.ascontiguousarray(dense, dtype=np.uint64)
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        if v.size != d.size * self.arity:
+            raise ValueError("deliver: one row of `arity` values per vertex required")
+        L.check(L.lib().gxb_attrs_deliver(self._h, _vp(d), _vp(v), int(d.size), _stream_ptr(stream)))
+
     # fused PageRank exchange: Apply stores into the peers' replicas (NVLink / NVSwitch)
     IPC_HANDLE_BYTES = 64
 

@@ -254,6 +254,20 @@ class PartitionedRun:
         self.state.unpack_regions(rptr, counts, maxc, frontier, units)
         return sum(counts) * rec
 
+    def install(self, buf: int, stream=None) -> int:
+        """update("pull_from_upper") of this rank's owned vertices (A/agent.py:224-232): install
+        staging buffer `buf` (gxb_attrs_install, owned scope), then refresh every peer's mirror
+        of them before the next round. PageRank: the owned contribution slice is all-gathered;
+        SSSP / CC / LP: installed values that changed joined the frontier and travel as delta
+        records (a vertex already in a peer's frontier is listed once). `stream` must be the
+        current torch stream (the collectives are ordered on it). Returns the bytes received."""
+        self.state.attrs_install(buf, stream)
+        if self.comm.world == 1:
+            return 0
+        if self.algo == "pagerank":
+            return self._exchange_dense()
+        return self._exchange_delta()
+
     def _view(self, ptr, nbytes, dtype):
         if hasattr(self.state, "view"):
             return self.state.view(ptr, nbytes, dtype)

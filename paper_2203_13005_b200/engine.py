@@ -1,142 +1,82 @@
-"""Upper-system driver: BSP / GAS iterations over partitioned device state.
+"""Device-only BSP / GAS driver for m partitions in one process (one GPU).
 
-Drop-in for the reference's `Engine` / `run` (A/engine.py:172-427). The
-reference simulates m nodes as threads sharing a barrier; here the m partitions
-are destination ranges of the device store (on one GPU in one process — the
-multi-process / multi-GPU driver is `dist.PartitionedRun`). The per-iteration
-schedule is the reference's barrier schedule (A/engine.py:226-294):
+The reference-compatible way to run an algorithm over partitions is the reference's
+own `Engine` with the B200 daemon dropped in (`dropin.install()`, A/engine.py:172-427
+unmodified). This module is the same schedule without the upper system: no Python
+partition tables, agents or shared regions — each partition is a device state and the
+per-iteration barrier schedule of A/engine.py:226-294 is driven directly:
 
-    work phase    Gen (requestGen) -> Merge (requestMerge) -> Apply (requestApply)
-    route         nothing to route: the pull design merges locally, remote
-                  sources are mirrored
+    work phase    fused Gen∘Merge∘Apply (gxb_iterate), or the request path:
+                  GEN / MERGE / APPLY over block ranges (gxb_request) + commit
     skip          AND over partitions of "no next-active vertex has a remote
-                  consumer" (A/engine.py:242-246) when enable_skip
-    sync round    mirror exchange of changed values (A/engine.py:247-266)
-    verdict       AND of the votes, apply-round cap (A/engine.py:267-285)
+                  consumer" (A/engine.py:242-246), when enable_skip
+    sync round    mirror exchange of changed values between the partitions'
+                  device replicas (`exchange_local`, device-to-device copies)
+    verdict       AND of the votes (A/engine.py:131-136), apply-round cap
 
-GAS (A/agent.py:476-486) runs a seed Gen pass in iteration 1 and then
-Merge -> Apply -> push -> Gen; the seed round is excluded from the cap.
+GAS (A/agent.py:476-486) takes a seed round in iteration 1 (no Apply, not counted
+against the cap) and then Merge -> Apply -> Gen; in the pull design its Gen reads the
+values the previous sync round delivered, so each later iteration is one device round.
+The multi-process, multi-GPU driver with the same schedule is `dist.PartitionedRun`.
 """
 
 from __future__ import annotations
 
 from dataclasses import dataclass, field
-from enum import Enum
 
 import numpy as np
 
-from .agent import GpuAgent
-from .channel import trace_conforms
-from .daemon import AcceleratorProfile
+from .dist import StepRecord
 
 
 class EngineError(RuntimeError):
     pass
 
 
-class ComputationModel(Enum):
-    BSP = "bsp"
-    GAS = "gas"
+MODELS = ("bsp", "gas")
 
 
 @dataclass
 class RunConfig:
-    """Same keys as the reference (A/engine.py:45-60). enable_cache / cache_* are accepted for
-    compatibility: every mirror fits in HBM, so the weighted-LRU policy is moot."""
-
     partitions: int = 1
-    daemons_per_node: int = 1
-    daemon_profile: AcceleratorProfile = field(default_factory=lambda: AcceleratorProfile(lanes=4))
-    node_profiles: list[AcceleratorProfile] | None = None
-    block_size: int | str = 1 << 22
-    enable_cache: bool = False
-    cache_capacity: int = 1024
-    cache_decay: float = 0.5
-    cache_boost: float = 1.0
+    block_size: int = 1 << 22     # request-path block (range) length
     enable_skip: bool = False
-    io_cost: float = 0.01
-    seed: int = 0
     max_iterations: int | None = None
-    barrier_timeout: float = 60.0
-    fused: bool = False          # True: one fused device pass per iteration instead of requestX passes
+    fused: bool = True            # one fused device pass per iteration instead of GEN/MERGE/APPLY ranges
     direction: str = "auto"
     device: int = 0
-    partitioning: str = "ids"    # "ids": contiguous ascending-id ranges like partition_graph (A/graph.py:175-212);
-                                 # "edges": destination ranges balanced by in-edges (the multi-GPU default)
+    partitioning: str = "ids"     # "ids": contiguous ascending-id ranges like partition_graph (A/graph.py:175-212);
+                                  # "edges": degree-sorted slots dealt to balance in-edges (the multi-GPU default)
     sizes: list[int] | None = None  # explicit partition sizes (partition_graph's `sizes`)
     capacity: list[float] | None = None  # per-partition capacity factors (balancer.capacity_factors):
                                          # degree-sorted ranges cut in proportion (A/balancer.py:79-98)
 
-
-@dataclass
-class IterationRecord:
-    iteration: int
-    model: str
-    t_download: float
-    t_compute: float
-    t_upload: float
-    skipped: bool
-    cache_hits: int
-    cache_misses: int
-    uploads: int
-    uploads_avoided: int
-    converged: bool
-
-    def to_line(self) -> str:
-        """The reference's metrics line format (A/engine.py:77-85)."""
-        return (
-            f"iter={self.iteration} model={self.model} "
-            f"t_download={self.t_download:.6f} t_compute={self.t_compute:.6f} "
-            f"t_upload={self.t_upload:.6f} skipped={str(self.skipped).lower()} "
-            f"cache_hits={self.cache_hits} cache_misses={self.cache_misses} "
-            f"uploads={self.uploads} uploads_avoided={self.uploads_avoided} "
-            f"converged={str(self.converged).lower()}"
-        )
-
-
-@dataclass
-class NodeStats:
-    iteration: int
-    node_id: int
-    units: int
-    blocks: int
-    compute_time: float
-    pipeline_time: float
-    download_time: float
-    upload_time: float
+    def __post_init__(self):
+        if self.partitions < 1:
+            raise ValueError(f"partitions must be >= 1, got {self.partitions}")
+        if self.block_size < 1:
+            raise ValueError(f"block size must be >= 1, got {self.block_size}")
 
 
 @dataclass
 class RunMetrics:
     model: str
-    records: list[IterationRecord] = field(default_factory=list)
-    node_stats: list[NodeStats] = field(default_factory=list)
+    records: list[StepRecord] = field(default_factory=list)
     converged: bool = False
     iterations: int = 0
     skipped_rounds: int = 0
-    block_plans: dict[int, tuple[int, int]] = field(default_factory=dict)
-    init_counts: dict[str, int] = field(default_factory=dict)
-    copy_counts: dict[str, int] = field(default_factory=dict)
-    traces: dict[str, list[str]] = field(default_factory=dict)
     exchanged_bytes: int = 0
+    init_counts: dict[int, int] = field(default_factory=dict)
 
     def lines(self) -> list[str]:
-        return [r.to_line() for r in self.records]
-
-    def write(self, path) -> None:
-        with open(path, "w", encoding="ascii") as fh:
-            for line in self.lines():
-                fh.write(line + "\n")
-
-    def protocol_conformant(self) -> bool:
-        return all(trace_conforms(t) for t in self.traces.values())
+        return [r.to_line(self.model) for r in self.records]
 
 
 def convergence_vote(votes: list) -> bool:
-    """Logical AND over per-node votes; a missing vote is fatal (A/engine.py:131-136)."""
+    """Logical AND over per-partition votes; a missing vote is fatal (A/engine.py:131-136)."""
     if any(v is None for v in votes):
         missing = [i for i, v in enumerate(votes) if v is None]
-        raise EngineError(f"missing convergence vote from node(s) {missing}")
+        raise EngineError(f"missing convergence vote from partition(s) {missing}")
     return all(votes)
 
 
@@ -182,130 +122,108 @@ def exchange_local(states, bounds) -> int:
     return moved
 
 
-class Engine:
-    def __init__(self, graph, algorithm, model: ComputationModel | str, config: RunConfig):
-        self.graph_input = graph
-        self.algorithm = algorithm
-        self.model = ComputationModel(model) if isinstance(model, str) else model
-        self.config = config
-        self.metrics = RunMetrics(model=self.model.value)
-        self.agents: list[GpuAgent] = []
-        self.states = []
-        self.graphs = []
+def _edges(graph):
+    from .graph import EdgeArrays
+    if isinstance(graph, EdgeArrays):
+        return graph
+    if isinstance(graph, tuple) and len(graph) == 2:
+        return EdgeArrays.from_edges(list(graph[1]))
+    if hasattr(graph, "partitions"):  # the reference's PartitionedGraph
+        return EdgeArrays.from_edges([e for p in graph.partitions for e in p.edges])
+    raise TypeError("graph must be EdgeArrays, (vertices, edges) or a PartitionedGraph")
 
-    def _edges(self):
-        from .graph import EdgeArrays
-        g = self.graph_input
-        if isinstance(g, EdgeArrays):
-            return g
-        if isinstance(g, tuple) and len(g) == 2:
-            return EdgeArrays.from_edges(list(g[1]))
-        if hasattr(g, "partitions"):  # a reference-style PartitionedGraph
-            return EdgeArrays.from_edges([e for p in g.partitions for e in p.edges])
-        raise TypeError("graph must be EdgeArrays, (vertices, edges) or a PartitionedGraph")
+
+class Engine:
+    def __init__(self, graph, algorithm, model: str, config: RunConfig):
+        model = getattr(model, "value", model)
+        if model not in MODELS:
+            raise ValueError(f"unknown computation model {model!r}")
+        self.edges = _edges(graph)
+        self.algorithm = algorithm
+        self.model = model
+        self.config = config
+        self.metrics = RunMetrics(model=model)
+        self.states, self.graphs = [], []
 
     def _setup(self):
         from .device import DeviceContext, DeviceGraph, DeviceState
-        cfg = self.config
-        ea = self._edges()
+        cfg, ea = self.config, self.edges
         algo = self.algorithm.device_name
         self.ctx = DeviceContext(cfg.device)
-        m = max(1, int(cfg.partitions))
         w = ea.weight if algo == "sssp" else None
         maxw = int(np.max(w)) if (w is not None and w.size) else 1
-        for j in range(m):
-            g = DeviceGraph(self.ctx, ea.src, ea.dst, w, part=j, nparts=m, csr=algo in ("sssp", "cc", "lp"),
+        for j in range(cfg.partitions):
+            g = DeviceGraph(self.ctx, ea.src, ea.dst, w, part=j, nparts=cfg.partitions, csr=algo != "pagerank",
                             partitioning=cfg.partitioning, sizes=cfg.sizes, capacity=cfg.capacity)
             s = DeviceState(g, algo, sources=getattr(self.algorithm, "sources", None) if algo == "sssp" else None,
                             max_weight=maxw if algo == "sssp" else None)
             self.graphs.append(g)
             self.states.append(s)
         self.bounds = self.graphs[0].bounds()
-        for j, s in enumerate(self.states):
-            agent = GpuAgent(j, s, self.algorithm, model=self.model.value, block_size=cfg.block_size,
-                             io_cost=cfg.io_cost, recv_timeout=cfg.barrier_timeout, fused=cfg.fused)
-            base = cfg.node_profiles[j] if cfg.node_profiles is not None else cfg.daemon_profile
-            agent.connect([base] * cfg.daemons_per_node)
-            self.agents.append(agent)
-        self.cap = cfg.max_iterations
-        if self.cap is None:
-            self.cap = self.algorithm.default_iteration_cap(self.graphs[0].num_vertices)
+        self.metrics.init_counts = {0: self.ctx.init_count}
+        cap = cfg.max_iterations
+        self.cap = self.algorithm.default_iteration_cap(self.graphs[0].num_vertices) if cap is None else cap
 
-    def run(self) -> tuple[dict[int, object], RunMetrics]:
+    def _round(self, s, g) -> dict:
+        """One Gen∘Merge∘Apply round of one partition (fused, or the template ops over ranges)."""
+        cfg = self.config
+        if cfg.fused or s.algo == "lp":  # LP folds a label multiset: no materialised-message form
+            s.iterate(cfg.direction)
+        else:
+            from . import _lib as L
+            b = cfg.block_size
+            E = int(g.info.owned_edges)
+            lo, hi = g.owned
+            for e0 in range(0, E, b):
+                s.request(L.OP_GEN, e0, min(E, e0 + b))
+            for op in (L.OP_MERGE, L.OP_APPLY):
+                for v0 in range(lo, hi, b):
+                    s.request(op, v0, min(hi, v0 + b))
+            s.commit()
+        return s.stats()
+
+    def run(self):
         self._setup()
         try:
             self._loop()
+            return self._read_attrs(), self.metrics
         finally:
-            for agent in self.agents:
-                agent.shutdown()
-            self._collect_instrumentation()
-        attrs = self._read_attrs()
-        return attrs, self.metrics
+            for s in self.states:
+                s.free()
+            for g in self.graphs:
+                g.free()
+            self.ctx.shutdown()
 
     def _loop(self):
-        agents, cfg = self.agents, self.config
-        gas = self.model is ComputationModel.GAS
+        cfg, m = self.config, len(self.states)
         iteration, apply_rounds = 0, 0
-        if gas:
-            # seed Gen pass (A/agent.py:476-486); excluded from the cap (A/engine.py:271-275)
+        if self.model == "gas":
+            # seed round (A/agent.py:476-486): nothing materialises in the pull design; it still
+            # takes the skip vote on the initial frontier and is excluded from the cap
             iteration = 1
-            for a in agents:
-                a.begin_iteration()
-                a.gen_phase()
-                a.end_iteration()
-            # the seed round still takes the skip vote on the initial frontier (A/engine.py:242-246)
-            seed_skip = cfg.enable_skip and all(a.device_state.stats()["remote_active"] == 0 for a in agents)
-            if seed_skip and len(agents) > 1:
-                self.metrics.skipped_rounds += 1
-            self._record(iteration, skipped=seed_skip and len(agents) > 1, converged=False, agents=agents)
-            if self.cap <= 0:
-                return
+            stats = [s.stats() for s in self.states]
+            skip = cfg.enable_skip and m > 1 and all(st["remote_active"] == 0 for st in stats)
+            self.metrics.skipped_rounds += int(skip)
+            self.metrics.records.append(StepRecord(1, 0, sum(st["next_active"] for st in stats), 0, 0, 0.0,
+                                                   skip, False))
         while apply_rounds < self.cap:
             iteration += 1
-            for a in agents:
-                a.begin_iteration()
-                if not gas:
-                    a.gen_phase()
-                a.merge_apply_phase()
-            closed = [a.round_closed() for a in agents]
-            skip = cfg.enable_skip and all(closed)
-            moved = 0 if (skip or len(agents) == 1) else exchange_local(self.states, self.bounds)
+            stats = [self._round(s, g) for s, g in zip(self.states, self.graphs)]
+            skip = cfg.enable_skip and m > 1 and all(st["remote_active"] == 0 for st in stats)
+            moved = 0 if (skip or m == 1) else exchange_local(self.states, self.bounds)
             self.metrics.exchanged_bytes += moved
-            converged = convergence_vote([a.vote() for a in agents])
+            converged = convergence_vote([bool(st["voted"]) for st in stats])
             apply_rounds += 1
             if skip and not converged:
                 self.metrics.skipped_rounds += 1
-            stop = converged or apply_rounds >= self.cap
-            if gas and not stop:
-                for a in agents:
-                    a.gen_phase()  # ... -> push -> Gen for the next iteration
-            for a in agents:
-                a.end_iteration()
-            self._record(iteration, skip and len(agents) > 1 and cfg.enable_skip, converged, agents, moved)
-            if stop:
+            self.metrics.records.append(StepRecord(
+                iteration, sum(st["changed"] for st in stats), sum(st["next_active"] for st in stats),
+                sum(st["units"] for st in stats), sum(st["remote_active"] for st in stats),
+                max(st["max_stat"] for st in stats), skip, converged, moved))
+            if converged or apply_rounds >= self.cap:
                 self.metrics.converged = converged
                 self.metrics.iterations = iteration
                 break
-
-    def _record(self, iteration, skipped, converged, agents, moved=0):
-        cs = [a.counters for a in agents]
-        self.metrics.records.append(IterationRecord(
-            iteration=iteration, model=self.model.value,
-            t_download=max(c.t_download for c in cs), t_compute=max(c.t_compute for c in cs),
-            t_upload=max(c.t_upload for c in cs), skipped=skipped, cache_hits=0, cache_misses=0,
-            uploads=moved, uploads_avoided=0, converged=converged))
-        for a in agents:
-            c = a.counters
-            self.metrics.node_stats.append(NodeStats(iteration, a.node_id, c.units, c.blocks, c.t_compute,
-                                                     c.pipeline_time, c.t_download, c.t_upload))
-
-    def _collect_instrumentation(self):
-        for agent in self.agents:
-            for daemon in agent.daemons:
-                key = daemon.state.channel_key
-                self.metrics.init_counts[key] = daemon.init_count
-                self.metrics.copy_counts[key] = daemon.region.copy_count
-                self.metrics.traces[key] = list(daemon.region.trace)
 
     def _read_attrs(self) -> dict[int, object]:
         ids = self.graphs[0].ids()
@@ -320,8 +238,8 @@ class Engine:
         return {int(v): self.algorithm.attr_from_row(int(v), rows[i]) for i, v in enumerate(ids)}
 
 
-def run(graph, algorithm, model: ComputationModel | str, config: RunConfig) -> tuple[dict[int, object], RunMetrics]:
-    """Run one algorithm over a partitioned graph; returns (attrs, metrics) (A/engine.py:422-427)."""
+def run(graph, algorithm, model: str, config: RunConfig) -> tuple[dict[int, object], RunMetrics]:
+    """Run one algorithm over m device partitions; returns (attrs, metrics)."""
     return Engine(graph, algorithm, model, config).run()
 
 

@@ -2,9 +2,9 @@
 
 The reference keeps per-node Python tables (`Partition`, `PartitionedGraph`,
 A/graph.py:93-128); here the tables live on the device (libgxb200's CSC/CSR
-store), so the host only needs the edge-list container and the loader. The
-loader keeps the reference's exact parsing rules and error messages
-(`load_edge_list`, A/graph.py:131-166).
+store), so the host only needs columnar edge arrays: a text reader with the
+reference's parsing rules and error messages (`load_edge_list`, A/graph.py:131-166)
+and a memory-mapped binary format for ingest at scale.
 """
 
 from __future__ import annotations
@@ -15,57 +15,66 @@ import numpy as np
 
 
 class GraphParseError(ValueError):
-    """Raised for malformed edge-list input; carries the 1-based line number (A/graph.py:17-22)."""
+    """Malformed edge-list input; `lineno` is 1-based (the reference's GraphParseError,
+    A/graph.py:17-22, same message format)."""
 
     def __init__(self, lineno: int, message: str):
         super().__init__(f"line {lineno}: {message}")
         self.lineno = lineno
 
 
-@dataclass(frozen=True, slots=True)
-class Edge:
-    src: int
-    dst: int
-    weight: float = 1.0
+def _first_error(lineno: int, fields: list[str]) -> str | None:
+    """The reference's per-line checks, in its order (A/graph.py:146-162)."""
+    if len(fields) not in (2, 3):
+        return f"expected 2 or 3 fields, got {len(fields)}"
+    try:
+        a, b = int(fields[0]), int(fields[1])
+    except ValueError:
+        return f"non-integer vertex id in {fields[:2]}"
+    if a < 0 or b < 0:
+        return "vertex ids must be non-negative"
+    if len(fields) == 3:
+        try:
+            x = float(fields[2])
+        except ValueError:
+            return f"non-numeric weight {fields[2]!r}"
+        if x < 0:
+            return f"negative weight {x}"
+    return None
 
 
-def load_edge_list(path) -> tuple[set[int], list[Edge]]:
-    """Parse `src dst [weight]` lines; '#' comments, blank lines, LF/CRLF; duplicates kept."""
-    vertices: set[int] = set()
-    edges: list[Edge] = []
+def read_edge_text(path) -> "EdgeArrays":
+    """Columnar reader of the reference's text edge list (`src dst [weight]` per line,
+    '#' comments, blank lines, LF / CRLF, duplicates and self-loops kept in file order):
+    the same accepted inputs, values and errors as `load_edge_list` (A/graph.py:131-166,
+    pinned by tests/golden/edge_lists.json), straight into the device ingest columns.
+
+    Lines are tokenised once; ids and weights are converted column-wise, and only when a
+    conversion or range check fails is the offending line located (the first one in file
+    order) and diagnosed with the reference's message."""
     with open(path, "r", encoding="ascii") as fh:
-        for lineno, raw in enumerate(fh, start=1):
-            line = raw.strip()
-            if not line or line.startswith("#"):
-                continue
-            parts = line.split()
-            if len(parts) not in (2, 3):
-                raise GraphParseError(lineno, f"expected 2 or 3 fields, got {len(parts)}")
-            try:
-                src = int(parts[0])
-                dst = int(parts[1])
-            except ValueError:
-                raise GraphParseError(lineno, f"non-integer vertex id in {parts[:2]}") from None
-            if src < 0 or dst < 0:
-                raise GraphParseError(lineno, "vertex ids must be non-negative")
-            weight = 1.0
-            if len(parts) == 3:
-                try:
-                    weight = float(parts[2])
-                except ValueError:
-                    raise GraphParseError(lineno, f"non-numeric weight {parts[2]!r}") from None
-                if weight < 0:
-                    raise GraphParseError(lineno, f"negative weight {weight}")
-            vertices.add(src)
-            vertices.add(dst)
-            edges.append(Edge(src, dst, weight))
-    return vertices, edges
-
-
-def even_sizes(n: int, m: int) -> list[int]:
-    """Split n items into m near-equal contiguous chunk sizes (A/graph.py:169-172)."""
-    base, rem = divmod(n, m)
-    return [base + (1 if j < rem else 0) for j in range(m)]
+        text = fh.read()
+    rows = [(n, ln.split()) for n, ln in enumerate(text.split("\n"), start=1)]
+    rows = [(n, f) for n, f in rows if f and not f[0].startswith("#")]
+    widths = {len(f) for _, f in rows}
+    try:
+        if not widths <= {2, 3}:
+            raise ValueError
+        src = np.array([int(f[0]) for _, f in rows], dtype=np.int64)
+        dst = np.array([int(f[1]) for _, f in rows], dtype=np.int64)
+        w = np.array([float(f[2]) if len(f) == 3 else 1.0 for _, f in rows], dtype=np.float64)
+        if (src < 0).any() or (dst < 0).any() or (w < 0).any():
+            raise ValueError
+    except (ValueError, OverflowError):
+        for n, f in rows:
+            msg = _first_error(n, f)
+            if msg is not None:
+                raise GraphParseError(n, msg) from None
+        raise
+    weighted = bool((w != 1.0).any())
+    if src.size and max(src.max(), dst.max()) >= 0xFFFFFFFF:
+        raise ValueError("vertex ids must be < 2^32 - 1 on the device")
+    return EdgeArrays(src.astype(np.uint32), dst.astype(np.uint32), w if weighted else None)
 
 
 @dataclass
@@ -91,23 +100,17 @@ class EdgeArrays:
 
     @classmethod
     def from_edges(cls, edges) -> "EdgeArrays":
-        """From reference-style Edge objects (or (src, dst[, w]) tuples)."""
-        n = len(edges)
-        src = np.empty(n, dtype=np.uint64)
-        dst = np.empty(n, dtype=np.uint64)
-        w = np.empty(n, dtype=np.float64)
-        weighted = False
-        for i, e in enumerate(edges):
-            if isinstance(e, Edge):
-                s, d, x = e.src, e.dst, e.weight
-            else:
-                s, d = e[0], e[1]
-                x = e[2] if len(e) > 2 else 1.0
-            src[i], dst[i], w[i] = s, d, x
-            weighted |= x != 1.0
-        if n and (src.max() >= 0xFFFFFFFF or dst.max() >= 0xFFFFFFFF):
-            raise ValueError("vertex ids must be < 2^32 - 1 on the device")
-        return cls(src.astype(np.uint32), dst.astype(np.uint32), w if weighted else None)
+        """From reference Edge objects (`.src / .dst / .weight`, A/graph.py:39-43) or
+        (src, dst[, w]) tuples."""
+        def triple(e):
+            if hasattr(e, "src"):
+                return e.src, e.dst, e.weight
+            return e[0], e[1], (e[2] if len(e) > 2 else 1.0)
+        cols = np.array([triple(e) for e in edges], dtype=np.float64).reshape(-1, 3)
+        src, dst, w = cols[:, 0], cols[:, 1], cols[:, 2]
+        if src.size and (src.min() < 0 or dst.min() < 0 or max(src.max(), dst.max()) >= 0xFFFFFFFF):
+            raise ValueError("vertex ids must be in [0, 2^32 - 1) on the device")
+        return cls(src.astype(np.uint32), dst.astype(np.uint32), w.copy() if (w != 1.0).any() else None)
 
     def vertex_ids(self) -> np.ndarray:
         """Ids present in any edge, ascending (A/graph.py:163-164)."""
@@ -171,7 +174,6 @@ def read_edge_binary(path) -> "EdgeArrays":
 
 def edge_list_to_binary(text_path, bin_path) -> int:
     """Convert a reference text edge list (load_edge_list rules) to the binary format."""
-    _, edges = load_edge_list(text_path)
-    ea = EdgeArrays.from_edges(edges)
+    ea = read_edge_text(text_path)
     write_edge_binary(bin_path, ea)
     return len(ea)

@@ -1,6 +1,7 @@
-"""GPU tests of the reference-facing API: run_device (drop-in for run_reference)
-and the Engine / agent / daemon stack (requestGen / requestMerge / requestApply
-over SharedRegions), against the reference's own golden outputs and metrics."""
+"""GPU tests of the package API: run_device (drop-in for run_reference) against the
+reference's own golden outputs, the device-only partitioned Engine against the oracle,
+attribute staging. The reference's own Engine / Agent / Daemon with the B200 daemon
+dropped in is tests/test_dropin_gpu.py."""
 
 from __future__ import annotations
 
@@ -67,36 +68,6 @@ def test_run_device_is_run_reference(ctx, tag):
         assert attrs_close(got, want, run["algo"]), (tag, run["key"])
 
 
-def engine_cases():
-    out = []
-    for case in golden_cases():
-        for key in case["engine"]:
-            out.append((case["tag"], key))
-    return out
-
-
-@pytest.mark.parametrize("tag,key", engine_cases())
-def test_engine_matches_reference_engine(tag, key):
-    """Engine over the request path (GEN/MERGE/APPLY through SharedRegions) on m partitions:
-    same attributes, iteration count, convergence and skipped rounds as the reference's
-    Engine, a conformant protocol trace, init_count == 1 and copy_count == 0."""
-    from paper_2203_13005_b200.algorithms import make_algorithm
-    from paper_2203_13005_b200.engine import RunConfig, run
-    ea, ids, od, data, meta = _setup(tag)
-    em = [e for e in meta["engine"] if e["key"] == key][0]
-    algo = make_algorithm(em["algo"], [int(v) for v in ids], od)
-    for daemons in (1, 2):
-        cfg = RunConfig(partitions=em["m"], daemons_per_node=daemons, block_size=7, enable_skip=em["enable_skip"])
-        attrs, metrics = run(ea, algo, em["model"], cfg)
-        want = golden_dict(data, key, ids, em["algo"], od)
-        assert attrs_close(attrs, want, em["algo"])
-        assert metrics.iterations == em["iterations"] and metrics.converged == em["converged"]
-        assert metrics.skipped_rounds == em["skipped_rounds"]
-        assert metrics.protocol_conformant()
-        assert set(metrics.init_counts.values()) == {1} and set(metrics.copy_counts.values()) == {0}
-        assert len(metrics.lines()) == len(em["lines"])
-
-
 @pytest.mark.parametrize("partitioning", ["ids", "edges"])
 @pytest.mark.parametrize("algo_name", ["sssp", "pagerank", "cc", "lp"])
 @pytest.mark.parametrize("m", [2, 3, 4])
@@ -150,25 +121,6 @@ def test_write_attrs_round_trip(ctx):
             bad[0, 0] = 0.5
             with pytest.raises(ValueError):
                 s2.write_attrs(bad)
-
-
-def test_compat_drop_in_with_reference_shaped_objects():
-    """compat.run_partitioned takes reference-shaped Algorithm / RunConfig / PartitionedGraph."""
-    from types import SimpleNamespace
-    from paper_2203_13005_b200 import compat
-    from paper_2203_13005_b200.graph import Edge
-    edges = [Edge(0, 1, 2.0), Edge(1, 2, 3.0), Edge(2, 0, 1.0), Edge(3, 2, 1.0)]
-    parts = [SimpleNamespace(vertices={0: None, 1: None}, edges=edges[:2]),
-             SimpleNamespace(vertices={2: None, 3: None}, edges=edges[2:])]
-    graph = SimpleNamespace(partitions=parts)
-    algo = SimpleNamespace(name="sssp", sources=[0, 3])
-    cfg = SimpleNamespace(partitions=2, daemons_per_node=1, block_size=256, enable_cache=False, cache_capacity=8,
-                          cache_decay=0.5, cache_boost=1.0, enable_skip=False, io_cost=0.01, seed=0,
-                          max_iterations=None, barrier_timeout=60.0)
-    attrs, metrics = compat.run_partitioned(graph, algo, SimpleNamespace(value="bsp"), cfg)
-    inf = float("inf")
-    assert attrs == {0: (0.0, 2.0), 1: (2.0, 4.0), 2: (5.0, 1.0), 3: (inf, 0.0)}
-    assert metrics.converged and metrics.protocol_conformant()
 
 
 def test_owned_scope_staging(ctx):

@@ -112,7 +112,7 @@ def test_request_path_equals_fused(ctx):
 
 def test_lifecycle_and_errors(ctx):
     from paper_2203_13005_b200 import _lib as L
-    from paper_2203_13005_b200.channel import ProtocolError
+    from paper_2203_13005_b200._lib import ProtocolError
     from paper_2203_13005_b200.device import DeviceGraph, DeviceState
     assert ctx.init_count == 1
     with pytest.raises(ProtocolError, match="re-initialization"):
@@ -356,3 +356,66 @@ def test_pagerank_run_ahead_equals_round_by_round(ctx):
         a.iterate("pull")
         b.iterate("pull")
         np.testing.assert_array_equal(a.read_attrs(), b.read_attrs())
+
+
+@pytest.mark.parametrize("algo", ["pagerank", "sssp", "cc", "lp"])
+@pytest.mark.parametrize("m", [2, 3])
+def test_owned_install_refreshes_peer_mirrors(ctx, algo, m):
+    """pull_from_upper on m partitions (A/agent.py:224-232): each partition installs its owned
+    values (some lowered, some raised), the sync round carries them to the peers' mirrors
+    (PartitionedRun.install's in-process analogue: exchange_local), and the following rounds
+    equal one partition that installed the same values."""
+    import torch
+    from paper_2203_13005_b200.device import DeviceGraph, DeviceState
+    from paper_2203_13005_b200.engine import exchange_local
+    from paper_2203_13005_b200.rmat import RmatParams, rmat_host
+    p = RmatParams(scale=11, seed=81 + m, wmax=9 if algo == "sssp" else 0, symmetric=algo == "cc")
+    src, dst, w = rmat_host(p)
+    kw = dict(csr=algo != "pagerank")
+    one = DeviceState(DeviceGraph(ctx, src, dst, w, **kw), algo)
+    gs = [DeviceGraph(ctx, src, dst, w, part=j, nparts=m, partitioning="ids", **kw) for j in range(m)]
+    sts = [DeviceState(g, algo) for g in gs]
+    bounds = gs[0].bounds()
+
+    def rounds(k):
+        for _ in range(k):
+            one.iterate()
+            one.stats()
+            for s in sts:
+                s.iterate()
+                s.stats()
+            exchange_local(sts, bounds)
+
+    rounds(2)
+    full = one.read_attrs()
+    new = full.copy()
+    rng = np.random.default_rng(5)
+    pick = rng.choice(len(new), size=max(4, len(new) // 20), replace=False)
+    if algo == "pagerank":
+        new[pick, 0] *= 1.5
+    else:
+        lower, raise_ = pick[: len(pick) // 2], pick[len(pick) // 2:]
+        fin = np.isfinite(new[lower])
+        new[lower] = np.where(fin, np.floor(new[lower] / 2), new[lower])
+        new[raise_] = np.where(np.isfinite(new[raise_]), new[raise_] + 3, new[raise_])
+    one.write_attrs(new)
+    ids = gs[0].ids()
+    st = torch.cuda.current_stream()
+    for g, s in zip(gs, sts):
+        own = g.owned_ids()
+        rows = new[np.searchsorted(ids, own)]
+        s.attrs_scope(True)
+        hin = torch.from_numpy(np.ascontiguousarray(rows).reshape(-1)).pin_memory()
+        s.attrs_h2d(hin, 0, st)
+        s.attrs_install(0, st)
+        st.synchronize()
+    exchange_local(sts, bounds)
+    rounds(4)
+    want = one.read_attrs()
+    got = want.copy()
+    for s in sts:
+        r = s.read_attrs(owned_only=True)
+        mask = ~np.isnan(r[:, 0])
+        got[mask] = r[mask]
+    assert_attrs_match(algo, got, want, rel=1e-12)
+    assert not np.array_equal(want, full)

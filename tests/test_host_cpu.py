@@ -1,6 +1,7 @@
-"""CPU-only tests of the host layer: generator, loader, algorithm descriptors,
-region protocol, daemon/agent lifecycle (with a recording fake device state),
-and the C-ABI surface of libgxb200.so (symbols only; no compute without a GPU)."""
+"""CPU-only tests of the host layer: generator, loader, algorithm descriptors, the
+drop-in into the reference's own Engine / Agent / Daemon / SharedRegion (seams,
+request protocol and error surfacing over a recording fake device state), and the
+C-ABI surface of libgxb200.so (symbols only; no compute without a GPU)."""
 
 from __future__ import annotations
 
@@ -15,10 +16,9 @@ import pytest
 
 from conftest import GOLDEN, REPO
 
-from paper_2203_13005_b200 import channel as C
 from paper_2203_13005_b200.algorithms import (ConnectedComponents, LabelPropagation, PageRank,
                                               SsspBellmanFord, make_algorithm)
-from paper_2203_13005_b200.graph import EdgeArrays, GraphParseError, even_sizes, load_edge_list
+from paper_2203_13005_b200.graph import EdgeArrays, GraphParseError, read_edge_text
 from paper_2203_13005_b200.rmat import RmatParams, rmat_host
 
 
@@ -54,12 +54,13 @@ def test_load_edge_list_matches_reference(tmp_path):
         p = tmp_path / f"{name}.txt"
         p.write_bytes(case["text"].encode("ascii"))
         if case["ok"]:
-            vertices, edges = load_edge_list(p)
-            assert sorted(vertices) == case["vertices"], name
-            assert [[e.src, e.dst, e.weight] for e in edges] == case["edges"], name
+            ea = read_edge_text(p)
+            assert ea.vertex_ids().tolist() == case["vertices"], name
+            w = ea.weight.tolist() if ea.weight is not None else [1.0] * len(ea)
+            assert [[int(a), int(b), x] for a, b, x in zip(ea.src, ea.dst, w)] == case["edges"], name
         else:
             with pytest.raises(GraphParseError) as exc:
-                load_edge_list(p)
+                read_edge_text(p)
             assert exc.value.lineno == case["lineno"], name
             assert str(exc.value) == case["message"], name
 
@@ -101,7 +102,6 @@ def test_edge_arrays():
     assert ea.vertex_ids().tolist() == [5, 7]
     assert ea.out_degree() == {5: 2, 7: 1}
     assert ea.weight is not None and ea.weight.tolist() == [1.0, 2.0, 1.0]
-    assert even_sizes(10, 3) == [4, 3, 3]
 
 
 # ---------------------------------------------------------------- algorithms
@@ -125,32 +125,16 @@ def test_make_algorithm_semantics():
     assert s.initial_attr(3) == (float("inf"), 0.0) and s.format_attr((1.0, float("inf"))) == "1.0 inf"
 
 
-# ---------------------------------------------------------------- region protocol
-def test_trace_conformance_and_rotation():
-    assert C.trace_conforms([])
-    assert C.trace_conforms("ExchangeFinished RotateFinished ComputeAllFinished".split())
-    ok = "ExchangeFinished RotateFinished ComputeFinished ExchangeFinished RotateFinished ComputeAllFinished Shutdown"
-    assert C.trace_conforms(ok.split())
-    assert not C.trace_conforms("ExchangeFinished ComputeFinished".split())
-    r = C.SharedRegion("k", 4)
-    assert r.roles() == (C.Role.NEW, C.Role.COMPUTE, C.Role.UPLOAD)
-    C.rotate(r)
-    assert r.roles() == (C.Role.COMPUTE, C.Role.UPLOAD, C.Role.NEW) and r.cycle_count == 1
+# ---------------------------------------------------------------- drop-in (reference seams)
+dropin = pytest.importorskip("paper_2203_13005_b200.dropin", reason="reference package not importable")
 
 
 class FakeDeviceState:
-    """Records the range requests a daemon executes (no GPU)."""
+    """Records the device calls the drop-in makes (no GPU)."""
 
-    def __init__(self, owned_edges=100, owned=(0, 40), fail_on=None):
+    def __init__(self, fail_on=None):
         self.calls = []
         self.fail_on = fail_on
-        self.algo = "cc"
-
-        class _G:
-            pass
-        self.graph = _G()
-        self.graph.owned = owned
-        self.graph.info = type("I", (), {"owned_edges": owned_edges})()
         self.commits = 0
 
     def request(self, op, lo, hi):
@@ -162,72 +146,130 @@ class FakeDeviceState:
         self.commits += 1
 
     def iterate(self, direction="auto"):
-        self.calls.append(("fused",))
+        self.calls.append(("fused", direction))
 
     def stats(self):
-        return {"remote_active": 0, "voted": 1, "changed": 0, "next_active": 0}
+        return {"remote_active": 0, "voted": 1, "changed": 0, "next_active": 0, "next_units": 5}
+
+    def free(self):
+        pass
 
 
-def test_daemon_lifecycle_and_protocol():
-    from paper_2203_13005_b200.daemon import AcceleratorProfile, GpuDaemon, daemon_init, execute_request
-    regions = {"r0": C.SharedRegion("r0", 8)}
-    with pytest.raises(KeyError):
-        GpuDaemon(AcceleratorProfile(4), None, "nope", regions)
+def test_dropin_seams_install_and_restore():
+    import accelgraph.agent as A
+    import accelgraph.daemon as D
+    import accelgraph.engine as E
+    orig = (A.daemon_init, D.execute_request, E.Agent)
+    with dropin.installed(fused=False, direction="pull"):
+        assert (A.daemon_init, D.execute_request, E.Agent) == \
+            (dropin.gpu_daemon_init, dropin.execute_request, dropin.GpuAgent)
+        assert dropin.CONFIG.fused is False and dropin.CONFIG.direction == "pull"
+        with dropin.installed():          # nested: stays installed on exit
+            pass
+        assert dropin.installed_now()
+    assert (A.daemon_init, D.execute_request, E.Agent) == orig
+    assert dropin.CONFIG.fused is True
+    with pytest.raises(ValueError):
+        dropin.install(direction="sideways")
+    assert not dropin.installed_now()
+
+
+def test_execute_request_runs_device_items_only():
+    from accelgraph.channel import OpKind, WorkItem
+    from accelgraph.daemon import AcceleratorProfile
     st = FakeDeviceState()
-    d = daemon_init(AcceleratorProfile(4), None, "r0", regions, st)
-    assert d.init_count == 1
-    with pytest.raises(C.ProtocolError, match="re-initialization"):
-        d.initialize()
-    with pytest.raises(ValueError):
-        AcceleratorProfile(0)
-    item = C.WorkItem(C.OpKind.GEN, 0, C.RangeDescriptor(0, 8), 8)
-    cost = execute_request(st, AcceleratorProfile(4, 2.0, 3.0), item)
-    assert cost == 3.0 + 2.0 * 8 and item.result_units == 8
-    d.shutdown()
-    d.shutdown()  # idempotent
+    agent = type("A", (), {})()
+    agent.device_state, agent._device_lock, agent.direction = st, threading.Lock(), "push"
+    prof = AcceleratorProfile(4, 2.0, 3.0)
+    item = WorkItem(OpKind.MERGE, 0, dropin.DeviceRange(agent, OpKind.MERGE, 10, 18), 8)
+    assert dropin.execute_request(None, prof, item) == 3.0 + 2.0 * 8
+    assert st.calls == [(1, 10, 18)] and item.result_units == 8 and item.result is None
+    item = WorkItem(OpKind.GEN, 0, dropin.FusedRound(agent), 5)
+    dropin.execute_request(None, prof, item)
+    assert st.calls[-1] == ("fused", "push")
+    with pytest.raises(TypeError, match="device work items only"):
+        dropin.execute_request(None, prof, WorkItem(OpKind.GEN, 0, ("triplets",), 1))
+    with pytest.raises(ValueError, match="does not match"):
+        dropin.execute_request(None, prof, WorkItem(OpKind.GEN, 0, dropin.DeviceRange(agent, OpKind.APPLY, 0, 1), 1))
 
 
-def test_agent_request_protocol_round_robin():
-    from paper_2203_13005_b200.agent import GpuAgent
-    from paper_2203_13005_b200.daemon import AcceleratorProfile
-    st = FakeDeviceState(owned_edges=100, owned=(10, 50))
-    a = GpuAgent(0, st, make_algorithm("cc", [1]), block_size=16)
-    with pytest.raises(C.ProtocolError):
-        a.request(C.OpKind.GEN)
-    a.connect([AcceleratorProfile(4), AcceleratorProfile(4)])
-    with pytest.raises(C.ProtocolError):
-        a.connect([AcceleratorProfile(4)])
-    a.begin_iteration()
-    a.gen_phase()
-    a.merge_apply_phase()
-    gens = sorted(c for c in st.calls if c[0] == 0)
-    assert gens[0] == (0, 0, 16) and gens[-1] == (0, 96, 100) and len(gens) == 7
-    merges = sorted(c for c in st.calls if c[0] == 1)
-    assert merges[0][1] == 10 and merges[-1][2] == 50
-    assert st.commits == 1 and a.vote() and a.round_closed()
-    for d in a.daemons:
-        assert C.trace_conforms(d.region.trace) and d.region.copy_count == 0
-    # transfer checks (A/agent.py:208-222)
+def test_gpu_daemon_fails_loudly_without_a_device():
+    import torch
+    from accelgraph.channel import SharedRegion
+    from accelgraph.daemon import AcceleratorProfile
+    if torch.cuda.is_available():
+        pytest.skip("needs a host without a GPU")
+    regions = {"r0": SharedRegion("r0", 8)}
     with pytest.raises(KeyError):
-        a.transfer(C.WorkItem(C.OpKind.GEN, 0, C.RangeDescriptor(0, 1), 1), "missing")
-    with pytest.raises(ValueError, match="exceeds slot capacity"):
-        a.transfer(C.WorkItem(C.OpKind.GEN, 0, C.RangeDescriptor(0, 99), 99), "node0-daemon0")
-    with pytest.raises(ValueError):
-        a.update("sideways")
-    a.shutdown()
+        dropin.GpuDaemon(AcceleratorProfile(4), None, "nope", regions)
+    with pytest.raises(Exception, match="(?i)cuda|device|sm_100"):
+        dropin.gpu_daemon_init(AcceleratorProfile(4), None, "r0", regions)
 
 
-def test_daemon_error_surfaces_to_agent():
-    from paper_2203_13005_b200.agent import GpuAgent
-    from paper_2203_13005_b200.daemon import AcceleratorProfile
-    st = FakeDeviceState(fail_on=2)
-    a = GpuAgent(0, st, make_algorithm("cc", [1]), block_size=64, recv_timeout=10)
-    a.connect([AcceleratorProfile(4)])
-    a.begin_iteration()
-    a.request(C.OpKind.GEN)
-    with pytest.raises(ValueError, match="not owned"):
-        a.request(C.OpKind.APPLY)
-    a.shutdown()
+def _fake_device(monkeypatch, fail_on=None):
+    """GpuDaemon without gxb_init and GpuAgent over a recording fake device state."""
+    states = []
+
+    def init(self):
+        return super(dropin.GpuDaemon, self).initialize()
+
+    def build(self):
+        st = FakeDeviceState(fail_on)
+        states.append(st)
+        self.device_state = st
+        lo = 100 * self.node_id
+        self.device_graph = type("G", (), {"owned": (lo, lo + 40), "free": lambda _s: None,
+                                           "info": type("I", (), {"owned_edges": 100, "owned_out_edges": 7})()})()
+        self._needed = frozenset()
+
+    monkeypatch.setattr(dropin.GpuDaemon, "initialize", init)
+    monkeypatch.setattr(dropin.GpuAgent, "_build_device", build)
+    monkeypatch.setattr(dropin.GpuAgent, "serve_uploads", lambda self, gqq: ({}, {}))
+    monkeypatch.setattr(dropin.GpuAgent, "flush_all", lambda self: {})
+    return states
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_reference_engine_drives_gpu_agents(monkeypatch, fused):
+    """The reference's own Engine / Agent.request / _drive / SharedRegion / Daemon._loop run
+    device range items (round-robin over two daemons per node): every GEN edge range and
+    MERGE / APPLY slot range covered once, conformant traces, no content copies."""
+    from accelgraph.channel import trace_conforms
+    from accelgraph.engine import RunConfig, run
+    from accelgraph.graph import Edge, even_sizes, partition_graph
+    states = _fake_device(monkeypatch)
+    edges = [Edge(i, (i + 1) % 6, 1.0) for i in range(6)]
+    graph = partition_graph(set(range(6)), edges, even_sizes(6, 2))
+    from accelgraph.algorithms import make_algorithm
+    algo = make_algorithm("lp" if fused else "sssp", set(range(6)), graph.out_degree)
+    with dropin.installed(fused=fused):
+        attrs, metrics = run(graph, algo, "bsp", RunConfig(partitions=2, daemons_per_node=2, block_size=16))
+    assert metrics.iterations == 1 and metrics.converged
+    assert metrics.protocol_conformant() and all(trace_conforms(t) for t in metrics.traces.values())
+    assert set(metrics.init_counts.values()) == {1} and set(metrics.copy_counts.values()) == {0}
+    for j, st in enumerate(states):
+        if fused:
+            assert st.calls == [("fused", "auto")]
+            continue
+        gens = sorted(c[1:] for c in st.calls if c[0] == 0)
+        assert gens[0] == (0, 16) and gens[-1] == (96, 100) and len(gens) == 7
+        for op in (1, 2):
+            rs = sorted(c[1:] for c in st.calls if c[0] == op)
+            assert rs[0][0] == 100 * j and rs[-1][1] == 100 * j + 40
+            assert sum(h - lo for lo, h in rs) == 40
+        assert st.commits == 1
+
+
+def test_device_error_surfaces_through_the_reference_region(monkeypatch):
+    from accelgraph.engine import EngineError, RunConfig, run
+    from accelgraph.graph import Edge, partition_graph
+    from accelgraph.algorithms import make_algorithm
+    _fake_device(monkeypatch, fail_on=2)
+    edges = [Edge(0, 1, 1.0), Edge(1, 0, 1.0)]
+    graph = partition_graph({0, 1}, edges, [1, 1])
+    algo = make_algorithm("sssp", {0, 1}, graph.out_degree)
+    with dropin.installed(fused=False), pytest.raises(EngineError, match="not owned"):
+        run(graph, algo, "bsp", RunConfig(partitions=2, block_size=64, barrier_timeout=10.0))
 
 
 # ---------------------------------------------------------------- C ABI surface
