@@ -166,42 +166,91 @@ def cpu_sample(algo, scale, over, iters, threads=0, seed=1):
                 result=r, graph=g)
 
 
+def python_reference_sample():
+    """The reference itself (pure Python, `accelgraph` from baseline/_ref or sys.path) on
+    config C1 — PageRank on R-MAT scale-16 — for one BSP iteration each of `run_reference`
+    (A/algorithms.py:298-342) and the `Engine` with one partition (A/engine.py:422-427,
+    RunConfig defaults). One core: the reference is GIL-bound."""
+    try:
+        from paper_2203_13005_b200.dropin import reference
+        reference()
+        from accelgraph.algorithms import make_algorithm, run_reference
+        from accelgraph.engine import RunConfig, run
+        from accelgraph.graph import Edge, partition_graph
+        from oracle import oracle
+    except Exception as exc:  # noqa: BLE001
+        return {"available": False, "why": f"{type(exc).__name__}: {exc}"}
+    src, dst, _ = oracle.rmat(16, 16, 1, 0.57, 0.19, 0.19, 0, True, False)
+    edges = [Edge(a, b) for a, b in zip(src.tolist(), dst.tolist())]
+    vertices = set(src.tolist()) | set(dst.tolist())
+    out = {"available": True, "config": "C1: PageRank on R-MAT scale-16 (1,048,576 edges), one BSP iteration",
+           "cores": 1, "cores_note": f"1 of {os.cpu_count()} cores (GIL)"}
+    graph = partition_graph(vertices, edges, [len(vertices)])
+    t = time.perf_counter()
+    run_reference(make_algorithm("pagerank", vertices, graph.out_degree), vertices, edges, max_iterations=1)
+    dt = time.perf_counter() - t
+    out["run_reference"] = {"seconds": round(dt, 3), "gteps": round(len(edges) / dt / 1e9, 7)}
+    t = time.perf_counter()
+    run(graph, make_algorithm("pagerank", vertices, graph.out_degree), "bsp", RunConfig(partitions=1, max_iterations=1))
+    dt = time.perf_counter() - t
+    out["engine_bsp_m1"] = {"seconds": round(dt, 3), "gteps": round(len(edges) / dt / 1e9, 7)}
+    return out
+
+
 def run_reference_arm(args):
+    """The reference's CPU path on the box's host cores, on the same workload and scale as
+    the GPU arm: oracle/gx_oracle.c (run_reference restated in C, OpenMP on every host
+    thread) over the same R-MAT graph; a step is one BSP iteration (PageRank) or one run to
+    convergence (frontier algorithms), the graph built once before the warm-up. The pure
+    Python reference is timed beside it on config C1 (python_reference)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    algo, scale, over, _, text = WORKLOADS[args.workload]
+    algo, scale, over, cap, text = WORKLOADS[args.workload]
+    if args.scale:
+        scale = args.scale
     threads = host_threads()
-    sample_scale = min(scale, args.cpu_scale)
-    # a step = the reference's fixed PageRank sample of 10 BSP iterations (configs C1 / C4),
-    # one iteration for the frontier algorithms; GTEPS over the iterations actually run
-    iters = 10 if algo == "pagerank" else 1
-    vals = []
-    for _ in range(args.warmup):
-        cpu_sample(algo, sample_scale, over, iters, threads)
-    t_total = 0.0
-    edges = 0
-    for _ in range(args.steps):
-        r = cpu_sample(algo, sample_scale, over, iters, threads)
-        vals.append(r["gteps"])
-        t_total += r["seconds"]
-        edges += r["edges"] * r["iterations"]
+    t_build = time.perf_counter()
+    g = cpu_graph(algo, scale, over)
+    t_build = time.perf_counter() - t_build
+    t_total, done, edges = 0.0, 0, 0
+    if algo == "pagerank":
+        # K consecutive BSP iterations of one run (the warm-up run has W): a step = one iteration
+        g.run(algo, max_iterations=args.warmup, nthreads=threads)
+        t = time.perf_counter()
+        r = g.run(algo, max_iterations=args.steps, nthreads=threads)
+        t_total = time.perf_counter() - t
+        done = r.iterations
+        edges = g.num_edges * r.iterations
+    else:
+        g.run(algo, max_iterations=cap, nthreads=threads)
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            r = g.run(algo, max_iterations=cap, nthreads=threads)
+            t_total += time.perf_counter() - t
+            done += 1
+            edges += g.num_edges * r.iterations
+            if t_total > 120.0:
+                break
     v = edges / t_total / 1e9
+    sample = (f"{done} step(s) of {'1 PageRank BSP iteration' if algo == 'pagerank' else 'one ' + algo + ' run'} "
+              f"on the workload's own graph (R-MAT scale-{scale}, {g.num_edges} edges, same generator and seed; "
+              f"host graph built once in {t_build:.0f} s, untimed); oracle/gx_oracle.c = run_reference "
+              "(A/algorithms.py:298-342) restated in C, OpenMP")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GTEPS",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * t_total / args.steps, 3), "higher_is_better": True,
+        "n_gpus": args.gpus, "steps": args.steps, "steps_timed": done, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * t_total / done, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64" if algo == "pagerank" else "u32",
         "data": "synthetic",
-        "config": {"workload": args.workload, "description": text, "rmat_scale": sample_scale,
-                   "edge_factor": 16, "seed": 1, "parallelism": "cpu"},
-        "cpu_baseline": {"value": round(v, 4), "unit": "GTEPS", "cores": threads, "kind": "port",
-                         "sample": f"{iters} {algo} BSP iteration(s) per step on R-MAT scale-{sample_scale} "
-                                   f"(same generator/seed; scale-{scale} does not fit a bounded CPU run); "
-                                   "oracle/gx_oracle.c = C restatement of run_reference (A/algorithms.py:298-342), "
-                                   "the reference itself is pure Python and GIL-bound"},
+        "config": {"workload": args.workload, "description": text, "rmat_scale": scale,
+                   "edge_factor": 16, "seed": 1, "parallelism": f"cpu x{threads}"},
+        "cpu_baseline": {"value": round(v, 4), "unit": "GTEPS", "cores": threads, "kind": "port", "sample": sample,
+                         "same_config": True},
         "e2e": {"value": round(v, 4), "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_python_reference:
+        line["python_reference"] = python_reference_sample()
     emit(line)
     return 0
 
@@ -273,7 +322,7 @@ def time_frontier_run(ctx, comm, dev, stream, name, algo, params, cap, peak=None
     return out
 
 
-def oracle_parity(algo, params, iterations, attrs, changed=None, units=None, cap=None):
+def oracle_parity(algo, params, iterations, attrs, changed=None, units=None, cap=None, keep=None):
     """Compare a device run with the CPU oracle (oracle/gx_oracle.c, run_reference restated,
     A/algorithms.py:298-342) on the same R-MAT stream: SSSP / CC / LP bit-exact with equal
     per-iteration changed / GEN-unit traces, PageRank within 1e-5 relative per vertex."""
@@ -301,13 +350,15 @@ def oracle_parity(algo, params, iterations, attrs, changed=None, units=None, cap
             out.update(mismatches=mism, bit_exact=mism == 0, traces_equal=bool(traces),
                        ok=bool(out["iterations_equal"] and mism == 0 and traces))
         out.update(oracle_threads=oracle.max_threads(), seconds=round(time.perf_counter() - t0, 1))
+        if keep is not None:
+            keep.append(og)  # the host graph of the same workload, reused by the CPU baseline
         del og
         return out
     except Exception as exc:  # noqa: BLE001
         return {"ok": False, "error": f"{type(exc).__name__}: {exc}"}
 
 
-def check_parity(snap, algo, params, world, rank, dev):
+def check_parity(snap, algo, params, world, rank, dev, keep=None):
     """The timed run's attributes against the oracle for the same number of iterations.
     N > 1: each rank contributes its owned vertices (a sum all-reduce over NaN-masked rows)."""
     import numpy as np
@@ -320,7 +371,7 @@ def check_parity(snap, algo, params, world, rank, dev):
         attrs = t.cpu().numpy()
         if rank != 0:
             return None
-    return oracle_parity(algo, params, rounds, attrs)
+    return oracle_parity(algo, params, rounds, attrs, keep=keep)
 
 
 _STDOUT_FD = None
@@ -347,6 +398,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed run")
+    ap.add_argument("--no-python-reference", action="store_true", help="skip timing the pure-Python reference (C1)")
     ap.add_argument("--no-run-ahead", action="store_true", help="PageRank: wait for every vote before the next round")
     args = ap.parse_args()
     # stdout carries exactly one JSON line: library banners (NCCL prints its version when a
@@ -578,24 +630,45 @@ def main():
                                                parity=not args.no_parity))
             torch.cuda.empty_cache()
 
+    parity, kept = None, []
+    if snap is not None:
+        parity = check_parity(snap, algo, params, world, rank, dev, keep=kept if world == 1 else None)
+
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            # a bounded sample of about args.cpu_seconds of CPU work: one timed iteration sizes it
-            cs = min(scale, args.cpu_scale)
-            r1 = cpu_sample(algo, cs, over, 1, host_threads())
-            iters = max(1, min(2000, int(args.cpu_seconds / max(r1["seconds"], 1e-6))))
-            r = cpu_sample(algo, cs, over, iters, host_threads())
-            cpu = {"value": round(r["gteps"], 4), "unit": "GTEPS", "cores": r["threads"], "kind": "port",
-                   "sample": f"{r['iterations']} {algo} BSP iterations on R-MAT scale-{cs} "
-                             f"({r['edges']} edges, {r['seconds']:.1f} s), oracle/gx_oracle.c OpenMP "
-                             "restatement of run_reference on every host core"}
+            threads = host_threads()
+            if kept:
+                # the same graph as the GPU run (built for the parity check): ~cpu_seconds of iterations
+                og = kept[0]
+                t = time.perf_counter()
+                og.run(algo, max_iterations=1, nthreads=threads)
+                t1 = time.perf_counter() - t
+                iters = max(1, min(200, int(args.cpu_seconds / max(t1, 1e-6))))
+                t = time.perf_counter()
+                rr = og.run(algo, max_iterations=iters, nthreads=threads)
+                dt = time.perf_counter() - t
+                cpu = {"value": round(og.num_edges * rr.iterations / dt / 1e9, 4), "unit": "GTEPS", "cores": threads,
+                       "kind": "port", "same_config": True,
+                       "sample": f"{rr.iterations} {algo} BSP iterations on the same R-MAT scale-{scale} graph "
+                                 f"({og.num_edges} edges, {dt:.1f} s), oracle/gx_oracle.c OpenMP restatement of "
+                                 "run_reference on every host core"}
+            else:
+                # a bounded sample of about args.cpu_seconds of CPU work: one timed iteration sizes it
+                cs = min(scale, args.cpu_scale)
+                r1 = cpu_sample(algo, cs, over, 1, threads)
+                iters = max(1, min(2000, int(args.cpu_seconds / max(r1["seconds"], 1e-6))))
+                r = cpu_sample(algo, cs, over, iters, threads)
+                cpu = {"value": round(r["gteps"], 4), "unit": "GTEPS", "cores": r["threads"], "kind": "port",
+                       "same_config": cs == scale,
+                       "sample": f"{r['iterations']} {algo} BSP iterations on R-MAT scale-{cs} "
+                                 f"({r['edges']} edges, {r['seconds']:.1f} s), oracle/gx_oracle.c OpenMP "
+                                 "restatement of run_reference on every host core"}
+            if not args.no_python_reference:
+                cpu["python_reference"] = python_reference_sample()
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": "GTEPS", "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
-
-    parity = None
-    if snap is not None:
-        parity = check_parity(snap, algo, params, world, rank, dev)
+    kept.clear()
 
     if rank == 0:
         line = {

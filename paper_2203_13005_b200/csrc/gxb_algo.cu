@@ -1372,7 +1372,8 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st, int chu
 // PageRank hub split (option pr_hub_slots, one partition)
 // ======================================================================
 // CSC segments are source-sorted, so the in-edges of a destination that come from the
-// H highest-out-degree sources (slots < H in the degree-sorted order) are a prefix of its
+// H first slots (the highest IN-degree vertices of the degree-sorted order; on R-MAT they are
+// also the highest out-degree ones) are a prefix of its
 // segment. Those "hub" edges are summed from a shared-memory copy of contrib[0, H)
 // (one table per SM, LDS instead of an L1 data-pipe wavefront per gathered element); the
 // remaining "cold" edges run the LDGSTS tile kernel. Both CSCs are compacted to their
@@ -1549,8 +1550,9 @@ int pr_split_prepare(gxb_state* s, cudaStream_t st) {
     if (nz) GXB_CUDA(cudaMemcpyAsync(hcnt.data(), d_hcnt, 4 * nz, cudaMemcpyDeviceToHost, st));
     GXB_CUDA(cudaStreamSynchronize(st));
     const std::vector<uint32_t>& deg = g->h_indeg_sorted;
-    int rc = GXB_OK;
-    for (int k = 0; k < 2 && rc == GXB_OK; ++k) {
+    // one compacted CSC (k = 0 cold, 1 hub); an early error return leaves the lambda only, so
+    // every failure reaches the single cleanup below (sync, then pr_split_free)
+    auto build_one = [&](int k) -> int {
         const bool hub = k == 1;
         std::vector<uint32_t> list, cdeg;
         for (uint64_t r = 0; r < nz; ++r) {
@@ -1585,16 +1587,18 @@ int pr_split_prepare(gxb_state* s, cudaStream_t st) {
         if (n) k_split_copy<<<grid_for(32 * n), kBlock, 0, st>>>(g->d_in_off, g->d_in_src, d_hcnt, s->d_split_slot[k],
                                                                   n, sg->d_in_off, hub ? 1 : 0, sg->d_in_src);
         GXB_CUDA(cudaStreamSynchronize(st));  // list / coff host buffers die with this scope
-        rc = build_tile_plan(sg, st);
-        if (rc != GXB_OK) break;
+        GXB_CHECK(build_tile_plan(sg, st));
         if (sg->tiles.num_spans)
             k_remap_u32<<<grid_for(sg->tiles.num_spans), kBlock, 0, st>>>(sg->tiles.d_span_slot, sg->tiles.num_spans,
                                                                           s->d_split_slot[k]);
         GXB_CHECK(dalloc(&s->d_split_partials[k], sizeof(PrOps::Acc) * (sg->tiles.num_partials + 1)));
         GXB_CHECK(dalloc_t(&s->d_split_sum[k], owned + 1));
         GXB_CUDA(cudaMemsetAsync(s->d_split_sum[k], 0, 8 * (owned + 1), st));
-    }
-    GXB_CUDA(cudaStreamSynchronize(st));
+        return GXB_OK;
+    };
+    int rc = GXB_OK;
+    for (int k = 0; k < 2 && rc == GXB_OK; ++k) rc = build_one(k);
+    if (cudaStreamSynchronize(st) != cudaSuccess && rc == GXB_OK) rc = fail(GXB_ECUDA, "pr_split_prepare: sync");
     if (rc != GXB_OK) {
         pr_split_free(s);
         return rc;

@@ -268,6 +268,17 @@ class PartitionedRun:
             return self._exchange_dense()
         return self._exchange_delta()
 
+    def _on_stream(self) -> dict:
+        """The library calls run on torch's current stream of this device (explicitly: the
+        NCCL collectives of the round are ordered on it, and a user stream context must not
+        leave the kernels on the legacy default stream)."""
+        if self.device is None:
+            return {}
+        import torch
+        if torch.device(self.device).type != "cuda":
+            return {}
+        return {"stream": torch.cuda.current_stream(self.device)}
+
     def _view(self, ptr, nbytes, dtype):
         if hasattr(self.state, "view"):
             return self.state.view(ptr, nbytes, dtype)
@@ -382,7 +393,7 @@ class PartitionedRun:
         if overlapped:
             moved_early = self._overlapped_pagerank_round()
         else:
-            self.state.iterate(direction)
+            self.state.iterate(direction, **self._on_stream())
         device_vote = (self.comm.world > 1 and hasattr(self.state, "stats_device")
                        and hasattr(self.comm, "vote_start_device"))
         async_delta = device_vote and self.algo != "pagerank" and hasattr(self.state, "pack_async")
@@ -394,8 +405,8 @@ class PartitionedRun:
             if getattr(self, "_vote_buf", None) is None:
                 self._vote_buf = torch.empty(6, dtype=torch.float64, device=self.device)
             if async_delta:
-                self.state.pack_async()
-            self.state.stats_device(self._vote_buf)
+                self.state.pack_async(**self._on_stream())
+            self.state.stats_device(self._vote_buf, **self._on_stream())
             handle = self.comm.vote_start_device(self._vote_buf)
             st = None
         else:
@@ -484,8 +495,8 @@ class PartitionedRun:
             launched = 0
 
             def launch(k):
-                self.state.iterate("pull")
-                self.state.stats_device(bufs[k % 2])
+                self.state.iterate("pull", **self._on_stream())
+                self.state.stats_device(bufs[k % 2], **self._on_stream())
                 rows = self.comm.vote_start_device(bufs[k % 2]) if world > 1 else bufs[k % 2]
                 host[k % 2].copy_(rows, non_blocking=True)
                 evs[k % 2].record()

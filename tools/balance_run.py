@@ -1,6 +1,6 @@
 """Heterogeneous balancing end to end (run under torchrun): every rank measures its own
-unit cost on its cost-balanced partition (`balancer.observe`: CUDA-event-timed pull
-rounds, unit = owned in-edge), the costs are
+unit cost on the same workload (the whole graph, the run's own direction schedule;
+`balancer.observe`: CUDA-event-timed rounds) in the graph store's cost units, the costs are
 all-gathered, and every rank rebuilds its partition with the same capacity factors
 (`DeviceGraph(capacity=...)` -> gxb_graph_build_balanced) and checks the run against
 the CPU oracle.
@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--scale", type=int, default=18)
     ap.add_argument("--algo", default="sssp")
     ap.add_argument("--slow-rank", type=int, default=-1)
+    ap.add_argument("--calib-rounds", type=int, default=8)
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -47,15 +48,20 @@ def main():
     src, dst, w = rmat_host(RmatParams(scale=args.scale, seed=91, **over))
     csr = args.algo in ("sssp", "cc", "lp")
 
-    # 1. measure this device on its even share (ranges partitioning, equal factors)
-    g = DeviceGraph(ctx, src, dst, w, part=rank, nparts=world, csr=csr, partitioning="ranges")
+    # 1. measure every device on the SAME workload — the whole graph as one partition, with the
+    #    direction schedule the run uses — in the store's cost units (12 B per in-edge + 64 B per
+    #    vertex, the cost line gxb_graph_build_balanced cuts), so the factors compare devices,
+    #    not the contents of their partitions
+    g = DeviceGraph(ctx, src, dst, w, part=0, nparts=1, csr=csr)
     s = DeviceState(g, args.algo)
-    obs = observe(s, iterations=8, direction="pull")
+    observe(s, iterations=2, direction="auto")   # warm-up (allocations, L2)
+    s.free()
+    s = DeviceState(g, args.algo)
+    obs = observe(s, iterations=args.calib_rounds, direction="auto")
     if rank == args.slow_rank:
         obs = [(u, b, 2.0 * t) for u, b, t in obs]
-    owned = max(1, int(g.info.owned_edges))
-    # a pull round scans every owned in-edge: time per round / owned in-edges
-    unit = float(np.median([t for _, _, t in obs])) / owned
+    cost_line = 12 * int(g.info.owned_edges) + 64 * int(g.num_vertices)
+    unit = sum(t for _, _, t in obs) / (len(obs) * cost_line)
     s.free()
     g.free()
     costs = [None] * world
