@@ -1936,6 +1936,7 @@ void gxb_lp_free(gxb_state* s);                     // gxb_lp.cu
 int gxb_lp_prepare(gxb_state* s, cudaStream_t st);  // gxb_lp.cu
 
 int gxb_state_create(gxb_graph* g, int algo, const uint32_t* sources, int nsrc, gxb_state** out) {
+    NvtxRange nvtx_("gxb_state_create");
     if (!g || !out) return fail(GXB_EINVAL, "gxb_state_create: null argument");
     if (algo < GXB_ALGO_SSSP || algo > GXB_ALGO_CC) return fail(GXB_EINVAL, "unknown algorithm");
     if (!g->ctx->alive) return fail(GXB_ESTATE, "gxb_state_create: daemon terminated");
@@ -2172,6 +2173,7 @@ int gxb_lp_push(gxb_state* s, cudaStream_t st, const uint32_t* rowpre);
 
 
 int gxb_iterate(gxb_state* s, int direction, void* stream) {
+    NvtxRange nvtx_("gxb_iterate");
     if (!s) return fail(GXB_EINVAL, "gxb_iterate: null state");
     if (s->in_round) return fail(GXB_ESTATE, "gxb_iterate: a request round is open (call gxb_commit)");
     if (!s->g->ctx->alive) return fail(GXB_ESTATE, "gxb_iterate: daemon terminated");
@@ -2316,6 +2318,7 @@ int gxb_iterate_end(gxb_state* s, void* stream) {
 }
 
 int gxb_request(gxb_state* s, int op, uint64_t lo, uint64_t hi, void* stream) {
+    NvtxRange nvtx_("gxb_request");
     if (!s) return fail(GXB_EINVAL, "gxb_request: null state");
     if (!s->g->ctx->alive) return fail(GXB_ESTATE, "gxb_request: daemon terminated");
     if (s->algo == GXB_ALGO_LP) return fail(GXB_EINVAL, "gxb_request: LP runs through gxb_iterate only");
@@ -2408,6 +2411,7 @@ int gxb_request(gxb_state* s, int op, uint64_t lo, uint64_t hi, void* stream) {
 }
 
 int gxb_commit(gxb_state* s, void* stream) {
+    NvtxRange nvtx_("gxb_commit");
     if (!s) return fail(GXB_EINVAL, "gxb_commit: null state");
     if (!s->in_round) {  // a partition with nothing to request still closes an (empty) round
         GXB_CHECK(collect_stats(s));
@@ -2501,6 +2505,7 @@ static int stage(gxb_state* s) {
 }
 
 int gxb_read_attrs(gxb_state* s, double* host_out, int owned_only, void* stream) {
+    NvtxRange nvtx_("gxb_read_attrs");
     if (!s) return fail(GXB_EINVAL, "gxb_read_attrs: null state");
     gxb_graph* g = s->g;
     const uint64_t V = g->V;
@@ -2531,6 +2536,7 @@ static int install_marks(gxb_state* s, cudaStream_t st, InstallMarks* m) {
 }
 
 int gxb_write_attrs(gxb_state* s, const double* host_in, void* stream) {
+    NvtxRange nvtx_("gxb_write_attrs");
     if (!s) return fail(GXB_EINVAL, "gxb_write_attrs: null state");
     if (s->in_round) return fail(GXB_ESTATE, "gxb_write_attrs: a round is open");
     gxb_graph* g = s->g;

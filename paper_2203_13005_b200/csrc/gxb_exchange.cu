@@ -301,6 +301,7 @@ int gxb_exchange_buffer(gxb_state* s, int which, void** dev_ptr, uint64_t* bytes
 }
 
 int gxb_exchange_pack(gxb_state* s, void* stream, uint64_t* count_out) {
+    NvtxRange nvtx_("gxb_exchange_pack");
     if (!s || !count_out) return fail(GXB_EINVAL, "gxb_exchange_pack: null argument");
     if (s->algo == GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "gxb_exchange_pack: PageRank uses the dense exchange");
     if (s->in_round) return fail(GXB_ESTATE, "gxb_exchange_pack: round still open");
@@ -328,6 +329,7 @@ int gxb_exchange_pack(gxb_state* s, void* stream, uint64_t* count_out) {
 // vote block (gxb_stats_device) and the host-side frontier length is refreshed when the
 // next round starts
 int gxb_exchange_pack_async(gxb_state* s, void* stream) {
+    NvtxRange nvtx_("gxb_exchange_pack_async");
     if (!s) return fail(GXB_EINVAL, "gxb_exchange_pack_async: null state");
     if (s->algo == GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "gxb_exchange_pack_async: PageRank uses the dense exchange");
     if (s->in_round) return fail(GXB_ESTATE, "gxb_exchange_pack_async: round still open");
@@ -351,6 +353,7 @@ int gxb_exchange_pack_async(gxb_state* s, void* stream) {
 int gxb_exchange_unpack_regions(gxb_state* s, const void* d_records, const uint64_t* counts, int nblocks,
                                 uint64_t block_records, uint64_t frontier_after, uint64_t units_after,
                                 void* stream) {
+    NvtxRange nvtx_("gxb_exchange_unpack_regions");
     if (!s || !counts || nblocks < 0) return fail(GXB_EINVAL, "gxb_exchange_unpack_regions: bad argument");
     if (s->algo == GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "gxb_exchange_unpack_regions: PageRank uses the dense exchange");
     if (!s->d_xscratch) GXB_CHECK(dalloc_t(&s->d_xscratch, 4));
@@ -384,6 +387,7 @@ int gxb_exchange_unpack_regions(gxb_state* s, const void* d_records, const uint6
 }
 
 int gxb_exchange_unpack(gxb_state* s, const void* d_records, uint64_t count, void* stream) {
+    NvtxRange nvtx_("gxb_exchange_unpack");
     if (!s) return fail(GXB_EINVAL, "gxb_exchange_unpack: null state");
     if (s->algo == GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "gxb_exchange_unpack: PageRank uses the dense exchange");
     if (count == 0) return GXB_OK;
@@ -408,6 +412,7 @@ int gxb_exchange_unpack(gxb_state* s, const void* d_records, uint64_t count, voi
 
 int gxb_attrs_deliver(gxb_state* s, const uint64_t* host_dense, const double* host_vals, uint64_t n,
                       void* stream) {
+    NvtxRange nvtx_("gxb_attrs_deliver");
     if (!s) return fail(GXB_EINVAL, "gxb_attrs_deliver: null state");
     if (s->in_round) return fail(GXB_ESTATE, "gxb_attrs_deliver: a round is open");
     if (n == 0) return GXB_OK;

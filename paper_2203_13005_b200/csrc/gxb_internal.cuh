@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../../include/gxb.h"
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges cost nothing without a tool attached
 
 #if !defined(__CUDA_ARCH__) || __CUDA_ARCH__ >= 1000
 #else
@@ -30,6 +31,14 @@ int cuda_fail(cudaError_t e, const char* what);
         int _rc = (call);                                                   \
         if (_rc != GXB_OK) return _rc;                                      \
     } while (0)
+
+// NVTX range over a host API call (visible in nsys / ncu --nvtx timelines)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 constexpr uint32_t kInf32 = 0xFFFFFFFFu;  // SSSP "inf" lane / invalid label
 constexpr int kBlock = 256;               // threads per CTA for the vertex/edge kernels

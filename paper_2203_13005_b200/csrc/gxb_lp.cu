@@ -38,6 +38,11 @@ struct LpPush;
 struct LpScratch {
     LpHub hub;
     uint64_t chunk_end = 0;
+    uint64_t big_end = 0;  // relative slots [0, big_end): in-degree > kLpBigDeg (chunked warps)
+    uint64_t big_items = 0;    // their chunk items (the plan's first items)
+    uint64_t big_entries = 0;  // their global table entries (a prefix of the tables)
+    uint64_t cta_end = 0;  // relative slots [big_end, cta_end): in-degree > kLpCtaMinDeg (one CTA each)
+    uint32_t* eff = nullptr;  // per slot: label if active, else kEmpty (rounds >= 2)
     uint32_t hot_end = 0;  // slots with in-degree >= kLpHotDegree: pushed through shared memory
     // sparse rounds (allocated on the first one)
     unsigned long long* pkeys = nullptr;
@@ -91,7 +96,16 @@ struct LpLaunch {
     unsigned bin_blocks[kNumGroupBins];
     LpHub hub;
     bool injective;  // labels are distinct (round 1): hub counts are edge multiplicities
+    // label of every ACTIVE source slot, kEmpty for inactive ones (k_lp_eff, rounds >= 2):
+    // one gather per edge instead of an active-bitmap test plus a label gather
+    const uint32_t* eff;
 };
+
+// the label a source contributes to its out-neighbours' multisets, or kEmpty
+__device__ __forceinline__ uint32_t lp_msg(const LpLaunch& L, uint32_t s) {
+    if (L.eff) return __ldg(L.eff + s);
+    return bit_test(L.active_cur, s) ? __ldg(L.lab_cur + s) : kEmpty;
+}
 
 __device__ __forceinline__ void lp_finish(const LpLaunch& L, uint32_t slot, unsigned long long best, LocalStats& st) {
     if (best == 0ull) return;  // no message: keep label, inactive (A/algorithms.py:195-196)
@@ -122,7 +136,7 @@ __device__ __forceinline__ void lp_group(const LpLaunch& L, int k, unsigned b, u
     uint32_t* my = buf + grp * kCap;
     for (uint32_t i = gl; i < deg; i += G) {
         const uint32_t s = __ldg(L.in_src + beg + i);
-        my[i] = bit_test(L.active_cur, s) ? __ldg(L.lab_cur + s) : kEmpty;
+        my[i] = lp_msg(L, s);
     }
     __syncwarp();
     unsigned long long best = 0ull;
@@ -181,9 +195,9 @@ __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint3
             src[j] = e < end ? __ldg(L.in_src + e) : kEmpty;
         }
 #pragma unroll
-        for (int j = 0; j < kB; ++j) ok[j] = src[j] != kEmpty && bit_test(L.active_cur, src[j]);
+        for (int j = 0; j < kB; ++j) lab[j] = src[j] != kEmpty ? lp_msg(L, src[j]) : kEmpty;
 #pragma unroll
-        for (int j = 0; j < kB; ++j) lab[j] = ok[j] ? __ldg(L.lab_cur + src[j]) : 0u;
+        for (int j = 0; j < kB; ++j) ok[j] = lab[j] != kEmpty;
 #pragma unroll
         for (int j = 0; j < kB; ++j) {
             const unsigned long long key = ok[j] ? (unsigned long long)lab[j] : (0x100000000ull | (unsigned)lane);
@@ -253,6 +267,197 @@ __device__ __forceinline__ void lp_chunk_injective(const LpLaunch& L, uint64_t i
         best = q > best ? q : best;
     }
     if (lane == 0 && best && best > __ldcg(L.hub.best + rel)) atomicMax(L.hub.best + rel, best);
+}
+
+// ---- dense rounds >= 2: hubs counted in shared memory ----
+// A destination with in-degree > kChunkMinDeg is counted by one CTA (in-degree >
+// kLpCtaMinDeg) or one warp (the rest) in an open-addressing (label, count) table in
+// shared memory sized to twice the in-degree (so it holds every distinct label at load
+// <= 1/2), capped at kLpCtaCap / kLpWarpCap entries. Equal labels of 32 edges are merged
+// first (__match_any_sync). A label whose bounded probe sequence finds no room goes to the
+// destination's global table (L2 atomics, running packed argmax); since shared slots are
+// never freed, such a label never lands in shared memory later, so each label is counted
+// in exactly one table and the argmax is the max of both. The owner clears the global
+// table it touched, so nothing is reset per round on the host side.
+constexpr uint32_t kLpCtaMinDeg = 512;
+constexpr uint32_t kLpBigDeg = 4096;  // above: chunked warps over all SMs + global tables (label-diverse hubs)
+constexpr int kLpCtaCap = 8192;    // 64 KB of (key, count) per CTA
+constexpr int kLpWarpCap = 1024;   // 8 KB per warp
+constexpr int kLpProbes = 16;
+
+__global__ void k_lp_eff(const uint32_t* __restrict__ active, const uint32_t* __restrict__ lab, uint64_t S,
+                         uint32_t* eff) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S; i += (uint64_t)gridDim.x * blockDim.x)
+        eff[i] = ((__ldg(active + (i >> 5)) >> (i & 31)) & 1u) ? __ldg(lab + i) : kEmpty;
+}
+
+// insert c copies of `lab` into a shared table; false when the probe sequence is full
+__device__ __forceinline__ bool smem_table_add(uint32_t* keys, uint32_t* cnts, uint32_t mask, uint32_t lab,
+                                               uint32_t c) {
+    uint32_t h = mix32(lab) & mask;
+#pragma unroll 1
+    for (int probe = 0; probe < kLpProbes; ++probe) {
+        uint32_t k = keys[h];
+        if (k == kEmpty) {
+            k = atomicCAS(keys + h, kEmpty, lab);
+            if (k == kEmpty) k = lab;
+        }
+        if (k == lab) {
+            atomicAdd(cnts + h, c);
+            return true;
+        }
+        h = (h + 1) & mask;
+    }
+    return false;
+}
+
+__device__ __forceinline__ unsigned long long pack_best(uint32_t count, uint32_t lab) {
+    return ((unsigned long long)count << 32) | (unsigned long long)(~lab);
+}
+
+// stream [beg, end) with `nthreads` threads (index t), 8 loads in flight per lane, and fold
+// each 32-edge group's labels into the shared table; returns whether anything overflowed
+__device__ __forceinline__ bool lp_count_edges(const LpLaunch& L, uint64_t rel, uint64_t beg, uint64_t end,
+                                               unsigned t, unsigned nthreads, uint32_t* keys, uint32_t* cnts,
+                                               uint32_t mask) {
+    constexpr int kB = 8;
+    const int lane = threadIdx.x & 31;
+    const unsigned warp0 = t - lane;  // first thread of this warp within the group
+    bool over = false;
+    const uint64_t gbase = L.hub.tab_off ? __ldg(L.hub.tab_off + rel) : 0;
+    const uint32_t gmask = L.hub.tab_mask ? __ldg(L.hub.tab_mask + rel) : 0;
+    for (uint64_t e0 = beg + (uint64_t)warp0 * kB; e0 < end; e0 += (uint64_t)nthreads * kB) {
+        uint32_t src[kB], lab[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            const uint64_t e = e0 + 32 * j + lane;
+            src[j] = e < end ? __ldg(L.in_src + e) : kEmpty;
+        }
+#pragma unroll
+        for (int j = 0; j < kB; ++j) lab[j] = src[j] != kEmpty ? lp_msg(L, src[j]) : kEmpty;
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            const bool ok = lab[j] != kEmpty;
+            const unsigned long long key = ok ? (unsigned long long)lab[j] : (0x100000000ull | (unsigned)lane);
+            const unsigned m = __match_any_sync(kFull, key);
+            if (ok && lane == __ffs(m) - 1) {
+                if (!smem_table_add(keys, cnts, mask, lab[j], (uint32_t)__popc(m))) {
+                    const uint32_t nc = table_add(L.hub.keys, L.hub.counts, gbase, gmask, lab[j], __popc(m));
+                    const unsigned long long pk = pack_best(nc, lab[j]);
+                    if (pk > __ldcg(L.hub.best + rel)) atomicMax(L.hub.best + rel, pk);
+                    over = true;
+                }
+            }
+        }
+    }
+    return over;
+}
+
+__global__ void __launch_bounds__(kBlock) k_lp_hub_cta(const LpLaunch L, uint64_t lo_rel, uint64_t cta_end) {
+    extern __shared__ uint32_t lp_dyn[];  // kLpCtaCap keys, then kLpCtaCap counts
+    uint32_t* keys = lp_dyn;
+    uint32_t* cnts = lp_dyn + kLpCtaCap;
+    __shared__ unsigned long long wbest[kBlock / 32];
+    __shared__ int over_any;
+    LocalStats st;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint64_t rel = lo_rel + blockIdx.x; rel < cta_end; rel += gridDim.x) {
+        const uint64_t beg = __ldg(L.in_off + rel), end = __ldg(L.in_off + rel + 1);
+        uint32_t C = 64;
+        while (C < kLpCtaCap && (uint64_t)C < 2 * (end - beg)) C <<= 1;
+        for (uint32_t i = threadIdx.x; i < C; i += kBlock) {
+            keys[i] = kEmpty;
+            cnts[i] = 0;
+        }
+        if (threadIdx.x == 0) over_any = 0;
+        __syncthreads();
+        const bool over = lp_count_edges(L, rel, beg, end, threadIdx.x, kBlock, keys, cnts, C - 1);
+        if (over) over_any = 1;
+        __syncthreads();
+        unsigned long long best = 0ull;
+        for (uint32_t i = threadIdx.x; i < C; i += kBlock) {
+            const uint32_t k = keys[i];
+            if (k != kEmpty) {
+                const unsigned long long pk = pack_best(cnts[i], k);
+                best = pk > best ? pk : best;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long q = __shfl_xor_sync(kFull, best, o);
+            best = q > best ? q : best;
+        }
+        if (lane == 0) wbest[warp] = best;
+        __syncthreads();
+        const bool spilled = over_any != 0;
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < kBlock / 32; ++w) best = wbest[w] > best ? wbest[w] : best;
+            if (spilled) {
+                const unsigned long long g = L.hub.best[rel];
+                best = g > best ? g : best;
+                L.hub.best[rel] = 0ull;
+            }
+            lp_finish(L, (uint32_t)(L.lo + rel), best, st);
+        }
+        if (spilled) {  // reset the global table this destination used
+            const uint64_t gb = L.hub.tab_off[rel];
+            const uint64_t gn = (uint64_t)L.hub.tab_mask[rel] + 1;
+            for (uint64_t i = threadIdx.x; i < gn; i += kBlock) {
+                L.hub.keys[gb + i] = kEmpty;
+                L.hub.counts[gb + i] = 0;
+            }
+        }
+        __syncthreads();  // the tables are reused by the next destination
+    }
+    flush_stats(st, L.stats);
+}
+
+__global__ void __launch_bounds__(kBlock) k_lp_hub_warp(const LpLaunch L, uint64_t lo_rel, uint64_t hi_rel) {
+    extern __shared__ uint32_t lp_dyn[];  // per warp: kLpWarpCap keys, then kLpWarpCap counts
+    LocalStats st;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* wk = lp_dyn + warp * 2 * kLpWarpCap;
+    uint32_t* wc = wk + kLpWarpCap;
+    const uint64_t nw = (uint64_t)gridDim.x * (kBlock / 32);
+    for (uint64_t rel = lo_rel + blockIdx.x * (uint64_t)(kBlock / 32) + warp; rel < hi_rel; rel += nw) {
+        const uint64_t beg = __ldg(L.in_off + rel), end = __ldg(L.in_off + rel + 1);
+        uint32_t C = 64;
+        while (C < kLpWarpCap && (uint64_t)C < 2 * (end - beg)) C <<= 1;
+        for (uint32_t i = lane; i < C; i += 32) {
+            wk[i] = kEmpty;
+            wc[i] = 0;
+        }
+        __syncwarp();
+        const bool over = __any_sync(kFull, lp_count_edges(L, rel, beg, end, lane, 32, wk, wc, C - 1));
+        __syncwarp();
+        unsigned long long best = 0ull;
+        for (uint32_t i = lane; i < C; i += 32) {
+            const uint32_t k = wk[i];
+            if (k != kEmpty) {
+                const unsigned long long pk = pack_best(wc[i], k);
+                best = pk > best ? pk : best;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long q = __shfl_xor_sync(kFull, best, o);
+            best = q > best ? q : best;
+        }
+        if (over) {
+            if (lane == 0) {
+                const unsigned long long g = L.hub.best[rel];
+                best = g > best ? g : best;
+                L.hub.best[rel] = 0ull;
+            }
+            const uint64_t gb = L.hub.tab_off[rel];
+            const uint64_t gn = (uint64_t)L.hub.tab_mask[rel] + 1;
+            for (uint64_t i = lane; i < gn; i += 32) {
+                L.hub.keys[gb + i] = kEmpty;
+                L.hub.counts[gb + i] = 0;
+            }
+        }
+        if (lane == 0) lp_finish(L, (uint32_t)(L.lo + rel), best, st);
+        __syncwarp();
+    }
+    flush_stats(st, L.stats);
 }
 
 __global__ void __launch_bounds__(kBlock) k_lp_pull(const LpLaunch L) {
@@ -496,6 +701,7 @@ static void lp_free(LpScratch* S) {
     dfree(S->pbest);
     dfree(S->ptargets);
     dfree(S->pntargets);
+    dfree(S->eff);
     delete S;
 }
 
@@ -506,6 +712,12 @@ static int lp_setup(gxb_state* s, cudaStream_t st) {
     const PullPlan& P = g->plan;
     LpScratch* S = new LpScratch();
     S->chunk_end = P.chunk_end;
+    while (S->big_end < P.chunk_end && g->h_indeg_sorted[S->big_end] > kLpBigDeg) {
+        S->big_items += (g->h_indeg_sorted[S->big_end] + kChunkEdges - 1) / kChunkEdges;
+        ++S->big_end;
+    }
+    S->cta_end = S->big_end;
+    while (S->cta_end < P.chunk_end && g->h_indeg_sorted[S->cta_end] > kLpCtaMinDeg) ++S->cta_end;
     while (S->hot_end < g->h_indeg_sorted.size() && g->h_indeg_sorted[S->hot_end] >= kLpHotDegree) ++S->hot_end;
     LpHub& H = S->hub;
     std::vector<uint64_t> off(P.chunk_end + 1);
@@ -518,6 +730,7 @@ static int lp_setup(gxb_state* s, cudaStream_t st) {
         acc += size;
     }
     H.entries = acc;
+    S->big_entries = off[S->big_end];
     int rc = GXB_OK;
     auto up = [&](auto** d, const auto& h) {
         if (rc != GXB_OK) return;
@@ -531,6 +744,7 @@ static int lp_setup(gxb_state* s, cudaStream_t st) {
     if (rc == GXB_OK) rc = dalloc_t(&H.keys, acc + 1);
     if (rc == GXB_OK) rc = dalloc_t(&H.counts, acc + 1);
     if (rc == GXB_OK) rc = dalloc_t(&H.best, P.chunk_end + 1);
+    if (rc == GXB_OK) rc = dalloc_t(&S->eff, g->S + 1);
     if (rc == GXB_OK) {
         cudaMemsetAsync(H.keys, 0xFF, 4 * (acc + 1), st);
         cudaMemsetAsync(H.counts, 0, 4 * (acc + 1), st);
@@ -607,6 +821,45 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
     }
     L.hub = S->hub;
     L.injective = s->lab_injective;
+    if (!L.injective) {
+        // rounds >= 2: effective labels, hubs counted in shared memory by CTAs / warps, then
+        // the small destinations by the group bins (no chunk items, no hub apply pass)
+        const uint64_t S_ = g->S;
+        if (S_) k_lp_eff<<<grid_for(S_), kBlock, 0, st>>>(s->d_active[0], s->d_lab_cur, S_, S->eff);
+        L.eff = S->eff;
+        static bool attrs_set[64] = {};
+        const int dev = g->ctx->device & 63;
+        if (!attrs_set[dev]) {
+            GXB_CUDA(cudaFuncSetAttribute(k_lp_hub_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          2 * 4 * kLpCtaCap));
+            GXB_CUDA(cudaFuncSetAttribute(k_lp_hub_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (kBlock / 32) * 2 * 4 * kLpWarpCap));
+            attrs_set[dev] = true;
+        }
+        // chunk items of the big hubs only (the plan lists items in slot order) + group bins
+        grid -= L.chunk_blocks;
+        L.num_items = S->big_items;
+        L.chunk_blocks = (unsigned)((S->big_items + (kBlock / 32) - 1) / (kBlock / 32));
+        grid += L.chunk_blocks;
+        if (grid) k_lp_pull<<<grid, kBlock, 0, st>>>(L);
+        if (S->cta_end > S->big_end) {
+            const unsigned gc = (unsigned)std::min<uint64_t>(S->cta_end - S->big_end, 3ull * kNumSMs);
+            k_lp_hub_cta<<<gc, kBlock, 2 * 4 * kLpCtaCap, st>>>(L, S->big_end, S->cta_end);
+        }
+        if (S->chunk_end > S->cta_end) {
+            const uint64_t n = S->chunk_end - S->cta_end;
+            const unsigned gw = (unsigned)std::min<uint64_t>((n + kBlock / 32 - 1) / (kBlock / 32), 6ull * kNumSMs);
+            k_lp_hub_warp<<<gw, kBlock, (kBlock / 32) * 2 * 4 * kLpWarpCap, st>>>(L, S->cta_end, S->chunk_end);
+        }
+        if (S->big_end) {
+            k_lp_hub_apply<<<grid_for(S->big_end), kBlock, 0, st>>>(L, S->big_end);
+            GXB_CUDA(cudaMemsetAsync(S->hub.keys, 0xFF, 4 * S->big_entries, st));
+            GXB_CUDA(cudaMemsetAsync(S->hub.counts, 0, 4 * S->big_entries, st));
+        }
+        s->launches += 3;  // + the caller's 2: eff, chunks + groups, CTA hubs, warp hubs, hub apply
+        GXB_CUDA(cudaGetLastError());
+        return GXB_OK;
+    }
     if (grid) k_lp_pull<<<grid, kBlock, 0, st>>>(L);
     if (S->chunk_end) {
         k_lp_hub_apply<<<grid_for(S->chunk_end), kBlock, 0, st>>>(L, S->chunk_end);

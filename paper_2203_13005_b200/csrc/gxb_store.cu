@@ -1035,6 +1035,7 @@ int gxb_graph_build(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst, cons
 int gxb_graph_build_sized(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint32_t* w,
                           uint64_t num_edges, int part, int nparts, const uint64_t* sizes, uint32_t flags,
                           void* stream, gxb_graph** out) {
+    NvtxRange nvtx_("gxb_graph_build_sized");
     if (!ctx || !ctx->alive) return fail(GXB_ESTATE, "gxb_graph_build: daemon not initialised");
     if (!out) return fail(GXB_EINVAL, "gxb_graph_build: null out");
     if (num_edges && (!src || !dst)) return fail(GXB_EINVAL, "gxb_graph_build: null edge arrays");
@@ -1063,6 +1064,7 @@ int gxb_graph_build_sized(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst
 int gxb_graph_build_balanced(gxb_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint32_t* w,
                              uint64_t num_edges, int part, int nparts, const double* capacity, uint32_t flags,
                              void* stream, gxb_graph** out) {
+    NvtxRange nvtx_("gxb_graph_build_balanced");
     if (!ctx || !ctx->alive) return fail(GXB_ESTATE, "gxb_graph_build: daemon not initialised");
     if (!out) return fail(GXB_EINVAL, "gxb_graph_build: null out");
     if (!capacity) return fail(GXB_EINVAL, "gxb_graph_build_balanced: null capacity factors");
