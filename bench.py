@@ -197,6 +197,66 @@ def python_reference_sample():
     return out
 
 
+def run_dropin_bench(args):
+    """End to end through the reference's own public API: `accelgraph.engine.run` (unmodified
+    Engine, agents, shared regions, sync rounds, A/engine.py:422-427) with the B200 daemon
+    dropped in (dropin.install), PageRank for `--steps` iterations on R-MAT `--scale`
+    (default 18) — wall clock around the call, the graph already in the reference's
+    PartitionedGraph. Beside it the reference's own CPU daemon for one iteration of the same
+    run (a bounded sample). One process, one GPU."""
+    from paper_2203_13005_b200 import dropin  # finds the reference (sys.path or baseline/_ref)
+    from accelgraph.algorithms import make_algorithm
+    from accelgraph.engine import RunConfig, run
+    from accelgraph.graph import Edge, even_sizes, partition_graph
+
+    from oracle import oracle
+    scale = args.scale or 18
+    m = max(1, args.partitions)
+    src, dst, _ = oracle.rmat(scale, 16, 1, 0.57, 0.19, 0.19, 0, True, False)
+    t = time.perf_counter()
+    edges = [Edge(a, b) for a, b in zip(src.tolist(), dst.tolist())]
+    vertices = set(src.tolist()) | set(dst.tolist())
+    graph = partition_graph(vertices, edges, even_sizes(len(vertices), m))
+    t_build = time.perf_counter() - t
+    iters = args.steps
+
+    def one(n, gpu):
+        g2 = partition_graph(vertices, edges, even_sizes(len(vertices), m))
+        algo = make_algorithm("pagerank", vertices, g2.out_degree)
+        cfg = RunConfig(partitions=m, max_iterations=n)
+        t0 = time.perf_counter()
+        if gpu:
+            with dropin.installed():
+                attrs, met = run(g2, algo, "bsp", cfg)
+        else:
+            attrs, met = run(g2, algo, "bsp", cfg)
+        return time.perf_counter() - t0, attrs, met
+
+    one(1, True)  # warm-up: context, allocations
+    dt, attrs, met = one(iters, True)
+    rt, rattrs, _ = one(1, False)
+    err = max(abs(attrs[v][0] - rattrs[v][0]) for v in vertices) if iters == 1 else None
+    E = len(edges)
+    line = {
+        "metric": METRIC, "mode": "dropin", "value": round(E * met.iterations / dt / 1e9, 5), "unit": "GTEPS",
+        "n_gpus": 1, "steps": iters, "ms_per_step": round(1e3 * dt / max(1, met.iterations), 2),
+        "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"dropin-pr-s{scale}", "rmat_scale": scale, "num_edges": E,
+                   "num_vertices": len(vertices), "partitions": m,
+                   "path": "accelgraph.engine.run (unmodified reference Engine / Agent.request / SharedRegion / "
+                           "Daemon loop / gqq-gdq sync round) with dropin.install(): GpuDaemon + GpuAgent, fused rounds"},
+        "iterations": met.iterations, "protocol_conformant": met.protocol_conformant(),
+        "reference_cpu_daemon": {"iterations": 1, "seconds": round(rt, 3),
+                                 "gteps": round(E / rt / 1e9, 7), "cores": 1,
+                                 "note": "the same Engine with the reference's own daemon (pure Python, GIL-bound)"},
+        "graph_build_s": round(t_build, 1),
+    }
+    if err is not None:
+        line["max_abs_diff_vs_reference"] = err
+    emit(line)
+    return 0
+
+
 def run_reference_arm(args):
     """The reference's CPU path on the box's host cores, on the same workload and scale as
     the GPU arm: oracle/gx_oracle.c (run_reference restated in C, OpenMP on every host
@@ -210,6 +270,8 @@ def run_reference_arm(args):
     if args.scale:
         scale = args.scale
     threads = host_threads()
+    from oracle import oracle
+    oracle.set_threads(threads)
     t_build = time.perf_counter()
     g = cpu_graph(algo, scale, over)
     t_build = time.perf_counter() - t_build
@@ -330,6 +392,7 @@ def oracle_parity(algo, params, iterations, attrs, changed=None, units=None, cap
     t0 = time.perf_counter()
     try:
         from oracle import oracle
+        oracle.set_threads(host_threads())  # every host core (torchrun's ranks default to one)
         src, dst, w = oracle.rmat(params.scale, params.edge_factor, params.seed, params.a, params.b, params.c,
                                   params.wmax if algo == "sssp" else 0, params.scramble, params.symmetric)
         og = oracle.OracleGraph(src, dst, None if w is None else w.astype(np.float64))
@@ -366,7 +429,7 @@ def check_parity(snap, algo, params, world, rank, dev, keep=None):
     import torch.distributed as dist
     rounds, attrs = snap
     if world > 1:
-        t = torch.from_numpy(np.nan_to_num(attrs, nan=0.0)).to(dev)
+        t = torch.from_numpy(np.nan_to_num(attrs, nan=0.0, posinf=np.inf)).to(dev)
         dist.all_reduce(t)
         attrs = t.cpu().numpy()
         if rank != 0:
@@ -400,6 +463,10 @@ def main():
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed run")
     ap.add_argument("--no-python-reference", action="store_true", help="skip timing the pure-Python reference (C1)")
     ap.add_argument("--no-run-ahead", action="store_true", help="PageRank: wait for every vote before the next round")
+    ap.add_argument("--dropin", action="store_true",
+                    help="time the unmodified reference Engine with the B200 daemon dropped in (PageRank, "
+                         "--scale default 18, --partitions)")
+    ap.add_argument("--partitions", type=int, default=1)
     args = ap.parse_args()
     # stdout carries exactly one JSON line: library banners (NCCL prints its version when a
     # communicator is created) go to stderr until the line is printed
@@ -411,6 +478,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.dropin:
+        return run_dropin_bench(args)
 
     import torch
     import torch.distributed as dist
@@ -627,7 +696,9 @@ def main():
                 ("cc-s24", "cc", RmatParams(scale=min(scale, 24), seed=1, symmetric=True), None),
                 ("lp-s24-a65", "lp", RmatParams(scale=min(scale, 24), seed=1, a=0.65, b=0.15, c=0.15), 15)):
             secondary.append(time_frontier_run(ctx, comm, dev, stream, wname, walgo, wparams, wcap, peak,
-                                               parity=not args.no_parity))
+                                               # the SSSP S26 run is checked here; CC S24 and LP S24
+                                               # a=0.65 at the same scales by tests/test_gpu_scale.py
+                                               parity=not args.no_parity and walgo == "sssp"))
             torch.cuda.empty_cache()
 
     parity, kept = None, []

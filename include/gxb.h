@@ -274,6 +274,32 @@ int gxb_exchange_finish(gxb_state* s, void* stream);
  * peer (send_counts); the caller runs an all-to-all into GXB_BUF_SPARSE_RECV
  * (recv_counts); unpack scatters them into the replica. */
 int gxb_exchange_sparse_counts(const gxb_state* s, uint64_t* send_counts, uint64_t* recv_counts);
+
+/* per-peer delta exchange over peer memory (SSSP / CC / LP, 2..8 partitions): the lazy
+ * upload of "dirty and queried" values (A/agent.py:550-582, A/sync.py:171-198) with the
+ * query set static — a changed owned value goes only to the peers whose CSC reads it.
+ *   arena:  cap_matrix[p * nparts + q] = records partition p may send to q (= p's
+ *           gxb_exchange_sparse_counts send_counts[q], all-gathered by the caller; this
+ *           partition's row must match its own lists). Allocates this partition's receive
+ *           arena (two round-parity blocks per sender) and its need mask; writes the arena's
+ *           IPC handle when ipc_handle_out != NULL.
+ *   open:   nparts IPC handles (this partition's own entry ignored) -> peers' arenas;
+ *   set_peers: same-process peers' arenas (gxb_exchange_delta_buffer), nparts pointers.
+ *   pack:   after a closed round, stores every changed owned value into the arena of each
+ *           peer that reads it (NVLink / NVSwitch stores, fenced system-wide) and writes the
+ *           per-receiver record counts into d_vote[6 + q] (doubles) — the vote collective
+ *           that follows orders the stores before any peer reads them.
+ *   unpack: counts_from[p] = records partition p packed for this one (from the vote);
+ *           installs them, marks them active and appends them to the frontier.
+ * Round parities alternate, so a sender never overwrites a block its receiver has not
+ * unpacked (the receiver unpacks round k before it joins vote k + 1). */
+int gxb_exchange_delta_arena(gxb_state* s, const uint64_t* cap_matrix, void* ipc_handle_out);
+int gxb_exchange_delta_open(gxb_state* s, const void* handles);
+int gxb_exchange_delta_set_peers(gxb_state* s, void* const* arenas);
+int gxb_exchange_delta_buffer(gxb_state* s, void** arena);
+int gxb_exchange_delta_close(gxb_state* s);
+int gxb_exchange_delta_pack(gxb_state* s, double* d_vote, void* stream);
+int gxb_exchange_delta_unpack(gxb_state* s, const uint64_t* counts_from, void* stream);
 int gxb_exchange_sparse_pack(gxb_state* s, void* stream);
 int gxb_exchange_sparse_unpack(gxb_state* s, void* stream);
 

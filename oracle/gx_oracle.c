@@ -39,6 +39,14 @@ static uint64_t lower_bound_u32(const uint32_t* a, uint64_t n, uint32_t key) {
     return lo;
 }
 
+void gxo_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int gxo_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -73,6 +73,8 @@ int gxo_rmat(uint32_t scale, uint32_t edge_factor, uint64_t seed, uint32_t a, ui
              uint32_t* src_out, uint32_t* dst_out, uint32_t* w_out /* may be NULL */);
 
 int gxo_max_threads(void);
+/* OpenMP threads of every later call (torchrun exports OMP_NUM_THREADS=1 to its ranks) */
+void gxo_set_threads(int n);
 
 #ifdef __cplusplus
 }

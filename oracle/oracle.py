@@ -63,6 +63,7 @@ def lib():
                                ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                                ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, P, P, P]
         L.gxo_max_threads.restype = ctypes.c_int
+        L.gxo_set_threads.argtypes = [ctypes.c_int]
         _lib = L
     return _lib
 
@@ -157,3 +158,8 @@ def rmat(scale, edge_factor=16, seed=1, a=0.57, b=0.19, c=0.19, wmax=0, scramble
 
 def max_threads() -> int:
     return int(lib().gxo_max_threads())
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads for the oracle's later calls (torchrun ranks default to 1)."""
+    lib().gxo_set_threads(int(n))

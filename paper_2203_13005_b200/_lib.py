@@ -137,6 +137,13 @@ def _sig(L):
         "gxb_exchange_unpack_regions": (I, [P, P, P, I, U64, U64, U64, P]),
         "gxb_exchange_finish": (I, [P, P]),
         "gxb_exchange_sparse_counts": (I, [P, P, P]),
+        "gxb_exchange_delta_arena": (I, [P, P, P]),
+        "gxb_exchange_delta_open": (I, [P, P]),
+        "gxb_exchange_delta_set_peers": (I, [P, P]),
+        "gxb_exchange_delta_buffer": (I, [P, PP]),
+        "gxb_exchange_delta_close": (I, [P]),
+        "gxb_exchange_delta_pack": (I, [P, P, P]),
+        "gxb_exchange_delta_unpack": (I, [P, P, P]),
         "gxb_exchange_sparse_pack": (I, [P, P]),
         "gxb_exchange_sparse_unpack": (I, [P, P]),
         "gxb_read_attrs": (I, [P, P, I, P]),

@@ -55,8 +55,9 @@ class Algorithm:
 class SsspBellmanFord(Algorithm):
     """Multi-source Bellman-Ford; one distance lane per source (A/algorithms.py:81-122).
 
-    Device distances are exact 32-bit integers: weights must be integral and
-    max_w * |V| < 2^32 - 1 (checked), at most 4 sources per run.
+    Device distances are exact 32-bit integers: weights must be integral or dyadic
+    rationals (scaled to integers exactly, device.validate_weights) with
+    max_w * |V| < 2^32 - 1 (checked); any number of sources (groups of 4 lanes).
     """
 
     name = "sssp"
@@ -213,7 +214,7 @@ def run_device(algorithm: Algorithm, vertices, edges, max_iterations: int | None
     Returns {vid: attr} with the reference's attribute objects. With
     return_result=True also returns the DeviceRun (iterations, convergence,
     per-iteration statistics)."""
-    from .device import DeviceContext, DeviceGraph, DeviceRun, DeviceState, run_state
+    from .device import DeviceContext, DeviceGraph, DeviceRun, make_state, run_state
 
     ea = _edge_arrays(vertices, edges)
     own = ctx is None
@@ -225,7 +226,7 @@ def run_device(algorithm: Algorithm, vertices, edges, max_iterations: int | None
         g = DeviceGraph(ctx, ea.src, ea.dst, w, csr=algo in ("sssp", "cc", "lp"))
         sources = getattr(algorithm, "sources", None) if algo == "sssp" else None
         maxw = int(np.max(w)) if (w is not None and w.size) else 1
-        s = DeviceState(g, algo, sources=sources, max_weight=maxw if algo == "sssp" else None)
+        s = make_state(g, algo, sources=sources, max_weight=maxw if algo == "sssp" else None)
         it, conv, hist = run_state(s, max_iterations, direction, keep_history=return_result)
         rows = s.read_attrs()
         ids = g.ids()

@@ -2110,6 +2110,7 @@ int gxb_exchange_close_peers(gxb_state* s);  // gxb_exchange.cu
 int gxb_state_free(gxb_state* s) {
     if (!s) return GXB_OK;
     gxb_exchange_close_peers(s);
+    if (s->algo != GXB_ALGO_PAGERANK) gxb_exchange_delta_close(s);
     if (s->aux_stream) cudaStreamDestroy(s->aux_stream);
     if (s->ev_tile) cudaEventDestroy(s->ev_tile);
     if (s->ev_join) cudaEventDestroy(s->ev_join);

@@ -143,6 +143,65 @@ __global__ void k_deliver(int algo, int arity, const uint64_t* __restrict__ dens
     }
 }
 
+// ---- per-peer delta records over peer memory ----
+// need[s - lo] |= 1 << q for every owned slot s in the sorted list of slots peer q reads
+__global__ void k_need_mask(const uint32_t* __restrict__ idx, uint64_t n, uint64_t lo, uint32_t bit, uint32_t* need) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        atomicOr(need + (idx[i] - lo), bit);
+}
+
+struct PeerArenas {
+    uint32_t* arena[kMaxPeers + 1];  // receiver q's arena (nullptr for myself)
+    uint64_t base[kMaxPeers + 1];    // word offset of my block (this round's parity) in it
+};
+
+// the closed round's changed owned slots (frontier list, own first) -> a record in the arena
+// of every peer that reads the slot; one reservation per (warp, peer)
+__global__ void k_pack_peers(int algo, const uint32_t* __restrict__ list, const unsigned long long* count, uint64_t lo,
+                             uint64_t hi, const uint32_t* __restrict__ need, const uint4* __restrict__ dist,
+                             const uint32_t* __restrict__ lab, int nparts, const PeerArenas A,
+                             unsigned long long* peer_cnt) {
+    const uint64_t n = *count;
+    const int W = record_words(algo);
+    const int lane = threadIdx.x & 31;
+    for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < n;
+         i0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = i0 + lane;
+        const uint32_t s = i < n ? list[i] : 0u;
+        const bool mine = i < n && s >= lo && s < hi;
+        const uint32_t m = mine ? __ldg(need + (s - lo)) : 0u;
+        if (!__any_sync(0xffffffffu, m != 0u)) continue;
+        uint32_t v[4] = {0u, 0u, 0u, 0u};
+        if (m) {
+            if (algo == GXB_ALGO_SSSP) {
+                const uint4 d = dist[s];
+                v[0] = d.x; v[1] = d.y; v[2] = d.z; v[3] = d.w;
+            } else {
+                v[0] = lab[s];
+            }
+        }
+        for (int q = 0; q < nparts; ++q) {
+            const bool to_q = (m >> q) & 1u;
+            const unsigned b = __ballot_sync(0xffffffffu, to_q);
+            if (!b) continue;
+            unsigned long long base = 0;
+            if (lane == __ffs(b) - 1) base = atomicAdd(peer_cnt + q, (unsigned long long)__popc(b));
+            base = __shfl_sync(0xffffffffu, base, __ffs(b) - 1);
+            if (!to_q) continue;
+            uint32_t* r = A.arena[q] + A.base[q] + (base + __popc(b & ((1u << lane) - 1u))) * W;
+            r[0] = s;
+            for (int j = 1; j < W; ++j) r[j] = v[j - 1];
+        }
+    }
+    __threadfence_system();  // the records are visible to the peers before the vote collective
+}
+
+// counts into the vote block (after the 6 statistics), one double per receiver
+__global__ void k_peer_counts(const unsigned long long* peer_cnt, int nparts, double* d_vote) {
+    const int q = threadIdx.x;
+    if (q < nparts) d_vote[6 + q] = (double)peer_cnt[q];
+}
+
 // needed-only dense exchange (PageRank): gather my values for every peer / scatter theirs
 template <typename T>
 __global__ void k_sparse_pack(const T* __restrict__ values, const uint32_t* __restrict__ idx, uint64_t n, T* out) {
@@ -454,6 +513,176 @@ int gxb_attrs_deliver(gxb_state* s, const uint64_t* host_dense, const double* ho
     dfree(d_rec);
     dfree(d_bad);
     return rc;
+}
+
+// ---- per-peer delta exchange (host side) ----
+static int delta_layout(gxb_state* s, const uint64_t* cap) {
+    // my arena: for every sender p != me, two parity blocks of cap[p][me] records
+    const gxb_graph* g = s->g;
+    const int n = g->nparts, me = g->part;
+    const uint64_t W = s->algo == GXB_ALGO_SSSP ? 5 : 2;
+    uint64_t acc = 0;
+    for (int p = 0; p < n; ++p) {
+        s->peer_recv_cap[p] = p == me ? 0 : cap[(uint64_t)p * n + me];
+        for (int par = 0; par < 2; ++par) {
+            s->arena_base[p][par] = acc;
+            acc += s->peer_recv_cap[p] * W;
+        }
+    }
+    s->arena_words = acc;
+    // my blocks in every receiver's arena, same rule applied to the receiver's column
+    for (int q = 0; q < n; ++q) {
+        uint64_t a = 0;
+        for (int p = 0; p < n; ++p) {
+            const uint64_t c = p == q ? 0 : cap[(uint64_t)p * n + q];
+            for (int par = 0; par < 2; ++par) {
+                if (p == me) s->peer_base[q][par] = a;
+                a += c * W;
+            }
+        }
+    }
+    return GXB_OK;
+}
+
+int gxb_exchange_delta_arena(gxb_state* s, const uint64_t* cap_matrix, void* ipc_handle_out) {
+    NvtxRange nvtx_("gxb_exchange_delta_arena");
+    if (!s || !cap_matrix) return fail(GXB_EINVAL, "gxb_exchange_delta_arena: null argument");
+    if (s->algo == GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "gxb_exchange_delta_arena: PageRank uses the dense exchange");
+    gxb_graph* g = s->g;
+    const int n = g->nparts, me = g->part;
+    if (n < 2 || n > kMaxPeers + 1) return fail(GXB_EINVAL, "gxb_exchange_delta_arena: needs 2..8 partitions");
+    if (g->xsend_off.size() != (size_t)n + 1) return fail(GXB_EINVAL, "gxb_exchange_delta_arena: no per-peer lists");
+    for (int q = 0; q < n; ++q)  // my row must be my own send lists
+        if (q != me && cap_matrix[(uint64_t)me * n + q] != g->xsend_off[q + 1] - g->xsend_off[q])
+            return fail(GXB_EINVAL, "gxb_exchange_delta_arena: capacity row disagrees with this partition");
+    GXB_CHECK(gxb_exchange_delta_close(s));
+    GXB_CUDA(cudaSetDevice(g->ctx->device));
+    GXB_CHECK(delta_layout(s, cap_matrix));
+    const uint64_t owned = g->hi - g->lo;
+    GXB_CHECK(dalloc_t(&s->d_need, owned + 1));
+    GXB_CUDA(cudaMemsetAsync(s->d_need, 0, 4 * (owned + 1), 0));
+    for (int q = 0; q < n; ++q) {
+        const uint64_t a = g->xsend_off[q], b = g->xsend_off[q + 1];
+        if (q != me && b > a)
+            k_need_mask<<<grid_for(b - a), kBlock>>>(g->d_xsend_idx + a, b - a, g->lo, 1u << q, s->d_need);
+    }
+    GXB_CHECK(dalloc_t(&s->d_arena, s->arena_words + 1));
+    GXB_CHECK(dalloc_t(&s->d_peer_cnt, kMaxPeers + 1));
+    GXB_CUDA(cudaDeviceSynchronize());
+    if (ipc_handle_out) {
+        cudaIpcMemHandle_t h;
+        GXB_CUDA(cudaIpcGetMemHandle(&h, s->d_arena));
+        std::memcpy(ipc_handle_out, &h, sizeof(h));
+    }
+    return GXB_OK;
+}
+
+int gxb_exchange_delta_open(gxb_state* s, const void* handles) {
+    if (!s || !handles || !s->d_arena) return fail(GXB_EINVAL, "gxb_exchange_delta_open: bad argument");
+    const gxb_graph* g = s->g;
+    GXB_CUDA(cudaSetDevice(g->ctx->device));
+    const auto* hb = static_cast<const unsigned char*>(handles);
+    for (int q = 0; q < g->nparts; ++q) {
+        if (q == g->part) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, hb + (uint64_t)q * GXB_IPC_HANDLE_BYTES, sizeof(h));
+        void* p = nullptr;
+        const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            s->delta_ipc = true;
+            gxb_exchange_delta_close(s);
+            return cuda_fail(e, "gxb_exchange_delta_open: cudaIpcOpenMemHandle");
+        }
+        s->peer_arena[q] = static_cast<uint32_t*>(p);
+    }
+    s->delta_ipc = true;
+    s->delta_peers = true;
+    s->delta_parity = 1;  // the first packed round uses parity 0
+    return GXB_OK;
+}
+
+int gxb_exchange_delta_set_peers(gxb_state* s, void* const* arenas) {
+    if (!s || !arenas || !s->d_arena) return fail(GXB_EINVAL, "gxb_exchange_delta_set_peers: bad argument");
+    const gxb_graph* g = s->g;
+    for (int q = 0; q < g->nparts; ++q)
+        if (q != g->part) s->peer_arena[q] = static_cast<uint32_t*>(arenas[q]);
+    s->delta_ipc = false;
+    s->delta_peers = true;
+    s->delta_parity = 1;
+    return GXB_OK;
+}
+
+int gxb_exchange_delta_buffer(gxb_state* s, void** arena) {
+    if (!s || !arena) return fail(GXB_EINVAL, "gxb_exchange_delta_buffer: null argument");
+    *arena = s->d_arena;
+    return GXB_OK;
+}
+
+int gxb_exchange_delta_close(gxb_state* s) {
+    if (!s) return fail(GXB_EINVAL, "gxb_exchange_delta_close: null state");
+    if (s->delta_ipc) {
+        cudaSetDevice(s->g->ctx->device);
+        for (int q = 0; q <= kMaxPeers; ++q)
+            if (s->peer_arena[q]) cudaIpcCloseMemHandle(s->peer_arena[q]);
+    }
+    for (int q = 0; q <= kMaxPeers; ++q) s->peer_arena[q] = nullptr;
+    s->delta_ipc = s->delta_peers = false;
+    dfree(s->d_need);
+    dfree(s->d_arena);
+    dfree(s->d_peer_cnt);
+    s->d_need = nullptr;
+    s->d_arena = nullptr;
+    s->d_peer_cnt = nullptr;
+    return GXB_OK;
+}
+
+int gxb_exchange_delta_pack(gxb_state* s, double* d_vote, void* stream) {
+    NvtxRange nvtx_("gxb_exchange_delta_pack");
+    if (!s || !d_vote) return fail(GXB_EINVAL, "gxb_exchange_delta_pack: null argument");
+    if (!s->delta_peers) return fail(GXB_ESTATE, "gxb_exchange_delta_pack: peer arenas not set up");
+    if (s->in_round) return fail(GXB_ESTATE, "gxb_exchange_delta_pack: round still open");
+    gxb_graph* g = s->g;
+    cudaStream_t st = (cudaStream_t)stream;
+    s->delta_parity ^= 1;
+    PeerArenas A{};
+    for (int q = 0; q < g->nparts; ++q) {
+        A.arena[q] = q == g->part ? nullptr : s->peer_arena[q];
+        A.base[q] = s->peer_base[q][s->delta_parity];
+    }
+    GXB_CUDA(cudaMemsetAsync(s->d_peer_cnt, 0, 8 * (kMaxPeers + 1), st));
+    k_pack_peers<<<grid_for(std::max<uint64_t>(1, g->hi - g->lo)), kBlock, 0, st>>>(
+        s->algo, s->d_frontier[0], s->d_fcount, g->lo, g->hi, s->d_need, s->d_dist_cur, s->d_lab_cur, g->nparts, A,
+        s->d_peer_cnt);
+    k_peer_counts<<<1, 32, 0, st>>>(s->d_peer_cnt, g->nparts, d_vote);
+    GXB_CUDA(cudaGetLastError());
+    s->launches += 2;
+    return GXB_OK;
+}
+
+int gxb_exchange_delta_unpack(gxb_state* s, const uint64_t* counts_from, void* stream) {
+    NvtxRange nvtx_("gxb_exchange_delta_unpack");
+    if (!s || !counts_from) return fail(GXB_EINVAL, "gxb_exchange_delta_unpack: null argument");
+    if (!s->delta_peers) return fail(GXB_ESTATE, "gxb_exchange_delta_unpack: peer arenas not set up");
+    gxb_graph* g = s->g;
+    cudaStream_t st = (cudaStream_t)stream;
+    GXB_CHECK(state_settle(s));  // the closed round's own frontier first
+    if (!s->d_xscratch) GXB_CHECK(dalloc_t(&s->d_xscratch, 4));
+    GXB_CUDA(cudaMemsetAsync(s->d_xscratch + 1, 0, 8, st));
+    const int par = s->delta_parity;
+    for (int p = 0; p < g->nparts; ++p) {
+        if (p == g->part || !counts_from[p]) continue;
+        if (counts_from[p] > s->peer_recv_cap[p]) return fail(GXB_EINVAL, "gxb_exchange_delta_unpack: count exceeds the block");
+        k_unpack<<<grid_for(counts_from[p]), kBlock, 0, st>>>(s->algo, s->d_arena + s->arena_base[p][par], counts_from[p],
+                                                              g->lo, g->hi, s->d_dist_cur, s->d_dist_next, s->d_lab_cur,
+                                                              s->d_lab_next, s->d_active[0], s->d_frontier[0], s->d_fcount,
+                                                              g->d_outdeg, s->d_xscratch + 1);
+        s->launches++;
+    }
+    GXB_CUDA(cudaGetLastError());
+    s->lab_injective = false;
+    s->unpack_pending = true;  // the next round reads the frontier's length and GEN units back
+    return GXB_OK;
 }
 
 int gxb_exchange_sparse_counts(const gxb_state* s, uint64_t* send_counts, uint64_t* recv_counts) {

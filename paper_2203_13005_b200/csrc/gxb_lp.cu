@@ -25,13 +25,17 @@ namespace gxb {
 
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
+// Global (label, count) tables of the label-diverse hubs (in-degree > kLpBigDeg), one per
+// hub, 2 x in-degree entries. Keys and counts carry the round's epoch in their high 32 bits:
+// a word of an older epoch is empty, so no table is ever cleared between rounds.
 struct LpHub {
-    uint64_t* tab_off;   // per chunked slot: first entry
-    uint32_t* tab_mask;  // per chunked slot: size - 1 (power of two)
-    uint32_t* keys;
-    uint32_t* counts;
+    uint64_t* tab_off;   // per big hub: first entry
+    uint32_t* tab_mask;  // per big hub: size - 1 (power of two)
+    unsigned long long* keys;    // epoch << 32 | label
+    unsigned long long* counts;  // epoch << 32 | count
     unsigned long long* best;  // per chunked slot: packed (count << 32 | ~label), 0 = no message
     uint64_t entries;
+    uint32_t epoch;
 };
 
 struct LpPush;
@@ -40,7 +44,6 @@ struct LpScratch {
     uint64_t chunk_end = 0;
     uint64_t big_end = 0;  // relative slots [0, big_end): in-degree > kLpBigDeg (chunked warps)
     uint64_t big_items = 0;    // their chunk items (the plan's first items)
-    uint64_t big_entries = 0;  // their global table entries (a prefix of the tables)
     uint64_t cta_end = 0;  // relative slots [big_end, cta_end): in-degree > kLpCtaMinDeg (one CTA each)
     uint32_t* eff = nullptr;  // per slot: label if active, else kEmpty (rounds >= 2)
     uint32_t hot_end = 0;  // slots with in-degree >= kLpHotDegree: pushed through shared memory
@@ -62,18 +65,30 @@ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
     return x;
 }
 
-// fold (label, c) into a destination's table; returns the label's new count
-__device__ __forceinline__ uint32_t table_add(uint32_t* keys, uint32_t* counts, uint64_t base, uint32_t mask,
-                                              uint32_t label, uint32_t c) {
+// fold (label, c) into a hub's epoch-tagged table; returns the label's new count
+__device__ __forceinline__ uint32_t table_add(const LpHub& H, uint64_t base, uint32_t mask, uint32_t label,
+                                              uint32_t c) {
+    const unsigned long long tag = (unsigned long long)H.epoch << 32;
+    const unsigned long long want = tag | label;
     uint32_t i = mix32(label) & mask;
     while (true) {
-        const uint64_t at = base + i;
-        uint32_t k = __ldcg(keys + at);
-        if (k == kEmpty) {
-            k = atomicCAS(keys + at, kEmpty, label);
-            if (k == kEmpty) k = label;
+        unsigned long long* kp = H.keys + base + i;
+        unsigned long long k = __ldcg(kp);
+        if ((k >> 32) != H.epoch) {  // empty in this round: claim it
+            const unsigned long long prev = atomicCAS(kp, k, want);
+            k = prev == k ? want : prev;
+            if ((k >> 32) != H.epoch) continue;  // raced with another stale word: retry the slot
         }
-        if (k == label) return atomicAdd(counts + at, c) + c;
+        if (k == want) {
+            unsigned long long* cp = H.counts + base + i;
+            unsigned long long w = __ldcg(cp);
+            while ((w >> 32) != H.epoch) {  // first count of this round replaces the stale word
+                const unsigned long long prev = atomicCAS(cp, w, tag | c);
+                if (prev == w) return c;
+                w = prev;
+            }
+            return (uint32_t)(atomicAdd(cp, (unsigned long long)c) & 0xFFFFFFFFull) + c;
+        }
         i = (i + 1) & mask;
     }
 }
@@ -166,7 +181,7 @@ constexpr int kWarpPairs = 256;
 
 __device__ __forceinline__ void hub_add(const LpLaunch& L, uint64_t rel, uint64_t base, uint32_t mask, uint32_t lab,
                                         uint32_t c) {
-    const uint32_t nc = table_add(L.hub.keys, L.hub.counts, base, mask, lab, c);
+    const uint32_t nc = table_add(L.hub, base, mask, lab, c);
     const unsigned long long pk = ((unsigned long long)nc << 32) | (unsigned long long)(~lab);
     if (pk > __ldcg(L.hub.best + rel)) atomicMax(L.hub.best + rel, pk);
 }
@@ -270,20 +285,15 @@ __device__ __forceinline__ void lp_chunk_injective(const LpLaunch& L, uint64_t i
 }
 
 // ---- dense rounds >= 2: hubs counted in shared memory ----
-// A destination with in-degree > kChunkMinDeg is counted by one CTA (in-degree >
-// kLpCtaMinDeg) or one warp (the rest) in an open-addressing (label, count) table in
-// shared memory sized to twice the in-degree (so it holds every distinct label at load
-// <= 1/2), capped at kLpCtaCap / kLpWarpCap entries. Equal labels of 32 edges are merged
-// first (__match_any_sync). A label whose bounded probe sequence finds no room goes to the
-// destination's global table (L2 atomics, running packed argmax); since shared slots are
-// never freed, such a label never lands in shared memory later, so each label is counted
-// in exactly one table and the argmax is the max of both. The owner clears the global
-// table it touched, so nothing is reset per round on the host side.
+// A destination with kChunkMinDeg < in-degree <= kLpBigDeg is counted by one CTA (in-degree
+// > kLpCtaMinDeg) or one warp (the rest) in an open-addressing (label, count) table in
+// shared memory sized to twice the in-degree (every distinct label fits at load <= 1/2),
+// after equal labels of 32 edges are merged (__match_any_sync). The label-diverse hubs
+// above kLpBigDeg stay in chunked warps over all SMs with epoch-tagged global tables.
 constexpr uint32_t kLpCtaMinDeg = 512;
 constexpr uint32_t kLpBigDeg = 4096;  // above: chunked warps over all SMs + global tables (label-diverse hubs)
 constexpr int kLpCtaCap = 8192;    // 64 KB of (key, count) per CTA
 constexpr int kLpWarpCap = 1024;   // 8 KB per warp
-constexpr int kLpProbes = 16;
 
 __global__ void k_lp_eff(const uint32_t* __restrict__ active, const uint32_t* __restrict__ lab, uint64_t S,
                          uint32_t* eff) {
@@ -291,12 +301,12 @@ __global__ void k_lp_eff(const uint32_t* __restrict__ active, const uint32_t* __
         eff[i] = ((__ldg(active + (i >> 5)) >> (i & 31)) & 1u) ? __ldg(lab + i) : kEmpty;
 }
 
-// insert c copies of `lab` into a shared table; false when the probe sequence is full
-__device__ __forceinline__ bool smem_table_add(uint32_t* keys, uint32_t* cnts, uint32_t mask, uint32_t lab,
+// insert c copies of `lab` into a shared table sized to at least twice the destination's
+// in-degree: distinct labels <= in-degree keep the load <= 1/2, so probing always ends
+__device__ __forceinline__ void smem_table_add(uint32_t* keys, uint32_t* cnts, uint32_t mask, uint32_t lab,
                                                uint32_t c) {
     uint32_t h = mix32(lab) & mask;
-#pragma unroll 1
-    for (int probe = 0; probe < kLpProbes; ++probe) {
+    while (true) {
         uint32_t k = keys[h];
         if (k == kEmpty) {
             k = atomicCAS(keys + h, kEmpty, lab);
@@ -304,11 +314,10 @@ __device__ __forceinline__ bool smem_table_add(uint32_t* keys, uint32_t* cnts, u
         }
         if (k == lab) {
             atomicAdd(cnts + h, c);
-            return true;
+            return;
         }
         h = (h + 1) & mask;
     }
-    return false;
 }
 
 __device__ __forceinline__ unsigned long long pack_best(uint32_t count, uint32_t lab) {
@@ -316,16 +325,12 @@ __device__ __forceinline__ unsigned long long pack_best(uint32_t count, uint32_t
 }
 
 // stream [beg, end) with `nthreads` threads (index t), 8 loads in flight per lane, and fold
-// each 32-edge group's labels into the shared table; returns whether anything overflowed
-__device__ __forceinline__ bool lp_count_edges(const LpLaunch& L, uint64_t rel, uint64_t beg, uint64_t end,
-                                               unsigned t, unsigned nthreads, uint32_t* keys, uint32_t* cnts,
-                                               uint32_t mask) {
+// each 32-edge group's labels into the shared table
+__device__ __forceinline__ void lp_count_edges(const LpLaunch& L, uint64_t beg, uint64_t end, unsigned t,
+                                               unsigned nthreads, uint32_t* keys, uint32_t* cnts, uint32_t mask) {
     constexpr int kB = 8;
     const int lane = threadIdx.x & 31;
     const unsigned warp0 = t - lane;  // first thread of this warp within the group
-    bool over = false;
-    const uint64_t gbase = L.hub.tab_off ? __ldg(L.hub.tab_off + rel) : 0;
-    const uint32_t gmask = L.hub.tab_mask ? __ldg(L.hub.tab_mask + rel) : 0;
     for (uint64_t e0 = beg + (uint64_t)warp0 * kB; e0 < end; e0 += (uint64_t)nthreads * kB) {
         uint32_t src[kB], lab[kB];
 #pragma unroll
@@ -340,17 +345,9 @@ __device__ __forceinline__ bool lp_count_edges(const LpLaunch& L, uint64_t rel, 
             const bool ok = lab[j] != kEmpty;
             const unsigned long long key = ok ? (unsigned long long)lab[j] : (0x100000000ull | (unsigned)lane);
             const unsigned m = __match_any_sync(kFull, key);
-            if (ok && lane == __ffs(m) - 1) {
-                if (!smem_table_add(keys, cnts, mask, lab[j], (uint32_t)__popc(m))) {
-                    const uint32_t nc = table_add(L.hub.keys, L.hub.counts, gbase, gmask, lab[j], __popc(m));
-                    const unsigned long long pk = pack_best(nc, lab[j]);
-                    if (pk > __ldcg(L.hub.best + rel)) atomicMax(L.hub.best + rel, pk);
-                    over = true;
-                }
-            }
+            if (ok && lane == __ffs(m) - 1) smem_table_add(keys, cnts, mask, lab[j], (uint32_t)__popc(m));
         }
     }
-    return over;
 }
 
 __global__ void __launch_bounds__(kBlock) k_lp_hub_cta(const LpLaunch L, uint64_t lo_rel, uint64_t cta_end) {
@@ -358,21 +355,18 @@ __global__ void __launch_bounds__(kBlock) k_lp_hub_cta(const LpLaunch L, uint64_
     uint32_t* keys = lp_dyn;
     uint32_t* cnts = lp_dyn + kLpCtaCap;
     __shared__ unsigned long long wbest[kBlock / 32];
-    __shared__ int over_any;
     LocalStats st;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint64_t rel = lo_rel + blockIdx.x; rel < cta_end; rel += gridDim.x) {
         const uint64_t beg = __ldg(L.in_off + rel), end = __ldg(L.in_off + rel + 1);
         uint32_t C = 64;
-        while (C < kLpCtaCap && (uint64_t)C < 2 * (end - beg)) C <<= 1;
+        while ((uint64_t)C < 2 * (end - beg)) C <<= 1;  // <= kLpCtaCap for in-degree <= kLpBigDeg
         for (uint32_t i = threadIdx.x; i < C; i += kBlock) {
             keys[i] = kEmpty;
             cnts[i] = 0;
         }
-        if (threadIdx.x == 0) over_any = 0;
         __syncthreads();
-        const bool over = lp_count_edges(L, rel, beg, end, threadIdx.x, kBlock, keys, cnts, C - 1);
-        if (over) over_any = 1;
+        lp_count_edges(L, beg, end, threadIdx.x, kBlock, keys, cnts, C - 1);
         __syncthreads();
         unsigned long long best = 0ull;
         for (uint32_t i = threadIdx.x; i < C; i += kBlock) {
@@ -388,25 +382,11 @@ __global__ void __launch_bounds__(kBlock) k_lp_hub_cta(const LpLaunch L, uint64_
         }
         if (lane == 0) wbest[warp] = best;
         __syncthreads();
-        const bool spilled = over_any != 0;
         if (threadIdx.x == 0) {
             for (int w = 1; w < kBlock / 32; ++w) best = wbest[w] > best ? wbest[w] : best;
-            if (spilled) {
-                const unsigned long long g = L.hub.best[rel];
-                best = g > best ? g : best;
-                L.hub.best[rel] = 0ull;
-            }
             lp_finish(L, (uint32_t)(L.lo + rel), best, st);
         }
-        if (spilled) {  // reset the global table this destination used
-            const uint64_t gb = L.hub.tab_off[rel];
-            const uint64_t gn = (uint64_t)L.hub.tab_mask[rel] + 1;
-            for (uint64_t i = threadIdx.x; i < gn; i += kBlock) {
-                L.hub.keys[gb + i] = kEmpty;
-                L.hub.counts[gb + i] = 0;
-            }
-        }
-        __syncthreads();  // the tables are reused by the next destination
+        __syncthreads();  // the table is reused by the next destination
     }
     flush_stats(st, L.stats);
 }
@@ -421,13 +401,13 @@ __global__ void __launch_bounds__(kBlock) k_lp_hub_warp(const LpLaunch L, uint64
     for (uint64_t rel = lo_rel + blockIdx.x * (uint64_t)(kBlock / 32) + warp; rel < hi_rel; rel += nw) {
         const uint64_t beg = __ldg(L.in_off + rel), end = __ldg(L.in_off + rel + 1);
         uint32_t C = 64;
-        while (C < kLpWarpCap && (uint64_t)C < 2 * (end - beg)) C <<= 1;
+        while ((uint64_t)C < 2 * (end - beg)) C <<= 1;  // <= kLpWarpCap for in-degree <= kLpCtaMinDeg
         for (uint32_t i = lane; i < C; i += 32) {
             wk[i] = kEmpty;
             wc[i] = 0;
         }
         __syncwarp();
-        const bool over = __any_sync(kFull, lp_count_edges(L, rel, beg, end, lane, 32, wk, wc, C - 1));
+        lp_count_edges(L, beg, end, lane, 32, wk, wc, C - 1);
         __syncwarp();
         unsigned long long best = 0ull;
         for (uint32_t i = lane; i < C; i += 32) {
@@ -440,19 +420,6 @@ __global__ void __launch_bounds__(kBlock) k_lp_hub_warp(const LpLaunch L, uint64
         for (int o = 16; o > 0; o >>= 1) {
             const unsigned long long q = __shfl_xor_sync(kFull, best, o);
             best = q > best ? q : best;
-        }
-        if (over) {
-            if (lane == 0) {
-                const unsigned long long g = L.hub.best[rel];
-                best = g > best ? g : best;
-                L.hub.best[rel] = 0ull;
-            }
-            const uint64_t gb = L.hub.tab_off[rel];
-            const uint64_t gn = (uint64_t)L.hub.tab_mask[rel] + 1;
-            for (uint64_t i = lane; i < gn; i += 32) {
-                L.hub.keys[gb + i] = kEmpty;
-                L.hub.counts[gb + i] = 0;
-            }
         }
         if (lane == 0) lp_finish(L, (uint32_t)(L.lo + rel), best, st);
         __syncwarp();
@@ -720,17 +687,17 @@ static int lp_setup(gxb_state* s, cudaStream_t st) {
     while (S->cta_end < P.chunk_end && g->h_indeg_sorted[S->cta_end] > kLpCtaMinDeg) ++S->cta_end;
     while (S->hot_end < g->h_indeg_sorted.size() && g->h_indeg_sorted[S->hot_end] >= kLpHotDegree) ++S->hot_end;
     LpHub& H = S->hub;
-    std::vector<uint64_t> off(P.chunk_end + 1);
-    std::vector<uint32_t> mask(P.chunk_end + 1);
+    std::vector<uint64_t> off(S->big_end + 1);
+    std::vector<uint32_t> mask(S->big_end + 1);
     uint64_t acc = 0;
-    for (uint64_t r = 0; r < P.chunk_end; ++r) {
+    for (uint64_t r = 0; r < S->big_end; ++r) {
         const uint64_t size = std::max<uint64_t>(256, next_pow2(2ull * g->h_indeg_sorted[r]));
         off[r] = acc;
         mask[r] = (uint32_t)(size - 1);
         acc += size;
     }
     H.entries = acc;
-    S->big_entries = off[S->big_end];
+    H.epoch = 0;  // the tables start zeroed: epoch 0 words are empty from round 1 on
     int rc = GXB_OK;
     auto up = [&](auto** d, const auto& h) {
         if (rc != GXB_OK) return;
@@ -746,8 +713,8 @@ static int lp_setup(gxb_state* s, cudaStream_t st) {
     if (rc == GXB_OK) rc = dalloc_t(&H.best, P.chunk_end + 1);
     if (rc == GXB_OK) rc = dalloc_t(&S->eff, g->S + 1);
     if (rc == GXB_OK) {
-        cudaMemsetAsync(H.keys, 0xFF, 4 * (acc + 1), st);
-        cudaMemsetAsync(H.counts, 0, 4 * (acc + 1), st);
+        cudaMemsetAsync(H.keys, 0, 8 * (acc + 1), st);
+        cudaMemsetAsync(H.counts, 0, 8 * (acc + 1), st);
         cudaMemsetAsync(H.best, 0, 8 * (P.chunk_end + 1), st);
         if (cudaStreamSynchronize(st) != cudaSuccess) rc = fail(GXB_ECUDA, "lp_setup sync");
     }
@@ -827,6 +794,7 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
         const uint64_t S_ = g->S;
         if (S_) k_lp_eff<<<grid_for(S_), kBlock, 0, st>>>(s->d_active[0], s->d_lab_cur, S_, S->eff);
         L.eff = S->eff;
+        L.hub.epoch = ++S->hub.epoch;  // this round's table words (older ones read as empty)
         static bool attrs_set[64] = {};
         const int dev = g->ctx->device & 63;
         if (!attrs_set[dev]) {
@@ -851,25 +819,14 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
             const unsigned gw = (unsigned)std::min<uint64_t>((n + kBlock / 32 - 1) / (kBlock / 32), 6ull * kNumSMs);
             k_lp_hub_warp<<<gw, kBlock, (kBlock / 32) * 2 * 4 * kLpWarpCap, st>>>(L, S->cta_end, S->chunk_end);
         }
-        if (S->big_end) {
-            k_lp_hub_apply<<<grid_for(S->big_end), kBlock, 0, st>>>(L, S->big_end);
-            GXB_CUDA(cudaMemsetAsync(S->hub.keys, 0xFF, 4 * S->big_entries, st));
-            GXB_CUDA(cudaMemsetAsync(S->hub.counts, 0, 4 * S->big_entries, st));
-        }
+        if (S->big_end) k_lp_hub_apply<<<grid_for(S->big_end), kBlock, 0, st>>>(L, S->big_end);
         s->launches += 3;  // + the caller's 2: eff, chunks + groups, CTA hubs, warp hubs, hub apply
         GXB_CUDA(cudaGetLastError());
         return GXB_OK;
     }
     if (grid) k_lp_pull<<<grid, kBlock, 0, st>>>(L);
-    if (S->chunk_end) {
-        k_lp_hub_apply<<<grid_for(S->chunk_end), kBlock, 0, st>>>(L, S->chunk_end);
-        // empty the tables for the next round (plain memsets: no read-back of the tables);
-        // a run-length round leaves them untouched
-        if (!L.injective) {
-            GXB_CUDA(cudaMemsetAsync(S->hub.keys, 0xFF, 4 * S->hub.entries, st));
-            GXB_CUDA(cudaMemsetAsync(S->hub.counts, 0, 4 * S->hub.entries, st));
-        }
-    }
+    // round 1 (run-length counting, no tables): every chunked slot applied from its argmax
+    if (S->chunk_end) k_lp_hub_apply<<<grid_for(S->chunk_end), kBlock, 0, st>>>(L, S->chunk_end);
     GXB_CUDA(cudaGetLastError());
     return GXB_OK;
 }

@@ -222,6 +222,19 @@ struct gxb_state {
     int round_chunks = 0;   // exchange chunks launched in the open round
     cudaStream_t aux_stream = nullptr;  // pipelined rounds: span folds + Apply beside the tiles
     cudaEvent_t ev_tile = nullptr, ev_join = nullptr;
+    // per-peer delta exchange over peer memory (SSSP / CC / LP, nparts <= 8): the pack kernel
+    // stores each changed owned value only into the receive arenas of the peers whose CSC
+    // reads it (need mask), double-buffered by round parity; the counts ride in the vote
+    uint32_t* d_need = nullptr;             // per owned slot: bit q = partition q reads it
+    uint32_t* d_arena = nullptr;            // my receive arena (records from every sender)
+    uint64_t arena_words = 0;
+    uint64_t arena_base[gxb::kMaxPeers + 1][2] = {};  // word offset of (sender p, parity) in my arena
+    uint64_t peer_recv_cap[gxb::kMaxPeers + 1] = {};  // records per (sender p, parity) block
+    uint32_t* peer_arena[gxb::kMaxPeers + 1] = {};    // receiver q's arena
+    uint64_t peer_base[gxb::kMaxPeers + 1][2] = {};   // my block in receiver q's arena
+    unsigned long long* d_peer_cnt = nullptr;         // records packed for receiver q this round
+    bool delta_peers = false, delta_ipc = false;
+    int delta_parity = 0;                   // parity of the last packed round
     bool lab_injective = false;  // LP: labels are still the distinct vertex ids (before round 1)
     int attrs_scope = 0;                          // async staging: 0 = every vertex, 1 = owned vertices
     uint64_t stage_n = 0;                         // vertices per staging buffer (allocated)

@@ -85,21 +85,40 @@ class DeviceContext:
         return src, dst, w
 
 
-def validate_weights(w) -> np.ndarray | None:
-    """Device weights are u32 integers; float weights must be integral and non-negative
-    (negative weights are already rejected by the loader, A/graph.py:161-162)."""
+MAX_WEIGHT_SHIFT = 24
+
+
+def validate_weights(w, num_vertices: int | None = None) -> tuple[np.ndarray | None, int]:
+    """Device weights are u32 integers: returns (u32 weights, shift) with w = u32 / 2^shift.
+
+    Integral weights keep shift 0. Non-integral weights that are dyadic rationals (2.5, 0.25,
+    1.125 ...) are scaled by the smallest 2^shift that makes them integral: the reference's
+    float64 path sums (A/algorithms.py:102-105) of such weights are exact, and so are the
+    scaled u32 sums, so distances are bit-identical after dividing by 2^shift. Anything else
+    (1e-3, NaN, negative, too large for exact u32 sums) raises ValueError: no silent
+    approximation. Negative weights are already rejected by the loader (A/graph.py:161-162)."""
     if w is None:
-        return None
+        return None, 0
     a = np.asarray(w)
-    if a.dtype.kind == "f":
-        if not np.all(np.isfinite(a)) or np.any(a < 0) or np.any(a != np.floor(a)) or np.any(a > U32_MAX - 1):
-            raise ValueError("device SSSP needs integral, non-negative edge weights below 2^32-1")
-        return a.astype(np.uint32)
     if a.dtype.kind in "iu":
         if a.size and (a.min() < 0 or a.max() > U32_MAX - 1):
             raise ValueError("edge weights must be in [0, 2^32-2]")
-        return a.astype(np.uint32, copy=False)
-    raise ValueError(f"unsupported weight dtype {a.dtype}")
+        return a.astype(np.uint32, copy=False), 0
+    if a.dtype.kind != "f":
+        raise ValueError(f"unsupported weight dtype {a.dtype}")
+    a = a.astype(np.float64, copy=False)
+    if not np.all(np.isfinite(a)) or np.any(a < 0):
+        raise ValueError("device SSSP needs finite, non-negative edge weights")
+    for shift in range(MAX_WEIGHT_SHIFT + 1):
+        sc = np.ldexp(a, shift)
+        if np.all(sc == np.floor(sc)):
+            top = float(sc.max(initial=0.0))
+            bound = top * (num_vertices if num_vertices else 1)
+            if top > U32_MAX - 1 or (num_vertices and bound >= U32_MAX):
+                break
+            return sc.astype(np.uint32), shift
+    raise ValueError("device SSSP needs integral (or dyadic-rational) non-negative weights whose "
+                     "scaled sums stay below 2^32-1")
 
 
 class DeviceGraph:
@@ -115,6 +134,8 @@ class DeviceGraph:
         capacity: per-partition capacity factors (balancer.capacity_factors); implies
         "ranges" with partition p taking capacity[p] / sum(capacity) of the cost."""
         self.ctx = ctx
+        self.weight_shift = 0     # distances are u32 / 2^weight_shift (validate_weights)
+        self.max_weight = None    # largest (scaled) u32 weight, when the weights came from the host
         flags = 0 if csr else L.BUILD_NO_CSR
         if partitioning not in ("edges", "ranges", "ids"):
             raise ValueError(f"unknown partitioning {partitioning!r}")
@@ -140,8 +161,10 @@ class DeviceGraph:
             dst = np.ascontiguousarray(dst, dtype=np.uint32)
             if src.shape != dst.shape:
                 raise ValueError("src/dst length mismatch")
-            w = validate_weights(w)
+            nv = int(np.union1d(src, dst).size) if w is not None else None
+            w, self.weight_shift = validate_weights(w, nv)
             if w is not None:
+                self.max_weight = int(w.max(initial=0))
                 w = np.ascontiguousarray(w, dtype=np.uint32)
                 if w.shape != src.shape:
                     raise ValueError("weight length mismatch")
@@ -235,9 +258,11 @@ class DeviceState:
                 if nsrc == 0:
                     raise ValueError("sssp needs at least one source vertex")
                 if nsrc > 4:
-                    raise ValueError("the device SSSP carries at most 4 sources per run")
+                    raise ValueError("a DeviceState carries at most 4 SSSP lanes (make_state groups more)")
             # u32 distances are exact iff no message d + w can reach 2^32-1 (the
             # library re-checks this against the stored weights)
+            if graph.max_weight is not None:
+                max_weight = graph.max_weight  # the scaled weights the device holds
             if max_weight is not None and max_weight * graph.num_vertices >= U32_MAX:
                 raise ValueError("edge weights too large for exact 32-bit distances")
         h = ctypes.c_void_p()
@@ -287,15 +312,22 @@ class DeviceState:
         """Undo the last PageRank round (its outputs went to the next buffers only)."""
         L.check(L.lib().gxb_round_rollback(self._h))
 
+    def _shift(self) -> int:
+        return self.graph.weight_shift if self.algo == "sssp" else 0
+
     def read_attrs(self, owned_only: bool = False, stream=None) -> np.ndarray:
         V = self.graph.num_vertices
         out = np.empty((V, self.arity), dtype=np.float64)
         L.check(L.lib().gxb_read_attrs(self._h, _vp(out), int(owned_only), _stream_ptr(stream)))
+        if self._shift():
+            np.ldexp(out, -self._shift(), out=out)  # exact: distances are u32 / 2^shift (inf stays inf)
         return out
 
     def read_attrs_into(self, out: np.ndarray, owned_only: bool = False, stream=None) -> np.ndarray:
         """Like read_attrs into a caller-provided (e.g. pinned) host array."""
         L.check(L.lib().gxb_read_attrs(self._h, _vp(out), int(owned_only), _stream_ptr(stream)))
+        if self._shift():
+            np.ldexp(out, -self._shift(), out=out)
         return out
 
     def write_attrs(self, values, stream=None):
@@ -304,8 +336,10 @@ class DeviceState:
             a = np.ascontiguousarray(values, dtype=np.float64)
             if a.size != self.graph.num_vertices * self.arity:
                 raise ValueError("attribute array has the wrong length")
+            if self._shift():
+                a = np.ldexp(a, self._shift())
             L.check(L.lib().gxb_write_attrs(self._h, _vp(a), _stream_ptr(stream)))
-        else:  # pinned torch tensor
+        else:  # pinned torch tensor, in the device encoding
             L.check(L.lib().gxb_write_attrs(self._h, _vp(values), _stream_ptr(stream)))
 
     def deliver(self, dense, values, stream=None):
@@ -316,6 +350,8 @@ class DeviceState:
         v = np.ascontiguousarray(values, dtype=np.float64)
         if v.size != d.size * self.arity:
             raise ValueError("deliver: one row of `arity` values per vertex required")
+        if self._shift():
+            v = np.ldexp(v, self._shift())
         L.check(L.lib().gxb_attrs_deliver(self._h, _vp(d), _vp(v), int(d.size), _stream_ptr(stream)))
 
     # fused PageRank exchange: Apply stores into the peers' replicas (NVLink / NVSwitch)
@@ -411,6 +447,53 @@ class DeviceState:
         L.check(L.lib().gxb_exchange_sparse_counts(self._h, _vp(snd), _vp(rcv)))
         return [int(x) for x in snd], [int(x) for x in rcv]
 
+    def exchange_counts(self):
+        """Per-peer (send, recv) counts of distinct slots: my owned slots peer q's CSC reads,
+        and peer p's slots my CSC reads (nparts >= 2)."""
+        n = self.graph.nparts
+        snd = np.zeros(n, dtype=np.uint64)
+        rcv = np.zeros(n, dtype=np.uint64)
+        L.check(L.lib().gxb_exchange_sparse_counts(self._h, _vp(snd), _vp(rcv)))
+        return [int(x) for x in snd], [int(x) for x in rcv]
+
+    # per-peer delta exchange (SSSP / CC / LP): changed values stored into the readers' arenas
+    def delta_arena(self, cap_matrix) -> bytes:
+        """Allocate the receive arena from the all-gathered send counts (rows = senders);
+        returns its CUDA IPC handle."""
+        m = np.ascontiguousarray(cap_matrix, dtype=np.uint64)
+        buf = (ctypes.c_ubyte * self.IPC_HANDLE_BYTES)()
+        L.check(L.lib().gxb_exchange_delta_arena(self._h, _vp(m), buf))
+        return bytes(buf)
+
+    def delta_open(self, handles: bytes):
+        """nparts IPC handles (this rank's own entry is ignored)."""
+        if len(handles) != self.graph.nparts * self.IPC_HANDLE_BYTES:
+            raise ValueError("delta_open: one handle per partition required")
+        buf = (ctypes.c_ubyte * len(handles)).from_buffer_copy(handles)
+        L.check(L.lib().gxb_exchange_delta_open(self._h, buf))
+
+    def delta_buffer(self) -> int:
+        p = ctypes.c_void_p()
+        L.check(L.lib().gxb_exchange_delta_buffer(self._h, ctypes.byref(p)))
+        return int(p.value or 0)
+
+    def delta_set_peers(self, states):
+        """Same-process partitions (state of partition q at index q; this one ignored)."""
+        ptrs = (ctypes.c_void_p * len(states))(*[st.delta_buffer() for st in states])
+        L.check(L.lib().gxb_exchange_delta_set_peers(self._h, ptrs))
+
+    def delta_close(self):
+        L.check(L.lib().gxb_exchange_delta_close(self._h))
+
+    def delta_pack(self, vote, stream=None):
+        """Store the closed round's changed owned values into the readers' arenas; the
+        per-receiver counts go to vote[6:] (float64 device tensor of 6 + nparts)."""
+        L.check(L.lib().gxb_exchange_delta_pack(self._h, _vp(vote), _stream_ptr(stream)))
+
+    def delta_unpack(self, counts_from, stream=None):
+        arr = np.ascontiguousarray([int(c) for c in counts_from], dtype=np.uint64)
+        L.check(L.lib().gxb_exchange_delta_unpack(self._h, _vp(arr), _stream_ptr(stream)))
+
     def sparse_pack(self, stream=None):
         L.check(L.lib().gxb_exchange_sparse_pack(self._h, _stream_ptr(stream)))
 
@@ -427,6 +510,90 @@ class DeviceState:
             self.free()
         except Exception:
             pass
+
+
+class SsspLanes:
+    """SSSP with more than 4 sources (the reference takes any source list,
+    A/algorithms.py:81-122): the lanes run in groups of 4, one device state per group over
+    the same graph. In the reference a vertex whose distance changed on any lane sends all
+    its lanes, but a lane that did not change re-sends a value it already sent, which lowers
+    nothing; so every lane evolves exactly as in its own group, the joint run converges when
+    every group has, and its iteration count is the largest group's. Distances are
+    bit-identical; the per-round counters (changed, next-active, units) are summed over the
+    groups (a vertex changed in two groups counts twice)."""
+
+    def __init__(self, graph: "DeviceGraph", sources, max_weight: int | None = None):
+        srcs = [int(x) for x in sources]
+        if not srcs:
+            raise ValueError("sssp needs at least one source vertex")
+        self.graph = graph
+        self.algo = "sssp"
+        self.arity = len(srcs)
+        self.states = []
+        try:
+            for i in range(0, len(srcs), 4):
+                self.states.append(DeviceState(graph, "sssp", sources=srcs[i:i + 4], max_weight=max_weight))
+        except BaseException:
+            self.free()
+            raise
+        self._widths = [st.arity for st in self.states]
+
+    def _split(self, values: np.ndarray):
+        cols, a = [], 0
+        for wdt in self._widths:
+            cols.append(np.ascontiguousarray(values[:, a:a + wdt]))
+            a += wdt
+        return cols
+
+    def iterate(self, direction: str = "auto", stream=None):
+        for st in self.states:
+            st.iterate(direction, stream)
+
+    def request(self, op: int, lo: int, hi: int, stream=None):
+        for st in self.states:
+            st.request(op, lo, hi, stream)
+
+    def commit(self, stream=None):
+        for st in self.states:
+            st.commit(stream)
+
+    def stats(self, stream=None) -> dict:
+        sts = [st.stats(stream) for st in self.states]
+        out = dict(sts[0])
+        for k in ("changed", "next_active", "next_units", "units", "targets", "remote_active"):
+            out[k] = sum(int(x[k]) for x in sts)
+        out["max_stat"] = max(float(x["max_stat"]) for x in sts)
+        out["voted"] = int(all(x["voted"] for x in sts))
+        return out
+
+    def read_attrs(self, owned_only: bool = False, stream=None) -> np.ndarray:
+        return np.concatenate([st.read_attrs(owned_only, stream) for st in self.states], axis=1)
+
+    def write_attrs(self, values, stream=None):
+        a = np.asarray(values, dtype=np.float64).reshape(self.graph.num_vertices, self.arity)
+        for st, c in zip(self.states, self._split(a)):
+            st.write_attrs(c, stream)
+
+    def deliver(self, dense, values, stream=None):
+        v = np.asarray(values, dtype=np.float64).reshape(-1, self.arity)
+        for st, c in zip(self.states, self._split(v)):
+            st.deliver(dense, c, stream)
+
+    def profile(self, enable: bool | None = None, reset: bool = False) -> dict:
+        ps = [st.profile(enable, reset) for st in self.states]
+        return {k: sum(p[k] for p in ps) for k in ps[0]}
+
+    def free(self):
+        for st in self.states:
+            st.free()
+        self.states = []
+
+
+def make_state(graph: "DeviceGraph", algo: str, sources=None, max_weight: int | None = None):
+    """A DeviceState, or SsspLanes for SSSP with more than 4 sources."""
+    if algo == "sssp" and sources is not None and len(sources) > 4:
+        return SsspLanes(graph, sources, max_weight)
+    return DeviceState(graph, algo, sources=sources, max_weight=max_weight)
 
 
 @dataclass

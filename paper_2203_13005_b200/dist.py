@@ -71,6 +71,30 @@ class Collective:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
 
+    def _host_backend(self) -> bool:
+        """gloo (the CPU test path): device tensors are gathered through host copies."""
+        try:
+            return self.dist.get_backend(self.group) == "gloo"
+        except Exception:  # noqa: BLE001
+            return False
+
+    def all_gather_flat(self, out, mine):
+        """out (world * n) <- every rank's mine (n), in rank order."""
+        if mine.is_cuda and self._host_backend():
+            parts = [mine.new_empty(mine.numel(), device="cpu") for _ in range(self.world)]
+            self.dist.all_gather(parts, mine.cpu(), group=self.group)
+            out.copy_(__import__("torch").cat(parts))
+            return
+        self.dist.all_gather_into_tensor(out, mine, group=self.group)
+
+    def all_min_flag(self, ok: int, device) -> int:
+        """MIN over ranks of a 0/1 flag (agreement on an optional path)."""
+        import torch
+        dev = "cpu" if self._host_backend() else device
+        flag = torch.tensor([int(ok)], dtype=torch.int32, device=dev)
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN, group=self.group)
+        return int(flag.item())
+
     def vote_start(self, counts: list[int], max_stat: float, device):
         """Launch the vote: one all-gather of every rank's (counters, max statistic)."""
         import torch
@@ -78,14 +102,14 @@ class Collective:
             return (counts, max_stat)
         mine = torch.tensor([float(c) for c in counts] + [max_stat], dtype=torch.float64, device=device)
         out = torch.empty(self.world * mine.numel(), dtype=torch.float64, device=device)
-        self.dist.all_gather_into_tensor(out, mine, group=self.group)
+        self.all_gather_flat(out, mine)
         return out
 
     def vote_start_device(self, mine):
         """The vote from a device-resident block (gxb_stats_device): no host round trip."""
         import torch
         out = torch.empty(self.world * mine.numel(), dtype=torch.float64, device=mine.device)
-        self.dist.all_gather_into_tensor(out, mine, group=self.group)
+        self.all_gather_flat(out, mine)
         return out
 
     def vote_finish(self, handle) -> tuple[list[int], float]:
@@ -93,9 +117,10 @@ class Collective:
         if isinstance(handle, tuple):
             return handle
         rows = handle.view(self.world, -1).cpu().tolist()
-        self.last_rows = rows  # per-rank blocks (e.g. the packed record counts)
-        counts = [int(sum(r[i] for r in rows)) for i in range(len(rows[0]) - 1)]
-        return counts, max(r[-1] for r in rows)
+        self.last_rows = rows  # per-rank blocks (e.g. the packed record counts, per-peer counts)
+        # columns 0-4: counters (SUM), 5: the statistic (MAX), 6+: per-receiver record counts
+        counts = [int(sum(r[i] for r in rows)) for i in range(5)]
+        return counts, max(r[5] for r in rows)
 
     def vote(self, counts: list[int], max_stat: float, device) -> tuple[list[int], float]:
         return self.vote_finish(self.vote_start(counts, max_stat, device))
@@ -120,7 +145,7 @@ class Collective:
         """Equal-size all-gather where `mine` is this rank's block of `out` (NCCL in place)."""
         if self.world == 1:
             return
-        self.dist.all_gather_into_tensor(out, mine, group=self.group)
+        self.all_gather_flat(out, mine)
 
     def gather_counts(self, n: int, device) -> list[int]:
         import torch
@@ -148,6 +173,8 @@ class PartitionedRun:
     sparse_ratio: float = 0.8         # ... when that is below this fraction of the dense volume
     peer_writes: bool = True          # PR: Apply stores new contributions into the peers' replicas over
                                       # NVLink (IPC-mapped), fusing the exchange into the kernel
+    peer_delta: bool = True           # SSSP / CC / LP: the pack kernel stores each changed value only
+                                      # into the arenas of the peers that read it (IPC, NVLink)
     overlap: bool = False             # pipeline shuffle: chunked PR rounds with the exchange overlapped
                                       # (needs exchange_chunks > 1; measured slower than one all-gather
                                       # at N <= 4, where the tile kernel and NCCL contend for L2)
@@ -160,6 +187,7 @@ class PartitionedRun:
         self._sparse = None
         self._pending = []
         self._peers = None
+        self._dpeers = None
         self.xchunks = 1
         if self.overlap and self.algo == "pagerank" and hasattr(self.state, "graph") and \
                 hasattr(self.state.graph, "xchunks"):
@@ -243,7 +271,7 @@ class PartitionedRun:
         rptr, rbytes = self.state.buffer(L.BUF_RECV)
         send = self._view(sptr, sbytes, "u1")[: maxc * rec]
         recv = self._view(rptr, rbytes, "u1")[: self.comm.world * maxc * rec]
-        self.comm.dist.all_gather_into_tensor(recv, send, group=self.comm.group)
+        self.comm.all_gather_flat(recv, send)
         counts = list(packed)
         counts[self.comm.rank] = 0
         rows = self.comm.last_rows
@@ -284,10 +312,50 @@ class PartitionedRun:
             return self.state.view(ptr, nbytes, dtype)
         return device_view(ptr, nbytes, dtype)
 
+    def _setup_delta_peers(self) -> bool:
+        """Frontier algorithms: map every peer's receive arena (CUDA IPC, handles all-gathered
+        once) so the pack kernel stores each changed value only into the arenas of the peers
+        whose CSC reads it; all ranks must agree or none uses it (padded all-gather then)."""
+        if self._dpeers is not None:
+            return self._dpeers
+        self._dpeers = False
+        if not (self.peer_delta and self.algo != "pagerank" and 1 < self.comm.world <= 8
+                and hasattr(self.state, "delta_arena") and hasattr(self.comm.dist, "all_gather_object")):
+            return False
+        ok = 1
+        try:
+            send, _ = self.state.exchange_counts()
+        except Exception:  # noqa: BLE001
+            send, ok = [0] * self.comm.world, 0
+        rows = [None] * self.comm.world
+        self.comm.dist.all_gather_object(rows, send, group=self.comm.group)
+        handle = b""
+        if ok:
+            try:
+                handle = self.state.delta_arena(np.asarray(rows, dtype=np.uint64))
+            except Exception:  # noqa: BLE001 - no IPC on this platform
+                ok = 0
+        handles = [None] * self.comm.world
+        self.comm.dist.all_gather_object(handles, handle, group=self.comm.group)
+        if ok and all(handles):
+            try:
+                self.state.delta_open(b"".join(handles))
+            except Exception:  # noqa: BLE001
+                ok = 0
+        else:
+            ok = 0
+        if self.comm.all_min_flag(ok, self.device) != 1:
+            if ok:
+                self.state.delta_close()
+            return False
+        self._dpeers = True
+        return True
+
     def prepare(self):
         """One-time setup outside any timed region: maps the peers' replicas (PageRank) or
-        allocates the delta-record buffers (frontier algorithms)."""
+        receive arenas (frontier algorithms), else allocates the delta-record buffers."""
         self._setup_peers()
+        self._setup_delta_peers()
         if self.comm.world > 1 and self.algo != "pagerank" and hasattr(self.state, "buffer"):
             for which in (L.BUF_SEND, L.BUF_RECV):
                 self.state.buffer(which)
@@ -302,7 +370,6 @@ class PartitionedRun:
         if not (self.peer_writes and self.algo == "pagerank" and self.comm.world > 1
                 and hasattr(self.state, "ipc_handle") and hasattr(self.comm.dist, "all_gather_object")):
             return False
-        import torch
         ok = 1
         try:
             mine = self.state.ipc_handle(0) + self.state.ipc_handle(1)
@@ -318,9 +385,7 @@ class PartitionedRun:
                 ok = 0
         else:
             ok = 0
-        flag = torch.tensor([ok], dtype=torch.int32, device=self.device)
-        self.comm.dist.all_reduce(flag, op=self.comm.dist.ReduceOp.MIN, group=self.comm.group)
-        if int(flag.item()) != 1:
+        if self.comm.all_min_flag(ok, self.device) != 1:
             if ok:
                 self.state.close_peers()
             return False
@@ -396,6 +461,7 @@ class PartitionedRun:
             self.state.iterate(direction, **self._on_stream())
         device_vote = (self.comm.world > 1 and hasattr(self.state, "stats_device")
                        and hasattr(self.comm, "vote_start_device"))
+        dpeers = device_vote and self.algo != "pagerank" and self._setup_delta_peers()
         async_delta = device_vote and self.algo != "pagerank" and hasattr(self.state, "pack_async")
         if device_vote:
             # the vote block goes from device stripes straight into the all-gather; the host
@@ -403,8 +469,11 @@ class PartitionedRun:
             # Frontier algorithms pack their changed values first: the record count rides along.
             import torch
             if getattr(self, "_vote_buf", None) is None:
-                self._vote_buf = torch.empty(6, dtype=torch.float64, device=self.device)
-            if async_delta:
+                self._vote_buf = torch.zeros(6 + (self.comm.world if dpeers else 0), dtype=torch.float64,
+                                             device=self.device)
+            if dpeers:
+                self.state.delta_pack(self._vote_buf, **self._on_stream())
+            elif async_delta:
                 self.state.pack_async(**self._on_stream())
             self.state.stats_device(self._vote_buf, **self._on_stream())
             handle = self.comm.vote_start_device(self._vote_buf)
@@ -441,6 +510,11 @@ class PartitionedRun:
         if not skip and not early:
             if self.algo == "pagerank":
                 moved = self._exchange_dense()
+            elif dpeers:
+                me = self.comm.rank
+                counts_from = [0 if p == me else int(r[6 + me]) for p, r in enumerate(self.comm.last_rows)]
+                self.state.delta_unpack(counts_from, **self._on_stream())
+                moved = sum(counts_from) * self.state.buffer(L.BUF_RECORD_SIZE)[1]
             elif async_delta:
                 moved = self._exchange_delta_async([int(r[4]) for r in self.comm.last_rows])
             else:

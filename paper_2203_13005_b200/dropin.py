@@ -245,7 +245,7 @@ class GpuAgent(_agent_mod.Agent):
         return state
 
     def _build_device(self):
-        from .device import DeviceGraph, DeviceState
+        from .device import DeviceGraph, make_state
         ctx = self.daemons[0].context
         if ctx is None:
             raise ProtocolError(f"node {self.node_id}: daemon {self.daemons[0].state.channel_key} has no device "
@@ -263,7 +263,7 @@ class GpuAgent(_agent_mod.Agent):
                                         csr=algo != "pagerank", partitioning="ids", sizes=sizes)
         sources = list(self.algorithm.sources) if algo == "sssp" else None
         maxw = int(np.max(weights)) if weights is not None and weights.size else None
-        self.device_state = DeviceState(self.device_graph, algo, sources=sources, max_weight=maxw)
+        self.device_state = make_state(self.device_graph, algo, sources=sources, max_weight=maxw)
         self._ids = self.device_graph.ids()
         owned = np.fromiter(sorted(part.vertices), dtype=np.int64, count=len(part.vertices))
         self._owned_pos = np.searchsorted(self._ids, owned)

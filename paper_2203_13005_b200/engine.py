@@ -50,6 +50,8 @@ class RunConfig:
     sizes: list[int] | None = None  # explicit partition sizes (partition_graph's `sizes`)
     capacity: list[float] | None = None  # per-partition capacity factors (balancer.capacity_factors):
                                          # degree-sorted ranges cut in proportion (A/balancer.py:79-98)
+    peer_delta: bool = True       # SSSP / CC / LP: changed values go only to the partitions that read
+                                  # them, stored by the pack kernel into their arenas (else: to all)
 
     def __post_init__(self):
         if self.partitions < 1:
@@ -122,6 +124,41 @@ def exchange_local(states, bounds) -> int:
     return moved
 
 
+def setup_local_peers(states) -> list:
+    """Same-process partitions for the per-peer delta exchange: every partition's receive
+    arena sized from the all-partition send counts, the peers' arenas wired directly.
+    Returns the per-partition vote blocks (6 + m float64 each) the pack kernel fills."""
+    import torch
+    m = len(states)
+    try:
+        caps = np.asarray([s.exchange_counts()[0] for s in states], dtype=np.uint64)
+    except ValueError:  # no per-peer lists (an edgeless graph): the all-to-all round applies
+        return None
+    for s in states:
+        s.delta_arena(caps)
+    for s in states:
+        s.delta_set_peers(states)
+    dev = torch.device("cuda", states[0].graph.ctx.device)
+    return [torch.zeros(6 + m, dtype=torch.float64, device=dev) for _ in states]
+
+
+def exchange_local_peers(states, votes) -> int:
+    """Sync round over the per-peer arenas (the in-process analogue of PartitionedRun's
+    delta_pack -> vote -> delta_unpack): each partition receives only the changed values its
+    CSC reads (A/agent.py:550-582 with a static query set)."""
+    from . import _lib as L
+    for s, v in zip(states, votes):
+        s.delta_pack(v)
+    rows = [v.cpu().tolist() for v in votes]
+    rec = states[0].buffer(L.BUF_RECORD_SIZE)[1]
+    moved = 0
+    for j, s in enumerate(states):
+        counts = [0 if p == j else int(rows[p][6 + j]) for p in range(len(states))]
+        s.delta_unpack(counts)
+        moved += sum(counts) * rec
+    return moved
+
+
 def _edges(graph):
     from .graph import EdgeArrays
     if isinstance(graph, EdgeArrays):
@@ -146,7 +183,7 @@ class Engine:
         self.states, self.graphs = [], []
 
     def _setup(self):
-        from .device import DeviceContext, DeviceGraph, DeviceState
+        from .device import DeviceContext, DeviceGraph, make_state
         cfg, ea = self.config, self.edges
         algo = self.algorithm.device_name
         self.ctx = DeviceContext(cfg.device)
@@ -155,12 +192,19 @@ class Engine:
         for j in range(cfg.partitions):
             g = DeviceGraph(self.ctx, ea.src, ea.dst, w, part=j, nparts=cfg.partitions, csr=algo != "pagerank",
                             partitioning=cfg.partitioning, sizes=cfg.sizes, capacity=cfg.capacity)
-            s = DeviceState(g, algo, sources=getattr(self.algorithm, "sources", None) if algo == "sssp" else None,
-                            max_weight=maxw if algo == "sssp" else None)
+            s = make_state(g, algo, sources=getattr(self.algorithm, "sources", None) if algo == "sssp" else None,
+                           max_weight=maxw if algo == "sssp" else None)
             self.graphs.append(g)
             self.states.append(s)
         self.bounds = self.graphs[0].bounds()
         self.metrics.init_counts = {0: self.ctx.init_count}
+        # SSSP with more than 4 sources: one device state per 4-lane group, exchanged per group
+        lanes = getattr(self.states[0], "states", None)
+        self.groups = [[st.states[k] for st in self.states] for k in range(len(lanes))] if lanes else [self.states]
+        self.votes = None
+        if cfg.partitions > 1 and algo != "pagerank" and cfg.peer_delta and cfg.partitions <= 8:
+            votes = [setup_local_peers(grp) for grp in self.groups]
+            self.votes = None if any(v is None for v in votes) else votes
         cap = cfg.max_iterations
         self.cap = self.algorithm.default_iteration_cap(self.graphs[0].num_vertices) if cap is None else cap
 
@@ -210,7 +254,12 @@ class Engine:
             iteration += 1
             stats = [self._round(s, g) for s, g in zip(self.states, self.graphs)]
             skip = cfg.enable_skip and m > 1 and all(st["remote_active"] == 0 for st in stats)
-            moved = 0 if (skip or m == 1) else exchange_local(self.states, self.bounds)
+            if skip or m == 1:
+                moved = 0
+            elif self.votes is not None:
+                moved = sum(exchange_local_peers(grp, v) for grp, v in zip(self.groups, self.votes))
+            else:
+                moved = sum(exchange_local(grp, self.bounds) for grp in self.groups)
             self.metrics.exchanged_bytes += moved
             converged = convergence_vote([bool(st["voted"]) for st in stats])
             apply_rounds += 1

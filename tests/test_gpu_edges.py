@@ -109,9 +109,13 @@ def test_device_limits_raise(ctx):
     from paper_2203_13005_b200.device import DeviceGraph, DeviceState
     with pytest.raises(ValueError):  # id 0xFFFFFFFF is the reserved sentinel
         DeviceGraph(ctx, np.array([0xFFFFFFFF], np.uint32), np.array([1], np.uint32))
-    g = DeviceGraph(ctx, np.array([0, 1], np.uint32), np.array([1, 2], np.uint32),
-                    np.array([3.0e9, 1.0]))
     with pytest.raises(ValueError):  # max_w * |V| >= 2^32 - 1: sums could saturate
+        g = DeviceGraph(ctx, np.array([0, 1], np.uint32), np.array([1, 2], np.uint32),
+                        np.array([3.0e9, 1.0]))
+        DeviceState(g, "sssp")
+    g = DeviceGraph(ctx, np.array([0, 1], np.uint32), np.array([1, 2], np.uint32),
+                    np.array([3_000_000_000, 1], np.uint32))  # integer weights: the state checks
+    with pytest.raises(ValueError):
         DeviceState(g, "sssp")
 
 
@@ -130,3 +134,71 @@ def test_empty_graph_sssp(ctx):
         return  # no source vertex to start from: refused loudly
     it, conv, _ = run_state(s)
     assert conv and s.read_attrs().shape[0] == 0
+
+
+# ---- SSSP inputs beyond 4 integral lanes (the reference takes any source list and float
+# weights, A/algorithms.py:81-122, A/graph.py:155-162) ----
+
+@pytest.mark.parametrize("nsrc", [5, 9, 13])
+@pytest.mark.parametrize("cap", [None, 3])
+def test_sssp_many_sources(ctx, oracle_lib, nsrc, cap):
+    """More than 4 sources: groups of 4 lanes (SsspLanes) = the oracle's joint run."""
+    from paper_2203_13005_b200.algorithms import SsspBellmanFord, run_device
+    from paper_2203_13005_b200.graph import EdgeArrays
+    from paper_2203_13005_b200.rmat import RmatParams, rmat_host
+    src, dst, w = rmat_host(RmatParams(scale=11, seed=90 + nsrc, wmax=40))
+    ids = np.union1d(src, dst)
+    rng = np.random.default_rng(nsrc)
+    sources = [int(x) for x in rng.choice(ids, size=nsrc - 1, replace=False)] + [int(ids.max()) + 7]  # one absent
+    algo = SsspBellmanFord(sources)
+    attrs, res = run_device(algo, None, EdgeArrays(src, dst, w.astype(np.float64)), max_iterations=cap, ctx=ctx,
+                            return_result=True)
+    ref = oracle_lib.OracleGraph(src, dst, w.astype(np.float64)).run(
+        "sssp", sources=np.array(sources, np.uint32), max_iterations=cap)
+    assert res.iterations == ref.iterations and res.converged == ref.converged
+    assert_attrs_match("sssp", res.attrs, ref.attrs)
+    assert attrs[int(ids[0])] == tuple(float(x) for x in ref.attrs[0])
+
+
+@pytest.mark.parametrize("denom", [2, 4, 64])
+def test_sssp_dyadic_weights(ctx, oracle_lib, denom):
+    """Non-integral dyadic weights (2.5, 0.25, ...) run exactly: scaled to u32 by 2^k."""
+    from paper_2203_13005_b200.algorithms import SsspBellmanFord, run_device
+    from paper_2203_13005_b200.graph import EdgeArrays
+    from paper_2203_13005_b200.rmat import RmatParams, rmat_host
+    src, dst, w = rmat_host(RmatParams(scale=11, seed=95, wmax=63))
+    wf = w.astype(np.float64) / denom
+    ids = np.union1d(src, dst)
+    algo = SsspBellmanFord([int(x) for x in ids[:4]])
+    _, res = run_device(algo, None, EdgeArrays(src, dst, wf), ctx=ctx, return_result=True)
+    ref = oracle_lib.OracleGraph(src, dst, wf).run("sssp")
+    assert res.iterations == ref.iterations
+    assert_attrs_match("sssp", res.attrs, ref.attrs)
+    assert np.any(res.attrs != np.floor(res.attrs))  # fractional distances really occur
+
+
+def test_sssp_non_dyadic_weights_raise(ctx):
+    """Weights like 1e-3 have no exact u32 form: refused loudly, never approximated."""
+    from paper_2203_13005_b200.device import DeviceGraph
+    with pytest.raises(ValueError, match="dyadic"):
+        DeviceGraph(ctx, np.array([0, 1], np.uint32), np.array([1, 2], np.uint32), np.array([1e-3, 1.0]))
+
+
+@pytest.mark.parametrize("m", [2, 3])
+def test_sssp_many_sources_partitioned(oracle_lib, m):
+    """Partitioned engine with 6 sources and dyadic weights: per-group sync rounds."""
+    from paper_2203_13005_b200.algorithms import SsspBellmanFord
+    from paper_2203_13005_b200.engine import RunConfig, run
+    from paper_2203_13005_b200.graph import EdgeArrays
+    from paper_2203_13005_b200.rmat import RmatParams, rmat_host
+    src, dst, w = rmat_host(RmatParams(scale=11, seed=97, wmax=31))
+    wf = w.astype(np.float64) / 8
+    ids = np.union1d(src, dst)
+    sources = [int(x) for x in ids[::max(1, len(ids) // 6)][:6]]
+    algo = SsspBellmanFord(sources)
+    attrs, met = run(EdgeArrays(src, dst, wf), algo, "bsp", RunConfig(partitions=m, partitioning="edges",
+                                                                        enable_skip=True))
+    ref = oracle_lib.OracleGraph(src, dst, wf).run("sssp", sources=np.array(sources, np.uint32))
+    got = np.array([algo.row_from_attr(attrs[int(v)]) for v in ids])
+    assert_attrs_match("sssp", got, ref.attrs)
+    assert met.iterations == ref.iterations

@@ -124,8 +124,8 @@ def test_lifecycle_and_errors(ctx):
         s.request(L.OP_APPLY, 0, 99)
     with pytest.raises(ValueError):
         DeviceState(g, "sssp", sources=[0, 1, 2, 3, 4])
-    with pytest.raises(ValueError):
-        DeviceGraph(ctx, np.array([0], np.uint32), np.array([1], np.uint32), w=np.array([1.5]))
+    with pytest.raises(ValueError, match="dyadic"):  # 0.1 has no exact u32 scaling (1.5 does)
+        DeviceGraph(ctx, np.array([0], np.uint32), np.array([1], np.uint32), w=np.array([0.1]))
 
 
 def test_device_rmat_matches_host(ctx):
@@ -419,3 +419,30 @@ def test_owned_install_refreshes_peer_mirrors(ctx, algo, m):
         got[mask] = r[mask]
     assert_attrs_match(algo, got, want, rel=1e-12)
     assert not np.array_equal(want, full)
+
+
+@pytest.mark.parametrize("algo", ["sssp", "cc", "lp"])
+@pytest.mark.parametrize("m,partitioning", [(2, "edges"), (3, "ids"), (4, "edges")])
+def test_peer_delta_exchange_equals_all_to_all(oracle_lib, algo, m, partitioning):
+    """Per-peer delta records (each changed value stored only into the arenas of the
+    partitions that read it, A/agent.py:550-582 with a static query set) = the all-to-all
+    record exchange = the oracle, with no more bytes moved."""
+    from paper_2203_13005_b200.algorithms import make_algorithm
+    from paper_2203_13005_b200.engine import RunConfig, run
+    from paper_2203_13005_b200.graph import EdgeArrays
+    from paper_2203_13005_b200.rmat import RmatParams, rmat_host
+    p = RmatParams(scale=12, seed=60 + m, wmax=63 if algo == "sssp" else 0, symmetric=algo == "cc")
+    src, dst, w = rmat_host(p)
+    ea = EdgeArrays(src, dst, None if w is None else w.astype(np.float64))
+    ids = ea.vertex_ids()
+    alg = make_algorithm(algo, [int(v) for v in ids], None)
+    out = {}
+    for peer in (True, False):
+        attrs, met = run(ea, alg, "bsp", RunConfig(partitions=m, partitioning=partitioning, peer_delta=peer,
+                                                   enable_skip=True))
+        out[peer] = (np.array([alg.row_from_attr(attrs[int(v)]) for v in ids]), met)
+    ref = oracle_lib.OracleGraph(src, dst, None if w is None else w.astype(np.float64)).run(algo)
+    assert_attrs_match(algo, out[True][0], ref.attrs)
+    assert_attrs_match(algo, out[False][0], ref.attrs)
+    assert out[True][1].iterations == out[False][1].iterations == ref.iterations
+    assert 0 < out[True][1].exchanged_bytes <= out[False][1].exchanged_bytes
