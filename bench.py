@@ -755,6 +755,7 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks.summary(), "wall_s": round(t_wall, 3),
+            "step_ms": [round(x, 4) for x in step_ms] if len(step_ms) <= 64 else None,
             "skipped_rounds": skipped_rounds,
         }
         if world > 1:  # mirror-exchange bytes each GPU receives per round, against NVLink 5
