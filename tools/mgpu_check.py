@@ -25,12 +25,18 @@ def main():
     ap.add_argument("--algos", default="pagerank,sssp,cc,lp")
     ap.add_argument("--partitioning", default="edges")
     ap.add_argument("--capacity", default=None, help="comma-separated capacity factors (one per rank)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: host-side collectives, several ranks may share a GPU (functional check of "
+                         "N ranks on fewer devices: IPC peer replicas / arenas work within one device)")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if args.backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group("gloo")
     from paper_2203_13005_b200.device import DeviceContext, DeviceGraph, DeviceState
     from paper_2203_13005_b200.dist import Collective, PartitionedRun
     from paper_2203_13005_b200.rmat import RmatParams
@@ -53,8 +59,9 @@ def main():
         torch.cuda.synchronize()
         dt = time.perf_counter() - t
         mine = st.read_attrs(owned_only=True)
-        gathered = [torch.empty_like(torch.from_numpy(mine)).to(dev) for _ in range(world)]
-        dist.all_gather(gathered, torch.from_numpy(mine).to(dev))
+        gdev = dev if args.backend == "nccl" else torch.device("cpu")
+        gathered = [torch.empty_like(torch.from_numpy(mine)).to(gdev) for _ in range(world)]
+        dist.all_gather(gathered, torch.from_numpy(mine).to(gdev))
         if rank == 0:
             from oracle import oracle
             rows = gathered[0].cpu().numpy()
@@ -73,11 +80,13 @@ def main():
                 err = int((rows != ref.attrs).sum())
                 ok = err == 0
             report[algo] = dict(ok=bool(ok and it == ref.iterations), iterations=it, ref_iterations=ref.iterations,
+                                peer_path=bool(run._peers if algo == "pagerank" else run._dpeers),
                                 err=err, seconds=round(dt, 4), skipped=run.skipped_rounds,
                                 exchanged_mb=round(sum(r.exchanged_bytes for r in run.records) / 2 ** 20, 2))
         del st, g
     if rank == 0:
-        print(json.dumps({"world": world, "scale": args.scale, "partitioning": args.partitioning, **report}))
+        print(json.dumps({"world": world, "devices": torch.cuda.device_count(), "backend": args.backend,
+                          "scale": args.scale, "partitioning": args.partitioning, **report}))
         bad = [a for a, r in report.items() if not r["ok"]]
         if bad:
             print("MISMATCH", bad)
