@@ -467,6 +467,8 @@ def main():
                     help="time the unmodified reference Engine with the B200 daemon dropped in (PageRank, "
                          "--scale default 18, --partitions)")
     ap.add_argument("--partitions", type=int, default=1)
+    ap.add_argument("--dense-frac", type=float, default=0.25,
+                    help="SSSP/CC/LP at N>1: dense mirror exchange after rounds changing this slot fraction (0 = off)")
     args = ap.parse_args()
     # stdout carries exactly one JSON line: library banners (NCCL prints its version when a
     # communicator is created) go to stderr until the line is printed
@@ -517,7 +519,7 @@ def main():
 
     def new_run():
         st = DeviceState(graph, algo)
-        return PartitionedRun(st, bounds, comm, enable_skip=True, device=dev).prepare()
+        return PartitionedRun(st, bounds, comm, enable_skip=True, device=dev, dense_frac=args.dense_frac).prepare()
 
     # ---- device-timed steps ----
     clocks = ClockSampler(local).__enter__()

@@ -300,6 +300,13 @@ int gxb_exchange_delta_buffer(gxb_state* s, void** arena);
 int gxb_exchange_delta_close(gxb_state* s);
 int gxb_exchange_delta_pack(gxb_state* s, double* d_vote, void* stream);
 int gxb_exchange_delta_unpack(gxb_state* s, const uint64_t* counts_from, void* stream);
+
+/* dense mirror exchange for the rounds where most vertices changed (SSSP / CC / LP): the
+ * caller all-gathers every owner's block of GXB_BUF_VALUES_NEXT in place (equal blocks:
+ * the dealt partitioning), then dense_install installs every mirror whose landed value
+ * differs from its current one (it changed in its owner's round), marks it active and
+ * appends it to the frontier — coalesced passes instead of per-record scatter. */
+int gxb_exchange_dense_install(gxb_state* s, void* stream);
 int gxb_exchange_sparse_pack(gxb_state* s, void* stream);
 int gxb_exchange_sparse_unpack(gxb_state* s, void* stream);
 

@@ -144,6 +144,7 @@ def _sig(L):
         "gxb_exchange_delta_close": (I, [P]),
         "gxb_exchange_delta_pack": (I, [P, P, P]),
         "gxb_exchange_delta_unpack": (I, [P, P, P]),
+        "gxb_exchange_dense_install": (I, [P, P]),
         "gxb_exchange_sparse_pack": (I, [P, P]),
         "gxb_exchange_sparse_unpack": (I, [P, P]),
         "gxb_read_attrs": (I, [P, P, I, P]),

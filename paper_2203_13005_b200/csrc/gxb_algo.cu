@@ -832,10 +832,11 @@ __global__ void __launch_bounds__(kBlock) k_apply_sums(const Ops ops, const type
         }
         if constexpr (Ops::kPublishes) publish_changed_warp<kU>(ops.f, slot, ch, st);
     }
+    flush_stats(st, stats);  // ends in a block barrier: every thread's peer stores precede ...
     if constexpr (std::is_same<Ops, PrOps>::value) {
-        if (ops.npeers) __threadfence_system();  // peer stores visible before the round's vote
+        // ... one cumulative system-scope fence per block: peer stores visible before the vote
+        if (ops.npeers && threadIdx.x == 0) __threadfence_system();
     }
-    flush_stats(st, stats);
 }
 
 // ======================================================================

@@ -193,7 +193,55 @@ __global__ void k_pack_peers(int algo, const uint32_t* __restrict__ list, const 
             for (int j = 1; j < W; ++j) r[j] = v[j - 1];
         }
     }
-    __threadfence_system();  // the records are visible to the peers before the vote collective
+    // one cumulative system-scope fence per block after a barrier (not one per thread): the
+    // block's records are visible to the peers before the vote collective
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
+}
+
+// Dense mirror exchange (rounds where most vertices changed): every owner's block of the
+// next-value replica was all-gathered in place; a mirror whose landed value differs from
+// the current one changed in its owner's round — install it, mark it active and append it
+// to the frontier (warp-aggregated over consecutive slots: one OR per bitmap word).
+template <class T>
+__device__ __forceinline__ bool val_ne(const T& a, const T& b);
+template <>
+__device__ __forceinline__ bool val_ne<uint4>(const uint4& a, const uint4& b) {
+    return a.x != b.x || a.y != b.y || a.z != b.z || a.w != b.w;
+}
+template <>
+__device__ __forceinline__ bool val_ne<uint32_t>(const uint32_t& a, const uint32_t& b) {
+    return a != b;
+}
+
+template <class T>
+__global__ void k_dense_install(const T* __restrict__ next, T* cur, uint64_t S, uint64_t lo, uint64_t hi,
+                                uint32_t* active, uint32_t* list, unsigned long long* count,
+                                const uint32_t* __restrict__ outdeg, unsigned long long* units) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long u = 0;
+    for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ull; b < S;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s = b + lane;  // a warp covers 32 consecutive slots = one bitmap word
+        bool ch = false;
+        if (s < S && (s < lo || s >= hi)) {
+            const T n = next[s];
+            if (val_ne<T>(n, cur[s])) {
+                cur[s] = n;
+                ch = true;
+                u += outdeg[s];
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, ch);
+        if (!m) continue;
+        if (lane == 0) atomicOr(active + (b >> 5), m);
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(count, (unsigned long long)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (ch) list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)s;
+    }
+    for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+    if (lane == 0 && u) atomicAdd(units, u);
 }
 
 // counts into the vote block (after the 6 statistics), one double per receiver
@@ -311,10 +359,20 @@ int gxb_exchange_buffer(gxb_state* s, int which, void** dev_ptr, uint64_t* bytes
             *dev_ptr = s->d_contrib[which == GXB_BUF_CONTRIB1 ? 1 : 0];
             *bytes = (s->msg32 ? 4 : 8) * V;
             return GXB_OK;
-        case GXB_BUF_VALUES_NEXT:  // PR: the contributions being written by the open round
-            if (s->algo != GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "GXB_BUF_VALUES_NEXT is PageRank-only");
-            *dev_ptr = s->d_contrib[s->cur ^ 1];
-            *bytes = (s->msg32 ? 4 : 8) * V;
+        case GXB_BUF_VALUES_NEXT:
+            // PR: the contributions being written by the open round; SSSP / CC / LP: the
+            // next-value replica (after a closed round the owned block equals the current
+            // values; the non-owned part is the landing area of the dense mirror exchange)
+            if (s->algo == GXB_ALGO_PAGERANK) {
+                *dev_ptr = s->d_contrib[s->cur ^ 1];
+                *bytes = (s->msg32 ? 4 : 8) * V;
+            } else if (s->algo == GXB_ALGO_SSSP) {
+                *dev_ptr = s->d_dist_next;
+                *bytes = 16 * V;
+            } else {
+                *dev_ptr = s->d_lab_next;
+                *bytes = 4 * V;
+            }
             return GXB_OK;
         case GXB_BUF_SPARSE_SEND:
         case GXB_BUF_SPARSE_RECV: {
@@ -677,6 +735,34 @@ int gxb_exchange_delta_unpack(gxb_state* s, const uint64_t* counts_from, void* s
                                                               g->lo, g->hi, s->d_dist_cur, s->d_dist_next, s->d_lab_cur,
                                                               s->d_lab_next, s->d_active[0], s->d_frontier[0], s->d_fcount,
                                                               g->d_outdeg, s->d_xscratch + 1);
+        s->launches++;
+    }
+    GXB_CUDA(cudaGetLastError());
+    s->lab_injective = false;
+    s->unpack_pending = true;  // the next round reads the frontier's length and GEN units back
+    return GXB_OK;
+}
+
+int gxb_exchange_dense_install(gxb_state* s, void* stream) {
+    NvtxRange nvtx_("gxb_exchange_dense_install");
+    if (!s) return fail(GXB_EINVAL, "gxb_exchange_dense_install: null state");
+    if (s->algo == GXB_ALGO_PAGERANK) return fail(GXB_EINVAL, "gxb_exchange_dense_install: PageRank uses the dense exchange");
+    if (s->in_round) return fail(GXB_ESTATE, "gxb_exchange_dense_install: round still open");
+    gxb_graph* g = s->g;
+    cudaStream_t st = (cudaStream_t)stream;
+    GXB_CHECK(state_settle(s));  // the closed round's own frontier first
+    if (!s->d_xscratch) GXB_CHECK(dalloc_t(&s->d_xscratch, 4));
+    GXB_CUDA(cudaMemsetAsync(s->d_xscratch + 1, 0, 8, st));
+    if (g->S) {
+        const unsigned grid = grid_for(g->S);
+        if (s->algo == GXB_ALGO_SSSP)
+            k_dense_install<uint4><<<grid, kBlock, 0, st>>>(s->d_dist_next, s->d_dist_cur, g->S, g->lo, g->hi,
+                                                            s->d_active[0], s->d_frontier[0], s->d_fcount, g->d_outdeg,
+                                                            s->d_xscratch + 1);
+        else
+            k_dense_install<uint32_t><<<grid, kBlock, 0, st>>>(s->d_lab_next, s->d_lab_cur, g->S, g->lo, g->hi,
+                                                               s->d_active[0], s->d_frontier[0], s->d_fcount,
+                                                               g->d_outdeg, s->d_xscratch + 1);
         s->launches++;
     }
     GXB_CUDA(cudaGetLastError());

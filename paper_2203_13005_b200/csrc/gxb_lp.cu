@@ -215,8 +215,9 @@ __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint3
         for (int j = 0; j < kB; ++j) ok[j] = lab[j] != kEmpty;
 #pragma unroll
         for (int j = 0; j < kB; ++j) {
-            const unsigned long long key = ok[j] ? (unsigned long long)lab[j] : (0x100000000ull | (unsigned)lane);
-            const unsigned m = __match_any_sync(kFull, key);
+            // 32-bit match: lanes without a message all carry kEmpty and group together,
+            // but their leader is not `ok`, so that group is dropped
+            const unsigned m = __match_any_sync(kFull, ok[j] ? lab[j] : kEmpty);
             if (ok[j] && lane == __ffs(m) - 1) {
                 uint32_t h = mix32(lab[j]) & (kWarpPairs - 1);
                 bool done = false;
@@ -343,8 +344,7 @@ __device__ __forceinline__ void lp_count_edges(const LpLaunch& L, uint64_t beg, 
 #pragma unroll
         for (int j = 0; j < kB; ++j) {
             const bool ok = lab[j] != kEmpty;
-            const unsigned long long key = ok ? (unsigned long long)lab[j] : (0x100000000ull | (unsigned)lane);
-            const unsigned m = __match_any_sync(kFull, key);
+            const unsigned m = __match_any_sync(kFull, lab[j]);  // no-message lanes group under kEmpty
             if (ok && lane == __ffs(m) - 1) smem_table_add(keys, cnts, mask, lab[j], (uint32_t)__popc(m));
         }
     }

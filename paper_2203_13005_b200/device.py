@@ -494,6 +494,10 @@ class DeviceState:
         arr = np.ascontiguousarray([int(c) for c in counts_from], dtype=np.uint64)
         L.check(L.lib().gxb_exchange_delta_unpack(self._h, _vp(arr), _stream_ptr(stream)))
 
+    def dense_install(self, stream=None):
+        """After the in-place all-gather of GXB_BUF_VALUES_NEXT: install the changed mirrors."""
+        L.check(L.lib().gxb_exchange_dense_install(self._h, _stream_ptr(stream)))
+
     def sparse_pack(self, stream=None):
         L.check(L.lib().gxb_exchange_sparse_pack(self._h, _stream_ptr(stream)))
 

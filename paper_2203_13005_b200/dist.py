@@ -173,6 +173,9 @@ class PartitionedRun:
     sparse_ratio: float = 0.8         # ... when that is below this fraction of the dense volume
     peer_writes: bool = True          # PR: Apply stores new contributions into the peers' replicas over
                                       # NVLink (IPC-mapped), fusing the exchange into the kernel
+    dense_frac: float = 0.25          # SSSP / CC / LP: a round after one that changed >= this fraction
+                                      # of the slots exchanges whole value blocks (all-gather in place +
+                                      # install of the changed mirrors) instead of records; 0 = never
     peer_delta: bool = True           # SSSP / CC / LP: the pack kernel stores each changed value only
                                       # into the arenas of the peers that read it (IPC, NVLink)
     overlap: bool = False             # pipeline shuffle: chunked PR rounds with the exchange overlapped
@@ -188,6 +191,7 @@ class PartitionedRun:
         self._pending = []
         self._peers = None
         self._dpeers = None
+        self._prev_changed = 0
         self.xchunks = 1
         if self.overlap and self.algo == "pagerank" and hasattr(self.state, "graph") and \
                 hasattr(self.state.graph, "xchunks"):
@@ -242,6 +246,24 @@ class PartitionedRun:
             views = [values[int(self.bounds[q]):int(self.bounds[q + 1])] for q in range(self.comm.world)]
             self.comm.allgatherv(views, views[r])
         return width * int(self.bounds[-1] - sizes[r])
+
+    def _equal_blocks(self) -> bool:
+        sizes = np.diff(self.bounds.astype(np.int64))
+        return bool(sizes.size > 1 and (sizes == sizes[0]).all())
+
+    def _exchange_dense_mirror(self) -> int:
+        """SSSP / CC / LP rounds where most vertices changed: all-gather every owner's block of
+        the next-value replica in place (one NCCL collective, no per-record packing), then
+        install the mirrors whose value differs (gxb_exchange_dense_install)."""
+        ptr, nbytes = self.state.buffer(L.BUF_VALUES_NEXT)
+        S = int(self.bounds[-1])
+        width = nbytes // max(1, S)
+        blk = (S // self.comm.world) * width
+        values = self._view(ptr, nbytes, "u1")
+        r = self.comm.rank
+        self.comm.allgather_inplace(values[: blk * self.comm.world], values[r * blk:(r + 1) * blk])
+        self.state.dense_install(**self._on_stream())
+        return blk * (self.comm.world - 1)
 
     def _exchange_delta(self) -> int:
         """SSSP / CC / LP: only changed owned values travel, as (slot, value) records."""
@@ -463,6 +485,10 @@ class PartitionedRun:
                        and hasattr(self.comm, "vote_start_device"))
         dpeers = device_vote and self.algo != "pagerank" and self._setup_delta_peers()
         async_delta = device_vote and self.algo != "pagerank" and hasattr(self.state, "pack_async")
+        # dense mirror exchange when the previous round changed most vertices (every rank
+        # decides from the same global count, so all agree without a collective)
+        dense = (device_vote and self.algo != "pagerank" and self.dense_frac > 0 and self._equal_blocks()
+                 and self._prev_changed >= self.dense_frac * int(self.bounds[-1]))
         if device_vote:
             # the vote block goes from device stripes straight into the all-gather; the host
             # reads the round's statistics after the collective (one synchronisation per round).
@@ -471,7 +497,10 @@ class PartitionedRun:
             if getattr(self, "_vote_buf", None) is None:
                 self._vote_buf = torch.zeros(6 + (self.comm.world if dpeers else 0), dtype=torch.float64,
                                              device=self.device)
-            if dpeers:
+            if dense:
+                if self._vote_buf.numel() > 6:
+                    self._vote_buf[6:].zero_()  # no records this round
+            elif dpeers:
                 self.state.delta_pack(self._vote_buf, **self._on_stream())
             elif async_delta:
                 self.state.pack_async(**self._on_stream())
@@ -502,6 +531,7 @@ class PartitionedRun:
             st = self.state.stats()  # the round is complete: no wait
         t0 = self._tick("vote", t0)
         changed, next_active, next_units, remote_active, _packed = counts
+        self._prev_changed = changed
         if self.algo == "pagerank":
             self._pr_remote = remote_active
         self.iteration += 1
@@ -510,6 +540,8 @@ class PartitionedRun:
         if not skip and not early:
             if self.algo == "pagerank":
                 moved = self._exchange_dense()
+            elif dense:
+                moved = self._exchange_dense_mirror()
             elif dpeers:
                 me = self.comm.rank
                 counts_from = [0 if p == me else int(r[6 + me]) for p, r in enumerate(self.comm.last_rows)]

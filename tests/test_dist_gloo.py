@@ -180,7 +180,7 @@ def _worker(rank, world, port, algo, src, dst, cap, out_q, enable_skip, cls=None
         vals = st.rank if algo == "pagerank" else st.label.astype(np.float64)
         lo, hi = st.lo, st.hi
         out_q.put((rank, it, conv, run.skipped_rounds, lo, hi, vals[lo:hi].copy(),
-                   [r.skipped for r in run.records]))
+                   [r.skipped for r in run.records], getattr(st, "dense_rounds", 0)))
     finally:
         dist.destroy_process_group()
 
@@ -251,6 +251,45 @@ def test_cc_async_delta_exchange_matches_oracle(oracle_lib):
     ref = oracle_lib.OracleGraph(src, dst).run("cc")
     assert all(r[1] == ref.iterations and r[2] == ref.converged for r in res)
     np.testing.assert_array_equal(got, ref.attrs[:, 0])
+
+
+class DenseNumpyPartition(AsyncNumpyPartition):
+    """Adds the dense mirror exchange surface: the next-value replica (GXB_BUF_VALUES_NEXT,
+    owned block = current values) all-gathered in place, then dense_install."""
+
+    dense_rounds = 0
+
+    def buffer(self, which):
+        if which == L.BUF_VALUES_NEXT:
+            self.nxt = self.label.astype(np.uint32)
+            return self._ptr(self.nxt), self.nxt.nbytes
+        return super().buffer(which)
+
+    def dense_install(self):
+        self.dense_rounds += 1
+        for slot in range(self.V):
+            if self.lo <= slot < self.hi:
+                continue
+            if self.nxt[slot] != self.label[slot]:
+                self.label[slot] = self.nxt[slot]
+                self.active[slot] = True
+
+
+@pytest.mark.timeout(300)
+def test_cc_dense_mirror_exchange_matches_oracle(oracle_lib):
+    """Rounds after one that changed most vertices exchange whole value blocks (in-place
+    all-gather of the next-value replica + install of the changed mirrors); the rest use
+    records — same labels and iteration count as the oracle."""
+    rng = np.random.default_rng(5)
+    n = 512  # every vertex present, V divisible by the 2 ranks: equal blocks
+    a = np.concatenate([np.arange(n), rng.integers(0, n, 3 * n)]).astype(np.uint32)
+    b = np.concatenate([(np.arange(n) + 1) % n, rng.integers(0, n, 3 * n)]).astype(np.uint32)
+    src, dst = np.concatenate([a, b]), np.concatenate([b, a])
+    res, got = _run("cc", src, dst, 1000, cls=DenseNumpyPartition)
+    ref = oracle_lib.OracleGraph(src, dst).run("cc")
+    assert all(r[1] == ref.iterations and r[2] == ref.converged for r in res)
+    np.testing.assert_array_equal(got, ref.attrs[:, 0])
+    assert all(r[8] > 0 for r in res)  # the dense exchange really ran
 
 
 class CapacityNumpyPartition(NumpyPartition):
