@@ -467,7 +467,7 @@ def main():
                     help="time the unmodified reference Engine with the B200 daemon dropped in (PageRank, "
                          "--scale default 18, --partitions)")
     ap.add_argument("--partitions", type=int, default=1)
-    ap.add_argument("--dense-frac", type=float, default=0.25,
+    ap.add_argument("--dense-frac", type=float, default=0.0,
                     help="SSSP/CC/LP at N>1: dense mirror exchange after rounds changing this slot fraction (0 = off)")
     args = ap.parse_args()
     # stdout carries exactly one JSON line: library banners (NCCL prints its version when a

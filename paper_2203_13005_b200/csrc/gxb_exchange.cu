@@ -58,30 +58,47 @@ __global__ void k_pack(int algo, const uint32_t* __restrict__ list, const unsign
     }
 }
 
+// kDedupe: a record may name a vertex already in the frontier (re-sent after an install, a
+// delivered mirror): list it once. The per-peer path receives each changed vertex once per
+// round from its single owner and none of them is in the (own-slot) frontier yet: it sets
+// the active bit with a fire-and-forget OR and writes only the current value (a mirror's
+// next value is never read: pull and push rounds write next only for owned slots).
+template <bool kDedupe>
 __global__ void k_unpack(int algo, const uint32_t* __restrict__ rec, uint64_t n, uint64_t lo, uint64_t hi,
                          uint4* dist_cur, uint4* dist_next, uint32_t* lab_cur, uint32_t* lab_next, uint32_t* active,
                          uint32_t* list, unsigned long long* count, const uint32_t* __restrict__ outdeg,
                          unsigned long long* units) {
+    __shared__ uint32_t stage_all[kBlock / 32][32 * 5];
     const int W = record_words(algo);
     const int lane = threadIdx.x & 31;
+    uint32_t* stage = stage_all[threadIdx.x >> 5];
     unsigned long long u = 0;
     for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < n;
          i0 += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t i = i0 + lane;
-        const uint32_t* r = rec + i * W;
+        // the warp's 32 records are contiguous: load them with consecutive lanes on
+        // consecutive words, then each lane reads its own from shared memory
+        const uint32_t words = (uint32_t)min((uint64_t)32, n - i0) * (uint32_t)W;
+        __syncwarp();
+        for (uint32_t k = lane; k < words; k += 32) stage[k] = rec[i0 * W + k];
+        __syncwarp();
+        const uint32_t* r = stage + lane * W;
         const uint32_t s = i < n ? r[0] : lo;
         bool take = i < n && (s < lo || s >= hi);  // skip own records echoed back by the all-gather
         if (take) {
             if (algo == GXB_ALGO_SSSP) {
                 const uint4 d = make_uint4(r[1], r[2], r[3], r[4]);
                 dist_cur[s] = d;
-                dist_next[s] = d;
+                if (kDedupe) dist_next[s] = d;
             } else {
                 lab_cur[s] = r[1];
-                lab_next[s] = r[1];
+                if (kDedupe) lab_next[s] = r[1];
             }
-            // a vertex already in the frontier (e.g. re-sent after an install) is listed once
-            take = bit_set_atomic(active, s);
+            if (kDedupe) {
+                take = bit_set_atomic(active, s);  // listed once
+            } else {
+                atomicOr(active + (s >> 5), 1u << (s & 31));  // result unused: a reduction
+            }
             if (take) u += outdeg[s];
         }
         const unsigned m = __ballot_sync(0xffffffffu, take);
@@ -156,46 +173,84 @@ struct PeerArenas {
 };
 
 // the closed round's changed owned slots (frontier list, own first) -> a record in the arena
-// of every peer that reads the slot; one reservation per (warp, peer)
-__global__ void k_pack_peers(int algo, const uint32_t* __restrict__ list, const unsigned long long* count, uint64_t lo,
-                             uint64_t hi, const uint32_t* __restrict__ need, const uint4* __restrict__ dist,
-                             const uint32_t* __restrict__ lab, int nparts, const PeerArenas A,
-                             unsigned long long* peer_cnt) {
+// of every peer that reads the slot. A block takes kPackPer x kBlock list entries per step;
+// the per-peer record positions come from one atomicAdd per (block step, peer) plus
+// shared-memory prefixes over the warps (per-warp reservations on a handful of counters
+// serialised in L2). A warp's records for one peer are one contiguous run: staged in shared
+// memory and stored with consecutive lanes on consecutive words (whole lines over NVLink).
+constexpr int kPackPer = 4;
+
+__global__ void __launch_bounds__(kBlock) k_pack_peers(int algo, const uint32_t* __restrict__ list,
+                                                        const unsigned long long* count, uint64_t lo, uint64_t hi,
+                                                        const uint32_t* __restrict__ need,
+                                                        const uint4* __restrict__ dist,
+                                                        const uint32_t* __restrict__ lab, int nparts,
+                                                        const PeerArenas A, unsigned long long* peer_cnt) {
+    constexpr int kWarps = kBlock / 32;
+    __shared__ uint32_t stage_all[kWarps][32 * 5];
+    __shared__ uint32_t wcnt[kWarps][kMaxPeers + 1];
+    __shared__ unsigned long long bbase[kMaxPeers + 1];
     const uint64_t n = *count;
     const int W = record_words(algo);
-    const int lane = threadIdx.x & 31;
-    for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < n;
-         i0 += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = i0 + lane;
-        const uint32_t s = i < n ? list[i] : 0u;
-        const bool mine = i < n && s >= lo && s < hi;
-        const uint32_t m = mine ? __ldg(need + (s - lo)) : 0u;
-        if (!__any_sync(0xffffffffu, m != 0u)) continue;
-        uint32_t v[4] = {0u, 0u, 0u, 0u};
-        if (m) {
-            if (algo == GXB_ALGO_SSSP) {
-                const uint4 d = dist[s];
-                v[0] = d.x; v[1] = d.y; v[2] = d.z; v[3] = d.w;
-            } else {
-                v[0] = lab[s];
-            }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* stage = stage_all[warp];
+    for (uint64_t t0 = (uint64_t)blockIdx.x * kPackPer * kBlock; t0 < n; t0 += (uint64_t)gridDim.x * kPackPer * kBlock) {
+        // this warp's kPackPer groups of 32 consecutive list entries
+        uint32_t sl[kPackPer], m[kPackPer];
+#pragma unroll
+        for (int j = 0; j < kPackPer; ++j) {
+            const uint64_t i = t0 + ((uint64_t)warp * kPackPer + j) * 32 + lane;
+            sl[j] = i < n ? list[i] : 0u;
+            const bool mine = i < n && sl[j] >= lo && sl[j] < hi;
+            m[j] = mine ? __ldg(need + (sl[j] - lo)) : 0u;
         }
         for (int q = 0; q < nparts; ++q) {
-            const bool to_q = (m >> q) & 1u;
-            const unsigned b = __ballot_sync(0xffffffffu, to_q);
-            if (!b) continue;
-            unsigned long long base = 0;
-            if (lane == __ffs(b) - 1) base = atomicAdd(peer_cnt + q, (unsigned long long)__popc(b));
-            base = __shfl_sync(0xffffffffu, base, __ffs(b) - 1);
-            if (!to_q) continue;
-            uint32_t* r = A.arena[q] + A.base[q] + (base + __popc(b & ((1u << lane) - 1u))) * W;
-            r[0] = s;
-            for (int j = 1; j < W; ++j) r[j] = v[j - 1];
+            uint32_t c = 0;
+#pragma unroll
+            for (int j = 0; j < kPackPer; ++j) c += __popc(__ballot_sync(0xffffffffu, (m[j] >> q) & 1u));
+            if (lane == 0) wcnt[warp][q] = c;
         }
+        __syncthreads();
+        if (threadIdx.x < nparts) {  // block total per peer -> one reservation; warp prefixes in place
+            const int q = threadIdx.x;
+            uint32_t acc = 0;
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t c = wcnt[w][q];
+                wcnt[w][q] = acc;
+                acc += c;
+            }
+            bbase[q] = acc ? atomicAdd(peer_cnt + q, (unsigned long long)acc) : 0ull;
+        }
+        __syncthreads();
+        for (int q = 0; q < nparts; ++q) {
+            unsigned long long base = bbase[q] + wcnt[warp][q];
+#pragma unroll
+            for (int j = 0; j < kPackPer; ++j) {
+                const bool to_q = (m[j] >> q) & 1u;
+                const unsigned b = __ballot_sync(0xffffffffu, to_q);
+                if (!b) continue;
+                if (to_q) {
+                    uint32_t* r = stage + __popc(b & ((1u << lane) - 1u)) * W;
+                    r[0] = sl[j];
+                    if (algo == GXB_ALGO_SSSP) {
+                        const uint4 d = dist[sl[j]];
+                        r[1] = d.x; r[2] = d.y; r[3] = d.z; r[4] = d.w;
+                    } else {
+                        r[1] = lab[sl[j]];
+                    }
+                }
+                __syncwarp();
+                const uint32_t words = (uint32_t)__popc(b) * (uint32_t)W;
+                uint32_t* dst = A.arena[q] + A.base[q] + base * W;
+                for (uint32_t k = lane; k < words; k += 32) dst[k] = stage[k];
+                base += __popc(b);
+                __syncwarp();
+            }
+        }
+        __syncthreads();  // wcnt / bbase are rewritten by the next step
     }
     // one cumulative system-scope fence per block after a barrier (not one per thread): the
     // block's records are visible to the peers before the vote collective
-    __syncthreads();
     if (threadIdx.x == 0) __threadfence_system();
 }
 
@@ -483,7 +538,7 @@ int gxb_exchange_unpack_regions(gxb_state* s, const void* d_records, const uint6
         if (counts[q] > block_records) return fail(GXB_EINVAL, "gxb_exchange_unpack_regions: count exceeds the block");
         if (!d_records) return fail(GXB_EINVAL, "gxb_exchange_unpack_regions: null records");
         const uint32_t* rec = (const uint32_t*)d_records + (uint64_t)q * block_records * W;
-        k_unpack<<<grid_for(counts[q]), kBlock, 0, st>>>(s->algo, rec, counts[q], g->lo, g->hi, s->d_dist_cur,
+        k_unpack<true><<<grid_for(counts[q]), kBlock, 0, st>>>(s->algo, rec, counts[q], g->lo, g->hi, s->d_dist_cur,
                                                          s->d_dist_next, s->d_lab_cur, s->d_lab_next, s->d_active[0],
                                                          s->d_frontier[0], s->d_fcount, g->d_outdeg, s->d_xscratch + 1);
         s->launches++;
@@ -514,7 +569,7 @@ int gxb_exchange_unpack(gxb_state* s, const void* d_records, uint64_t count, voi
     GXB_CHECK(state_settle(s));  // the closed round's frontier first, then the records on top
     unsigned long long* d_units = reinterpret_cast<unsigned long long*>(s->d_fcount) + 1;
     GXB_CUDA(cudaMemsetAsync(d_units, 0, 8, st));
-    k_unpack<<<grid_for(count), kBlock, 0, st>>>(s->algo, (const uint32_t*)d_records, count, g->lo, g->hi,
+    k_unpack<true><<<grid_for(count), kBlock, 0, st>>>(s->algo, (const uint32_t*)d_records, count, g->lo, g->hi,
                                                  s->d_dist_cur, s->d_dist_next, s->d_lab_cur, s->d_lab_next,
                                                  s->d_active[0], s->d_frontier[0], s->d_fcount, g->d_outdeg, d_units);
     GXB_CUDA(cudaGetLastError());
@@ -709,7 +764,7 @@ int gxb_exchange_delta_pack(gxb_state* s, double* d_vote, void* stream) {
         A.base[q] = s->peer_base[q][s->delta_parity];
     }
     GXB_CUDA(cudaMemsetAsync(s->d_peer_cnt, 0, 8 * (kMaxPeers + 1), st));
-    k_pack_peers<<<grid_for(std::max<uint64_t>(1, g->hi - g->lo)), kBlock, 0, st>>>(
+    k_pack_peers<<<grid_for(std::max<uint64_t>(1, (g->hi - g->lo) / kPackPer)), kBlock, 0, st>>>(
         s->algo, s->d_frontier[0], s->d_fcount, g->lo, g->hi, s->d_need, s->d_dist_cur, s->d_lab_cur, g->nparts, A,
         s->d_peer_cnt);
     k_peer_counts<<<1, 32, 0, st>>>(s->d_peer_cnt, g->nparts, d_vote);
@@ -731,7 +786,7 @@ int gxb_exchange_delta_unpack(gxb_state* s, const uint64_t* counts_from, void* s
     for (int p = 0; p < g->nparts; ++p) {
         if (p == g->part || !counts_from[p]) continue;
         if (counts_from[p] > s->peer_recv_cap[p]) return fail(GXB_EINVAL, "gxb_exchange_delta_unpack: count exceeds the block");
-        k_unpack<<<grid_for(counts_from[p]), kBlock, 0, st>>>(s->algo, s->d_arena + s->arena_base[p][par], counts_from[p],
+        k_unpack<false><<<grid_for(counts_from[p]), kBlock, 0, st>>>(s->algo, s->d_arena + s->arena_base[p][par], counts_from[p],
                                                               g->lo, g->hi, s->d_dist_cur, s->d_dist_next, s->d_lab_cur,
                                                               s->d_lab_next, s->d_active[0], s->d_frontier[0], s->d_fcount,
                                                               g->d_outdeg, s->d_xscratch + 1);

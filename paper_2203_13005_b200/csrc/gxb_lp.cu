@@ -295,6 +295,7 @@ constexpr uint32_t kLpCtaMinDeg = 512;
 constexpr uint32_t kLpBigDeg = 4096;  // above: chunked warps over all SMs + global tables (label-diverse hubs)
 constexpr int kLpCtaCap = 8192;    // 64 KB of (key, count) per CTA
 constexpr int kLpWarpCap = 1024;   // 8 KB per warp
+constexpr int kLpWarpMinBin = 4;   // group bins >= this (G = 16, 32: in-degree 33-128) use warp tables
 
 __global__ void k_lp_eff(const uint32_t* __restrict__ active, const uint32_t* __restrict__ lab, uint64_t S,
                          uint32_t* eff) {
@@ -804,20 +805,28 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
                                           (kBlock / 32) * 2 * 4 * kLpWarpCap));
             attrs_set[dev] = true;
         }
-        // chunk items of the big hubs only (the plan lists items in slot order) + group bins
+        // chunk items of the big hubs only (the plan lists items in slot order) + group bins;
+        // the G = 32 and G = 16 bins (in-degree 33-128) go to the warp tables below instead of
+        // the quadratic in-group count
         grid -= L.chunk_blocks;
         L.num_items = S->big_items;
         L.chunk_blocks = (unsigned)((S->big_items + (kBlock / 32) - 1) / (kBlock / 32));
         grid += L.chunk_blocks;
+        uint64_t warp_end = S->chunk_end;
+        for (int k = kNumGroupBins - 1; k >= kLpWarpMinBin; --k) {
+            warp_end = std::max(warp_end, L.bin_hi[k]);
+            grid -= L.bin_blocks[k];
+            L.bin_blocks[k] = 0;
+        }
         if (grid) k_lp_pull<<<grid, kBlock, 0, st>>>(L);
         if (S->cta_end > S->big_end) {
             const unsigned gc = (unsigned)std::min<uint64_t>(S->cta_end - S->big_end, 3ull * kNumSMs);
             k_lp_hub_cta<<<gc, kBlock, 2 * 4 * kLpCtaCap, st>>>(L, S->big_end, S->cta_end);
         }
-        if (S->chunk_end > S->cta_end) {
-            const uint64_t n = S->chunk_end - S->cta_end;
+        if (warp_end > S->cta_end) {
+            const uint64_t n = warp_end - S->cta_end;
             const unsigned gw = (unsigned)std::min<uint64_t>((n + kBlock / 32 - 1) / (kBlock / 32), 6ull * kNumSMs);
-            k_lp_hub_warp<<<gw, kBlock, (kBlock / 32) * 2 * 4 * kLpWarpCap, st>>>(L, S->cta_end, S->chunk_end);
+            k_lp_hub_warp<<<gw, kBlock, (kBlock / 32) * 2 * 4 * kLpWarpCap, st>>>(L, S->cta_end, warp_end);
         }
         if (S->big_end) k_lp_hub_apply<<<grid_for(S->big_end), kBlock, 0, st>>>(L, S->big_end);
         s->launches += 3;  // + the caller's 2: eff, chunks + groups, CTA hubs, warp hubs, hub apply

@@ -173,9 +173,11 @@ class PartitionedRun:
     sparse_ratio: float = 0.8         # ... when that is below this fraction of the dense volume
     peer_writes: bool = True          # PR: Apply stores new contributions into the peers' replicas over
                                       # NVLink (IPC-mapped), fusing the exchange into the kernel
-    dense_frac: float = 0.25          # SSSP / CC / LP: a round after one that changed >= this fraction
+    dense_frac: float = 0.0           # SSSP / CC / LP: a round after one that changed >= this fraction
                                       # of the slots exchanges whole value blocks (all-gather in place +
                                       # install of the changed mirrors) instead of records; 0 = never
+                                      # (measured slower than the per-peer records: SSSP S26 at N = 4
+                                      # 802 vs 929 GTEPS — records move only changed and needed values)
     peer_delta: bool = True           # SSSP / CC / LP: the pack kernel stores each changed value only
                                       # into the arenas of the peers that read it (IPC, NVLink)
     overlap: bool = False             # pipeline shuffle: chunked PR rounds with the exchange overlapped
@@ -481,6 +483,7 @@ class PartitionedRun:
             moved_early = self._overlapped_pagerank_round()
         else:
             self.state.iterate(direction, **self._on_stream())
+        t0 = self._tick("iterate", t0)
         device_vote = (self.comm.world > 1 and hasattr(self.state, "stats_device")
                        and hasattr(self.comm, "vote_start_device"))
         dpeers = device_vote and self.algo != "pagerank" and self._setup_delta_peers()
@@ -504,6 +507,7 @@ class PartitionedRun:
                 self.state.delta_pack(self._vote_buf, **self._on_stream())
             elif async_delta:
                 self.state.pack_async(**self._on_stream())
+            t0 = self._tick("pack", t0)
             self.state.stats_device(self._vote_buf, **self._on_stream())
             handle = self.comm.vote_start_device(self._vote_buf)
             st = None
