@@ -789,53 +789,52 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
     }
     L.hub = S->hub;
     L.injective = s->lab_injective;
+    static bool attrs_set[64] = {};
+    const int dev = g->ctx->device & 63;
+    if (!attrs_set[dev]) {
+        GXB_CUDA(cudaFuncSetAttribute(k_lp_hub_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4 * kLpCtaCap));
+        GXB_CUDA(cudaFuncSetAttribute(k_lp_hub_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (kBlock / 32) * 2 * 4 * kLpWarpCap));
+        attrs_set[dev] = true;
+    }
+    // effective labels: one gather per edge (label of an active source, else empty)
+    if (g->S) k_lp_eff<<<grid_for(g->S), kBlock, 0, st>>>(s->d_active[0], s->d_lab_cur, g->S, S->eff);
+    L.eff = S->eff;
+    // rounds >= 2: the G = 32 and G = 16 bins (in-degree 33-128) are counted in warp shared
+    // tables instead of the quadratic in-group count (round 1's labels are all distinct, where
+    // the in-group count is cheaper: measured)
+    uint64_t warp_end = S->chunk_end;
+    for (int k = kNumGroupBins - 1; k >= kLpWarpMinBin && !L.injective; --k) {
+        warp_end = std::max(warp_end, L.bin_hi[k]);
+        grid -= L.bin_blocks[k];
+        L.bin_blocks[k] = 0;
+    }
+    uint64_t warp_lo = S->chunk_end;  // round 1: the chunked hubs are run-length counted
     if (!L.injective) {
-        // rounds >= 2: effective labels, hubs counted in shared memory by CTAs / warps, then
-        // the small destinations by the group bins (no chunk items, no hub apply pass)
-        const uint64_t S_ = g->S;
-        if (S_) k_lp_eff<<<grid_for(S_), kBlock, 0, st>>>(s->d_active[0], s->d_lab_cur, S_, S->eff);
-        L.eff = S->eff;
+        // rounds >= 2: chunk items of the label-diverse big hubs only (the plan lists items
+        // in slot order; epoch-tagged global tables), CTA tables for 513-4096, warp tables
+        // for 33-512
         L.hub.epoch = ++S->hub.epoch;  // this round's table words (older ones read as empty)
-        static bool attrs_set[64] = {};
-        const int dev = g->ctx->device & 63;
-        if (!attrs_set[dev]) {
-            GXB_CUDA(cudaFuncSetAttribute(k_lp_hub_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          2 * 4 * kLpCtaCap));
-            GXB_CUDA(cudaFuncSetAttribute(k_lp_hub_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (kBlock / 32) * 2 * 4 * kLpWarpCap));
-            attrs_set[dev] = true;
-        }
-        // chunk items of the big hubs only (the plan lists items in slot order) + group bins;
-        // the G = 32 and G = 16 bins (in-degree 33-128) go to the warp tables below instead of
-        // the quadratic in-group count
         grid -= L.chunk_blocks;
         L.num_items = S->big_items;
         L.chunk_blocks = (unsigned)((S->big_items + (kBlock / 32) - 1) / (kBlock / 32));
         grid += L.chunk_blocks;
-        uint64_t warp_end = S->chunk_end;
-        for (int k = kNumGroupBins - 1; k >= kLpWarpMinBin; --k) {
-            warp_end = std::max(warp_end, L.bin_hi[k]);
-            grid -= L.bin_blocks[k];
-            L.bin_blocks[k] = 0;
-        }
-        if (grid) k_lp_pull<<<grid, kBlock, 0, st>>>(L);
-        if (S->cta_end > S->big_end) {
-            const unsigned gc = (unsigned)std::min<uint64_t>(S->cta_end - S->big_end, 3ull * kNumSMs);
-            k_lp_hub_cta<<<gc, kBlock, 2 * 4 * kLpCtaCap, st>>>(L, S->big_end, S->cta_end);
-        }
-        if (warp_end > S->cta_end) {
-            const uint64_t n = warp_end - S->cta_end;
-            const unsigned gw = (unsigned)std::min<uint64_t>((n + kBlock / 32 - 1) / (kBlock / 32), 6ull * kNumSMs);
-            k_lp_hub_warp<<<gw, kBlock, (kBlock / 32) * 2 * 4 * kLpWarpCap, st>>>(L, S->cta_end, warp_end);
-        }
-        if (S->big_end) k_lp_hub_apply<<<grid_for(S->big_end), kBlock, 0, st>>>(L, S->big_end);
-        s->launches += 3;  // + the caller's 2: eff, chunks + groups, CTA hubs, warp hubs, hub apply
-        GXB_CUDA(cudaGetLastError());
-        return GXB_OK;
+        warp_lo = S->cta_end;
     }
     if (grid) k_lp_pull<<<grid, kBlock, 0, st>>>(L);
-    // round 1 (run-length counting, no tables): every chunked slot applied from its argmax
-    if (S->chunk_end) k_lp_hub_apply<<<grid_for(S->chunk_end), kBlock, 0, st>>>(L, S->chunk_end);
+    if (!L.injective && S->cta_end > S->big_end) {
+        const unsigned gc = (unsigned)std::min<uint64_t>(S->cta_end - S->big_end, 3ull * kNumSMs);
+        k_lp_hub_cta<<<gc, kBlock, 2 * 4 * kLpCtaCap, st>>>(L, S->big_end, S->cta_end);
+    }
+    if (warp_end > warp_lo) {
+        const uint64_t n = warp_end - warp_lo;
+        const unsigned gw = (unsigned)std::min<uint64_t>((n + kBlock / 32 - 1) / (kBlock / 32), 6ull * kNumSMs);
+        k_lp_hub_warp<<<gw, kBlock, (kBlock / 32) * 2 * 4 * kLpWarpCap, st>>>(L, warp_lo, warp_end);
+    }
+    // slots counted by chunk items: applied from their packed argmax
+    const uint64_t applied = L.injective ? S->chunk_end : S->big_end;
+    if (applied) k_lp_hub_apply<<<grid_for(applied), kBlock, 0, st>>>(L, applied);
+    s->launches += 3;  // + the caller's 2: eff, chunks + groups, CTA hubs, warp hubs, hub apply
     GXB_CUDA(cudaGetLastError());
     return GXB_OK;
 }
