@@ -302,3 +302,36 @@ def test_options_roundtrip():
         L.set_option("no_such_knob", 1)
     with pytest.raises(ValueError):
         L.set_option("tile_minblocks", 3)
+
+
+# ---------------------------------------------------------------- device weight encoding
+def test_validate_weights_dyadic_scaling():
+    """Integral weights keep shift 0; dyadic rationals scale exactly by the smallest 2^k;
+    anything inexact or out of range raises (device.validate_weights)."""
+    from paper_2203_13005_b200.device import validate_weights
+    w, k = validate_weights(np.array([1.0, 2.0, 63.0]))
+    assert k == 0 and w.dtype == np.uint32 and w.tolist() == [1, 2, 63]
+    w, k = validate_weights(np.array([2.5, 0.25, 1.0]))
+    assert k == 2 and w.tolist() == [10, 1, 4]
+    assert np.array_equal(np.ldexp(w.astype(np.float64), -k), [2.5, 0.25, 1.0])
+    w, k = validate_weights(np.array([3, 4], dtype=np.int64))
+    assert k == 0 and w.tolist() == [3, 4]
+    assert validate_weights(None) == (None, 0)
+    for bad in ([1e-3], [0.1, 1.0], [-1.0], [np.inf], [np.nan]):
+        with pytest.raises(ValueError):
+            validate_weights(np.array(bad))
+    with pytest.raises(ValueError):  # exact, but sums over |V| vertices could reach 2^32 - 1
+        validate_weights(np.array([2.0 ** 30 + 0.5]), num_vertices=8)
+    with pytest.raises(ValueError):
+        validate_weights(np.array([-3], dtype=np.int64))
+
+
+def test_engine_config_validation():
+    from paper_2203_13005_b200.engine import RunConfig, convergence_vote, EngineError
+    with pytest.raises(ValueError):
+        RunConfig(partitions=0)
+    with pytest.raises(ValueError):
+        RunConfig(block_size=0)
+    assert convergence_vote([True, True]) and not convergence_vote([True, False])
+    with pytest.raises(EngineError, match="missing convergence vote"):
+        convergence_vote([True, None])
