@@ -255,3 +255,21 @@ def test_reference_cli_sources_and_float_weights(tmp_path):
         rc, out = _cli(argv)
     assert rc == rc_ref == 0 and out == out_ref
     assert ".5" in out
+
+
+@pytest.mark.parametrize("algo_name", ["sssp", "pagerank", "lp", "cc"])
+@pytest.mark.parametrize("model", ["bsp", "gas"])
+def test_reference_engine_cache_and_auto_blocks(algo_name, model):
+    """RunConfig(enable_cache=True, block_size="auto") on three partitions: the lazy upload
+    serves dirty and queried values, the rest is flushed at the end (A/agent.py:550-611);
+    attributes equal the reference's own run of the same configuration."""
+    from accelgraph.engine import RunConfig, run
+    cfg = dict(partitions=3, enable_cache=True, cache_capacity=8, block_size="auto", enable_skip=True)
+    graph, vertices, _, _ = _ref_graph("gen_random40", 3)
+    want, wmet = run(graph, _algo(algo_name, vertices, graph), model, RunConfig(**cfg))
+    graph, vertices, _, _ = _ref_graph("gen_random40", 3)
+    with ag.installed(fused=algo_name != "sssp"):
+        got, met = run(graph, _algo(algo_name, vertices, graph), model, RunConfig(**cfg))
+    _close(got, want, algo_name)
+    assert met.iterations == wmet.iterations and met.converged == wmet.converged
+    assert met.skipped_rounds == wmet.skipped_rounds and met.protocol_conformant()
