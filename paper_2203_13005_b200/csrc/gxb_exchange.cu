@@ -58,58 +58,97 @@ __global__ void k_pack(int algo, const uint32_t* __restrict__ list, const unsign
     }
 }
 
+constexpr int kUnpackPer = 4;
+
 // kDedupe: a record may name a vertex already in the frontier (re-sent after an install, a
 // delivered mirror): list it once. The per-peer path receives each changed vertex once per
 // round from its single owner and none of them is in the (own-slot) frontier yet: it sets
 // the active bit with a fire-and-forget OR and writes only the current value (a mirror's
 // next value is never read: pull and push rounds write next only for owned slots).
 template <bool kDedupe>
-__global__ void k_unpack(int algo, const uint32_t* __restrict__ rec, uint64_t n, uint64_t lo, uint64_t hi,
-                         uint4* dist_cur, uint4* dist_next, uint32_t* lab_cur, uint32_t* lab_next, uint32_t* active,
-                         uint32_t* list, unsigned long long* count, const uint32_t* __restrict__ outdeg,
-                         unsigned long long* units) {
-    __shared__ uint32_t stage_all[kBlock / 32][32 * 5];
+__global__ void __launch_bounds__(kBlock) k_unpack(int algo, const uint32_t* __restrict__ rec, uint64_t n,
+                                                   uint64_t lo, uint64_t hi, uint4* dist_cur, uint4* dist_next,
+                                                   uint32_t* lab_cur, uint32_t* lab_next, uint32_t* active,
+                                                   uint32_t* list, unsigned long long* count,
+                                                   const uint32_t* __restrict__ outdeg, unsigned long long* units) {
+    // A block takes kUnpackPer x kBlock records per step. The frontier slots of the step are
+    // reserved with one atomicAdd per block (warp prefixes in shared memory) — a reservation
+    // per warp on the single frontier counter serialises in L2 at millions of records.
+    constexpr int kWarps = kBlock / 32;
+    __shared__ uint32_t stage_all[kWarps][32 * 5];
+    __shared__ uint32_t wcnt[kWarps];
+    __shared__ unsigned long long bbase;
+    __shared__ unsigned long long bunits[kWarps];
     const int W = record_words(algo);
-    const int lane = threadIdx.x & 31;
-    uint32_t* stage = stage_all[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* stage = stage_all[warp];
     unsigned long long u = 0;
-    for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < n;
-         i0 += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = i0 + lane;
-        // the warp's 32 records are contiguous: load them with consecutive lanes on
-        // consecutive words, then each lane reads its own from shared memory
-        const uint32_t words = (uint32_t)min((uint64_t)32, n - i0) * (uint32_t)W;
-        __syncwarp();
-        for (uint32_t k = lane; k < words; k += 32) stage[k] = rec[i0 * W + k];
-        __syncwarp();
-        const uint32_t* r = stage + lane * W;
-        const uint32_t s = i < n ? r[0] : lo;
-        bool take = i < n && (s < lo || s >= hi);  // skip own records echoed back by the all-gather
-        if (take) {
-            if (algo == GXB_ALGO_SSSP) {
-                const uint4 d = make_uint4(r[1], r[2], r[3], r[4]);
-                dist_cur[s] = d;
-                if (kDedupe) dist_next[s] = d;
-            } else {
-                lab_cur[s] = r[1];
-                if (kDedupe) lab_next[s] = r[1];
+    for (uint64_t t0 = (uint64_t)blockIdx.x * kUnpackPer * kBlock; t0 < n;
+         t0 += (uint64_t)gridDim.x * kUnpackPer * kBlock) {
+        uint32_t slot[kUnpackPer];
+        unsigned m[kUnpackPer];
+        uint32_t c = 0;
+#pragma unroll
+        for (int j = 0; j < kUnpackPer; ++j) {
+            const uint64_t g0 = t0 + ((uint64_t)warp * kUnpackPer + j) * 32;  // this group's first record
+            const uint64_t i = g0 + lane;
+            // the group's 32 records are contiguous: load them with consecutive lanes on
+            // consecutive words, then each lane reads its own from shared memory
+            const uint32_t words = g0 < n ? (uint32_t)min((uint64_t)32, n - g0) * (uint32_t)W : 0u;
+            for (uint32_t k = lane; k < words; k += 32) stage[k] = rec[g0 * W + k];
+            __syncwarp();
+            const uint32_t* r = stage + lane * W;
+            const uint32_t s = i < n ? r[0] : lo;
+            bool take = i < n && (s < lo || s >= hi);  // skip own records echoed back by an all-gather
+            if (take) {
+                if (algo == GXB_ALGO_SSSP) {
+                    const uint4 d = make_uint4(r[1], r[2], r[3], r[4]);
+                    dist_cur[s] = d;
+                    if (kDedupe) dist_next[s] = d;
+                } else {
+                    lab_cur[s] = r[1];
+                    if (kDedupe) lab_next[s] = r[1];
+                }
+                if (kDedupe) {
+                    take = bit_set_atomic(active, s);  // listed once
+                } else {
+                    atomicOr(active + (s >> 5), 1u << (s & 31));  // result unused: a reduction
+                }
+                if (take) u += outdeg[s];
             }
-            if (kDedupe) {
-                take = bit_set_atomic(active, s);  // listed once
-            } else {
-                atomicOr(active + (s >> 5), 1u << (s & 31));  // result unused: a reduction
-            }
-            if (take) u += outdeg[s];
+            __syncwarp();  // the stage is reloaded by the next group
+            slot[j] = s;
+            m[j] = __ballot_sync(0xffffffffu, take);
+            c += __popc(m[j]);
         }
-        const unsigned m = __ballot_sync(0xffffffffu, take);
-        if (!m) continue;
-        unsigned long long base = 0;
-        if (lane == __ffs(m) - 1) base = atomicAdd(count, (unsigned long long)__popc(m));
-        base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-        if (take) list[base + __popc(m & ((1u << lane) - 1u))] = s;
+        if (lane == 0) wcnt[warp] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t acc = 0;
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t x = wcnt[w];
+                wcnt[w] = acc;
+                acc += x;
+            }
+            bbase = acc ? atomicAdd(count, (unsigned long long)acc) : 0ull;
+        }
+        __syncthreads();
+        unsigned long long base = bbase + wcnt[warp];
+#pragma unroll
+        for (int j = 0; j < kUnpackPer; ++j) {
+            if ((m[j] >> lane) & 1u) list[base + __popc(m[j] & ((1u << lane) - 1u))] = slot[j];
+            base += __popc(m[j]);
+        }
+        __syncthreads();  // wcnt / bbase are rewritten by the next step
     }
     for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
-    if (lane == 0 && u) atomicAdd(units, u);
+    if (lane == 0) bunits[warp] = u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < kWarps; ++w) t += bunits[w];
+        if (t) atomicAdd(units, t);
+    }
 }
 
 // the sync round's deliver (A/agent.py:584-592) from host values: (dense index, value) pairs
@@ -538,7 +577,7 @@ int gxb_exchange_unpack_regions(gxb_state* s, const void* d_records, const uint6
         if (counts[q] > block_records) return fail(GXB_EINVAL, "gxb_exchange_unpack_regions: count exceeds the block");
         if (!d_records) return fail(GXB_EINVAL, "gxb_exchange_unpack_regions: null records");
         const uint32_t* rec = (const uint32_t*)d_records + (uint64_t)q * block_records * W;
-        k_unpack<true><<<grid_for(counts[q]), kBlock, 0, st>>>(s->algo, rec, counts[q], g->lo, g->hi, s->d_dist_cur,
+        k_unpack<true><<<grid_for((counts[q] + kUnpackPer - 1) / kUnpackPer), kBlock, 0, st>>>(s->algo, rec, counts[q], g->lo, g->hi, s->d_dist_cur,
                                                          s->d_dist_next, s->d_lab_cur, s->d_lab_next, s->d_active[0],
                                                          s->d_frontier[0], s->d_fcount, g->d_outdeg, s->d_xscratch + 1);
         s->launches++;
@@ -569,7 +608,7 @@ int gxb_exchange_unpack(gxb_state* s, const void* d_records, uint64_t count, voi
     GXB_CHECK(state_settle(s));  // the closed round's frontier first, then the records on top
     unsigned long long* d_units = reinterpret_cast<unsigned long long*>(s->d_fcount) + 1;
     GXB_CUDA(cudaMemsetAsync(d_units, 0, 8, st));
-    k_unpack<true><<<grid_for(count), kBlock, 0, st>>>(s->algo, (const uint32_t*)d_records, count, g->lo, g->hi,
+    k_unpack<true><<<grid_for((count + kUnpackPer - 1) / kUnpackPer), kBlock, 0, st>>>(s->algo, (const uint32_t*)d_records, count, g->lo, g->hi,
                                                  s->d_dist_cur, s->d_dist_next, s->d_lab_cur, s->d_lab_next,
                                                  s->d_active[0], s->d_frontier[0], s->d_fcount, g->d_outdeg, d_units);
     GXB_CUDA(cudaGetLastError());
@@ -786,7 +825,7 @@ int gxb_exchange_delta_unpack(gxb_state* s, const uint64_t* counts_from, void* s
     for (int p = 0; p < g->nparts; ++p) {
         if (p == g->part || !counts_from[p]) continue;
         if (counts_from[p] > s->peer_recv_cap[p]) return fail(GXB_EINVAL, "gxb_exchange_delta_unpack: count exceeds the block");
-        k_unpack<false><<<grid_for(counts_from[p]), kBlock, 0, st>>>(s->algo, s->d_arena + s->arena_base[p][par], counts_from[p],
+        k_unpack<false><<<grid_for((counts_from[p] + kUnpackPer - 1) / kUnpackPer), kBlock, 0, st>>>(s->algo, s->d_arena + s->arena_base[p][par], counts_from[p],
                                                               g->lo, g->hi, s->d_dist_cur, s->d_dist_next, s->d_lab_cur,
                                                               s->d_lab_next, s->d_active[0], s->d_frontier[0], s->d_fcount,
                                                               g->d_outdeg, s->d_xscratch + 1);

@@ -133,6 +133,34 @@ __device__ __forceinline__ void lp_finish(const LpLaunch& L, uint32_t slot, unsi
     }
 }
 
+// lp_finish for a whole warp, each lane with its own (slot, best) or none: the changed
+// slots are published with one frontier reservation for the warp (a reservation per
+// destination on the single frontier counter serialises in L2 at ~10^5 destinations)
+__device__ __forceinline__ void lp_finish_lanes(const LpLaunch& L, bool valid, uint32_t slot, unsigned long long best,
+                                                LocalStats& st) {
+    bool ch = false;
+    if (valid && best != 0ull) {
+        st.targets++;
+        const uint32_t nl = ~(uint32_t)(best & 0xFFFFFFFFull);
+        if (nl != L.lab_cur[slot]) {
+            L.lab_next[slot] = nl;
+            ch = true;
+            st.changed++;
+            st.next_active++;
+            st.next_units += __ldg(L.f.outdeg + slot);
+            if (bit_test(L.f.remote_src, slot)) st.remote_active++;
+            atomicOr(L.f.active_next + (slot >> 5), 1u << (slot & 31));
+        }
+    }
+    const unsigned m = __ballot_sync(kFull, ch);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(L.f.frontier_count, (unsigned long long)__popc(m));
+    base = __shfl_sync(kFull, base, __ffs(m) - 1);
+    if (ch) L.f.frontier_next[base + __popc(m & ((1u << lane) - 1u))] = slot;
+}
+
 // small destinations: stage labels in shared memory, count candidates
 template <int G>
 __device__ __forceinline__ void lp_group(const LpLaunch& L, int k, unsigned b, uint32_t* buf, LocalStats& st) {
@@ -399,6 +427,11 @@ __global__ void __launch_bounds__(kBlock) k_lp_hub_warp(const LpLaunch L, uint64
     uint32_t* wk = lp_dyn + warp * 2 * kLpWarpCap;
     uint32_t* wc = wk + kLpWarpCap;
     const uint64_t nw = (uint64_t)gridDim.x * (kBlock / 32);
+    // lane k keeps the result of this warp's k-th destination of a batch of 32; the batch
+    // is finished (and published) together
+    uint32_t pslot = 0;
+    unsigned long long pbest = 0ull;
+    int nb = 0;
     for (uint64_t rel = lo_rel + blockIdx.x * (uint64_t)(kBlock / 32) + warp; rel < hi_rel; rel += nw) {
         const uint64_t beg = __ldg(L.in_off + rel), end = __ldg(L.in_off + rel + 1);
         uint32_t C = 64;
@@ -422,9 +455,17 @@ __global__ void __launch_bounds__(kBlock) k_lp_hub_warp(const LpLaunch L, uint64
             const unsigned long long q = __shfl_xor_sync(kFull, best, o);
             best = q > best ? q : best;
         }
-        if (lane == 0) lp_finish(L, (uint32_t)(L.lo + rel), best, st);
+        if (lane == nb) {
+            pslot = (uint32_t)(L.lo + rel);
+            pbest = best;
+        }
+        if (++nb == 32) {
+            lp_finish_lanes(L, true, pslot, pbest, st);
+            nb = 0;
+        }
         __syncwarp();
     }
+    lp_finish_lanes(L, lane < nb, pslot, pbest, st);
     flush_stats(st, L.stats);
 }
 

@@ -168,14 +168,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, algo, src, dst, cap, out_q, enable_skip, cls=None):
+def _worker(rank, world, port, algo, src, dst, cap, out_q, enable_skip, cls=None, run_kw=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2203_13005_b200.dist import Collective, PartitionedRun
         st = (cls or NumpyPartition)(src, dst, algo, rank, world)
-        run = PartitionedRun(st, st.bounds, Collective(), enable_skip=enable_skip, device=None)
+        run = PartitionedRun(st, st.bounds, Collective(), enable_skip=enable_skip, device=None, **(run_kw or {}))
         it, conv = run.run(cap)
         vals = st.rank if algo == "pagerank" else st.label.astype(np.float64)
         lo, hi = st.lo, st.hi
@@ -185,11 +185,11 @@ def _worker(rank, world, port, algo, src, dst, cap, out_q, enable_skip, cls=None
         dist.destroy_process_group()
 
 
-def _run(algo, src, dst, cap, enable_skip=True, world=2, cls=None):
+def _run(algo, src, dst, cap, enable_skip=True, world=2, cls=None, run_kw=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, algo, src, dst, cap, q, enable_skip, cls))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, algo, src, dst, cap, q, enable_skip, cls, run_kw))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -285,7 +285,7 @@ def test_cc_dense_mirror_exchange_matches_oracle(oracle_lib):
     a = np.concatenate([np.arange(n), rng.integers(0, n, 3 * n)]).astype(np.uint32)
     b = np.concatenate([(np.arange(n) + 1) % n, rng.integers(0, n, 3 * n)]).astype(np.uint32)
     src, dst = np.concatenate([a, b]), np.concatenate([b, a])
-    res, got = _run("cc", src, dst, 1000, cls=DenseNumpyPartition)
+    res, got = _run("cc", src, dst, 1000, cls=DenseNumpyPartition, run_kw={"dense_frac": 0.25})
     ref = oracle_lib.OracleGraph(src, dst).run("cc")
     assert all(r[1] == ref.iterations and r[2] == ref.converged for r in res)
     np.testing.assert_array_equal(got, ref.attrs[:, 0])
