@@ -224,7 +224,8 @@ __global__ void __launch_bounds__(kBlock) k_pack_peers(int algo, const uint32_t*
                                                         const uint32_t* __restrict__ need,
                                                         const uint4* __restrict__ dist,
                                                         const uint32_t* __restrict__ lab, int nparts,
-                                                        const PeerArenas A, unsigned long long* peer_cnt) {
+                                                        const __grid_constant__ PeerArenas A,
+                                                        unsigned long long* peer_cnt) {
     constexpr int kWarps = kBlock / 32;
     __shared__ uint32_t stage_all[kWarps][32 * 5];
     __shared__ uint32_t wcnt[kWarps][kMaxPeers + 1];
@@ -236,12 +237,21 @@ __global__ void __launch_bounds__(kBlock) k_pack_peers(int algo, const uint32_t*
     for (uint64_t t0 = (uint64_t)blockIdx.x * kPackPer * kBlock; t0 < n; t0 += (uint64_t)gridDim.x * kPackPer * kBlock) {
         // this warp's kPackPer groups of 32 consecutive list entries
         uint32_t sl[kPackPer], m[kPackPer];
+        uint4 val[kPackPer];
 #pragma unroll
         for (int j = 0; j < kPackPer; ++j) {
             const uint64_t i = t0 + ((uint64_t)warp * kPackPer + j) * 32 + lane;
             sl[j] = i < n ? list[i] : 0u;
             const bool mine = i < n && sl[j] >= lo && sl[j] < hi;
             m[j] = mine ? __ldg(need + (sl[j] - lo)) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < kPackPer; ++j) {  // each value is loaded once, for every peer
+            val[j] = make_uint4(0u, 0u, 0u, 0u);
+            if (m[j]) {
+                if (algo == GXB_ALGO_SSSP) val[j] = dist[sl[j]];
+                else val[j].x = lab[sl[j]];
+            }
         }
         for (int q = 0; q < nparts; ++q) {
             uint32_t c = 0;
@@ -271,11 +281,9 @@ __global__ void __launch_bounds__(kBlock) k_pack_peers(int algo, const uint32_t*
                 if (to_q) {
                     uint32_t* r = stage + __popc(b & ((1u << lane) - 1u)) * W;
                     r[0] = sl[j];
+                    r[1] = val[j].x;
                     if (algo == GXB_ALGO_SSSP) {
-                        const uint4 d = dist[sl[j]];
-                        r[1] = d.x; r[2] = d.y; r[3] = d.z; r[4] = d.w;
-                    } else {
-                        r[1] = lab[sl[j]];
+                        r[2] = val[j].y; r[3] = val[j].z; r[4] = val[j].w;
                     }
                 }
                 __syncwarp();
