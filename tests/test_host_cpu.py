@@ -335,3 +335,23 @@ def test_engine_config_validation():
     assert convergence_vote([True, True]) and not convergence_vote([True, False])
     with pytest.raises(EngineError, match="missing convergence vote"):
         convergence_vote([True, None])
+
+
+def test_protocol_errors_are_the_reference_type():
+    """With the reference loaded, a library protocol error is both this package's and the
+    reference's ProtocolError (A/channel.py), so the reference's handlers catch it."""
+    import accelgraph.channel as ch
+    from paper_2203_13005_b200 import _lib as L
+    with pytest.raises(ch.ProtocolError) as exc:
+        L.check(L.GXB_EPROTO)
+    assert isinstance(exc.value, L.ProtocolError)
+    with pytest.raises(ValueError):
+        L.check(L.GXB_EINVAL)
+    with pytest.raises(MemoryError):
+        L.check(L.GXB_ENOMEM)
+
+
+def test_oracle_thread_control(oracle_lib):
+    oracle_lib.set_threads(2)
+    assert oracle_lib.max_threads() == 2
+    oracle_lib.set_threads(os.cpu_count() or 1)
