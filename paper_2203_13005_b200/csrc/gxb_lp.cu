@@ -26,16 +26,17 @@ namespace gxb {
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
 // Global (label, count) tables of the label-diverse hubs (in-degree > kLpBigDeg), one per
-// hub, 2 x in-degree entries. Keys and counts carry the round's epoch in their high 32 bits:
-// a word of an older epoch is empty, so no table is ever cleared between rounds.
+// hub, 2 x in-degree entries. One 64-bit word per entry: epoch (8 bits) | count (24 bits) |
+// label (32 bits). A word of another epoch is empty, so no table is cleared between rounds
+// (every 255 rounds the tables are zeroed once); an insert is a read plus one CAS (new
+// label) or one atomicAdd on the count field (known label).
 struct LpHub {
     uint64_t* tab_off;   // per big hub: first entry
     uint32_t* tab_mask;  // per big hub: size - 1 (power of two)
-    unsigned long long* keys;    // epoch << 32 | label
-    unsigned long long* counts;  // epoch << 32 | count
+    unsigned long long* words;
     unsigned long long* best;  // per chunked slot: packed (count << 32 | ~label), 0 = no message
     uint64_t entries;
-    uint32_t epoch;
+    uint32_t epoch;      // 1..255
 };
 
 struct LpPush;
@@ -68,26 +69,21 @@ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
 // fold (label, c) into a hub's epoch-tagged table; returns the label's new count
 __device__ __forceinline__ uint32_t table_add(const LpHub& H, uint64_t base, uint32_t mask, uint32_t label,
                                               uint32_t c) {
-    const unsigned long long tag = (unsigned long long)H.epoch << 32;
-    const unsigned long long want = tag | label;
+    const unsigned long long ep = (unsigned long long)H.epoch << 56;
     uint32_t i = mix32(label) & mask;
     while (true) {
-        unsigned long long* kp = H.keys + base + i;
-        unsigned long long k = __ldcg(kp);
-        if ((k >> 32) != H.epoch) {  // empty in this round: claim it
-            const unsigned long long prev = atomicCAS(kp, k, want);
-            k = prev == k ? want : prev;
-            if ((k >> 32) != H.epoch) continue;  // raced with another stale word: retry the slot
+        unsigned long long* wp = H.words + base + i;
+        unsigned long long w = __ldcg(wp);
+        if ((uint32_t)(w >> 56) != H.epoch) {  // empty in this round: claim it
+            const unsigned long long nw = ep | ((unsigned long long)c << 32) | label;
+            const unsigned long long prev = atomicCAS(wp, w, nw);
+            if (prev == w) return c;
+            w = prev;
+            if ((uint32_t)(w >> 56) != H.epoch) continue;  // raced with another stale word: retry the slot
         }
-        if (k == want) {
-            unsigned long long* cp = H.counts + base + i;
-            unsigned long long w = __ldcg(cp);
-            while ((w >> 32) != H.epoch) {  // first count of this round replaces the stale word
-                const unsigned long long prev = atomicCAS(cp, w, tag | c);
-                if (prev == w) return c;
-                w = prev;
-            }
-            return (uint32_t)(atomicAdd(cp, (unsigned long long)c) & 0xFFFFFFFFull) + c;
+        if ((uint32_t)w == label) {
+            const unsigned long long old = atomicAdd(wp, (unsigned long long)c << 32);
+            return (uint32_t)((old >> 32) & 0xFFFFFFull) + c;
         }
         i = (i + 1) & mask;
     }
@@ -207,11 +203,14 @@ __device__ __forceinline__ void lp_group(const LpLaunch& L, int k, unsigned b, u
 // the final counts).
 constexpr int kWarpPairs = 256;
 
-__device__ __forceinline__ void hub_add(const LpLaunch& L, uint64_t rel, uint64_t base, uint32_t mask, uint32_t lab,
-                                        uint32_t c) {
+// the returned (count, ~label) of every insert only grows per label, and the last insert of
+// a label returns its final count: the max over one lane's inserts, reduced over the warp
+// at the end of the chunk, needs one atomicMax per chunk
+__device__ __forceinline__ void hub_add(const LpLaunch& L, uint64_t base, uint32_t mask, uint32_t lab, uint32_t c,
+                                        unsigned long long& lbest) {
     const uint32_t nc = table_add(L.hub, base, mask, lab, c);
     const unsigned long long pk = ((unsigned long long)nc << 32) | (unsigned long long)(~lab);
-    if (pk > __ldcg(L.hub.best + rel)) atomicMax(L.hub.best + rel, pk);
+    lbest = pk > lbest ? pk : lbest;
 }
 
 __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint32_t* wkeys, uint32_t* wcnts,
@@ -228,6 +227,7 @@ __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint3
     }
     if (lane == 0) *wfull = 0u;
     __syncwarp();
+    unsigned long long lbest = 0ull;
     constexpr int kB = 8;  // the loads of 8 steps are issued together
     for (uint64_t e0 = beg; e0 < end; e0 += 32 * kB) {
         uint32_t src[kB], lab[kB];
@@ -262,14 +262,19 @@ __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint3
                 }
                 if (!done) {
                     *reinterpret_cast<volatile uint32_t*>(wfull) = 1u;
-                    hub_add(L, rel, base, mask, lab[j], __popc(m));
+                    hub_add(L, base, mask, lab[j], __popc(m), lbest);
                 }
             }
         }
     }
     __syncwarp();
     for (int i = lane; i < kWarpPairs; i += 32)
-        if (wkeys[i] != kEmpty) hub_add(L, rel, base, mask, wkeys[i], wcnts[i]);
+        if (wkeys[i] != kEmpty) hub_add(L, base, mask, wkeys[i], wcnts[i], lbest);
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long q = __shfl_xor_sync(kFull, lbest, o);
+        lbest = q > lbest ? q : lbest;
+    }
+    if (lane == 0 && lbest && lbest > __ldcg(L.hub.best + rel)) atomicMax(L.hub.best + rel, lbest);
 }
 
 // Round 1 (labels = distinct vertex ids): a label's count at a hub is the multiplicity of
@@ -277,34 +282,66 @@ __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint3
 // chunk — no hash table, no atomics per edge. A run belongs to the chunk / lane where it
 // starts: a lane skips a leading run that continues from the previous edge and extends its
 // last run past its range (and past the chunk end) until the source changes.
+__device__ __forceinline__ void lp_run_candidate(const LpLaunch& L, uint32_t src, uint64_t len,
+                                                 unsigned long long& best) {
+    if (!bit_test(L.active_cur, src)) return;
+    const unsigned long long pk = ((unsigned long long)len << 32) | (unsigned long long)(~__ldg(L.lab_cur + src));
+    best = pk > best ? pk : best;
+}
+
+// Warp-wide over 32 consecutive edges per step (coalesced loads, no per-lane serial walk):
+// run starts come from comparing each source with its predecessor; a run closes at the
+// next start, so a start lane knows its run length when another start follows in the same
+// window, the window's last run stays open into the next window, and the run open at the
+// chunk's end is followed past it until its source changes.
 __device__ __forceinline__ void lp_chunk_injective(const LpLaunch& L, uint64_t item) {
     const int lane = threadIdx.x & 31;
     const uint32_t rel = __ldg(L.item_slot + item);
     const uint64_t seg_beg = __ldg(L.in_off + rel), seg_end = __ldg(L.in_off + rel + 1);
     const uint64_t beg = __ldg(L.item_begin + item);
     const uint64_t end = min(beg + (uint64_t)kChunkEdges, seg_end);
-    constexpr uint32_t kPer = kChunkEdges / 32;
-    uint64_t e = beg + (uint64_t)lane * kPer;
-    const uint64_t stop = min(e + kPer, end);
     unsigned long long best = 0ull;
-    if (e < stop) {
-        if (e > seg_beg) {  // a run continuing from the previous edge is counted where it starts
-            const uint32_t prev = __ldg(L.in_src + e - 1);
-            while (e < stop && __ldg(L.in_src + e) == prev) ++e;
+    uint32_t prev = beg > seg_beg ? __ldg(L.in_src + beg - 1) : kNone;
+    bool open = false;  // warp-uniform: a run that started in this chunk is still open
+    uint32_t open_src = 0;
+    uint64_t open_start = 0;
+    for (uint64_t w0 = beg; w0 < end; w0 += 32) {
+        const uint64_t e = w0 + lane;
+        const bool in = e < end;
+        const uint32_t s = in ? __ldg(L.in_src + e) : kNone;
+        uint32_t p = __shfl_up_sync(kFull, s, 1);
+        if (lane == 0) p = prev;
+        const bool start = in && s != p;  // (a run continuing from the previous chunk is not counted here)
+        const unsigned M = __ballot_sync(kFull, start);
+        if (open && M) {
+            if (lane == 0) lp_run_candidate(L, open_src, w0 + (__ffs(M) - 1) - open_start, best);
+            open = false;
         }
-        while (e < stop) {
-            const uint32_t s = __ldg(L.in_src + e);
-            uint32_t c = 0;
-            while (e < seg_end && __ldg(L.in_src + e) == s) {
-                ++c;
-                ++e;
-            }
-            if (bit_test(L.active_cur, s)) {
-                const uint32_t lab = __ldg(L.lab_cur + s);
-                const unsigned long long pk = ((unsigned long long)c << 32) | (unsigned long long)(~lab);
-                best = pk > best ? pk : best;
+        if (start) {
+            const unsigned above = M & ~((2u << lane) - 1u);
+            if (above) lp_run_candidate(L, s, (uint64_t)(__ffs(above) - 1 - lane), best);
+        }
+        if (M) {
+            const int last = 31 - __clz(M);
+            open = true;
+            open_src = __shfl_sync(kFull, s, last);
+            open_start = w0 + last;
+        }
+        prev = __shfl_sync(kFull, s, 31);
+    }
+    if (open) {  // follow the last run past the chunk end
+        uint64_t len = 0;
+        for (uint64_t e0 = end;; e0 += 32) {
+            const uint64_t e = e0 + lane;
+            const bool in = e < seg_end;
+            const uint32_t s = in ? __ldg(L.in_src + e) : kNone;
+            const unsigned D = __ballot_sync(kFull, !in || s != open_src);
+            if (D) {
+                len = e0 + (__ffs(D) - 1) - open_start;
+                break;
             }
         }
+        if (lane == 0) lp_run_candidate(L, open_src, len, best);
     }
     for (int o = 16; o > 0; o >>= 1) {
         const unsigned long long q = __shfl_xor_sync(kFull, best, o);
@@ -702,8 +739,7 @@ static void lp_free(LpScratch* S) {
     LpHub& H = S->hub;
     dfree(H.tab_off);
     dfree(H.tab_mask);
-    dfree(H.keys);
-    dfree(H.counts);
+    dfree(H.words);
     dfree(H.best);
     dfree(S->pkeys);
     dfree(S->pcounts);
@@ -740,6 +776,10 @@ static int lp_setup(gxb_state* s, cudaStream_t st) {
     }
     H.entries = acc;
     H.epoch = 0;  // the tables start zeroed: epoch 0 words are empty from round 1 on
+    if (S->big_end && g->h_indeg_sorted[0] >= (1u << 24)) {
+        lp_free(S);
+        return fail(GXB_ERANGE, "LabelPropagation: an in-degree >= 2^24 exceeds the hub tables' count field");
+    }
     int rc = GXB_OK;
     auto up = [&](auto** d, const auto& h) {
         if (rc != GXB_OK) return;
@@ -750,13 +790,11 @@ static int lp_setup(gxb_state* s, cudaStream_t st) {
     };
     up(&H.tab_off, off);
     up(&H.tab_mask, mask);
-    if (rc == GXB_OK) rc = dalloc_t(&H.keys, acc + 1);
-    if (rc == GXB_OK) rc = dalloc_t(&H.counts, acc + 1);
+    if (rc == GXB_OK) rc = dalloc_t(&H.words, acc + 1);
     if (rc == GXB_OK) rc = dalloc_t(&H.best, P.chunk_end + 1);
     if (rc == GXB_OK) rc = dalloc_t(&S->eff, g->S + 1);
     if (rc == GXB_OK) {
-        cudaMemsetAsync(H.keys, 0, 8 * (acc + 1), st);
-        cudaMemsetAsync(H.counts, 0, 8 * (acc + 1), st);
+        cudaMemsetAsync(H.words, 0, 8 * (acc + 1), st);
         cudaMemsetAsync(H.best, 0, 8 * (P.chunk_end + 1), st);
         if (cudaStreamSynchronize(st) != cudaSuccess) rc = fail(GXB_ECUDA, "lp_setup sync");
     }
@@ -841,11 +879,10 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
     // effective labels: one gather per edge (label of an active source, else empty)
     if (g->S) k_lp_eff<<<grid_for(g->S), kBlock, 0, st>>>(s->d_active[0], s->d_lab_cur, g->S, S->eff);
     L.eff = S->eff;
-    // rounds >= 2: the G = 32 and G = 16 bins (in-degree 33-128) are counted in warp shared
-    // tables instead of the quadratic in-group count (round 1's labels are all distinct, where
-    // the in-group count is cheaper: measured)
+    // the G = 32 and G = 16 bins (in-degree 33-128) are counted in warp shared tables instead
+    // of the quadratic in-group count (every round, the first included: measured)
     uint64_t warp_end = S->chunk_end;
-    for (int k = kNumGroupBins - 1; k >= kLpWarpMinBin && !L.injective; --k) {
+    for (int k = kNumGroupBins - 1; k >= kLpWarpMinBin; --k) {
         warp_end = std::max(warp_end, L.bin_hi[k]);
         grid -= L.bin_blocks[k];
         L.bin_blocks[k] = 0;
@@ -855,7 +892,11 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
         // rounds >= 2: chunk items of the label-diverse big hubs only (the plan lists items
         // in slot order; epoch-tagged global tables), CTA tables for 513-4096, warp tables
         // for 33-512
-        L.hub.epoch = ++S->hub.epoch;  // this round's table words (older ones read as empty)
+        if (++S->hub.epoch > 255) {  // 8-bit epochs: zero the tables once per 255 rounds
+            S->hub.epoch = 1;
+            if (S->hub.entries) GXB_CUDA(cudaMemsetAsync(S->hub.words, 0, 8 * S->hub.entries, st));
+        }
+        L.hub.epoch = S->hub.epoch;  // this round's table words (older ones read as empty)
         grid -= L.chunk_blocks;
         L.num_items = S->big_items;
         L.chunk_blocks = (unsigned)((S->big_items + (kBlock / 32) - 1) / (kBlock / 32));
