@@ -6,16 +6,18 @@
 // otherwise take the most frequent label, ties to the smallest label, and be
 // active iff it changed. Counts are exact integers, so the result is bit-exact.
 //
-// Two regimes over the degree-sorted slots (same bins as the pull merge):
-//  * in-degree <= 4G with G lanes per destination (G = 1..32): the group stages
-//    its labels in shared memory and every lane counts its candidates against
-//    the staged multiset; the group takes the max of (count << 32 | ~label).
-//  * in-degree > kChunkMinDeg: warps stream kChunkEdges-edge chunks, pre-merge
-//    equal labels inside the warp with __match_any_sync, and fold (label, count)
-//    into a per-destination open-addressing table in global memory (L2
-//    atomics); every update also raises the destination's running packed
-//    argmax (count << 32 | ~label) with atomicMax, so no table scan is needed;
-//    a last pass applies and the tables are reset with memsets.
+// Dense rounds, over the in-degree-sorted slots:
+//  * in-degree <= 32 (k_lp_pull): G lanes per destination stage its labels in shared
+//    memory and count each candidate against the staged multiset;
+//  * 33-512 (k_lp_hub_warp) and 513-4096 (k_lp_hub_cta): a warp / CTA counts the
+//    destination in a shared (label, count) table twice its in-degree, after equal labels
+//    of 32 edges are merged with __match_any_sync;
+//  * above 4096 (k_lp_chunks): warps stream 1024-edge chunks into per-warp shared tables
+//    and flush them into per-hub epoch-tagged global tables (L2 atomics); the packed
+//    argmax (count << 32 | ~label) is raised once per chunk, k_lp_hub_apply applies it.
+// Round 1 (labels = distinct ids) counts every hub by run length over its sorted sources
+// (k_lp_chunks_runs, and k_lp_hub_warp's run-length branch). Sparse rounds push the
+// frontier's labels into a (destination, label) pair table (k_lp_push).
 #include <algorithm>
 #include <vector>
 
@@ -203,12 +205,30 @@ __device__ __forceinline__ void lp_group(const LpLaunch& L, int k, unsigned b, u
 // the final counts).
 constexpr int kWarpPairs = 256;
 
-// the returned (count, ~label) of every insert only grows per label, and the last insert of
+// The returned (count, ~label) of every insert only grows per label, and the last insert of
 // a label returns its final count: the max over one lane's inserts, reduced over the warp
-// at the end of the chunk, needs one atomicMax per chunk
+// at the end of the chunk, needs one atomicMax per chunk.
+// The home word is tried before table_add's probe loop (one read, then one CAS on a stale
+// word or one add when the label is there; a lost CAS or a collision falls back to the
+// loop): the same operations, measured faster than entering the loop directly.
 __device__ __forceinline__ void hub_add(const LpLaunch& L, uint64_t base, uint32_t mask, uint32_t lab, uint32_t c,
                                         unsigned long long& lbest) {
-    const uint32_t nc = table_add(L.hub, base, mask, lab, c);
+    const uint32_t ep = L.hub.epoch;
+    const unsigned long long w = __ldcg(L.hub.words + base + (mix32(lab) & mask));
+    unsigned long long* wp = L.hub.words + base + (mix32(lab) & mask);
+    unsigned long long r = 0ull;
+    bool cas = false, add = false;
+    if ((uint32_t)(w >> 56) != ep) {
+        r = atomicCAS(wp, w, ((unsigned long long)ep << 56) | ((unsigned long long)c << 32) | lab);
+        cas = true;
+    } else if ((uint32_t)w == lab) {
+        r = atomicAdd(wp, (unsigned long long)c << 32);
+        add = true;
+    }
+    uint32_t nc;
+    if (cas && r == w) nc = c;
+    else if (add) nc = (uint32_t)((r >> 32) & 0xFFFFFFull) + c;
+    else nc = table_add(L.hub, base, mask, lab, c);
     const unsigned long long pk = ((unsigned long long)nc << 32) | (unsigned long long)(~lab);
     lbest = pk > lbest ? pk : lbest;
 }
@@ -268,8 +288,21 @@ __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint3
         }
     }
     __syncwarp();
-    for (int i = lane; i < kWarpPairs; i += 32)
-        if (wkeys[i] != kEmpty) hub_add(L, base, mask, wkeys[i], wcnts[i], lbest);
+    {
+        // the warp table's pairs to the hub's table, keys and counts read first
+        constexpr int kPerLane = kWarpPairs / 32;
+        uint32_t fk[kPerLane], fc[kPerLane];
+        unsigned fv = 0u;
+#pragma unroll
+        for (int k = 0; k < kPerLane; ++k) {
+            fk[k] = wkeys[lane + 32 * k];
+            fc[k] = wcnts[lane + 32 * k];
+            if (fk[k] != kEmpty) fv |= 1u << k;
+        }
+#pragma unroll
+        for (int k = 0; k < kPerLane; ++k)
+            if ((fv >> k) & 1u) hub_add(L, base, mask, fk[k], fc[k], lbest);
+    }
     for (int o = 16; o > 0; o >>= 1) {
         const unsigned long long q = __shfl_xor_sync(kFull, lbest, o);
         lbest = q > lbest ? q : lbest;
@@ -282,27 +315,35 @@ __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint3
 // chunk — no hash table, no atomics per edge. A run belongs to the chunk / lane where it
 // starts: a lane skips a leading run that continues from the previous edge and extends its
 // last run past its range (and past the chunk end) until the source changes.
-__device__ __forceinline__ void lp_run_candidate(const LpLaunch& L, uint32_t src, uint64_t len,
+// Only a run at least as long as the longest seen so far (this warp's runs, and the hub's
+// running best from chunks already done) can win, so only those gather their label: on
+// R-MAT hubs most runs are single edges below a longer run, and the label gathers — one
+// random load per edge when every run was a candidate — are the kernel's cost. (A run's
+// length raises the bar whether or not its source is active: sound because the labels are
+// injective only before round 1 of a fresh state, where every source is active —
+// gxb_state_create; every call that changes the active set clears lab_injective.)
+__device__ __forceinline__ void lp_run_candidate(const LpLaunch& L, uint32_t src, uint32_t len, uint32_t bar,
                                                  unsigned long long& best) {
-    if (!bit_test(L.active_cur, src)) return;
-    const unsigned long long pk = ((unsigned long long)len << 32) | (unsigned long long)(~__ldg(L.lab_cur + src));
+    if (len < bar) return;
+    const uint32_t lab = lp_msg(L, src);
+    if (lab == kEmpty) return;
+    const unsigned long long pk = ((unsigned long long)len << 32) | (unsigned long long)(~lab);
     best = pk > best ? pk : best;
 }
 
 // Warp-wide over 32 consecutive edges per step (coalesced loads, no per-lane serial walk):
 // run starts come from comparing each source with its predecessor; a run closes at the
 // next start, so a start lane knows its run length when another start follows in the same
-// window, the window's last run stays open into the next window, and the run open at the
-// chunk's end is followed past it until its source changes.
-__device__ __forceinline__ void lp_chunk_injective(const LpLaunch& L, uint64_t item) {
+// window, the window's last run stays open into the next window, and the run open at `end`
+// is followed past it (up to the segment end) until its source changes. Counts the runs
+// that start in [beg, end) of the segment [seg_beg, seg_end); returns the warp's best
+// packed (count, ~label) in every lane.
+__device__ __forceinline__ unsigned long long lp_runs(const LpLaunch& L, uint64_t seg_beg, uint64_t seg_end,
+                                                      uint64_t beg, uint64_t end, uint32_t bar) {
     const int lane = threadIdx.x & 31;
-    const uint32_t rel = __ldg(L.item_slot + item);
-    const uint64_t seg_beg = __ldg(L.in_off + rel), seg_end = __ldg(L.in_off + rel + 1);
-    const uint64_t beg = __ldg(L.item_begin + item);
-    const uint64_t end = min(beg + (uint64_t)kChunkEdges, seg_end);
     unsigned long long best = 0ull;
     uint32_t prev = beg > seg_beg ? __ldg(L.in_src + beg - 1) : kNone;
-    bool open = false;  // warp-uniform: a run that started in this chunk is still open
+    bool open = false;  // warp-uniform: a run that started in this range is still open
     uint32_t open_src = 0;
     uint64_t open_start = 0;
     for (uint64_t w0 = beg; w0 < end; w0 += 32) {
@@ -311,16 +352,17 @@ __device__ __forceinline__ void lp_chunk_injective(const LpLaunch& L, uint64_t i
         const uint32_t s = in ? __ldg(L.in_src + e) : kNone;
         uint32_t p = __shfl_up_sync(kFull, s, 1);
         if (lane == 0) p = prev;
-        const bool start = in && s != p;  // (a run continuing from the previous chunk is not counted here)
+        const bool start = in && s != p;  // (a run continuing from before `beg` is not counted here)
         const unsigned M = __ballot_sync(kFull, start);
-        if (open && M) {
-            if (lane == 0) lp_run_candidate(L, open_src, w0 + (__ffs(M) - 1) - open_start, best);
-            open = false;
-        }
+        uint32_t len = 0, len_open = 0;  // the runs that close in this window
+        if (open && M && lane == 0) len_open = (uint32_t)(w0 + (__ffs(M) - 1) - open_start);
         if (start) {
             const unsigned above = M & ~((2u << lane) - 1u);
-            if (above) lp_run_candidate(L, s, (uint64_t)(__ffs(above) - 1 - lane), best);
+            if (above) len = (uint32_t)(__ffs(above) - 1 - lane);
         }
+        bar = max(bar, __reduce_max_sync(kFull, max(len, len_open)));
+        if (len_open) lp_run_candidate(L, open_src, len_open, bar, best);
+        if (len) lp_run_candidate(L, s, len, bar, best);
         if (M) {
             const int last = 31 - __clz(M);
             open = true;
@@ -329,9 +371,9 @@ __device__ __forceinline__ void lp_chunk_injective(const LpLaunch& L, uint64_t i
         }
         prev = __shfl_sync(kFull, s, 31);
     }
-    if (open) {  // follow the last run past the chunk end
-        uint64_t len = 0;
-        for (uint64_t e0 = end;; e0 += 32) {
+    if (open) {  // follow the last run past `end`
+        uint64_t len = seg_end - open_start;
+        for (uint64_t e0 = end; e0 < seg_end; e0 += 32) {
             const uint64_t e = e0 + lane;
             const bool in = e < seg_end;
             const uint32_t s = in ? __ldg(L.in_src + e) : kNone;
@@ -341,12 +383,24 @@ __device__ __forceinline__ void lp_chunk_injective(const LpLaunch& L, uint64_t i
                 break;
             }
         }
-        if (lane == 0) lp_run_candidate(L, open_src, len, best);
+        if (lane == 0) lp_run_candidate(L, open_src, (uint32_t)len, bar, best);
     }
     for (int o = 16; o > 0; o >>= 1) {
         const unsigned long long q = __shfl_xor_sync(kFull, best, o);
         best = q > best ? q : best;
     }
+    return best;
+}
+
+__device__ __forceinline__ void lp_chunk_injective(const LpLaunch& L, uint64_t item) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t rel = __ldg(L.item_slot + item);
+    const uint64_t seg_beg = __ldg(L.in_off + rel), seg_end = __ldg(L.in_off + rel + 1);
+    const uint64_t beg = __ldg(L.item_begin + item);
+    const uint64_t end = min(beg + (uint64_t)kChunkEdges, seg_end);
+    // the hub's running best from chunks already done is a lower bound for a winning count
+    const uint32_t bar = (uint32_t)(__ldcg(L.hub.best + rel) >> 32);
+    const unsigned long long best = lp_runs(L, seg_beg, seg_end, beg, end, bar);
     if (lane == 0 && best && best > __ldcg(L.hub.best + rel)) atomicMax(L.hub.best + rel, best);
 }
 
@@ -471,26 +525,30 @@ __global__ void __launch_bounds__(kBlock) k_lp_hub_warp(const LpLaunch L, uint64
     int nb = 0;
     for (uint64_t rel = lo_rel + blockIdx.x * (uint64_t)(kBlock / 32) + warp; rel < hi_rel; rel += nw) {
         const uint64_t beg = __ldg(L.in_off + rel), end = __ldg(L.in_off + rel + 1);
-        uint32_t C = 64;
-        while ((uint64_t)C < 2 * (end - beg)) C <<= 1;  // <= kLpWarpCap for in-degree <= kLpCtaMinDeg
-        for (uint32_t i = lane; i < C; i += 32) {
-            wk[i] = kEmpty;
-            wc[i] = 0;
-        }
-        __syncwarp();
-        lp_count_edges(L, beg, end, lane, 32, wk, wc, C - 1);
-        __syncwarp();
         unsigned long long best = 0ull;
-        for (uint32_t i = lane; i < C; i += 32) {
-            const uint32_t k = wk[i];
-            if (k != kEmpty) {
-                const unsigned long long pk = pack_best(wc[i], k);
-                best = pk > best ? pk : best;
+        if (L.injective) {
+            best = lp_runs(L, beg, end, beg, end, 0u);  // round 1: run-length, no table
+        } else {
+            uint32_t C = 64;
+            while ((uint64_t)C < 2 * (end - beg)) C <<= 1;  // <= kLpWarpCap for in-degree <= kLpCtaMinDeg
+            for (uint32_t i = lane; i < C; i += 32) {
+                wk[i] = kEmpty;
+                wc[i] = 0;
             }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long q = __shfl_xor_sync(kFull, best, o);
-            best = q > best ? q : best;
+            __syncwarp();
+            lp_count_edges(L, beg, end, lane, 32, wk, wc, C - 1);
+            __syncwarp();
+            for (uint32_t i = lane; i < C; i += 32) {
+                const uint32_t k = wk[i];
+                if (k != kEmpty) {
+                    const unsigned long long pk = pack_best(wc[i], k);
+                    best = pk > best ? pk : best;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long q = __shfl_xor_sync(kFull, best, o);
+                best = q > best ? q : best;
+            }
         }
         if (lane == nb) {
             pslot = (uint32_t)(L.lo + rel);
@@ -506,22 +564,29 @@ __global__ void __launch_bounds__(kBlock) k_lp_hub_warp(const LpLaunch L, uint64
     flush_stats(st, L.stats);
 }
 
-__global__ void __launch_bounds__(kBlock) k_lp_pull(const LpLaunch L) {
-    // group path: 4 labels per thread; chunk path: a (label, count) table per warp
-    __shared__ uint32_t buf[4 * kBlock > 2 * kWarpPairs * (kBlock / 32) ? 4 * kBlock : 2 * kWarpPairs * (kBlock / 32)];
+// chunk items of the hubs (rounds >= 2): one warp per kChunkEdges-edge chunk. Kernels of
+// their own, apart from the group bins (which run at 32 registers instead of the chunk
+// path's 40) and from round 1's run-length chunks
+__global__ void __launch_bounds__(kBlock) k_lp_chunks(const LpLaunch L) {
+    __shared__ uint32_t buf[2 * kWarpPairs * (kBlock / 32)];
     __shared__ uint32_t wfull[kBlock / 32];
+    const uint64_t item = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+    uint32_t* wk = buf + (threadIdx.x >> 5) * 2 * kWarpPairs;
+    if (item < L.num_items) lp_chunk(L, item, wk, wk + kWarpPairs, wfull + (threadIdx.x >> 5));
+    // chunked slots are applied by k_lp_hub_apply
+}
+
+// round 1's chunk items: run-length counting
+__global__ void __launch_bounds__(kBlock) k_lp_chunks_runs(const LpLaunch L) {
+    const uint64_t item = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+    if (item < L.num_items) lp_chunk_injective(L, item);
+}
+
+// the group bins (in-degree <= 32; 33-128 go to the warp tables)
+__global__ void __launch_bounds__(kBlock) k_lp_pull(const LpLaunch L) {
+    __shared__ uint32_t buf[4 * kBlock];  // 4 labels per thread
     LocalStats st;
     unsigned b = blockIdx.x;
-    if (b < L.chunk_blocks) {
-        const uint64_t item = (uint64_t)b * (kBlock / 32) + (threadIdx.x >> 5);
-        uint32_t* wk = buf + (threadIdx.x >> 5) * 2 * kWarpPairs;  // the group path's buffer, reused
-        if (item < L.num_items) {
-            if (L.injective) lp_chunk_injective(L, item);
-            else lp_chunk(L, item, wk, wk + kWarpPairs, wfull + (threadIdx.x >> 5));
-        }
-        return;  // chunked slots are applied by k_lp_hub_apply
-    }
-    b -= L.chunk_blocks;
     int k = kNumGroupBins - 1;
     for (; k > 0; --k) {
         if (b < L.bin_blocks[k]) break;
@@ -903,6 +968,11 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
         grid += L.chunk_blocks;
         warp_lo = S->cta_end;
     }
+    if (L.chunk_blocks) {
+        if (L.injective) k_lp_chunks_runs<<<L.chunk_blocks, kBlock, 0, st>>>(L);
+        else k_lp_chunks<<<L.chunk_blocks, kBlock, 0, st>>>(L);
+    }
+    grid -= L.chunk_blocks;
     if (grid) k_lp_pull<<<grid, kBlock, 0, st>>>(L);
     if (!L.injective && S->cta_end > S->big_end) {
         const unsigned gc = (unsigned)std::min<uint64_t>(S->cta_end - S->big_end, 3ull * kNumSMs);
@@ -916,7 +986,7 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
     // slots counted by chunk items: applied from their packed argmax
     const uint64_t applied = L.injective ? S->chunk_end : S->big_end;
     if (applied) k_lp_hub_apply<<<grid_for(applied), kBlock, 0, st>>>(L, applied);
-    s->launches += 3;  // + the caller's 2: eff, chunks + groups, CTA hubs, warp hubs, hub apply
+    s->launches += 4;  // + the caller's 2: eff, chunks, groups, CTA hubs, warp hubs, hub apply
     GXB_CUDA(cudaGetLastError());
     return GXB_OK;
 }
