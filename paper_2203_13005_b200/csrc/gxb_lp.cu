@@ -236,6 +236,7 @@ __device__ __forceinline__ void hub_add(const LpLaunch& L, uint64_t base, uint32
 __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint32_t* wkeys, uint32_t* wcnts,
                                          uint32_t* wfull) {
     const int lane = threadIdx.x & 31;
+    const unsigned lower = (1u << lane) - 1u;  // a group's leader has no lower lane in it (no ffs on the XU pipe)
     const uint32_t rel = __ldg(L.item_slot + item);
     const uint64_t beg = __ldg(L.item_begin + item);
     const uint64_t end = min(beg + (uint64_t)kChunkEdges, __ldg(L.in_off + rel + 1));
@@ -266,7 +267,7 @@ __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint3
             // 32-bit match: lanes without a message all carry kEmpty and group together,
             // but their leader is not `ok`, so that group is dropped
             const unsigned m = __match_any_sync(kFull, ok[j] ? lab[j] : kEmpty);
-            if (ok[j] && lane == __ffs(m) - 1) {
+            if (ok[j] && !(m & lower)) {
                 uint32_t h = mix32(lab[j]) & (kWarpPairs - 1);
                 bool done = false;
                 // once a probe sequence has failed the table is crowded: look at the home slot only
@@ -451,6 +452,7 @@ __device__ __forceinline__ void lp_count_edges(const LpLaunch& L, uint64_t beg, 
                                                unsigned nthreads, uint32_t* keys, uint32_t* cnts, uint32_t mask) {
     constexpr int kB = 8;
     const int lane = threadIdx.x & 31;
+    const unsigned lower = (1u << lane) - 1u;  // a group's leader has no lower lane in it (no ffs on the XU pipe)
     const unsigned warp0 = t - lane;  // first thread of this warp within the group
     for (uint64_t e0 = beg + (uint64_t)warp0 * kB; e0 < end; e0 += (uint64_t)nthreads * kB) {
         uint32_t src[kB], lab[kB];
@@ -465,7 +467,7 @@ __device__ __forceinline__ void lp_count_edges(const LpLaunch& L, uint64_t beg, 
         for (int j = 0; j < kB; ++j) {
             const bool ok = lab[j] != kEmpty;
             const unsigned m = __match_any_sync(kFull, lab[j]);  // no-message lanes group under kEmpty
-            if (ok && lane == __ffs(m) - 1) smem_table_add(keys, cnts, mask, lab[j], (uint32_t)__popc(m));
+            if (ok && !(m & lower)) smem_table_add(keys, cnts, mask, lab[j], (uint32_t)__popc(m));
         }
     }
 }
@@ -511,12 +513,15 @@ __global__ void __launch_bounds__(kBlock) k_lp_hub_cta(const LpLaunch L, uint64_
     flush_stats(st, L.stats);
 }
 
+// kCap: table entries per warp — 2 x the largest in-degree of the launch's slots (the
+// 33-128 slots run with 256-entry tables: a quarter of the shared memory, more warps per SM)
+template <int kCap>
 __global__ void __launch_bounds__(kBlock) k_lp_hub_warp(const LpLaunch L, uint64_t lo_rel, uint64_t hi_rel) {
-    extern __shared__ uint32_t lp_dyn[];  // per warp: kLpWarpCap keys, then kLpWarpCap counts
+    extern __shared__ uint32_t lp_dyn[];  // per warp: kCap keys, then kCap counts
     LocalStats st;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t* wk = lp_dyn + warp * 2 * kLpWarpCap;
-    uint32_t* wc = wk + kLpWarpCap;
+    uint32_t* wk = lp_dyn + warp * 2 * kCap;
+    uint32_t* wc = wk + kCap;
     const uint64_t nw = (uint64_t)gridDim.x * (kBlock / 32);
     // lane k keeps the result of this warp's k-th destination of a batch of 32; the batch
     // is finished (and published) together
@@ -530,7 +535,7 @@ __global__ void __launch_bounds__(kBlock) k_lp_hub_warp(const LpLaunch L, uint64
             best = lp_runs(L, beg, end, beg, end, 0u);  // round 1: run-length, no table
         } else {
             uint32_t C = 64;
-            while ((uint64_t)C < 2 * (end - beg)) C <<= 1;  // <= kLpWarpCap for in-degree <= kLpCtaMinDeg
+            while ((uint64_t)C < 2 * (end - beg)) C <<= 1;  // <= kCap
             for (uint32_t i = lane; i < C; i += 32) {
                 wk[i] = kEmpty;
                 wc[i] = 0;
@@ -717,6 +722,7 @@ __global__ void __launch_bounds__(kBlock) k_lp_push(const uint32_t* __restrict__
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
+    const unsigned lower = (1u << lane) - 1u;  // a group's leader has no lower lane in it (no ffs on the XU pipe)
     const uint64_t total = nfront ? rowpre[nfront - 1] : 0;
     const uint64_t items = (total + kLpItemEdges - 1) / kLpItemEdges;
     const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
@@ -743,7 +749,7 @@ __global__ void __launch_bounds__(kBlock) k_lp_push(const uint32_t* __restrict__
             const unsigned long long key = ok ? ((unsigned long long)rel << 32 | lab) : (~0ull - 1 - lane);
             const unsigned m = __match_any_sync(kFull, key);
             bool first = false;
-            if (ok && lane == __ffs(m) - 1) {
+            if (ok && !(m & lower)) {
                 if (!(rel < hub_end && smem_pair_add(skeys, scounts, key, __popc(m))))
                     first = global_pair(P, mask, key, __popc(m));
             }
@@ -937,7 +943,7 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
     const int dev = g->ctx->device & 63;
     if (!attrs_set[dev]) {
         GXB_CUDA(cudaFuncSetAttribute(k_lp_hub_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4 * kLpCtaCap));
-        GXB_CUDA(cudaFuncSetAttribute(k_lp_hub_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        GXB_CUDA(cudaFuncSetAttribute(k_lp_hub_warp<kLpWarpCap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (kBlock / 32) * 2 * 4 * kLpWarpCap));
         attrs_set[dev] = true;
     }
@@ -978,15 +984,21 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
         const unsigned gc = (unsigned)std::min<uint64_t>(S->cta_end - S->big_end, 3ull * kNumSMs);
         k_lp_hub_cta<<<gc, kBlock, 2 * 4 * kLpCtaCap, st>>>(L, S->big_end, S->cta_end);
     }
-    if (warp_end > warp_lo) {
-        const uint64_t n = warp_end - warp_lo;
-        const unsigned gw = (unsigned)std::min<uint64_t>((n + kBlock / 32 - 1) / (kBlock / 32), 6ull * kNumSMs);
-        k_lp_hub_warp<<<gw, kBlock, (kBlock / 32) * 2 * 4 * kLpWarpCap, st>>>(L, warp_lo, warp_end);
-    }
+    // warp tables: in-degree 129-512 (rounds >= 2) with 1024 entries, 33-128 with 256
+    auto warp_grid = [](uint64_t n) {
+        return (unsigned)std::min<uint64_t>((n + kBlock / 32 - 1) / (kBlock / 32), 6ull * kNumSMs);
+    };
+    const uint64_t small_lo = std::max(warp_lo, S->chunk_end);
+    if (small_lo > warp_lo)
+        k_lp_hub_warp<kLpWarpCap><<<warp_grid(small_lo - warp_lo), kBlock, (kBlock / 32) * 2 * 4 * kLpWarpCap, st>>>(
+            L, warp_lo, small_lo);
+    if (warp_end > small_lo)
+        k_lp_hub_warp<2 * kChunkMinDeg><<<warp_grid(warp_end - small_lo), kBlock, (kBlock / 32) * 2 * 4 * 2 * kChunkMinDeg,
+                                           st>>>(L, small_lo, warp_end);
     // slots counted by chunk items: applied from their packed argmax
     const uint64_t applied = L.injective ? S->chunk_end : S->big_end;
     if (applied) k_lp_hub_apply<<<grid_for(applied), kBlock, 0, st>>>(L, applied);
-    s->launches += 4;  // + the caller's 2: eff, chunks, groups, CTA hubs, warp hubs, hub apply
+    s->launches += 5;  // + the caller's 2: eff, chunks, groups, CTA hubs, 2 x warp hubs, hub apply
     GXB_CUDA(cudaGetLastError());
     return GXB_OK;
 }
