@@ -442,6 +442,34 @@ __device__ __forceinline__ void smem_table_add(uint32_t* keys, uint32_t* cnts, u
     }
 }
 
+// The same for epoch-tagged shared tables: one 64-bit word per entry, epoch (8 bits) |
+// count (24) | label (32), like the hubs' global tables. A word of another epoch is empty,
+// so a table is not cleared between destinations (every 255), and the insert returns the
+// label's running count: the max of the returned (count, ~label) is the destination's
+// best (a label's count only grows), so the table is not scanned either.
+__device__ __forceinline__ uint32_t smem_ep_add(unsigned long long* tab, uint32_t mask, uint32_t ep, uint32_t lab,
+                                                uint32_t c) {
+    uint32_t h = mix32(lab) & mask;
+    unsigned long long w = tab[h];
+    while (true) {
+        if ((uint32_t)(w >> 56) != ep) {  // empty for this destination: claim
+            const unsigned long long nw = ((unsigned long long)ep << 56) | ((unsigned long long)c << 32) | lab;
+            const unsigned long long prev = atomicCAS(tab + h, w, nw);
+            if (prev == w) return c;
+            w = prev;
+            continue;
+        }
+        if ((uint32_t)w == lab) {  // the label's entry: add (CAS retry on a concurrent add)
+            const unsigned long long prev = atomicCAS(tab + h, w, w + ((unsigned long long)c << 32));
+            if (prev == w) return (uint32_t)((w >> 32) & 0xFFFFFFull) + c;
+            w = prev;
+            continue;
+        }
+        h = (h + 1) & mask;
+        w = tab[h];
+    }
+}
+
 __device__ __forceinline__ unsigned long long pack_best(uint32_t count, uint32_t lab) {
     return ((unsigned long long)count << 32) | (unsigned long long)(~lab);
 }
@@ -472,22 +500,59 @@ __device__ __forceinline__ void lp_count_edges(const LpLaunch& L, uint64_t beg, 
     }
 }
 
+// lp_count_edges into an epoch-tagged table; returns this thread's best packed (count, ~label)
+__device__ __forceinline__ unsigned long long lp_count_edges_ep(const LpLaunch& L, uint64_t beg, uint64_t end,
+                                                                unsigned t, unsigned nthreads, unsigned long long* tab,
+                                                                uint32_t mask, uint32_t ep) {
+    constexpr int kB = 8;
+    const int lane = threadIdx.x & 31;
+    const unsigned lower = (1u << lane) - 1u;
+    const unsigned warp0 = t - lane;
+    unsigned long long best = 0ull;
+    for (uint64_t e0 = beg + (uint64_t)warp0 * kB; e0 < end; e0 += (uint64_t)nthreads * kB) {
+        uint32_t src[kB], lab[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            const uint64_t e = e0 + 32 * j + lane;
+            src[j] = e < end ? __ldg(L.in_src + e) : kEmpty;
+        }
+#pragma unroll
+        for (int j = 0; j < kB; ++j) lab[j] = src[j] != kEmpty ? lp_msg(L, src[j]) : kEmpty;
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            const bool ok = lab[j] != kEmpty;
+            const unsigned m = __match_any_sync(kFull, lab[j]);
+            if (ok && !(m & lower)) {
+                const unsigned long long pk = pack_best(smem_ep_add(tab, mask, ep, lab[j], (uint32_t)__popc(m)), lab[j]);
+                best = pk > best ? pk : best;
+            }
+        }
+    }
+    return best;
+}
+
+// One CTA per destination, a (label, count) table in shared memory (32-bit keys and counts:
+// native shared atomics, which the hot labels' contention between the CTA's warps needs —
+// an epoch-tagged 64-bit word table was measured 10% slower here). The scan for the best
+// entry also empties the table for the next destination, and thread 0 finishes a
+// destination from its parity's row of warp results: two barriers per destination.
 __global__ void __launch_bounds__(kBlock) k_lp_hub_cta(const LpLaunch L, uint64_t lo_rel, uint64_t cta_end) {
     extern __shared__ uint32_t lp_dyn[];  // kLpCtaCap keys, then kLpCtaCap counts
     uint32_t* keys = lp_dyn;
     uint32_t* cnts = lp_dyn + kLpCtaCap;
-    __shared__ unsigned long long wbest[kBlock / 32];
+    __shared__ unsigned long long wbest[2][kBlock / 32];
     LocalStats st;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint64_t rel = lo_rel + blockIdx.x; rel < cta_end; rel += gridDim.x) {
+    for (uint32_t i = threadIdx.x; i < kLpCtaCap; i += kBlock) {
+        keys[i] = kEmpty;
+        cnts[i] = 0;
+    }
+    __syncthreads();
+    int par = 0;
+    for (uint64_t rel = lo_rel + blockIdx.x; rel < cta_end; rel += gridDim.x, par ^= 1) {
         const uint64_t beg = __ldg(L.in_off + rel), end = __ldg(L.in_off + rel + 1);
         uint32_t C = 64;
         while ((uint64_t)C < 2 * (end - beg)) C <<= 1;  // <= kLpCtaCap for in-degree <= kLpBigDeg
-        for (uint32_t i = threadIdx.x; i < C; i += kBlock) {
-            keys[i] = kEmpty;
-            cnts[i] = 0;
-        }
-        __syncthreads();
         lp_count_edges(L, beg, end, threadIdx.x, kBlock, keys, cnts, C - 1);
         __syncthreads();
         unsigned long long best = 0ull;
@@ -496,19 +561,20 @@ __global__ void __launch_bounds__(kBlock) k_lp_hub_cta(const LpLaunch L, uint64_
             if (k != kEmpty) {
                 const unsigned long long pk = pack_best(cnts[i], k);
                 best = pk > best ? pk : best;
+                keys[i] = kEmpty;
+                cnts[i] = 0;
             }
         }
         for (int o = 16; o > 0; o >>= 1) {
             const unsigned long long q = __shfl_xor_sync(kFull, best, o);
             best = q > best ? q : best;
         }
-        if (lane == 0) wbest[warp] = best;
-        __syncthreads();
+        if (lane == 0) wbest[par][warp] = best;
+        __syncthreads();  // the table is empty again, the warp results are in
         if (threadIdx.x == 0) {
-            for (int w = 1; w < kBlock / 32; ++w) best = wbest[w] > best ? wbest[w] : best;
+            for (int w = 1; w < kBlock / 32; ++w) best = wbest[par][w] > best ? wbest[par][w] : best;
             lp_finish(L, (uint32_t)(L.lo + rel), best, st);
         }
-        __syncthreads();  // the table is reused by the next destination
     }
     flush_stats(st, L.stats);
 }
@@ -517,11 +583,11 @@ __global__ void __launch_bounds__(kBlock) k_lp_hub_cta(const LpLaunch L, uint64_
 // 33-128 slots run with 256-entry tables: a quarter of the shared memory, more warps per SM)
 template <int kCap>
 __global__ void __launch_bounds__(kBlock) k_lp_hub_warp(const LpLaunch L, uint64_t lo_rel, uint64_t hi_rel) {
-    extern __shared__ uint32_t lp_dyn[];  // per warp: kCap keys, then kCap counts
+    extern __shared__ unsigned long long lp_tab[];  // per warp: kCap epoch-tagged words
     LocalStats st;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t* wk = lp_dyn + warp * 2 * kCap;
-    uint32_t* wc = wk + kCap;
+    unsigned long long* wt = lp_tab + warp * kCap;
+    uint32_t ep = 255;  // wraps to 1 (and clears the table) on the first destination
     const uint64_t nw = (uint64_t)gridDim.x * (kBlock / 32);
     // lane k keeps the result of this warp's k-th destination of a batch of 32; the batch
     // is finished (and published) together
@@ -534,22 +600,14 @@ __global__ void __launch_bounds__(kBlock) k_lp_hub_warp(const LpLaunch L, uint64
         if (L.injective) {
             best = lp_runs(L, beg, end, beg, end, 0u);  // round 1: run-length, no table
         } else {
+            if (++ep == 256) {
+                ep = 1;
+                for (uint32_t i = lane; i < kCap; i += 32) wt[i] = 0ull;
+                __syncwarp();
+            }
             uint32_t C = 64;
             while ((uint64_t)C < 2 * (end - beg)) C <<= 1;  // <= kCap
-            for (uint32_t i = lane; i < C; i += 32) {
-                wk[i] = kEmpty;
-                wc[i] = 0;
-            }
-            __syncwarp();
-            lp_count_edges(L, beg, end, lane, 32, wk, wc, C - 1);
-            __syncwarp();
-            for (uint32_t i = lane; i < C; i += 32) {
-                const uint32_t k = wk[i];
-                if (k != kEmpty) {
-                    const unsigned long long pk = pack_best(wc[i], k);
-                    best = pk > best ? pk : best;
-                }
-            }
+            best = lp_count_edges_ep(L, beg, end, lane, 32, wt, C - 1, ep);
             for (int o = 16; o > 0; o >>= 1) {
                 const unsigned long long q = __shfl_xor_sync(kFull, best, o);
                 best = q > best ? q : best;
