@@ -215,8 +215,11 @@ struct PeerArenas {
 // of every peer that reads the slot. A block takes kPackPer x kBlock list entries per step;
 // the per-peer record positions come from one atomicAdd per (block step, peer) plus
 // shared-memory prefixes over the warps (per-warp reservations on a handful of counters
-// serialised in L2). A warp's records for one peer are one contiguous run: staged in shared
-// memory and stored with consecutive lanes on consecutive words (whole lines over NVLink).
+// serialised in L2). The block's records for one peer are one contiguous run of up to
+// kPackPer x kBlock records: staged in shared memory, then stored by the whole block with
+// consecutive threads on consecutive words, shifted so that every warp store covers one
+// aligned 128-B line (full-line writes over NVLink; a run per warp and peer cut most lines
+// into two partial writes).
 constexpr int kPackPer = 4;
 
 __global__ void __launch_bounds__(kBlock) k_pack_peers(int algo, const uint32_t* __restrict__ list,
@@ -227,13 +230,14 @@ __global__ void __launch_bounds__(kBlock) k_pack_peers(int algo, const uint32_t*
                                                         const __grid_constant__ PeerArenas A,
                                                         unsigned long long* peer_cnt) {
     constexpr int kWarps = kBlock / 32;
-    __shared__ uint32_t stage_all[kWarps][32 * 5];
+    __shared__ uint32_t stage[kPackPer * kBlock * 5];  // one peer's records of a block step
     __shared__ uint32_t wcnt[kWarps][kMaxPeers + 1];
     __shared__ unsigned long long bbase[kMaxPeers + 1];
+    __shared__ uint32_t btot[kMaxPeers + 1];
     const uint64_t n = *count;
     const int W = record_words(algo);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t* stage = stage_all[warp];
+    const unsigned lower = (1u << lane) - 1u;
     for (uint64_t t0 = (uint64_t)blockIdx.x * kPackPer * kBlock; t0 < n; t0 += (uint64_t)gridDim.x * kPackPer * kBlock) {
         // this warp's kPackPer groups of 32 consecutive list entries
         uint32_t sl[kPackPer], m[kPackPer];
@@ -268,33 +272,36 @@ __global__ void __launch_bounds__(kBlock) k_pack_peers(int algo, const uint32_t*
                 wcnt[w][q] = acc;
                 acc += c;
             }
+            btot[q] = acc;
             bbase[q] = acc ? atomicAdd(peer_cnt + q, (unsigned long long)acc) : 0ull;
         }
         __syncthreads();
         for (int q = 0; q < nparts; ++q) {
-            unsigned long long base = bbase[q] + wcnt[warp][q];
+            const uint32_t total = btot[q];
+            if (!total) continue;  // block-uniform
+            uint32_t pos = wcnt[warp][q];
 #pragma unroll
             for (int j = 0; j < kPackPer; ++j) {
                 const bool to_q = (m[j] >> q) & 1u;
                 const unsigned b = __ballot_sync(0xffffffffu, to_q);
-                if (!b) continue;
                 if (to_q) {
-                    uint32_t* r = stage + __popc(b & ((1u << lane) - 1u)) * W;
+                    uint32_t* r = stage + (pos + __popc(b & lower)) * W;
                     r[0] = sl[j];
                     r[1] = val[j].x;
                     if (algo == GXB_ALGO_SSSP) {
                         r[2] = val[j].y; r[3] = val[j].z; r[4] = val[j].w;
                     }
                 }
-                __syncwarp();
-                const uint32_t words = (uint32_t)__popc(b) * (uint32_t)W;
-                uint32_t* dst = A.arena[q] + A.base[q] + base * W;
-                for (uint32_t k = lane; k < words; k += 32) dst[k] = stage[k];
-                base += __popc(b);
-                __syncwarp();
+                pos += __popc(b);
             }
+            __syncthreads();
+            uint32_t* dst = A.arena[q] + A.base[q] + bbase[q] * W;
+            const int64_t words = (int64_t)total * W;
+            const int64_t mis = (int64_t)((reinterpret_cast<uintptr_t>(dst) >> 2) & 31u);  // words past a line start
+            for (int64_t k = (int64_t)threadIdx.x - mis; k < words; k += kBlock)
+                if (k >= 0) dst[k] = stage[k];
+            __syncthreads();  // the stage is reused for the next peer
         }
-        __syncthreads();  // wcnt / bbase are rewritten by the next step
     }
     // one cumulative system-scope fence per block after a barrier (not one per thread): the
     // block's records are visible to the peers before the vote collective

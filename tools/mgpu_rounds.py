@@ -1,4 +1,5 @@
-"""Per-phase timing of partitioned frontier-algorithm runs under torchrun (development aid).
+"""Per-phase timing (totals and per round) of partitioned frontier-algorithm runs under
+torchrun (development aid).
 
     python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 \
         --master-port 29512 tools/mgpu_rounds.py cc 24
@@ -42,12 +43,22 @@ def main():
         dist.barrier()
         torch.cuda.synchronize()
         t = time.perf_counter()
-        run.run(cap)
+        per_round = []
+        while run.iteration < cap:
+            before = dict(run.phase_times or {})
+            rec = run.step()
+            if rep:
+                now = run.phase_times
+                per_round.append({"dir": rec.direction, "changed": rec.changed,
+                                  **{k: round(1e3 * (now.get(k, 0.0) - before.get(k, 0.0)), 3) for k in now}})
+            if rec.converged:
+                break
+        run.finish()
         torch.cuda.synchronize()
         el = time.perf_counter() - t
         st.free()
     out = {"rank": rank, "algo": algo, "iterations": run.iteration, "ms_total": round(1e3 * el, 3),
-           **{k: round(1e3 * v, 3) for k, v in (run.phase_times or {}).items()}}
+           **{k: round(1e3 * v, 3) for k, v in (run.phase_times or {}).items()}, "rounds": per_round}
     allv = [None] * world
     dist.all_gather_object(allv, out)
     if rank == 0:
