@@ -481,12 +481,14 @@ __device__ __forceinline__ void lp_count_edges(const LpLaunch& L, uint64_t beg, 
     constexpr int kB = 8;
     const int lane = threadIdx.x & 31;
     const unsigned lower = (1u << lane) - 1u;  // a group's leader has no lower lane in it (no ffs on the XU pipe)
-    const unsigned warp0 = t - lane;  // first thread of this warp within the group
-    for (uint64_t e0 = beg + (uint64_t)warp0 * kB; e0 < end; e0 += (uint64_t)nthreads * kB) {
+    // 32-edge groups dealt round-robin over the warps (group g to warp g mod nw), kB per
+    // step: with one CTA per destination, every warp has edges down to in-degree 32 x nw
+    const uint64_t nw = nthreads / 32, wi = (t - lane) / 32;
+    for (uint64_t g0 = wi; beg + g0 * 32 < end; g0 += nw * kB) {
         uint32_t src[kB], lab[kB];
 #pragma unroll
         for (int j = 0; j < kB; ++j) {
-            const uint64_t e = e0 + 32 * j + lane;
+            const uint64_t e = beg + (g0 + j * nw) * 32 + lane;
             src[j] = e < end ? __ldg(L.in_src + e) : kEmpty;
         }
 #pragma unroll
