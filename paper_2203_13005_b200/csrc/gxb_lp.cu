@@ -203,7 +203,7 @@ __device__ __forceinline__ void lp_group(const LpLaunch& L, int k, unsigned b, u
 // (overflow goes straight to it). Each global update also raises the hub's running packed
 // argmax (a label's (count, ~label) only grows, so the max over all updates is the max over
 // the final counts).
-constexpr int kWarpPairs = 256;
+constexpr int kWarpPairs = 128;  // measured: 64 ~ 128 < 256 (the flush scans every entry) << 512
 
 // The returned (count, ~label) of every insert only grows per label, and the last insert of
 // a label returns its final count: the max over one lane's inserts, reduced over the warp
