@@ -197,6 +197,15 @@ int gxb_state_arity(const gxb_state* s, int* out);
  * stats on the device; gxb_stats() synchronises `stream` and reads them. */
 int gxb_iterate(gxb_state* s, int direction, void* stream);
 
+/* Split rounds (option split_overlap, SSSP / CC at N > 1): launch the NEXT round's
+ * local-source pass (in-edges from this partition's own slots) on an internal stream
+ * ordered after `stream`, so it runs while the closed round's records travel to and from
+ * the peers (SURVEY.md §8(e) overlap; the reference's sync round A/engine.py:247-266 sits
+ * between two rounds the same way). The next gxb_iterate, if it is a tile pull, gathers
+ * only the remote sources and combines. A no-op unless the last round was a dense pull;
+ * *launched (optional) = 1 when the pass was launched. */
+int gxb_iterate_local(gxb_state* s, void* stream, int* launched);
+
 /* API-faithful template ops over a WorkItem range descriptor (A/daemon.py:86-130):
  *   GEN:   [lo, hi) = owned CSC edge range; materialises one message per edge
  *          whose source is active (A/algorithms.py:232-240)

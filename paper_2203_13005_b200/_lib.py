@@ -127,6 +127,7 @@ def _sig(L):
         "gxb_state_free": (I, [P]),
         "gxb_state_arity": (I, [P, ctypes.POINTER(I)]),
         "gxb_iterate": (I, [P, I, P]),
+        "gxb_iterate_local": (I, [P, P, ctypes.POINTER(ctypes.c_int)]),
         "gxb_request": (I, [P, I, U64, U64, P]),
         "gxb_commit": (I, [P, P]),
         "gxb_stats": (I, [P, P, ctypes.POINTER(IterStats)]),

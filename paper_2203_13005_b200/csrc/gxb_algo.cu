@@ -142,6 +142,15 @@ __device__ __forceinline__ bool eq4(uint4 a, uint4 b) {
     return a.x == b.x && a.y == b.y && a.z == b.z && a.w == b.w;
 }
 
+// Which sources a pull pass gathers: all (mode 0), the partition's own slots [lo, lo + n)
+// (1), or the others (2). A frontier round at N > 1 can run its local-source pass while
+// the previous round's records still travel, then the remote-source pass (split rounds).
+struct SourceSel {
+    uint32_t lo = 0, n = 0;
+    int mode = 0;
+    __device__ bool take(uint32_t s) const { return mode == 0 || ((s - lo < n) == (mode == 1)); }
+};
+
 struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-122)
     static constexpr bool kPublishes = true;
     // The accumulator is the lane-wise min; "received a message" <=> some lane is
@@ -165,6 +174,7 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
     bool check_active;
     HotPrefix hp;
     uint32_t hot, hot1;
+    SourceSel sel;
     static constexpr bool kWeighted = true;
 
     __device__ static Acc identity() { return {make_uint4(kInf32, kInf32, kInf32, kInf32)}; }
@@ -182,7 +192,7 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
     __device__ static bool has(const Acc& a) { return (a.m.x & a.m.y & a.m.z & a.m.w) != kInf32; }
     // Gen: d + w per lane from an active source (102-105); inf stays inf
     __device__ bool gen(uint32_t s, uint32_t w, Msg& m) const {
-        if (check_active && !bit_test(active_cur, s)) return false;
+        if (!sel.take(s) || (check_active && !bit_test(active_cur, s))) return false;
         const uint32_t r = hp.rank(s);
         const uint64_t pol = r < hot ? l2_evict_last() : l2_evict_first();
         const uint4 d = r < hot1 ? ld_l1_v4(dist_cur + s, pol) : ld_nol1_v4(dist_cur + s, pol);
@@ -193,7 +203,7 @@ struct SsspOps {  // multi-source Bellman-Ford, 4 u32 lanes (A/algorithms.py:81-
     using Raw = uint4;
     __device__ static Raw identity_raw() { return make_uint4(kInf32, kInf32, kInf32, kInf32); }
     __device__ bool gather_async(uint32_t saddr, uint32_t s) const {
-        if (check_active && !bit_test(active_cur, s)) return false;
+        if (!sel.take(s) || (check_active && !bit_test(active_cur, s))) return false;
         const uint32_t r = hp.rank(s);
         const uint64_t pol = r < hot ? l2_evict_last() : l2_evict_first();
         if (r < hot1) cp_async_ca<16>(saddr, dist_cur + s, pol);
@@ -240,6 +250,7 @@ struct CcOps {  // min-label propagation; labels < 0xFFFF
     bool check_active;  // see SsspOps::check_active (labels only decrease)
     HotPrefix hp;
     uint32_t hot, hot1;
+    SourceSel sel;
     static constexpr bool kWeighted = false;
 
     __device__ static Acc identity() { return {kInf32}; }
@@ -250,7 +261,7 @@ struct CcOps {  // min-label propagation; labels < 0xFFFF
     __device__ static Acc ld_cg(const Acc* p) { return {__ldcg(&p->m)}; }
     __device__ static bool has(const Acc& a) { return a.m != kInf32; }
     __device__ bool gen(uint32_t s, uint32_t, Msg& m) const {
-        if (check_active && !bit_test(active_cur, s)) return false;
+        if (!sel.take(s) || (check_active && !bit_test(active_cur, s))) return false;
         const uint32_t r = hp.rank(s);
         const uint64_t pol = r < hot ? l2_evict_last() : l2_evict_first();
         m = r < hot1 ? ld_l1_u32(lab_cur + s, pol) : ld_nol1_u32(lab_cur + s, pol);
@@ -260,7 +271,7 @@ struct CcOps {  // min-label propagation; labels < 0xFFFF
     using Raw = uint32_t;
     __device__ static Raw identity_raw() { return kInf32; }
     __device__ bool gather_async(uint32_t saddr, uint32_t s) const {
-        if (check_active && !bit_test(active_cur, s)) return false;
+        if (!sel.take(s) || (check_active && !bit_test(active_cur, s))) return false;
         const uint32_t r = hp.rank(s);
         const uint64_t pol = r < hot ? l2_evict_last() : l2_evict_first();
         cp_async_ca<4>(saddr, lab_cur + s, pol);
@@ -490,6 +501,7 @@ struct TileLaunch {
     void* partials;
     void* sums;   // per relative slot: folded accumulator
     const uint32_t* key_slot;  // compacted plan (PageRank hub split): plan key -> owned slot, else null
+    bool accumulate;  // combine into the sums of an earlier pass over the same plan (split rounds)
 };
 
 __device__ __forceinline__ uint4 ldg_v4(const uint32_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
@@ -504,7 +516,8 @@ __device__ __forceinline__ void tile_emit(const Pol& p, const TileLaunch& L, uin
     if (head != kNone && key == __ldg(L.span_slot + head)) span = head;
     else if (tail != kNone && key == __ldg(L.span_slot + tail)) span = tail;
     if (span == kNone) {
-        reinterpret_cast<Acc*>(L.sums)[key] = total;
+        Acc* d = reinterpret_cast<Acc*>(L.sums) + key;
+        *d = L.accumulate ? Ops::combine(*d, total) : total;
     } else {
         // folded by k_span_fold after the kernel boundary (no fences on the hot path)
         reinterpret_cast<Acc*>(L.partials)[__ldg(L.span_pbase + span) + (t - __ldg(L.span_first + span))] = total;
@@ -610,7 +623,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_t(const Pol p, cons
                     fval = acc;
                     first = false;
                 } else {
-                    reinterpret_cast<Acc*>(L.sums)[L.key_slot ? __ldg(L.key_slot + key) : key] = acc;
+                    Acc* d = reinterpret_cast<Acc*>(L.sums) + (L.key_slot ? __ldg(L.key_slot + key) : key);
+                    *d = L.accumulate ? Ops::combine(*d, acc) : acc;
                 }
                 ++key;
                 acc = Ops::identity();
@@ -725,7 +739,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_tile_a(const Pol p, cons
                     fval = acc;
                     first = false;
                 } else {
-                    reinterpret_cast<Acc*>(L.sums)[L.key_slot ? __ldg(L.key_slot + key) : key] = acc;
+                    Acc* d = reinterpret_cast<Acc*>(L.sums) + (L.key_slot ? __ldg(L.key_slot + key) : key);
+                    *d = L.accumulate ? Ops::combine(*d, acc) : acc;
                 }
                 ++key;
                 acc = Ops::identity();
@@ -766,7 +781,7 @@ __global__ void __launch_bounds__(kBlock) k_span_fold(const uint32_t* __restrict
                                                       const uint32_t* __restrict__ span_count,
                                                       const uint64_t* __restrict__ span_pbase, uint64_t span_lo,
                                                       uint64_t span_hi, const typename Ops::Acc* __restrict__ partials,
-                                                      typename Ops::Acc* sums) {
+                                                      typename Ops::Acc* sums, bool accumulate = false) {
     using Acc = typename Ops::Acc;
     constexpr uint32_t kLong = 16;
     const int lane = threadIdx.x & 31;
@@ -781,6 +796,7 @@ __global__ void __launch_bounds__(kBlock) k_span_fold(const uint32_t* __restrict
             const uint64_t b = span_pbase[k];
             Acc tot = Ops::identity();
             for (uint32_t i = 0; i < n; ++i) tot = Ops::combine(tot, partials[b + i]);
+            if (accumulate) tot = Ops::combine(sums[span_slot[k]], tot);
             sums[span_slot[k]] = tot;
         }
         unsigned big = __ballot_sync(kFull, n >= kLong);
@@ -795,7 +811,7 @@ __global__ void __launch_bounds__(kBlock) k_span_fold(const uint32_t* __restrict
             for (uint32_t i = lane; i < nn; i += 32) tot = Ops::combine(tot, partials[b + i]);
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) tot = Ops::combine(tot, Ops::shfl(tot, o));
-            if (lane == 0) sums[span_slot[kk]] = tot;
+            if (lane == 0) sums[span_slot[kk]] = accumulate ? Ops::combine(sums[span_slot[kk]], tot) : tot;
         }
     }
 }
@@ -1266,6 +1282,7 @@ TileLaunch tile_launch(gxb_state* s) {
     L.partials = s->d_tile_partials;
     L.sums = s->d_sums;
     L.key_slot = nullptr;
+    L.accumulate = false;
     return L;
 }
 
@@ -1293,9 +1310,12 @@ int drain_kring(gxb_state* s, int n) {
 // one exchange chunk (or all of them for k < 0): Gen∘Merge tiles, span folds, Apply
 // With `ast`, the chunk's span fold and Apply run on that stream after the tile kernel
 // (an event orders them), so Apply(k) — and its peer stores — overlap the tiles of k+1.
+// pass: 0 = a whole round; 1 = a split round's local-source tiles and span folds (no
+// Apply, a few SMs left to the exchange kernels beside it); 2 = its remote-source tiles
+// and folds combined into pass 1's sums, then Apply
 template <class Ops>
 int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st, int chunk = -1,
-                          cudaStream_t ast = nullptr) {
+                          cudaStream_t ast = nullptr, int pass = 0) {
     const gxb_graph* g = s->g;
     const TilePlan& T = g->tiles;
     const int K = T.num_xchunks;
@@ -1303,6 +1323,7 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st, int chu
     TileLaunch L = tile_launch(s);
     L.tile_begin = T.xchunk_tile[k0];
     L.num_tiles = T.xchunk_tile[k1];
+    L.accumulate = pass == 2;
     const uint64_t span_lo = T.xchunk_span[k0], span_hi = T.xchunk_span[k1];
     const uint64_t r_lo = T.xchunk_slot[k0], r_hi = T.xchunk_slot[k1];
     FusedPolicy<Ops> p{ops, g->d_in_w};
@@ -1326,13 +1347,16 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st, int chu
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, 0);
     // chunked rounds leave SMs free for the NCCL kernels of the overlapped exchange
-    const int sms = chunk >= 0 ? std::max(1, kNumSMs - (int)options().overlap_reserve_sms) : kNumSMs;
+    const int sms = chunk >= 0  ? std::max(1, kNumSMs - (int)options().overlap_reserve_sms)
+                    : pass == 1 ? std::max(1, kNumSMs - (int)options().split_reserve_sms)
+                                : kNumSMs;
     const int max_blocks = std::max(1, per_sm) * sms;
     const uint64_t ntiles = L.num_tiles - L.tile_begin;
     if (ntiles) {
         const uint64_t want = (ntiles + (kBlock / 32) - 1) / (kBlock / 32);
         const unsigned grid = (unsigned)std::min<uint64_t>(want, (uint64_t)max_blocks);
-        const bool first = chunk < 0 || s->round_chunks == 0, last = chunk < 0 || s->round_chunks == K - 1;
+        const bool first = pass != 1 && (chunk < 0 || s->round_chunks == 0);
+        const bool last = pass != 1 && (chunk < 0 || s->round_chunks == K - 1);
         if (s->timing && first) GXB_CUDA(cudaEventRecord(kev_at(s, 0), st));
         kern<<<grid, kBlock, 0, st>>>(p, L);
         if (s->timing && last) {
@@ -1351,9 +1375,13 @@ int launch_tile_and_apply(gxb_state* s, const Ops& ops, cudaStream_t st, int chu
         if (span_hi > span_lo) {
             k_span_fold<Ops><<<grid_for(span_hi - span_lo), kBlock, 0, st>>>(
                 T.d_span_slot, T.d_span_count, T.d_span_pbase, span_lo, span_hi,
-                (const typename Ops::Acc*)s->d_tile_partials, (typename Ops::Acc*)s->d_sums);
+                (const typename Ops::Acc*)s->d_tile_partials, (typename Ops::Acc*)s->d_sums, pass == 2);
             s->launches++;
         }
+    }
+    if (pass == 1) {
+        GXB_CUDA(cudaGetLastError());
+        return GXB_OK;
     }
     Ops aops = ops;
     if constexpr (!std::is_same<Ops, PrOps>::value) {
@@ -1778,7 +1806,18 @@ bool dense_pull(const gxb_state* s) {
     return !s->nonmonotone && div != 0 && s->units_cur * (uint64_t)div >= s->g->E;
 }
 
+// the local-source pass of the next round (split rounds, gxb_iterate_local): wait for it on
+// `st` before anything touches the sums it writes; its result stays usable only for the
+// next gxb_iterate, which takes it when that round is a tile pull
+int join_local(gxb_state* s, cudaStream_t st) {
+    if (s->local_launched) GXB_CUDA(cudaStreamWaitEvent(st, s->ev_local, 0));
+    s->local_launched = false;
+    s->local_valid = false;
+    return GXB_OK;
+}
+
 int begin_round(gxb_state* s, cudaStream_t st) {
+    GXB_CHECK(join_local(s, st));
     if (s->stats_pending) {
         GXB_CUDA(cudaEventSynchronize(s->stats_ready));
         s->stats_pending = false;
@@ -2115,6 +2154,7 @@ int gxb_state_free(gxb_state* s) {
     if (s->aux_stream) cudaStreamDestroy(s->aux_stream);
     if (s->ev_tile) cudaEventDestroy(s->ev_tile);
     if (s->ev_join) cudaEventDestroy(s->ev_join);
+    if (s->ev_local) cudaEventDestroy(s->ev_local);
     dfree(s->d_rank[0]);
     dfree(s->d_rank[1]);
     dfree(s->d_contrib[0]);
@@ -2174,6 +2214,46 @@ int gxb_lp_pull(gxb_state* s, cudaStream_t st);  // gxb_lp.cu
 int gxb_lp_push(gxb_state* s, cudaStream_t st, const uint32_t* rowpre);
 
 
+int gxb_iterate_local(gxb_state* s, void* stream, int* launched) {
+    NvtxRange nvtx_("gxb_iterate_local");
+    if (launched) *launched = 0;
+    if (!s) return fail(GXB_EINVAL, "gxb_iterate_local: null state");
+    if (s->in_round) return fail(GXB_ESTATE, "gxb_iterate_local: a request round is open");
+    gxb_graph* g = s->g;
+    // only behind a dense tile pull of SSSP / CC at N > 1 (the next round is most likely
+    // one too); otherwise nothing is launched and the next round runs whole
+    if (!options().split_overlap || g->nparts < 2 || (s->algo != GXB_ALGO_SSSP && s->algo != GXB_ALGO_CC) ||
+        use_binned_pull() || s->last_direction != GXB_DIR_PULL || !s->last_dense || s->local_launched ||
+        s->iteration == 0)
+        return GXB_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!s->aux_stream) {
+        GXB_CUDA(cudaStreamCreateWithFlags(&s->aux_stream, cudaStreamNonBlocking));
+        GXB_CUDA(cudaEventCreateWithFlags(&s->ev_tile, cudaEventDisableTiming));
+        GXB_CUDA(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+    }
+    if (!s->ev_local) GXB_CUDA(cudaEventCreateWithFlags(&s->ev_local, cudaEventDisableTiming));
+    GXB_CUDA(cudaEventRecord(s->ev_join, st));  // after the round that produced the values
+    GXB_CUDA(cudaStreamWaitEvent(s->aux_stream, s->ev_join, 0));
+    const SourceSel sel{(uint32_t)g->lo, (uint32_t)(g->hi - g->lo), 1};
+    if (s->algo == GXB_ALGO_SSSP) {
+        SsspOps o = sssp_ops(s);
+        o.check_active = false;  // exact either way (see SsspOps::check_active)
+        o.sel = sel;
+        GXB_CHECK(launch_tile_and_apply(s, o, s->aux_stream, -1, nullptr, 1));
+    } else {
+        CcOps o = cc_ops(s);
+        o.check_active = false;
+        o.sel = sel;
+        GXB_CHECK(launch_tile_and_apply(s, o, s->aux_stream, -1, nullptr, 1));
+    }
+    GXB_CUDA(cudaEventRecord(s->ev_local, s->aux_stream));
+    s->local_launched = true;
+    s->local_valid = true;
+    if (launched) *launched = 1;
+    return GXB_OK;
+}
+
 int gxb_iterate(gxb_state* s, int direction, void* stream) {
     NvtxRange nvtx_("gxb_iterate");
     if (!s) return fail(GXB_EINVAL, "gxb_iterate: null state");
@@ -2183,7 +2263,8 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
     gxb_graph* g = s->g;
     GXB_CHECK(collect_stats(s));
     GXB_CHECK(settle_unpack(s));
-    GXB_CHECK(begin_round(s, st));
+    const bool local_done = s->local_valid;
+    GXB_CHECK(begin_round(s, st));  // joins the local pass
     int dir = GXB_DIR_PULL;
     if (s->algo == GXB_ALGO_SSSP || s->algo == GXB_ALGO_CC) {
         if (direction == GXB_DIR_PUSH) dir = GXB_DIR_PUSH;
@@ -2225,13 +2306,17 @@ int gxb_iterate(gxb_state* s, int direction, void* stream) {
             case GXB_ALGO_SSSP: {
                 SsspOps o = sssp_ops(s);
                 o.check_active = !dense_pull(s);
-                GXB_CHECK(launch_tile_and_apply(s, o, st));
+                if (local_done) o.sel = SourceSel{(uint32_t)g->lo, (uint32_t)(g->hi - g->lo), 2};
+                GXB_CHECK(launch_tile_and_apply(s, o, st, -1, nullptr, local_done ? 2 : 0));
+                s->last_dense = !o.check_active;
                 break;
             }
             case GXB_ALGO_CC: {
                 CcOps o = cc_ops(s);
                 o.check_active = !dense_pull(s);
-                GXB_CHECK(launch_tile_and_apply(s, o, st));
+                if (local_done) o.sel = SourceSel{(uint32_t)g->lo, (uint32_t)(g->hi - g->lo), 2};
+                GXB_CHECK(launch_tile_and_apply(s, o, st, -1, nullptr, local_done ? 2 : 0));
+                s->last_dense = !o.check_active;
                 break;
             }
         }
@@ -2547,6 +2632,7 @@ int gxb_write_attrs(gxb_state* s, const double* host_in, void* stream) {
     if (!host_in) return fail(GXB_EINVAL, "gxb_write_attrs: null input");
     cudaStream_t st = (cudaStream_t)stream;
     s->lab_injective = false;  // installed labels need not be distinct
+    GXB_CHECK(join_local(s, st));  // installed owned values void a local pass already run
     GXB_CHECK(collect_stats(s));
     GXB_CHECK(stage(s));
     GXB_CUDA(cudaMemcpyAsync(s->d_stage, host_in, 8 * V * s->arity, cudaMemcpyHostToDevice, st));
@@ -2618,6 +2704,7 @@ int gxb_attrs_install(gxb_state* s, int buf, void* stream) {
     if (!s || buf < 0 || buf > 1) return fail(GXB_EINVAL, "gxb_attrs_install: bad argument");
     if (s->in_round) return fail(GXB_ESTATE, "gxb_attrs_install: a round is open");
     s->lab_injective = false;
+    GXB_CHECK(join_local(s, (cudaStream_t)stream));  // installed values void a local pass already run
     GXB_CHECK(stage_pair(s));
     gxb_graph* g = s->g;
     const uint32_t* d2s;

@@ -309,6 +309,8 @@ struct Options {
     int64_t carveout = -1;        // tile kernel shared-memory carveout in % (-1 = driver default)
     int64_t exchange_chunks = 2;  // multi-GPU: exchange chunks (pipelined peer-write rounds; 2 measured best at N = 4)
     int64_t overlap_reserve_sms = 0;  // SMs left free while a chunked round computes (0 measured best)
+    int64_t split_overlap = 0;        // SSSP / CC at N > 1: the next round's local-source pass beside the exchange
+    int64_t split_reserve_sms = 16;   // SMs left to the exchange kernels during that pass
     int64_t pr_message_bits = 64; // PageRank message (rank / out_deg) precision: 64 or 32 (f64 accumulation)
     int64_t pr_hub_slots = 0;     // PageRank, one partition: in-edges from the first H source slots (the
                                   // highest out-degrees) are summed from a shared-memory table (<= 28672)

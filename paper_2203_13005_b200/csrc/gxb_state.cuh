@@ -221,6 +221,11 @@ struct gxb_state {
     bool peer_ipc = false;  // opened with cudaIpcOpenMemHandle (closed on free)
     int round_chunks = 0;   // exchange chunks launched in the open round
     cudaStream_t aux_stream = nullptr;  // pipelined rounds: span folds + Apply beside the tiles
+    // split rounds (gxb_iterate_local): the next round's local-source pass on aux_stream
+    cudaEvent_t ev_local = nullptr;
+    bool local_launched = false;  // ev_local pending: join before the sums are touched
+    bool local_valid = false;     // its sums are the next round's pass 1
+    bool last_dense = false;      // the last tile pull gathered without the active bitmap
     cudaEvent_t ev_tile = nullptr, ev_join = nullptr;
     // per-peer delta exchange over peer memory (SSSP / CC / LP, nparts <= 8): the pack kernel
     // stores each changed owned value only into the receive arenas of the peers whose CSC

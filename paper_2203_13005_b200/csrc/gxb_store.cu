@@ -40,6 +40,8 @@ Options& options() {
         if (const char* e = getenv("GXB_XCHUNK_POWER")) o.xchunk_power = std::min(4L, std::max(1L, atol(e)));
         if (const char* e = getenv("GXB_EXCHANGE_CHUNKS")) o.exchange_chunks = std::min(64L, std::max(1L, atol(e)));
         if (const char* e = getenv("GXB_OVERLAP_RESERVE_SMS")) o.overlap_reserve_sms = std::min(140L, std::max(0L, atol(e)));
+        if (const char* e = getenv("GXB_SPLIT_OVERLAP")) o.split_overlap = atol(e) ? 1 : 0;
+        if (const char* e = getenv("GXB_SPLIT_RESERVE_SMS")) o.split_reserve_sms = std::min(140L, std::max(0L, atol(e)));
     }
     return o;
 }
@@ -963,6 +965,12 @@ int gxb_set_option(const char* name, int64_t value) {
     } else if (n == "overlap_reserve_sms") {
         if (value < 0 || value > 140) return fail(GXB_EINVAL, "overlap_reserve_sms: 0..140");
         o.overlap_reserve_sms = value;
+    } else if (n == "split_overlap") {
+        if (value != 0 && value != 1) return fail(GXB_EINVAL, "split_overlap: 0 or 1");
+        o.split_overlap = value;
+    } else if (n == "split_reserve_sms") {
+        if (value < 0 || value > 140) return fail(GXB_EINVAL, "split_reserve_sms: 0..140");
+        o.split_reserve_sms = value;
     } else if (n == "carveout") {
         if (value < -1 || value > 100) return fail(GXB_EINVAL, "carveout: -1 or 0..100");
         o.carveout = value;
@@ -998,6 +1006,8 @@ int gxb_get_option(const char* name, int64_t* value) {
     else if (n == "pr_hub_slots") *value = o.pr_hub_slots;
     else if (n == "carveout") *value = o.carveout;
     else if (n == "overlap_reserve_sms") *value = o.overlap_reserve_sms;
+    else if (n == "split_overlap") *value = o.split_overlap;
+    else if (n == "split_reserve_sms") *value = o.split_reserve_sms;
     else if (n == "exchange_chunks") *value = o.exchange_chunks;
     else if (n == "l1_hot_kb") *value = o.l1_hot_kb;
     else return fail(GXB_EINVAL, "unknown option " + n);

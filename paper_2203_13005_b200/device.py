@@ -268,6 +268,7 @@ class DeviceState:
         h = ctypes.c_void_p()
         L.check(L.lib().gxb_state_create(graph.handle, ALGO_IDS[algo], _vp(srcs), nsrc, ctypes.byref(h)))
         self._h = h
+        self.local_passes = 0  # split rounds: local-source passes launched (iterate_local)
         ar = ctypes.c_int()
         L.check(L.lib().gxb_state_arity(h, ctypes.byref(ar)))
         self.arity = ar.value
@@ -278,6 +279,15 @@ class DeviceState:
 
     def iterate(self, direction: str = "auto", stream=None):
         L.check(L.lib().gxb_iterate(self._h, DIRECTIONS[direction], _stream_ptr(stream)))
+
+    def iterate_local(self, stream=None):
+        """Launch the next round's local-source pass beside the exchange (split rounds:
+        option ``split_overlap``; a no-op unless the last round was a dense SSSP / CC pull
+        at N > 1). The next :meth:`iterate` combines it with the remote-source pass."""
+        launched = ctypes.c_int(0)
+        L.check(L.lib().gxb_iterate_local(self._h, _stream_ptr(stream), ctypes.byref(launched)))
+        self.local_passes += launched.value
+        return bool(launched.value)
 
     def iterate_begin(self, stream=None):
         L.check(L.lib().gxb_iterate_begin(self._h, _stream_ptr(stream)))
@@ -552,6 +562,13 @@ class SsspLanes:
     def iterate(self, direction: str = "auto", stream=None):
         for st in self.states:
             st.iterate(direction, stream)
+
+    def iterate_local(self, stream=None):
+        return any([st.iterate_local(stream) for st in self.states])
+
+    @property
+    def local_passes(self) -> int:
+        return sum(st.local_passes for st in self.states)
 
     def request(self, op: int, lo: int, hi: int, stream=None):
         for st in self.states:

@@ -504,6 +504,10 @@ class PartitionedRun:
                 if self._vote_buf.numel() > 6:
                     self._vote_buf[6:].zero_()  # no records this round
             elif dpeers:
+                # split rounds (option split_overlap): the next round's local-source pass runs
+                # beside this round's pack, vote and unpack (a no-op unless this was a dense pull)
+                if hasattr(self.state, "iterate_local"):
+                    self.state.iterate_local(**self._on_stream())
                 self.state.delta_pack(self._vote_buf, **self._on_stream())
             elif async_delta:
                 self.state.pack_async(**self._on_stream())

@@ -68,6 +68,7 @@ class RunMetrics:
     iterations: int = 0
     skipped_rounds: int = 0
     exchanged_bytes: int = 0
+    split_passes: int = 0  # local-source passes run beside an exchange (option split_overlap)
     init_counts: dict[int, int] = field(default_factory=dict)
 
     def lines(self) -> list[str]:
@@ -147,6 +148,8 @@ def exchange_local_peers(states, votes) -> int:
     delta_pack -> vote -> delta_unpack): each partition receives only the changed values its
     CSC reads (A/agent.py:550-582 with a static query set)."""
     from . import _lib as L
+    for s in states:  # split rounds (option split_overlap): the next round's local pass first
+        s.iterate_local()
     for s, v in zip(states, votes):
         s.delta_pack(v)
     rows = [v.cpu().tolist() for v in votes]
@@ -261,6 +264,7 @@ class Engine:
             else:
                 moved = sum(exchange_local(grp, self.bounds) for grp in self.groups)
             self.metrics.exchanged_bytes += moved
+            self.metrics.split_passes = sum(getattr(s, "local_passes", 0) for s in self.states)
             converged = convergence_vote([bool(st["voted"]) for st in stats])
             apply_rounds += 1
             if skip and not converged:

@@ -446,3 +446,38 @@ def test_peer_delta_exchange_equals_all_to_all(oracle_lib, algo, m, partitioning
     assert_attrs_match(algo, out[False][0], ref.attrs)
     assert out[True][1].iterations == out[False][1].iterations == ref.iterations
     assert 0 < out[True][1].exchanged_bytes <= out[False][1].exchanged_bytes
+
+
+@pytest.mark.parametrize("algo", ["sssp", "cc"])
+@pytest.mark.parametrize("m", [2, 3, 4])
+@pytest.mark.parametrize("forced", [False, True])
+def test_split_rounds_equal_oracle(oracle_lib, algo, m, forced):
+    """Split rounds (option split_overlap, SURVEY.md §8(e) overlap): behind a dense pull the
+    next round's local-source pass runs while the records travel, then the remote-source
+    pass combines into it. Results, iteration count and the per-round changed trace equal
+    the oracle's; `forced` makes every round a dense pull (each round from the
+    second on is split), else the auto direction splits only the dense middle rounds."""
+    from paper_2203_13005_b200 import _lib as L
+    from paper_2203_13005_b200.algorithms import make_algorithm
+    from paper_2203_13005_b200.engine import RunConfig, run
+    from paper_2203_13005_b200.graph import EdgeArrays
+    from paper_2203_13005_b200.rmat import RmatParams, rmat_host
+    p = RmatParams(scale=13, seed=70 + m, wmax=63 if algo == "sssp" else 0, symmetric=algo == "cc")
+    src, dst, w = rmat_host(p)
+    ea = EdgeArrays(src, dst, None if w is None else w.astype(np.float64))
+    ids = ea.vertex_ids()
+    alg = make_algorithm(algo, [int(v) for v in ids], None)
+    L.set_option("split_overlap", 1)
+    if forced:
+        L.set_option("pull_dense_div", 1 << 20)
+    try:
+        attrs, met = run(ea, alg, "bsp", RunConfig(partitions=m, peer_delta=True, enable_skip=True,
+                                                   direction="pull" if forced else "auto"))
+    finally:
+        L.set_option("split_overlap", 0)
+        L.set_option("pull_dense_div", 4)
+    ref = oracle_lib.OracleGraph(src, dst, None if w is None else w.astype(np.float64)).run(algo)
+    assert_attrs_match(algo, np.array([alg.row_from_attr(attrs[int(v)]) for v in ids]), ref.attrs)
+    assert met.iterations == ref.iterations
+    assert [r.changed for r in met.records] == list(ref.changed)
+    assert met.split_passes > 0, "no split round ran"

@@ -26,7 +26,7 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, algo, out_path):
+def _worker(rank, world, port, algo, out_path, split=False):
     sys.path.insert(0, REPO)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     import torch
@@ -36,6 +36,9 @@ def _worker(rank, world, port, algo, out_path):
     from paper_2203_13005_b200.rmat import RmatParams, rmat_host
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
+    if split:  # split rounds: the local-source pass beside the cross-process exchange
+        from paper_2203_13005_b200 import _lib as L
+        L.set_option("split_overlap", 1)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         p = RmatParams(scale=12, seed=77, wmax=63 if algo == "sssp" else 0, symmetric=algo == "cc")
@@ -66,14 +69,15 @@ def _worker(rank, world, port, algo, out_path):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("algo", ["pagerank", "sssp", "cc", "lp"])
-def test_two_processes_ipc_paths(tmp_path, oracle_lib, algo):
+@pytest.mark.parametrize("algo,split", [("pagerank", False), ("sssp", False), ("cc", False), ("lp", False),
+                                        ("sssp", True), ("cc", True)])
+def test_two_processes_ipc_paths(tmp_path, oracle_lib, algo, split):
     import multiprocessing as mp
     from paper_2203_13005_b200.rmat import RmatParams, rmat_host
     port = _free_port()
     out = os.path.join(tmp_path, "out.json")
     ctx = mp.get_context("spawn")
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, algo, out)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, algo, out, split)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
