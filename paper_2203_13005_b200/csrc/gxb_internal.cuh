@@ -299,7 +299,7 @@ struct Options {
     int64_t tile_minblocks = 0;   // __launch_bounds__ min-blocks variant of the tile kernel (0/4/6/8)
     int64_t l2_hot_mb = 64;       // L2 budget (MB) of the evict-last prefix of gathered values
     int64_t l1_hot_kb = 160;      // L1 budget (KB) of the L1-allocating prefix (others bypass L1)
-    int64_t push_alpha = 20;      // push when frontier out-edges * alpha < |E|
+    int64_t push_alpha = 10;      // push when frontier out-edges * alpha < |E| (10 vs 20: CC S24 -14%, SSSP / LP same)
     int64_t pull_dense_div = 4;   // SSSP/CC pull skips the active bitmap when frontier out-edges * div >= |E|
     int64_t pull_kernel = 0;
     int64_t pipeline_apply = 0;   // PageRank: pipelined chunk rounds even without peer replicas (N = 1)
