@@ -1004,7 +1004,7 @@ __global__ void __launch_bounds__(kBlock) k_push(const Op op, const PushLaunch L
         uint64_t f = a;
 #pragma unroll 1
         for (uint64_t gl = g0 + lane; gl < g1; gl += 32) {
-            while (__ldg(rowpre + f) <= gl) ++f;
+            f = row_advance(rowpre, L.nfront, f, gl);
             const uint32_t s = __ldg(L.frontier + f);
             const uint64_t e = __ldg(L.out_off + s) + (gl - (f ? __ldg(rowpre + f - 1) : 0));
             const uint32_t t = __ldg(L.out_dst + e);

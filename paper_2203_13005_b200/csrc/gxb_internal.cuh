@@ -164,6 +164,27 @@ namespace gxb {
 __device__ __forceinline__ bool bit_test(const uint32_t* bm, uint32_t i) {
     return (__ldg(bm + (i >> 5)) >> (i & 31)) & 1u;
 }
+// Push rounds walk the concatenated frontier rows (rowpre = inclusive prefix of the row
+// lengths, rowpre[n - 1] > g): move row cursor f to the row of edge g, the first f' >= f
+// with rowpre[f'] > g. Usually the next row or two; at N > 1 a frontier holds many rows
+// with no local out-edge (changed vertices whose out-edges all leave the partition), so a
+// run of empty rows is crossed by galloping plus a binary search instead of one load each.
+__device__ __forceinline__ uint64_t row_advance(const uint32_t* __restrict__ rowpre, uint64_t n, uint64_t f,
+                                                uint64_t g) {
+    if (__ldg(rowpre + f) > g) return f;
+    uint64_t lo = f + 1, hi = lo, step = 1;  // every row before lo ends at or before g
+    while (__ldg(rowpre + hi) <= g) {
+        lo = hi + 1;
+        hi = min(hi + step, n - 1);
+        step <<= 1;
+    }
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (__ldg(rowpre + mid) > g) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
 __device__ __forceinline__ bool bit_set_atomic(uint32_t* bm, uint32_t i) {
     const uint32_t m = 1u << (i & 31);
     return (atomicOr(bm + (i >> 5), m) & m) == 0u;  // true if newly set

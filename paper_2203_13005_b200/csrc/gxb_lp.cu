@@ -800,7 +800,7 @@ __global__ void __launch_bounds__(kBlock) k_lp_push(const uint32_t* __restrict__
             const bool ok = gl < g1;
             uint32_t rel = 0, lab = 0;
             if (ok) {
-                while (__ldg(rowpre + f) <= gl) ++f;
+                f = row_advance(rowpre, nfront, f, gl);
                 const uint32_t s = __ldg(frontier + f);
                 const uint64_t e = __ldg(out_off + s) + (gl - (f ? __ldg(rowpre + f - 1) : 0));
                 rel = (uint32_t)(__ldg(out_dst + e) - lo);

@@ -49,7 +49,8 @@ def main():
             rec = run.step()
             if rep:
                 now = run.phase_times
-                per_round.append({"dir": rec.direction, "changed": rec.changed,
+                per_round.append({"dir": rec.direction, "changed": rec.changed, "units": rec.units,
+                                  "next_active": rec.next_active,
                                   **{k: round(1e3 * (now.get(k, 0.0) - before.get(k, 0.0)), 3) for k in now}})
             if rec.converged:
                 break
