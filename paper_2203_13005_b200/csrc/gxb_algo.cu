@@ -2151,7 +2151,10 @@ int gxb_state_free(gxb_state* s) {
     if (!s) return GXB_OK;
     gxb_exchange_close_peers(s);
     if (s->algo != GXB_ALGO_PAGERANK) gxb_exchange_delta_close(s);
-    if (s->aux_stream) cudaStreamDestroy(s->aux_stream);
+    if (s->aux_stream) {
+        cudaStreamSynchronize(s->aux_stream);  // a local pass may still read / write the buffers below
+        cudaStreamDestroy(s->aux_stream);
+    }
     if (s->ev_tile) cudaEventDestroy(s->ev_tile);
     if (s->ev_join) cudaEventDestroy(s->ev_join);
     if (s->ev_local) cudaEventDestroy(s->ev_local);
