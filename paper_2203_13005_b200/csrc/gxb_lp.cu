@@ -174,10 +174,10 @@ __device__ __forceinline__ void lp_group(const LpLaunch& L, int k, unsigned b, u
         beg = __ldg(L.in_off + rel);
         deg = (uint32_t)(__ldg(L.in_off + rel + 1) - beg);
     }
-    uint32_t* my = buf + grp * kCap;
-    for (uint32_t i = gl; i < deg; i += G) {
-        const uint32_t s = __ldg(L.in_src + beg + i);
-        my[i] = lp_msg(L, s);
+    uint32_t* my = buf + grp * kCap;  // 16-B aligned: kCap is a multiple of 4
+    const uint32_t deg4 = (deg + 3u) & ~3u;
+    for (uint32_t i = gl; i < deg4; i += G) {  // padded with kEmpty, which is never a candidate
+        my[i] = i < deg ? lp_msg(L, __ldg(L.in_src + beg + i)) : kEmpty;
     }
     __syncwarp();
     unsigned long long best = 0ull;
@@ -185,7 +185,10 @@ __device__ __forceinline__ void lp_group(const LpLaunch& L, int k, unsigned b, u
         const uint32_t lab = my[i];
         if (lab == kEmpty) continue;
         uint32_t c = 0;
-        for (uint32_t j = 0; j < deg; ++j) c += (my[j] == lab) ? 1u : 0u;
+        for (uint32_t j = 0; j < deg4; j += 4) {  // four staged labels per 16-B load
+            const uint4 q = *reinterpret_cast<const uint4*>(my + j);
+            c += (q.x == lab) + (q.y == lab) + (q.z == lab) + (q.w == lab);
+        }
         const unsigned long long p = ((unsigned long long)c << 32) | (unsigned long long)(~lab);
         best = p > best ? p : best;
     }
@@ -649,7 +652,7 @@ __global__ void __launch_bounds__(kBlock) k_lp_chunks_runs(const LpLaunch L) {
 
 // the group bins (in-degree <= 32; 33-128 go to the warp tables)
 __global__ void __launch_bounds__(kBlock) k_lp_pull(const LpLaunch L) {
-    __shared__ uint32_t buf[4 * kBlock];  // 4 labels per thread
+    __shared__ __align__(16) uint32_t buf[4 * kBlock];  // 4 labels per thread
     LocalStats st;
     unsigned b = blockIdx.x;
     int k = kNumGroupBins - 1;
