@@ -202,3 +202,32 @@ def test_sssp_many_sources_partitioned(oracle_lib, m):
     got = np.array([algo.row_from_attr(attrs[int(v)]) for v in ids])
     assert_attrs_match("sssp", got, ref.attrs)
     assert met.iterations == ref.iterations
+
+
+def test_sssp_many_sources_split_rounds(oracle_lib):
+    """Split rounds (option split_overlap) with lane groups (6 sources, dyadic weights,
+    3 partitions, every round a dense pull): each group's states run their local-source
+    passes beside the group's exchange; results equal the oracle."""
+    from paper_2203_13005_b200 import _lib as L
+    from paper_2203_13005_b200.algorithms import SsspBellmanFord
+    from paper_2203_13005_b200.engine import RunConfig, run
+    from paper_2203_13005_b200.graph import EdgeArrays
+    from paper_2203_13005_b200.rmat import RmatParams, rmat_host
+    src, dst, w = rmat_host(RmatParams(scale=12, seed=98, wmax=31))
+    wf = w.astype(np.float64) / 4
+    ids = np.union1d(src, dst)
+    sources = [int(x) for x in ids[::max(1, len(ids) // 6)][:6]]
+    algo = SsspBellmanFord(sources)
+    L.set_option("split_overlap", 1)
+    L.set_option("pull_dense_div", 1 << 20)
+    try:
+        attrs, met = run(EdgeArrays(src, dst, wf), algo, "bsp",
+                         RunConfig(partitions=3, enable_skip=True, direction="pull"))
+    finally:
+        L.set_option("split_overlap", 0)
+        L.set_option("pull_dense_div", 4)
+    ref = oracle_lib.OracleGraph(src, dst, wf).run("sssp", sources=np.array(sources, np.uint32))
+    got = np.array([algo.row_from_attr(attrs[int(v)]) for v in ids])
+    assert_attrs_match("sssp", got, ref.attrs)
+    assert met.iterations == ref.iterations
+    assert met.split_passes > 0
