@@ -302,6 +302,16 @@ def test_options_roundtrip():
         L.set_option("no_such_knob", 1)
     with pytest.raises(ValueError):
         L.set_option("tile_minblocks", 3)
+    # split rounds: off by default (measured slower), 0/1 only; reserve 0..140 SMs
+    assert L.get_option("split_overlap") == 0
+    assert L.get_option("push_alpha") == 10
+    for name, bad in (("split_overlap", 2), ("split_reserve_sms", 141), ("split_reserve_sms", -1)):
+        with pytest.raises(ValueError):
+            L.set_option(name, bad)
+    old = L.get_option("split_reserve_sms")
+    L.set_option("split_reserve_sms", 32)
+    assert L.get_option("split_reserve_sms") == 32
+    L.set_option("split_reserve_sms", old)
 
 
 # ---------------------------------------------------------------- device weight encoding
