@@ -48,6 +48,7 @@ struct LpScratch {
     uint64_t big_end = 0;  // relative slots [0, big_end): in-degree > kLpBigDeg (chunked warps)
     uint64_t big_items = 0;    // their chunk items (the plan's first items)
     uint64_t cta_end = 0;  // relative slots [big_end, cta_end): in-degree > kLpCtaMinDeg (one CTA each)
+    uint64_t cta_half = 0;  // [cta_half, cta_end): in-degree <= kLpCtaHalfDeg (half a CTA each)
     uint32_t* eff = nullptr;  // per slot: label if active, else kEmpty (rounds >= 2)
     uint32_t hot_end = 0;  // slots with in-degree >= kLpHotDegree: pushed through shared memory
     // sparse rounds (allocated on the first one)
@@ -584,6 +585,55 @@ __global__ void __launch_bounds__(kBlock) k_lp_hub_cta(const LpLaunch L, uint64_
     flush_stats(st, L.stats);
 }
 
+// The same with each half of the CTA on its own destination (in-degree <= kLpCtaHalfDeg):
+// named barriers per half, so one half's finish and scan do not hold the other's counting.
+constexpr uint32_t kLpCtaHalfDeg = kLpCtaCap / 4;
+__global__ void __launch_bounds__(kBlock) k_lp_hub_cta2(const LpLaunch L, uint64_t lo_rel, uint64_t hi_rel) {
+    constexpr int kHalf = kBlock / 2, kCap = kLpCtaCap / 2;
+    extern __shared__ uint32_t lp_dyn[];  // per half: kCap keys, then kCap counts
+    const int half = threadIdx.x / kHalf, t = threadIdx.x % kHalf;
+    uint32_t* keys = lp_dyn + half * 2 * kCap;
+    uint32_t* cnts = keys + kCap;
+    __shared__ unsigned long long wbest[2][kBlock / 32];
+    LocalStats st;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto half_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + half), "r"(kHalf) : "memory"); };
+    for (uint32_t i = t; i < kCap; i += kHalf) {
+        keys[i] = kEmpty;
+        cnts[i] = 0;
+    }
+    half_sync();
+    int par = 0;
+    for (uint64_t rel = lo_rel + 2ull * blockIdx.x + half; rel < hi_rel; rel += 2ull * gridDim.x, par ^= 1) {
+        const uint64_t beg = __ldg(L.in_off + rel), end = __ldg(L.in_off + rel + 1);
+        uint32_t C = 64;
+        while ((uint64_t)C < 2 * (end - beg)) C <<= 1;  // <= kCap
+        lp_count_edges(L, beg, end, t, kHalf, keys, cnts, C - 1);
+        half_sync();
+        unsigned long long best = 0ull;
+        for (uint32_t i = t; i < C; i += kHalf) {
+            const uint32_t k = keys[i];
+            if (k != kEmpty) {
+                const unsigned long long pk = pack_best(cnts[i], k);
+                best = pk > best ? pk : best;
+                keys[i] = kEmpty;
+                cnts[i] = 0;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long q = __shfl_xor_sync(kFull, best, o);
+            best = q > best ? q : best;
+        }
+        if (lane == 0) wbest[par][warp] = best;
+        half_sync();
+        if (t == 0) {
+            for (int w = 1; w < kHalf / 32; ++w) best = wbest[par][warp + w] > best ? wbest[par][warp + w] : best;
+            lp_finish(L, (uint32_t)(L.lo + rel), best, st);
+        }
+    }
+    flush_stats(st, L.stats);
+}
+
 // kCap: table entries per warp — 2 x the largest in-degree of the launch's slots (the
 // 33-128 slots run with 256-entry tables: a quarter of the shared memory, more warps per SM)
 template <int kCap>
@@ -896,6 +946,9 @@ static int lp_setup(gxb_state* s, cudaStream_t st) {
         ++S->big_end;
     }
     S->cta_end = S->big_end;
+    S->cta_half = S->big_end;
+    while (S->cta_half < P.chunk_end && g->h_indeg_sorted[S->cta_half] > kLpCtaHalfDeg) ++S->cta_half;
+    S->cta_end = S->cta_half;
     while (S->cta_end < P.chunk_end && g->h_indeg_sorted[S->cta_end] > kLpCtaMinDeg) ++S->cta_end;
     while (S->hot_end < g->h_indeg_sorted.size() && g->h_indeg_sorted[S->hot_end] >= kLpHotDegree) ++S->hot_end;
     LpHub& H = S->hub;
@@ -1006,6 +1059,7 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
     const int dev = g->ctx->device & 63;
     if (!attrs_set[dev]) {
         GXB_CUDA(cudaFuncSetAttribute(k_lp_hub_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4 * kLpCtaCap));
+        GXB_CUDA(cudaFuncSetAttribute(k_lp_hub_cta2, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4 * kLpCtaCap));
         GXB_CUDA(cudaFuncSetAttribute(k_lp_hub_warp<kLpWarpCap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (kBlock / 32) * 2 * 4 * kLpWarpCap));
         attrs_set[dev] = true;
@@ -1043,9 +1097,13 @@ extern "C" int gxb_lp_pull(gxb_state* s, cudaStream_t st) {
     }
     grid -= L.chunk_blocks;
     if (grid) k_lp_pull<<<grid, kBlock, 0, st>>>(L);
-    if (!L.injective && S->cta_end > S->big_end) {
-        const unsigned gc = (unsigned)std::min<uint64_t>(S->cta_end - S->big_end, 3ull * kNumSMs);
-        k_lp_hub_cta<<<gc, kBlock, 2 * 4 * kLpCtaCap, st>>>(L, S->big_end, S->cta_end);
+    if (!L.injective && S->cta_end > S->big_end) {  // CTA tables: a whole CTA above kLpCtaHalfDeg, else half
+        if (S->cta_half > S->big_end)
+            k_lp_hub_cta<<<(unsigned)std::min<uint64_t>(S->cta_half - S->big_end, 3ull * kNumSMs), kBlock,
+                           2 * 4 * kLpCtaCap, st>>>(L, S->big_end, S->cta_half);
+        if (S->cta_end > S->cta_half)
+            k_lp_hub_cta2<<<(unsigned)std::min<uint64_t>((S->cta_end - S->cta_half + 1) / 2, 3ull * kNumSMs), kBlock,
+                            2 * 4 * kLpCtaCap, st>>>(L, S->cta_half, S->cta_end);
     }
     // warp tables: in-degree 129-512 (rounds >= 2) with 1024 entries, 33-128 with 256
     auto warp_grid = [](uint64_t n) {
