@@ -9,9 +9,9 @@
 // Dense rounds, over the in-degree-sorted slots:
 //  * in-degree <= 32 (k_lp_pull): G lanes per destination stage its labels in shared
 //    memory and count each candidate against the staged multiset;
-//  * 33-512 (k_lp_hub_warp) and 513-4096 (k_lp_hub_cta): a warp / CTA counts the
-//    destination in a shared (label, count) table twice its in-degree, after equal labels
-//    of 32 edges are merged with __match_any_sync;
+//  * 33-512 (k_lp_hub_warp) and 513-4096 (k_lp_hub_cta, half a CTA up to 2048:
+//    k_lp_hub_cta2): a warp / CTA counts the destination in a shared (label, count) table
+//    twice its in-degree, after equal labels of 32 edges are merged with __match_any_sync;
 //  * above 4096 (k_lp_chunks): warps stream 1024-edge chunks into per-warp shared tables
 //    and flush them into per-hub epoch-tagged global tables (L2 atomics); the packed
 //    argmax (count << 32 | ~label) is raised once per chunk, k_lp_hub_apply applies it.
