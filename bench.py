@@ -607,8 +607,12 @@ def main():
     kname = "k_tile_a" if L.get_option("tile_async") else "k_tile_t"
     traffic = None
     try:  # dram bytes per launch of the same kernel from the committed ncu --set full capture
-        with open(os.path.join(HERE, "profiles", "r01_traffic.json")) as fh:
-            tr = json.load(fh).get(f"{algo}-s{scale}", {}).get(kname)
+        tr = None
+        for name in ("r02_traffic.json", "r01_traffic.json"):  # the latest capture that has it
+            path = os.path.join(HERE, "profiles", name)
+            if os.path.exists(path) and tr is None:
+                with open(path) as fh:
+                    tr = json.load(fh).get(f"{algo}-s{scale}", {}).get(kname)
         if tr and world == 1:
             traffic = int(tr["dram_read_bytes"] + tr["dram_write_bytes"])
     except Exception:  # noqa: BLE001
