@@ -847,18 +847,45 @@ __global__ void __launch_bounds__(kBlock) k_lp_push(const uint32_t* __restrict__
             if (__ldg(rowpre + mid) > g0) b = mid; else a = mid + 1;
         }
         uint64_t f = a;  // this lane's row cursor (monotone over its edges)
-#pragma unroll 1
-        for (uint32_t j = 0; j < kLpItemEdges / 32; ++j) {
+        // the item's dependent loads level by level for all of a lane's edges (row -> source
+        // -> edge -> destination, label), so each level has kJ loads in flight, then the
+        // counting over the loaded (destination, label) pairs
+        constexpr int kJ = kLpItemEdges / 32;
+        uint32_t relj[kJ], labj[kJ];
+        uint64_t ej[kJ];
+        unsigned okm = 0u;
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
             const uint64_t gl = g0 + j * 32 + lane;
-            const bool ok = gl < g1;
-            uint32_t rel = 0, lab = 0;
-            if (ok) {
+            if (gl < g1) {
+                okm |= 1u << j;
                 f = row_advance(rowpre, nfront, f, gl);
-                const uint32_t s = __ldg(frontier + f);
-                const uint64_t e = __ldg(out_off + s) + (gl - (f ? __ldg(rowpre + f - 1) : 0));
-                rel = (uint32_t)(__ldg(out_dst + e) - lo);
-                lab = __ldg(lab_cur + s);
+                ej[j] = f;  // the row for now
             }
+        }
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+            if ((okm >> j) & 1u) {
+                const uint64_t fj = ej[j];
+                labj[j] = __ldg(frontier + fj);  // the source for now
+                ej[j] = (g0 + j * 32 + lane) - (fj ? __ldg(rowpre + fj - 1) : 0);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kJ; ++j)
+            if ((okm >> j) & 1u) ej[j] += __ldg(out_off + labj[j]);
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+            relj[j] = 0u;
+            if ((okm >> j) & 1u) {
+                relj[j] = (uint32_t)(__ldg(out_dst + ej[j]) - lo);
+                labj[j] = __ldg(lab_cur + labj[j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+            const bool ok = (okm >> j) & 1u;
+            const uint32_t rel = relj[j], lab = ok ? labj[j] : 0u;
             const unsigned long long key = ok ? ((unsigned long long)rel << 32 | lab) : (~0ull - 1 - lane);
             const unsigned m = __match_any_sync(kFull, key);
             bool first = false;
