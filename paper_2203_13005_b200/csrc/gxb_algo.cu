@@ -959,6 +959,7 @@ struct SsspPush {
     const uint4* dist_cur;
     uint4* dist_next;
     using Val = uint4;
+    static constexpr int kBatch = 8;  // edges per lane whose loads are issued together (k_push)
     __device__ Val load(uint32_t s) const { return __ldg(dist_cur + s); }
     __device__ bool relax(Val d, uint32_t t, uint32_t w) const {
         const uint4 c = make_uint4(sat_add(d.x, w), sat_add(d.y, w), sat_add(d.z, w), sat_add(d.w, w));
@@ -977,6 +978,7 @@ struct CcPush {
     const uint32_t* lab_cur;
     uint32_t* lab_next;
     using Val = uint32_t;
+    static constexpr int kBatch = 1;
     __device__ Val load(uint32_t s) const { return __ldg(lab_cur + s); }
     __device__ bool relax(Val v, uint32_t t, uint32_t) const {
         return v < __ldcg(lab_next + t) && atomicMin(lab_next + t, v) > v;
@@ -1002,15 +1004,46 @@ __global__ void __launch_bounds__(kBlock) k_push(const Op op, const PushLaunch L
             if (__ldg(rowpre + mid) > g0) b = mid; else a = mid + 1;
         }
         uint64_t f = a;
+        // Op::kBatch of a lane's edges at a time, their dependent loads level by level (row
+        // -> source -> edge -> target, weight): kBatch loads in flight per level, then the
+        // relaxes (SSSP: 8, the whole chunk; CC: 1 — its lighter relax lost occupancy to the
+        // batch's registers, measured)
+        constexpr int kJ = Op::kBatch;
 #pragma unroll 1
-        for (uint64_t gl = g0 + lane; gl < g1; gl += 32) {
-            f = row_advance(rowpre, L.nfront, f, gl);
-            const uint32_t s = __ldg(L.frontier + f);
-            const uint64_t e = __ldg(L.out_off + s) + (gl - (f ? __ldg(rowpre + f - 1) : 0));
-            const uint32_t t = __ldg(L.out_dst + e);
-            const uint32_t w = L.out_w ? __ldg(L.out_w + e) : 1u;
-            if (op.relax(op.load(s), t, w) && bit_set_atomic(L.touched, (uint32_t)(t - L.lo)))
-                warp_append(L.list_next, L.count_next, t);
+        for (uint64_t gb = g0 + lane; gb < g1; gb += 32 * kJ) {
+            uint64_t ej[kJ];
+            uint32_t sj[kJ], tj[kJ], wj[kJ];
+            unsigned okm = 0u;
+#pragma unroll
+            for (int j = 0; j < kJ; ++j) {
+                const uint64_t gl = gb + 32 * j;
+                if (gl < g1) {
+                    okm |= 1u << j;
+                    f = row_advance(rowpre, L.nfront, f, gl);
+                    ej[j] = f;  // the row for now
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kJ; ++j)
+                if ((okm >> j) & 1u) {
+                    const uint64_t fj = ej[j];
+                    sj[j] = __ldg(L.frontier + fj);
+                    ej[j] = (gb + 32 * j) - (fj ? __ldg(rowpre + fj - 1) : 0);
+                }
+#pragma unroll
+            for (int j = 0; j < kJ; ++j)
+                if ((okm >> j) & 1u) ej[j] += __ldg(L.out_off + sj[j]);
+#pragma unroll
+            for (int j = 0; j < kJ; ++j)
+                if ((okm >> j) & 1u) {
+                    tj[j] = __ldg(L.out_dst + ej[j]);
+                    wj[j] = L.out_w ? __ldg(L.out_w + ej[j]) : 1u;
+                }
+#pragma unroll
+            for (int j = 0; j < kJ; ++j)
+                if (((okm >> j) & 1u) && op.relax(op.load(sj[j]), tj[j], wj[j]) &&
+                    bit_set_atomic(L.touched, (uint32_t)(tj[j] - L.lo)))
+                    warp_append(L.list_next, L.count_next, tj[j]);
         }
     }
 }
