@@ -253,7 +253,7 @@ __device__ __forceinline__ void lp_chunk(const LpLaunch& L, uint64_t item, uint3
     if (lane == 0) *wfull = 0u;
     __syncwarp();
     unsigned long long lbest = 0ull;
-    constexpr int kB = 8;  // the loads of 8 steps are issued together
+    constexpr int kB = 4;  // the loads of 4 steps are issued together (measured: 4 beats 2, 8 and 16)
     for (uint64_t e0 = beg; e0 < end; e0 += 32 * kB) {
         uint32_t src[kB], lab[kB];
         bool ok[kB];
@@ -482,7 +482,7 @@ __device__ __forceinline__ unsigned long long pack_best(uint32_t count, uint32_t
 // each 32-edge group's labels into the shared table
 __device__ __forceinline__ void lp_count_edges(const LpLaunch& L, uint64_t beg, uint64_t end, unsigned t,
                                                unsigned nthreads, uint32_t* keys, uint32_t* cnts, uint32_t mask) {
-    constexpr int kB = 8;
+    constexpr int kB = 4;  // 32-edge groups loaded together per lane (measured: 4 beats 2 and 8)
     const int lane = threadIdx.x & 31;
     const unsigned lower = (1u << lane) - 1u;  // a group's leader has no lower lane in it (no ffs on the XU pipe)
     // 32-edge groups dealt round-robin over the warps (group g to warp g mod nw), kB per
@@ -510,7 +510,7 @@ __device__ __forceinline__ void lp_count_edges(const LpLaunch& L, uint64_t beg, 
 __device__ __forceinline__ unsigned long long lp_count_edges_ep(const LpLaunch& L, uint64_t beg, uint64_t end,
                                                                 unsigned t, unsigned nthreads, unsigned long long* tab,
                                                                 uint32_t mask, uint32_t ep) {
-    constexpr int kB = 8;
+    constexpr int kB = 4;  // 32-edge groups loaded together per lane (measured: 4 beats 2 and 8)
     const int lane = threadIdx.x & 31;
     const unsigned lower = (1u << lane) - 1u;
     const unsigned warp0 = t - lane;
