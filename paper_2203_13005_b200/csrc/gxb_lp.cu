@@ -819,7 +819,7 @@ __device__ __forceinline__ void append_targets(const LpPush& P, bool first, uint
 // of row lengths): a warp takes 256 consecutive edges, finds the first one's row with one
 // binary search, and each lane walks forward to its own rows — many short rows cost no
 // more than one long one.
-constexpr uint32_t kLpItemEdges = 256;
+constexpr uint32_t kLpItemEdges = 128;  // edges per warp work item (128 vs 256: push rounds -3%)
 
 __global__ void __launch_bounds__(kBlock) k_lp_push(const uint32_t* __restrict__ frontier, uint64_t nfront,
                                                     const uint32_t* __restrict__ rowpre,
